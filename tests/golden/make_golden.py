@@ -1,0 +1,77 @@
+"""Generate golden vectors from the UNMODIFIED reference implementation.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+For every case, inputs come from the reference's own ``random_inputs``
+(machine.py:1064-1070) on the LAYER_WISE schedule, are rounded to fp16 (so
+the GPU path consumes exactly the same values), and the reference's
+``execute_numeric`` (machine.py:1053) evaluates both the LAYER_WISE and the
+BLOCK_FUSION schedules. The .npz files are committed; the GPU box never reads
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def main() -> None:
+    sys.path.insert(0, REF)
+    from waterline.core import ConvFirst, ExecutionScheme, FFN, MBConv, TensorDims  # noqa: E402
+    from waterline.machine import build_schedule, execute_numeric, random_inputs, simulate_traffic  # noqa: E402
+
+    cases = [
+        ("convfirst_t8_a6_relu", ConvFirst(8, 6, 1, "relu"), (2, 8, 8, 16), 0),
+        ("convfirst_t8_a3_relu_rect", ConvFirst(8, 3, 1, "relu"), (1, 12, 10, 32), 1),
+        ("convfirst_t1_a4_relu", ConvFirst(1, 4, 1, "relu"), (2, 8, 8, 16), 2),
+        ("convfirst_t8_a4_silu_7x7", ConvFirst(8, 4, 1, "silu"), (2, 7, 7, 24), 3),
+        ("convfirst_t8_a6_relu_c48", ConvFirst(8, 6, 1, "relu"), (1, 14, 14, 48), 4),
+        ("mbconv_t8_a4_se25", MBConv(8, 4, 0.25, 1, "silu"), (2, 7, 7, 32), 5),
+        ("mbconv_t1_a4_se25", MBConv(1, 4, 0.25, 1, "silu"), (2, 8, 8, 16), 6),
+        ("mbconv_t8_a4_se25_14", MBConv(8, 4, 0.25, 1, "silu"), (1, 14, 14, 48), 7),
+        ("mbconv_t8_a4_se25_c128_7", MBConv(8, 4, 0.25, 1, "silu"), (2, 7, 7, 128), 8),
+        ("ffn_a4_relu", FFN(4, "relu"), (1, 8, 8, 16), 9),
+    ]
+    index = {}
+    for name, block, dims, seed in cases:
+        td = TensorDims(*dims)
+        lw = build_schedule(block, td, ExecutionScheme.LAYER_WISE)
+        bf = build_schedule(block, td, ExecutionScheme.BLOCK_FUSION)
+        inputs = random_inputs(lw, np.random.default_rng(seed))
+        inputs = {k: v.astype(np.float16).astype(np.float32) for k, v in inputs.items()}
+        out_lw = execute_numeric(lw, inputs)
+        out_bf = execute_numeric(bf, inputs)
+        traffic = simulate_traffic(bf)
+        meta = {
+            "block": type(block).__name__,
+            "params": {k: getattr(block, k) for k in block.__dataclass_fields__},
+            "dims": list(dims),
+            "seed": seed,
+            "fused_dram_bytes": traffic.dram_bytes,
+            "macs": traffic.mac_ops,
+            "fused_vs_layerwise_max_abs": float(np.max(np.abs(out_lw - out_bf))),
+        }
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"),
+            out_layerwise=out_lw,
+            out_fused=out_bf,
+            meta=json.dumps(meta),
+            **{"in_" + k: v.astype(np.float16) for k, v in inputs.items()},
+        )
+        index[name] = meta
+        print(name, dims, "max|out|=%.3g" % np.abs(out_lw).max(), "lw-vs-fused %.2g" % meta["fused_vs_layerwise_max_abs"])
+    with open(os.path.join(HERE, "index.json"), "w") as fh:
+        json.dump(index, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
