@@ -1,0 +1,188 @@
+"""ctypes binding of libwlfuse.so (the C ABI in include/wlfuse.h).
+
+The library is built in-tree (``paper_2404_03617_b200/libwlfuse.so``) by
+``__graft_entry__.build()``. There is no fallback: if the library or a GPU is
+missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from functools import lru_cache
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libwlfuse.so")
+
+WL_OK, WL_EINVAL, WL_EUNSUPPORTED, WL_ECUDA = 0, -1, -2, -3
+KIND_CONVFIRST, KIND_MBCONV, KIND_STEM, KIND_HEAD = 1, 2, 4, 5
+ACTS = {"identity": 0, "relu": 1, "silu": 2, "sigmoid": 3, "gelu": 4}
+NORM_NONE, NORM_LAYERNORM = 0, 1
+
+# every symbol include/wlfuse.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "wl_version",
+    "wl_last_error",
+    "wl_init",
+    "wl_validate",
+    "wl_weight_count",
+    "wl_weight_numel",
+    "wl_packed_bytes",
+    "wl_pack_weights",
+    "wl_workspace_bytes",
+    "wl_block_forward",
+    "wl_convfirst_fwd",
+    "wl_mbconv_fwd",
+    "wl_stem_fwd",
+    "wl_head_fwd",
+    "wl_execute_numeric",
+    "wl_output_dims",
+)
+
+
+class BlockDesc(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("n", ctypes.c_int32),
+        ("h", ctypes.c_int32),
+        ("w", ctypes.c_int32),
+        ("c", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("expansion", ctypes.c_int32),
+        ("group_width", ctypes.c_int32),
+        ("ksize", ctypes.c_int32),
+        ("stride", ctypes.c_int32),
+        ("se_sq", ctypes.c_int32),
+        ("norm", ctypes.c_int32),
+        ("act", ctypes.c_int32),
+        ("ln_eps", ctypes.c_float),
+        ("embed", ctypes.c_int32),
+        ("classes", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 4),
+    ]
+
+    def as_tuple(self):
+        return tuple(getattr(self, f) for f, _ in self._fields_[:-1])
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+class WlError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        self.code = code
+        super().__init__(message)
+
+
+@lru_cache(maxsize=1)
+def lib() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise LibraryMissing(
+            f"{LIB_PATH} is not built; run __graft_entry__.build() (there is no CPU fallback)"
+        )
+    so = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    D = P(BlockDesc)
+    vp = ctypes.c_void_p
+    sig = {
+        "wl_version": (ctypes.c_int, []),
+        "wl_last_error": (ctypes.c_char_p, []),
+        "wl_init": (ctypes.c_int, [ctypes.c_int]),
+        "wl_validate": (ctypes.c_int, [D]),
+        "wl_weight_count": (ctypes.c_int, [D]),
+        "wl_weight_numel": (ctypes.c_int64, [D, ctypes.c_int]),
+        "wl_packed_bytes": (ctypes.c_int64, [D]),
+        "wl_pack_weights": (ctypes.c_int, [D, P(P(ctypes.c_float)), ctypes.c_int, vp]),
+        "wl_workspace_bytes": (ctypes.c_int64, [D]),
+        "wl_block_forward": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_convfirst_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_mbconv_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_stem_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_head_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_execute_numeric": (
+            ctypes.c_int,
+            [D, P(ctypes.c_float), P(P(ctypes.c_float)), ctypes.c_int, P(ctypes.c_float)],
+        ),
+        "wl_output_dims": (ctypes.c_int, [D] + [P(ctypes.c_int32)] * 4),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(so, name)
+        fn.restype = res
+        fn.argtypes = args
+    return so
+
+
+def last_error() -> str:
+    return lib().wl_last_error().decode(errors="replace")
+
+
+def check(code: int, what: str = "") -> int:
+    """Map a negative ABI status to the reference's exception types."""
+    if code >= 0:
+        return code
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if code == WL_EINVAL:
+        raise ValueError(msg)
+    if code == WL_EUNSUPPORTED:
+        from .machine import ScheduleError
+
+        raise ScheduleError(msg)
+    raise WlError(code, msg)
+
+
+def float_ptr_array(arrays):
+    """Keep-alive list of contiguous float32 arrays + a float** to them."""
+    keep = [np.ascontiguousarray(a, dtype=np.float32) for a in arrays]
+    ptrs = (ctypes.POINTER(ctypes.c_float) * len(keep))(
+        *[a.ctypes.data_as(ctypes.POINTER(ctypes.c_float)) for a in keep]
+    )
+    return keep, ptrs
+
+
+def output_dims(desc: BlockDesc):
+    n, h, w, c = (ctypes.c_int32() for _ in range(4))
+    check(lib().wl_output_dims(ctypes.byref(desc), *(ctypes.byref(v) for v in (n, h, w, c))), "wl_output_dims")
+    return n.value, h.value, w.value, c.value
+
+
+def pack_weights(desc: BlockDesc, weights) -> np.ndarray:
+    """Pack reference float32 tensors (reference order) into the device blob."""
+    L = lib()
+    check(L.wl_validate(ctypes.byref(desc)), "wl_validate")
+    count = check(L.wl_weight_count(ctypes.byref(desc)))
+    if len(weights) != count:
+        raise ValueError(f"expected {count} weight tensors, got {len(weights)}")
+    for i, wt in enumerate(weights):
+        want = L.wl_weight_numel(ctypes.byref(desc), i)
+        if int(np.size(wt)) != want:
+            raise ValueError(f"weight tensor {i} has {np.size(wt)} elements, expected {want}")
+    nbytes = check(L.wl_packed_bytes(ctypes.byref(desc)))
+    out = np.zeros(nbytes, dtype=np.uint8)
+    keep, ptrs = float_ptr_array(weights)
+    check(L.wl_pack_weights(ctypes.byref(desc), ptrs, len(keep), out.ctypes.data_as(ctypes.c_void_p)), "pack")
+    return out
+
+
+def execute_numeric_host(desc: BlockDesc, x: np.ndarray, weights) -> np.ndarray:
+    """Host-buffer forward through the ABI (H2D, launch, D2H inside)."""
+    L = lib()
+    n, h, w, c = output_dims(desc)
+    out = np.empty((n, h, w, c), dtype=np.float32)
+    xk = np.ascontiguousarray(x, dtype=np.float32)
+    keep, ptrs = float_ptr_array(weights)
+    check(
+        L.wl_execute_numeric(
+            ctypes.byref(desc),
+            xk.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+            ptrs,
+            len(keep),
+            out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+        ),
+        "wl_execute_numeric",
+    )
+    return out

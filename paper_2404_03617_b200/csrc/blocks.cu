@@ -1,0 +1,54 @@
+// blocks.cu — dispatch of the C ABI over block families.
+#include "launch.h"
+
+namespace wl {
+
+static const Family* family_of(const wl_block_desc& d) {
+  switch (d.kind) {
+    case WL_KIND_CONVFIRST: return &kCfFamily;
+    case WL_KIND_MBCONV: return &kMbFamily;
+    case WL_KIND_STEM: return &kStemFamily;
+    case WL_KIND_HEAD: return &kHeadFamily;
+  }
+  return nullptr;
+}
+
+int init_kernels() {
+  static int status = 1;
+  if (status == 1) {
+    status = WL_OK;
+    for (const Family* f : {&kCfFamily, &kCf2Family, &kMbFamily, &kStemFamily, &kHeadFamily})
+      if (f->init && (status = f->init()) != WL_OK) break;
+  }
+  return status;
+}
+
+int validate_desc(const wl_block_desc& d) {
+  const Family* f = family_of(d);
+  if (!f) return set_error(WL_EINVAL, "unknown block kind %d", d.kind);
+  return f->validate(d);
+}
+int weight_count(const wl_block_desc& d) { return family_of(d)->weight_count(d); }
+int64_t weight_numel(const wl_block_desc& d, int i) { return family_of(d)->weight_numel(d, i); }
+int64_t packed_bytes(const wl_block_desc& d) { return family_of(d)->packed_bytes(d); }
+int pack_weights(const wl_block_desc& d, const float* const* w, uint8_t* out) { return family_of(d)->pack(d, w, out); }
+int64_t workspace_bytes(const wl_block_desc& d) { return family_of(d)->workspace_bytes(d); }
+int forward(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  return family_of(d)->forward(d, x, p, z, ws, st);
+}
+
+void output_dims(const wl_block_desc& d, int32_t* n, int32_t* h, int32_t* w, int32_t* c) {
+  *n = d.n;
+  if (d.kind == WL_KIND_HEAD) {
+    *h = 1;
+    *w = 1;
+    *c = d.classes;
+    return;
+  }
+  const int s = d.kind == WL_KIND_STEM ? 2 : d.stride;
+  *h = d.h / s;
+  *w = d.w / s;
+  *c = d.k;
+}
+
+}  // namespace wl

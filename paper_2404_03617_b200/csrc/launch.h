@@ -1,0 +1,47 @@
+// launch.h — host-side interface between the C ABI and the block families.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "../../include/wlfuse.h"
+
+namespace wl {
+
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+int encode_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                const uint32_t* box);
+void put_h(uint8_t* base, size_t off, float v);
+static inline size_t core_off_h(int row, int k, int lbo) {
+  return (size_t)(k / 8) * lbo + (size_t)(row / 8) * 128 + (size_t)(row % 8) * 16 + (size_t)(k % 8) * 2;
+}
+
+// dispatch over block kinds (blocks.cu)
+int init_kernels();
+int validate_desc(const wl_block_desc& d);
+int weight_count(const wl_block_desc& d);
+int64_t weight_numel(const wl_block_desc& d, int i);
+int64_t packed_bytes(const wl_block_desc& d);
+int pack_weights(const wl_block_desc& d, const float* const* w, uint8_t* out);
+int64_t workspace_bytes(const wl_block_desc& d);
+void output_dims(const wl_block_desc& d, int32_t* n, int32_t* h, int32_t* w, int32_t* c);
+int forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st);
+
+// one family = one set of these (cf_fused.cu, cf_s2.cu, mbconv.cu, stem_head.cu)
+struct Family {
+  int (*validate)(const wl_block_desc&);
+  int (*weight_count)(const wl_block_desc&);
+  int64_t (*weight_numel)(const wl_block_desc&, int);
+  int64_t (*packed_bytes)(const wl_block_desc&);
+  int (*pack)(const wl_block_desc&, const float* const*, uint8_t*);
+  int64_t (*workspace_bytes)(const wl_block_desc&);
+  int (*forward)(const wl_block_desc&, const void*, const void*, void*, void*, cudaStream_t);
+  int (*init)();
+};
+extern const Family kCfFamily;
+extern const Family kCf2Family;
+extern const Family kMbFamily;
+extern const Family kStemFamily;
+extern const Family kHeadFamily;
+
+}  // namespace wl
