@@ -1,0 +1,841 @@
+// mbconv.cu — MBConv + squeeze-excite on sm_100a (core.py:112-122; fused
+// schedule machine.py:649-733; layer-wise numerics machine.py:593-646).
+//
+// Two launches per block; the hidden activation is never materialised at
+// full width in HBM by design — it passes between the launches through the
+// 126 MB L2 (the tensor machine's GLOBAL tier, machine.py:667-687):
+//   front : one CTA per (image group, hidden range). Whole image(s) stacked in
+//           a flat padded layout (row width W+1: the left pad column of row
+//           y+1 doubles as the right pad of row y), so every 3x3 tap is a
+//           constant shift of the flat index and an M=128 conv tile is 16
+//           consecutive 8-pixel core-matrix rows. Per hidden chunk:
+//             expand  (SS MMA, x smem x U_j)            -> TMEM E
+//             E + b_exp, phi, pads -> 0                 -> smem h1 planes
+//             grouped 3x3 conv (block-diagonal MMAs for T=8, CUDA cores T=1)
+//             + b_conv, phi [-> BlurPool 3x3 stride 2]  -> h2 (fp16, global)
+//             spatial sums of h2 reduced on chip        -> pool (fp32 mean)
+//   back  : one CTA per (128 consecutive output pixels, output-channel range).
+//           SE on CUDA cores: s = relu(pool W_sq + b_sq), e = sigmoid(s W_ex +
+//           b_ex); h2 tiles arrive by TMA, are gated in shared memory, the
+//           projection accumulates in TMEM; z = Z + b_prj (+ x for stride 1).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include "common.cuh"
+#include "plan.h"
+
+namespace wl {
+
+struct MbFrontArgs {
+  int C, hid, HR, HC, nch;  // nch: chunks per hidden range
+  int T8, stride;
+  int H, W, Wp, imgs;
+  int total_rows, n_et, n_ct, conv_base, flat_h1, x_alloc;  // conv_base = Wp + 1
+  int Ho, Wo, ranges;
+  int h1_bytes;
+  int hdr_bytes, chunk_bytes, u_bytes;  // per-range hdr = [b_exp | b_conv | (T1) convw fp32 [9][HR]]
+  int o_bconv, o_convw;
+  int s_x, s_h1, s_stage, s_hdr, s_ring, s_pool, s_bar;
+  int ring_stages;
+  int t_e, t_c, tmem_cols;
+  const uint8_t* wpack;
+  __half* h2;   // (n, Ho*Wo, hid)
+  float* pool;  // (n, hid) spatial mean
+};
+
+struct MbBackArgs {
+  int hid, sq, K, KR, HCb, nchb, stride;
+  int P, pix_per_img, rows;  // total pixels, pixels per image, tile rows (128)
+  int kranges;
+  int residual;
+  int o_wsq, o_bsq, o_wex, o_bex, o_bprj, se_bytes;  // SE block in the back blob
+  int vchunk_bytes;
+  int s_a, s_gate, s_se, s_ring, s_bar, a_bytes, ring_stages;
+  int t_z, tmem_cols;
+  const uint8_t* wpack;  // back blob: [SE fp32 ...][V chunks per (krange, j)]
+  const float* pool;
+  const __half* x;  // residual (n, H, W, K)
+  __half* z;        // (n, Ho, Wo, K)
+};
+
+namespace mbk {
+constexpr int kThreads = 384;
+struct FrontBars {
+  uint64_t hdr_full, x_full;
+  uint64_t w_full[4], w_empty[4];
+  uint64_t e_full, h1_full, h1_empty, c_full, c_empty;
+  uint32_t tmem_base;
+};
+struct BackBars {
+  uint64_t a_full[2], a_empty[2], a_ready[2];
+  uint64_t v_full[4], v_empty[4];
+  uint64_t z_full;
+  uint32_t tmem_base;
+};
+}  // namespace mbk
+
+// flat position f holds a real pixel (not a pad row / pad column)
+__device__ __forceinline__ bool mb_real(int f, int Wp, int W, int H, int total_rows) {
+  const int row = f / Wp, col = f - row * Wp;
+  return col >= 1 && col <= W && row < total_rows - 1 && (row % (H + 1)) != 0;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  return v;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+template <int ACT>
+__global__ void __launch_bounds__(mbk::kThreads, 1)
+    mb_front_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ MbFrontArgs a) {
+  using namespace mbk;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* s_x = smem + a.s_x;
+  uint8_t* s_h1 = smem + a.s_h1;
+  __half* s_stage = reinterpret_cast<__half*>(smem + a.s_stage);
+  uint8_t* s_hdr = smem + a.s_hdr;
+  uint8_t* s_ring = smem + a.s_ring;
+  float* s_pool = reinterpret_cast<float*>(smem + a.s_pool);  // [imgs][HR]
+  FrontBars& B = *reinterpret_cast<FrontBars*>(smem + a.s_bar);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int group = blockIdx.x / a.ranges, range = blockIdx.x % a.ranges;
+  const int n0 = group * a.imgs;
+  const int h0 = range * a.HR;
+  const int S = a.ring_stages, HC = a.HC, nch = a.nch;
+  const int img_flat = (a.H + 1) * a.Wp;
+  const int x_valid = a.imgs * img_flat;  // flat positions holding loaded x rows
+
+  for (int i = threadIdx.x; i < a.h1_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < a.imgs * a.HR; i += blockDim.x) s_pool[i] = 0.f;
+  {
+    const int tail = a.x_alloc - x_valid, planes = a.C / 8;
+    for (int i = threadIdx.x; i < planes * tail; i += blockDim.x) {
+      const int pl = i / tail, f = x_valid + i % tail;
+      *reinterpret_cast<uint4*>(s_x + ((size_t)pl * a.x_alloc + f) * 16) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&B.hdr_full, 1);
+    mbar_init(&B.x_full, 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&B.w_full[i], 1);
+      mbar_init(&B.w_empty[i], 1);
+    }
+    mbar_init(&B.e_full, 1);
+    mbar_init(&B.h1_full, 128);
+    mbar_init(&B.h1_empty, a.T8 ? 1 : 128);
+    mbar_init(&B.c_full, 1);
+    mbar_init(&B.c_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap_x);
+      mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
+      bulk_g2s(s_hdr, a.wpack + (size_t)range * a.hdr_bytes, a.hdr_bytes, &B.hdr_full);
+      const int planes = a.C / 8;
+      const int box_bytes = img_flat * 16;
+      mbar_arrive_expect_tx(&B.x_full, box_bytes * planes * a.imgs);
+      for (int i = 0; i < a.imgs; ++i)
+        for (int g = 0; g < planes; ++g)
+          tma_load_5d(s_x + ((size_t)g * a.x_alloc + i * img_flat) * 16, &tmap_x, 0, -1, -1, g, n0 + i, &B.x_full);
+      const uint8_t* chunks = a.wpack + (size_t)a.ranges * a.hdr_bytes;
+      for (int j = 0; j < nch; ++j) {
+        const int slot = j % S, use = j / S;
+        mbar_wait(&B.w_empty[slot], (use & 1) ^ 1);
+        mbar_arrive_expect_tx(&B.w_full[slot], a.chunk_bytes);
+        bulk_g2s(s_ring + slot * a.chunk_bytes, chunks + (size_t)(range * nch + j) * a.chunk_bytes, a.chunk_bytes,
+                 &B.w_full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_e = make_idesc_f16(128, HC);
+      const uint32_t idesc_c = make_idesc_f16(128, 16);
+      const uint32_t x0 = smem_u32(s_x), h10 = smem_u32(s_h1), ring0 = smem_u32(s_ring);
+      mbar_wait(&B.x_full, 0);
+      tc_fence_after();
+      for (int j = 0; j < nch; ++j) {
+        const int slot = j % S;
+        mbar_wait(&B.w_full[slot], (j / S) & 1);
+        if (j > 0) mbar_wait(&B.h1_full, (j - 1) & 1);  // expand epilogue done reading E
+        tc_fence_after();
+        const uint32_t ub = ring0 + slot * a.chunk_bytes;
+        for (int t = 0; t < a.n_et; ++t)
+          for (int kk = 0; kk < a.C / 16; ++kk) {
+            const uint64_t ad = make_sdesc(x0 + (kk * 2 * a.x_alloc + t * 128) * 16, a.x_alloc * 16, 128);
+            const uint64_t bd = make_sdesc(ub + kk * 2 * (HC * 16), HC * 16, 128);
+            mma_ss(tmem + a.t_e + t * HC, ad, bd, idesc_e, kk > 0);
+          }
+        mma_commit(&B.e_full);
+        if (a.T8) {
+          mbar_wait(&B.h1_full, j & 1);
+          if (j > 0) mbar_wait(&B.c_empty, (j - 1) & 1);
+          tc_fence_after();
+          const uint32_t cw = ub + a.u_bytes;
+          for (int t = 0; t < a.n_ct; ++t)
+            for (int pr = 0; pr < HC / 16; ++pr)
+              for (int tap = 0; tap < 9; ++tap) {
+                const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+                const int f = a.conv_base + t * 128 + dy * a.Wp + dx;
+                const uint64_t ad = make_sdesc(h10 + (2 * pr * a.flat_h1 + f) * 16, a.flat_h1 * 16, 128);
+                const uint64_t bd = make_sdesc(cw + (pr * 9 + tap) * 512, 256, 128);
+                mma_ss(tmem + a.t_c + t * HC + 16 * pr, ad, bd, idesc_c, tap > 0);
+              }
+          mma_commit(&B.c_full);
+          mma_commit(&B.h1_empty);
+        }
+        mma_commit(&B.w_empty[slot]);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------- expand epilogue: E + b_exp -> phi -> pads 0 -> h1 planes
+    const int q = warp - 4;
+    const float* s_bexp = reinterpret_cast<const float*>(s_hdr);
+    mbar_wait(&B.hdr_full, 0);
+    for (int j = 0; j < nch; ++j) {
+      mbar_wait(&B.e_full, j & 1);
+      if (j > 0) mbar_wait(&B.h1_empty, (j - 1) & 1);
+      tc_fence_after();
+      for (int t = 0; t < a.n_et; ++t) {
+        const int f = t * 128 + q * 32 + lane;
+        const bool real = f < x_valid && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
+        for (int c0 = 0; c0 < HC; c0 += 16) {
+          uint32_t v[16];
+          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + t * HC + c0), v);
+          tmem_ld_wait();
+          float fv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) fv[i] = real ? act<ACT>(__uint_as_float(v[i]) + s_bexp[j * HC + c0 + i]) : 0.f;
+          if (f < a.flat_h1) {
+            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + f) * 16) = pack8(fv);
+            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + f) * 16) = pack8(fv + 8);
+          }
+        }
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&B.h1_full);
+    }
+  } else if (warp >= 8 && warp < 12) {
+    // ------------- conv epilogue: (Cacc | stencil) + b_conv -> phi -> [blur] -> h2, pool
+    const int q = warp - 8;
+    const int tid = q * 32 + lane;
+    const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
+    const float* s_cw = reinterpret_cast<const float*>(s_hdr + a.o_convw);  // [9][HR] (T1)
+    mbar_wait(&B.hdr_full, 0);
+    const int conv_end = (a.total_rows - 1) * a.Wp;
+    for (int j = 0; j < nch; ++j) {
+      if (a.T8) {
+        mbar_wait(&B.c_full, j & 1);
+        tc_fence_after();
+      } else {
+        mbar_wait(&B.h1_full, j & 1);
+      }
+      for (int t = 0; t < a.n_ct; ++t) {
+        const int f = a.conv_base + t * 128 + tid;
+        const bool real = f < conv_end && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
+        const int row = f / a.Wp, img = row / (a.H + 1);
+        const int y = row - img * (a.H + 1) - 1, x = f - row * a.Wp - 1;
+        for (int c0 = 0; c0 < HC; c0 += 16) {
+          float fv[16];
+          if (a.T8) {
+            uint32_t v[16];
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * HC + c0), v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) fv[i] = __uint_as_float(v[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) fv[i] = 0.f;
+            if (real) {
+              for (int tap = 0; tap < 9; ++tap) {
+                const int ff = f + (tap / 3 - 1) * a.Wp + (tap % 3 - 1);
+                float hv[16];
+                unpack8(*reinterpret_cast<const uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + ff) * 16), hv);
+                unpack8(*reinterpret_cast<const uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + ff) * 16), hv + 8);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) fv[i] += hv[i] * s_cw[tap * a.HR + j * HC + c0 + i];
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) fv[i] = real ? act<ACT>(fv[i] + s_bconv[j * HC + c0 + i]) : 0.f;
+          if (a.stride == 1) {
+            if (real) {
+              __half* dst = a.h2 + ((size_t)(n0 + img) * a.H * a.W + (size_t)y * a.W + x) * a.hid + h0 + j * HC + c0;
+              reinterpret_cast<uint4*>(dst)[0] = pack8(fv);
+              reinterpret_cast<uint4*>(dst)[1] = pack8(fv + 8);
+            }
+            // pool: per-image warp sums of the 16 channels
+            for (int im = 0; im < a.imgs; ++im) {
+              const unsigned m = __ballot_sync(0xffffffffu, real && img == im);
+              if (!m) continue;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float s = warp_sum((real && img == im) ? fv[i] : 0.f);
+                if (lane == 0) atomicAdd(&s_pool[im * a.HR + j * HC + c0 + i], s);
+              }
+            }
+          } else {
+            // stage the full-resolution activation for the blur
+            if (real) {
+              const size_t o = ((size_t)(img * a.H + y) * a.W + x) * HC + c0;
+              reinterpret_cast<uint4*>(s_stage + o)[0] = pack8(fv);
+              reinterpret_cast<uint4*>(s_stage + o)[1] = pack8(fv + 8);
+            }
+          }
+        }
+      }
+      if (a.T8) {
+        tc_fence_before();
+        mbar_arrive(&B.c_empty);
+      } else {
+        mbar_arrive(&B.h1_empty);
+      }
+      if (a.stride == 2) {
+        named_bar(1, 128);
+        // BlurPool Triangle-3 x Triangle-3 / 16, stride 2, reflect pad (-1 -> 1)
+        const int npix = a.imgs * a.Ho * a.Wo;
+        for (int pidx = tid; pidx < npix; pidx += 128) {
+          const int im = pidx / (a.Ho * a.Wo), rem = pidx % (a.Ho * a.Wo);
+          const int yo = rem / a.Wo, xo = rem % a.Wo;
+          int ys[3] = {2 * yo - 1, 2 * yo, 2 * yo + 1}, xs[3] = {2 * xo - 1, 2 * xo, 2 * xo + 1};
+          if (ys[0] < 0) ys[0] = 1;
+          if (xs[0] < 0) xs[0] = 1;
+          const float wt[3] = {0.25f, 0.5f, 0.25f};
+          for (int c0 = 0; c0 < HC; c0 += 8) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int dy = 0; dy < 3; ++dy)
+              for (int dx = 0; dx < 3; ++dx) {
+                float hv[8];
+                unpack8(*reinterpret_cast<const uint4*>(s_stage + ((size_t)(im * a.H + ys[dy]) * a.W + xs[dx]) * HC + c0),
+                        hv);
+                const float w = wt[dy] * wt[dx];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] += w * hv[i];
+              }
+            __half* dst = a.h2 + ((size_t)(n0 + im) * a.Ho * a.Wo + rem) * a.hid + h0 + j * HC + c0;
+            *reinterpret_cast<uint4*>(dst) = pack8(acc);
+            // pool on the fp16-rounded values the projection will consume
+            float rv[8];
+            unpack8(pack8(acc), rv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) atomicAdd(&s_pool[im * a.HR + j * HC + c0 + i], rv[i]);
+          }
+        }
+        named_bar(1, 128);
+      }
+    }
+    named_bar(1, 128);
+    const float inv = 1.f / (float)(a.Ho * a.Wo);
+    for (int i = tid; i < a.imgs * a.HR; i += 128) {
+      const int im = i / a.HR, c = i % a.HR;
+      a.pool[(size_t)(n0 + im) * a.hid + h0 + c] = s_pool[i] * inv;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
+}
+
+// ----------------------------------------------------------------- back
+// CTA: 128 consecutive output pixels (any images) x output channels
+// [k0, k0 + KR). Threads: w0 producer, w1 MMA, w2 alloc, w3 idle, w4-7
+// SE + gating + epilogue.
+template <int dummy>
+__global__ void __launch_bounds__(256, 1)
+    mb_back_kernel(const __grid_constant__ CUtensorMap tmap_h2, const __grid_constant__ MbBackArgs a) {
+  using namespace mbk;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* s_a = smem + a.s_a;          // 2 x [HCb/8][128][8] fp16
+  float* s_gate = reinterpret_cast<float*>(smem + a.s_gate);  // [4 imgs][hid]
+  float* s_se = reinterpret_cast<float*>(smem + a.s_se);      // [4][sq] scratch
+  uint8_t* s_ring = smem + a.s_ring;
+  BackBars& B = *reinterpret_cast<BackBars*>(smem + a.s_bar);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile = blockIdx.x / a.kranges, kr = blockIdx.x % a.kranges;
+  const int p0 = tile * 128;
+  const int k0 = kr * a.KR;
+  const int S = a.ring_stages, nch = a.nchb, HCb = a.HCb;
+  const int img_first = p0 / a.pix_per_img;
+  const int img_last = min(a.P - 1, p0 + 127) / a.pix_per_img;
+  const int nimg = img_last - img_first + 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.a_full[i], 1);
+      mbar_init(&B.a_empty[i], 1);
+      mbar_init(&B.a_ready[i], 128);
+    }
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&B.v_full[i], 1);
+      mbar_init(&B.v_empty[i], 1);
+    }
+    mbar_init(&B.z_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_base;
+  const int a_stage_bytes = 128 * HCb * 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap_h2);
+      const uint8_t* vchunks = a.wpack + a.se_bytes;
+      for (int j = 0; j < nch; ++j) {
+        const int ab = j & 1;
+        mbar_wait(&B.a_empty[ab], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&B.a_full[ab], a_stage_bytes);
+        // 3-D view of h2: (8, P, hid/8) -> smem [HCb/8][128][8]
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4}], [%5];" ::"r"(smem_u32(s_a + ab * a_stage_bytes)),
+            "l"(&tmap_h2), "r"(0), "r"(p0), "r"(j * HCb / 8), "r"(smem_u32(&B.a_full[ab]))
+            : "memory");
+        const int slot = j % S;
+        mbar_wait(&B.v_empty[slot], ((j / S) & 1) ^ 1);
+        mbar_arrive_expect_tx(&B.v_full[slot], a.vchunk_bytes);
+        bulk_g2s(s_ring + slot * a.vchunk_bytes, vchunks + (size_t)(kr * nch + j) * a.vchunk_bytes, a.vchunk_bytes,
+                 &B.v_full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_f16(128, a.KR);
+      const uint32_t a0 = smem_u32(s_a), ring0 = smem_u32(s_ring);
+      for (int j = 0; j < nch; ++j) {
+        const int ab = j & 1, slot = j % S;
+        mbar_wait(&B.a_ready[ab], (j >> 1) & 1);
+        mbar_wait(&B.v_full[slot], (j / S) & 1);
+        tc_fence_after();
+        for (int kk = 0; kk < HCb / 16; ++kk) {
+          const uint64_t ad = make_sdesc(a0 + ab * a_stage_bytes + kk * 2 * 2048, 2048, 128);
+          const uint64_t bd = make_sdesc(ring0 + slot * a.vchunk_bytes + kk * 2 * (a.KR * 16), a.KR * 16, 128);
+          mma_ss(tmem + a.t_z, ad, bd, idesc, (j > 0 || kk > 0));
+        }
+        mma_commit(&B.a_empty[ab]);
+        mma_commit(&B.v_empty[slot]);
+      }
+      mma_commit(&B.z_full);
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4, tid = q * 32 + lane;
+    const float* wsq = reinterpret_cast<const float*>(a.wpack + a.o_wsq);  // [hid][sq]
+    const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
+    const float* wex = reinterpret_cast<const float*>(a.wpack + a.o_wex);  // [sq][hid]
+    const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_bex);
+    // ---- squeeze-excite for every image the tile touches
+    for (int im = 0; im < nimg; ++im) {
+      const float* pool = a.pool + (size_t)(img_first + im) * a.hid;
+      // s[j] = relu(sum_i pool[i] wsq[i][j] + bsq[j]); 128 threads: j = tid % sq, part = tid / sq
+      const int parts = 128 / a.sq;
+      if (tid < parts * a.sq) {
+        const int jj = tid % a.sq, part = tid / a.sq;
+        float acc = 0.f;
+        for (int i = part; i < a.hid; i += parts) acc += pool[i] * wsq[(size_t)i * a.sq + jj];
+        s_se[tid] = acc;
+      }
+      named_bar(1, 128);
+      if (tid < a.sq) {
+        float acc = bsq[tid];
+        for (int p = 0; p < parts; ++p) acc += s_se[p * a.sq + tid];
+        s_se[128 + tid] = fmaxf(acc, 0.f);
+      }
+      named_bar(1, 128);
+      for (int i = tid; i < a.hid; i += 128) {
+        float acc = bex[i];
+        for (int jj = 0; jj < a.sq; ++jj) acc += s_se[128 + jj] * wex[(size_t)jj * a.hid + i];
+        s_gate[im * a.hid + i] = __fdividef(1.f, 1.f + __expf(-acc));
+      }
+      named_bar(1, 128);
+    }
+    // ---- gate each h2 chunk in shared memory (row = pixel = TMEM lane)
+    const int p = p0 + tid;
+    const int im = min(p, a.P - 1) / a.pix_per_img - img_first;
+    for (int j = 0; j < nch; ++j) {
+      const int ab = j & 1;
+      mbar_wait(&B.a_full[ab], (j >> 1) & 1);
+      uint8_t* base = s_a + ab * a_stage_bytes;
+      const float* g = s_gate + im * a.hid + j * HCb;
+      for (int c8 = 0; c8 < HCb / 8; ++c8) {
+        uint4* ptr = reinterpret_cast<uint4*>(base + (c8 * 128 + tid) * 16);
+        float f[8];
+        unpack8(*ptr, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] *= g[c8 * 8 + i];
+        *ptr = pack8(f);
+      }
+      fence_async_smem();
+      mbar_arrive(&B.a_ready[ab]);
+    }
+    // ---- epilogue: z = Z + b_prj (+ x)
+    mbar_wait(&B.z_full, 0);
+    tc_fence_after();
+    const float* bprj = reinterpret_cast<const float*>(a.wpack + a.o_bprj);
+    const bool inside = p < a.P;
+    for (int c0 = 0; c0 < a.KR; c0 += 16) {
+      uint32_t v[16];
+      WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + c0), v);
+      tmem_ld_wait();
+      if (!inside) continue;
+      float f[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bprj[k0 + c0 + i];
+      if (a.residual) {
+        float r[16];
+        const uint4* xp = reinterpret_cast<const uint4*>(a.x + (size_t)p * a.K + k0 + c0);
+        unpack8(xp[0], r);
+        unpack8(xp[1], r + 8);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) f[i] += r[i];
+      }
+      uint4* zp = reinterpret_cast<uint4*>(a.z + (size_t)p * a.K + k0 + c0);
+      zp[0] = pack8(f);
+      zp[1] = pack8(f + 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
+}
+
+}  // namespace wl
+
+// =================================================================== host
+#include <algorithm>
+#include <cstring>
+#include "launch.h"
+
+namespace wl {
+namespace {
+
+constexpr int kSmemMaxMb = 232448;
+
+struct MbPlanH {
+  MbFrontArgs f;
+  MbBackArgs b;
+  int64_t front_bytes, back_bytes;
+  int64_t h2_bytes, pool_bytes;
+};
+
+bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
+  memset(&P, 0, sizeof(P));
+  MbFrontArgs& f = P.f;
+  MbBackArgs& b = P.b;
+  const int C = d.c, hid = d.expansion * d.c, K = d.k;
+  if (C % 16 || hid % 16 || K % 16) return false;
+  f.C = C;
+  f.hid = hid;
+  f.T8 = d.group_width == 8;
+  f.stride = d.stride;
+  f.H = d.h;
+  f.W = d.w;
+  f.imgs = (d.h * d.w <= 64 && d.n % 2 == 0) ? 2 : 1;
+  // row pitch: >= W + 1, and each stacked image must start 128-byte aligned (TMA)
+  f.Wp = d.w + 1;
+  while (f.imgs > 1 && ((d.h + 1) * f.Wp) % 8) ++f.Wp;
+  f.Ho = d.h / d.stride;
+  f.Wo = d.w / d.stride;
+  f.total_rows = f.imgs * (f.H + 1) + 1;
+  const int x_valid = f.imgs * (f.H + 1) * f.Wp;
+  f.n_et = (x_valid + 127) / 128;
+  f.x_alloc = f.n_et * 128;
+  f.conv_base = f.Wp + 1;
+  const int conv_end = (f.total_rows - 1) * f.Wp;
+  f.n_ct = (conv_end - f.conv_base + 127) / 128;
+  f.flat_h1 = align_up(f.conv_base + f.n_ct * 128 + f.Wp + 2, 8);
+  const int groups = d.n / f.imgs;
+  // hidden ranges: enough CTAs to cover the SMs
+  f.ranges = 1;
+  while (groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
+  f.HR = hid / f.ranges;
+  // hidden chunk: largest multiple of 16 dividing HR that fits TMEM and smem
+  const int tiles = f.T8 ? f.n_et + f.n_ct : f.n_et;
+  f.HC = 0;
+  for (int hc = 128; hc >= 16; hc -= 16) {
+    if (f.HR % hc || tiles * hc > 512) continue;
+    // smem estimate
+    const int x_bytes = (C / 8) * f.x_alloc * 16;
+    const int h1_bytes = (hc / 8) * f.flat_h1 * 16;
+    const int stage = f.stride == 2 ? f.imgs * f.H * f.W * hc * 2 : 0;
+    const int hdr = align_up(f.HR * 4, 16) * 2 + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
+    const int chunk = hc * C * 2 + (f.T8 ? (hc / 16) * 9 * 512 : 0);
+    const int total = x_bytes + h1_bytes + stage + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048;
+    if (total <= kSmemMaxMb) {
+      f.HC = hc;
+      break;
+    }
+  }
+  if (!f.HC) return false;
+  f.nch = f.HR / f.HC;
+  f.h1_bytes = (f.HC / 8) * f.flat_h1 * 16;
+  f.o_bconv = align_up(f.HR * 4, 16);
+  f.o_convw = f.o_bconv + align_up(f.HR * 4, 16);
+  f.hdr_bytes = f.o_convw + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
+  f.u_bytes = f.HC * C * 2;
+  f.chunk_bytes = f.u_bytes + (f.T8 ? (f.HC / 16) * 9 * 512 : 0);
+  f.ring_stages = 2;
+  int o = 0;
+  f.s_x = o;
+  o = align_up(o + (C / 8) * f.x_alloc * 16, 128);
+  f.s_h1 = o;
+  o = align_up(o + f.h1_bytes, 128);
+  f.s_stage = o;
+  o = align_up(o + (f.stride == 2 ? f.imgs * f.H * f.W * f.HC * 2 : 0), 128);
+  f.s_hdr = o;
+  o = align_up(o + f.hdr_bytes, 128);
+  f.s_ring = o;
+  o = align_up(o + f.ring_stages * f.chunk_bytes, 128);
+  f.s_pool = o;
+  o = align_up(o + f.imgs * f.HR * 4, 128);
+  f.s_bar = o;
+  o += 512;
+  if (o > kSmemMaxMb) return false;
+  f.t_e = 0;
+  f.t_c = f.n_et * f.HC;
+  const int cols = tiles * f.HC;
+  f.tmem_cols = 32;
+  while (f.tmem_cols < cols) f.tmem_cols *= 2;
+  P.front_bytes = (int64_t)f.ranges * f.hdr_bytes + (int64_t)f.ranges * f.nch * f.chunk_bytes;
+
+  // ---- back
+  b.hid = hid;
+  b.sq = d.se_sq;
+  b.K = K;
+  b.stride = d.stride;
+  b.P = d.n * f.Ho * f.Wo;
+  b.pix_per_img = f.Ho * f.Wo;
+  b.residual = d.stride == 1;
+  const int ntiles = (b.P + 127) / 128;
+  b.KR = K;
+  while (b.KR > 256 || (ntiles * (K / b.KR) < kNumSMs && b.KR % 32 == 0 && b.KR >= 64)) b.KR /= 2;
+  if (K % b.KR || b.KR % 16) return false;
+  b.kranges = K / b.KR;
+  b.HCb = hid % 64 == 0 ? 64 : (hid % 32 == 0 ? 32 : 16);
+  b.nchb = hid / b.HCb;
+  if (b.sq < 1 || b.sq > 128) return false;
+  int so = 0;
+  b.o_wsq = so;
+  so = align_up(so + hid * b.sq * 4, 16);
+  b.o_bsq = so;
+  so = align_up(so + b.sq * 4, 16);
+  b.o_wex = so;
+  so = align_up(so + b.sq * hid * 4, 16);
+  b.o_bex = so;
+  so = align_up(so + hid * 4, 16);
+  b.o_bprj = so;
+  so = align_up(so + K * 4, 16);
+  b.se_bytes = so;
+  b.vchunk_bytes = b.KR * b.HCb * 2;
+  b.ring_stages = 3;
+  o = 0;
+  b.s_a = o;
+  o += 2 * 128 * b.HCb * 2;
+  b.s_gate = o;
+  o = align_up(o + 4 * hid * 4, 128);
+  b.s_se = o;
+  o = align_up(o + (128 + 128) * 4, 128);
+  b.s_ring = o;
+  o = align_up(o + b.ring_stages * b.vchunk_bytes, 128);
+  b.s_bar = o;
+  o += 512;
+  b.a_bytes = o;
+  if (o > kSmemMaxMb) return false;
+  b.t_z = 0;
+  b.tmem_cols = 32;
+  while (b.tmem_cols < b.KR) b.tmem_cols *= 2;
+  P.back_bytes = (int64_t)b.se_bytes + (int64_t)b.kranges * b.nchb * b.vchunk_bytes;
+  P.h2_bytes = (int64_t)d.n * f.Ho * f.Wo * hid * 2;
+  P.pool_bytes = (int64_t)d.n * hid * 4;
+  return true;
+}
+
+using FrontK = void (*)(const CUtensorMap, const MbFrontArgs);
+using BackK = void (*)(const CUtensorMap, const MbBackArgs);
+
+FrontK front_kernel(int act) {
+  switch (act) {
+    case kRelu: return mb_front_kernel<kRelu>;
+    case kSilu: return mb_front_kernel<kSilu>;
+    case kGelu: return mb_front_kernel<kGelu>;
+  }
+  return nullptr;
+}
+
+int mb_validate(const wl_block_desc& d) {
+  if (d.n < 1 || d.h < 1 || d.w < 1 || d.c < 1 || d.k < 1) return set_error(WL_EINVAL, "dims must be positive");
+  if (d.expansion < 1) return set_error(WL_EINVAL, "expansion must be at least 1");
+  const int hid = d.expansion * d.c;
+  if (d.group_width < 1 || hid % d.group_width)
+    return set_error(WL_EINVAL, "group width %d does not divide %d hidden channels", d.group_width, hid);
+  if (d.stride != 1 && d.stride != 2) return set_error(WL_EINVAL, "stride must be 1 or 2");
+  if (d.stride == 1 && d.k != d.c) return set_error(WL_EINVAL, "stride-1 blocks keep their channel count");
+  if (d.stride == 2 && (d.h % 2 || d.w % 2)) return set_error(WL_EINVAL, "stride 2 needs an even resolution");
+  if (d.se_sq < 1) return set_error(WL_EINVAL, "se_ratio must give at least one squeeze channel");
+  if (d.ksize != 3) return set_error(WL_EUNSUPPORTED, "MBConv conv is 3x3 (complexity.py:38)");
+  if (d.group_width != 8 && d.group_width != 1)
+    return set_error(WL_EUNSUPPORTED, "MBConv kernel supports group width 8 or 1, got %d", d.group_width);
+  if (!front_kernel(d.act)) return set_error(WL_EUNSUPPORTED, "MBConv supports relu/silu/gelu");
+  MbPlanH P;
+  if (!mb_plan(d, P)) return set_error(WL_EUNSUPPORTED, "no MBConv launch plan for C=%d hid=%d %dx%d", d.c, hid, d.h, d.w);
+  return WL_OK;
+}
+
+int mb_weight_count(const wl_block_desc&) { return 10; }
+
+int64_t mb_weight_numel(const wl_block_desc& d, int i) {
+  const int64_t c = d.c, hid = (int64_t)d.expansion * d.c, sq = d.se_sq, k = d.k;
+  switch (i) {
+    case 0: return c * hid;                      // w_exp (C, hid)
+    case 1: return hid;                          // b_exp
+    case 2: return hid * 9 * d.group_width;      // w_conv (hid, 3, 3, T)
+    case 3: return hid;                          // b_conv
+    case 4: return hid * sq;                     // w_sq (hid, sq)
+    case 5: return sq;                           // b_sq
+    case 6: return sq * hid;                     // w_ex (sq, hid)
+    case 7: return hid;                          // b_ex
+    case 8: return hid * k;                      // w_prj (hid, K)
+    case 9: return k;                            // b_prj
+  }
+  return set_error(WL_EINVAL, "weight index %d out of range", i);
+}
+
+int64_t mb_packed_bytes(const wl_block_desc& d) {
+  MbPlanH P;
+  mb_plan(d, P);
+  return P.front_bytes + P.back_bytes;
+}
+
+int64_t mb_workspace(const wl_block_desc& d) {
+  MbPlanH P;
+  mb_plan(d, P);
+  return align_up((int)0, 1) + ((P.h2_bytes + 255) / 256) * 256 + P.pool_bytes;
+}
+
+int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  MbPlanH P;
+  mb_plan(d, P);
+  const MbFrontArgs& f = P.f;
+  const MbBackArgs& b = P.b;
+  memset(out, 0, (size_t)(P.front_bytes + P.back_bytes));
+  const int C = d.c, hid = f.hid, T = d.group_width, K = d.k, sq = d.se_sq;
+  const float *wexp = w[0], *bexp = w[1], *wconv = w[2], *bconv = w[3];
+  for (int r = 0; r < f.ranges; ++r) {
+    uint8_t* hdr = out + (size_t)r * f.hdr_bytes;
+    float* fb = reinterpret_cast<float*>(hdr);
+    float* fc = reinterpret_cast<float*>(hdr + f.o_bconv);
+    float* fw = reinterpret_cast<float*>(hdr + f.o_convw);
+    for (int i = 0; i < f.HR; ++i) {
+      const int h = r * f.HR + i;
+      fb[i] = bexp[h];
+      fc[i] = bconv[h];
+      if (!f.T8)
+        for (int t = 0; t < 9; ++t) fw[t * f.HR + i] = wconv[(size_t)h * 9 + t];
+    }
+    for (int j = 0; j < f.nch; ++j) {
+      uint8_t* ch = out + (size_t)f.ranges * f.hdr_bytes + (size_t)(r * f.nch + j) * f.chunk_bytes;
+      const int hb = r * f.HR + j * f.HC;
+      for (int n = 0; n < f.HC; ++n)
+        for (int k = 0; k < C; ++k) put_h(ch, core_off_h(n, k, f.HC * 16), wexp[(size_t)k * hid + hb + n]);
+      if (f.T8) {
+        uint8_t* cw = ch + f.u_bytes;
+        for (int pr = 0; pr < f.HC / 16; ++pr)
+          for (int t = 0; t < 9; ++t)
+            for (int nn = 0; nn < 16; ++nn)
+              for (int kk = 0; kk < 16; ++kk) {
+                if (nn / 8 != kk / 8) continue;
+                const int oc = hb + 16 * pr + nn;
+                put_h(cw + (pr * 9 + t) * 512, core_off_h(nn, kk, 256), wconv[((size_t)oc * 9 + t) * T + kk % 8]);
+              }
+      }
+    }
+  }
+  uint8_t* bk = out + P.front_bytes;
+  float* fsq = reinterpret_cast<float*>(bk + b.o_wsq);
+  float* fbsq = reinterpret_cast<float*>(bk + b.o_bsq);
+  float* fex = reinterpret_cast<float*>(bk + b.o_wex);
+  float* fbex = reinterpret_cast<float*>(bk + b.o_bex);
+  float* fbp = reinterpret_cast<float*>(bk + b.o_bprj);
+  memcpy(fsq, w[4], sizeof(float) * hid * sq);
+  memcpy(fbsq, w[5], sizeof(float) * sq);
+  memcpy(fex, w[6], sizeof(float) * sq * hid);
+  memcpy(fbex, w[7], sizeof(float) * hid);
+  memcpy(fbp, w[9], sizeof(float) * K);
+  const float* wprj = w[8];
+  for (int kr = 0; kr < b.kranges; ++kr)
+    for (int j = 0; j < b.nchb; ++j) {
+      uint8_t* vc = bk + b.se_bytes + (size_t)(kr * b.nchb + j) * b.vchunk_bytes;
+      for (int n = 0; n < b.KR; ++n)
+        for (int k = 0; k < b.HCb; ++k)
+          put_h(vc, core_off_h(n, k, b.KR * 16), wprj[(size_t)(j * b.HCb + k) * K + kr * b.KR + n]);
+    }
+  return WL_OK;
+}
+
+int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st) {
+  MbPlanH P;
+  mb_plan(d, P);
+  MbFrontArgs f = P.f;
+  MbBackArgs b = P.b;
+  __half* h2 = reinterpret_cast<__half*>(ws);
+  float* pool = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((P.h2_bytes + 255) / 256) * 256);
+  f.wpack = reinterpret_cast<const uint8_t*>(packed);
+  f.h2 = h2;
+  f.pool = pool;
+  CUtensorMap tx;
+  {
+    const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)(d.c / 8), (uint64_t)d.n};
+    const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, 16, (uint64_t)d.h * d.w * d.c * 2};
+    const uint32_t box[5] = {8, (uint32_t)f.Wp, (uint32_t)(f.H + 1), 1, 1};
+    if (int e = encode_tmap(&tx, x, 5, dims, strides, box)) return e;
+  }
+  const int groups = d.n / f.imgs;
+  front_kernel(d.act)<<<groups * f.ranges, mbk::kThreads, f.s_bar + 512, st>>>(tx, f);
+  if (int e = check_cuda(cudaGetLastError(), "mb_front launch")) return e;
+  CUtensorMap th;
+  {
+    const uint64_t dims[3] = {8, (uint64_t)b.P, (uint64_t)(b.hid / 8)};
+    const uint64_t strides[2] = {(uint64_t)b.hid * 2, 16};
+    const uint32_t box[3] = {8, 128, (uint32_t)(b.HCb / 8)};
+    if (int e = encode_tmap(&th, h2, 3, dims, strides, box)) return e;
+  }
+  b.wpack = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
+  b.pool = pool;
+  b.x = reinterpret_cast<const __half*>(x);
+  b.z = reinterpret_cast<__half*>(z);
+  const int ntiles = (b.P + 127) / 128;
+  mb_back_kernel<0><<<ntiles * b.kranges, 256, b.a_bytes, st>>>(th, b);
+  return check_cuda(cudaGetLastError(), "mb_back launch");
+}
+
+int mb_init() {
+  for (int a : {kRelu, kSilu, kGelu})
+    if (int e = check_cuda(cudaFuncSetAttribute(front_kernel(a), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
+                           "cudaFuncSetAttribute(mb_front)"))
+      return e;
+  return check_cuda(cudaFuncSetAttribute(mb_back_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
+                    "cudaFuncSetAttribute(mb_back)");
+}
+
+}  // namespace
+
+const Family kMbFamily = {mb_validate, mb_weight_count, mb_weight_numel, mb_packed_bytes,
+                          mb_pack,     mb_workspace,    mb_forward,      mb_init};
+
+}  // namespace wl

@@ -11,7 +11,7 @@ int64_t ws0(const wl_block_desc&) { return 0; }
 int fw0(const wl_block_desc& d, const void*, const void*, void*, void*, cudaStream_t) { return unsup(d); }
 }  // namespace
 const Family kCf2Family = {unsup, wc0, wn0, pb0, pk0, ws0, fw0, nullptr};
-const Family kMbFamily = {unsup, wc0, wn0, pb0, pk0, ws0, fw0, nullptr};
+
 const Family kStemFamily = {unsup, wc0, wn0, pb0, pk0, ws0, fw0, nullptr};
 const Family kHeadFamily = {unsup, wc0, wn0, pb0, pk0, ws0, fw0, nullptr};
 }  // namespace wl
