@@ -1,0 +1,416 @@
+// cf_s2.cu — fused downsampling ConvFirst block on sm_100a.
+//
+// The reference keeps stride-2 schedules traffic-countable only
+// (machine.py:423-425, 476-482) and fixes just the op-count convention
+// (complexity.py:185-191): conv at H x W, expansion at H/2 x W, projection at
+// H/2 x W/2 -> K. The numerics here follow that convention with BlurPool
+// Triangle-3 as the downsampler:
+//   xc = conv3x3_T8(x) + b_conv                   (full resolution)
+//   xh = blur_H(xc)                               ([1,2,1]/4, stride 2 along H)
+//   y  = phi(xh U + a)                            (H/2 x W)
+//   yq = blur_W(y)                                (stride 2 along W)
+//   z  = yq V + b                                 (H/2 x W/2, K channels)
+// One CTA owns R output rows of one image: the x rows it needs arrive by TMA
+// in the flat padded layout, the grouped conv runs as block-diagonal
+// tcgen05 MMAs, the blurs run on CUDA cores between shared-memory operand
+// tiles, expansion (N = hidden chunk) and projection (N = K) run on tcgen05
+// with fp32 accumulators in TMEM. Only x and z cross HBM.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include "common.cuh"
+#include "plan.h"
+
+namespace wl {
+
+struct Cf2Args {
+  int C, K, hid, r, nch;
+  int H, W, Ho, Wo, R, tiles_y, Wp;
+  int n_ct, n_eh, n_pt, conv_base, x_alloc, x_rows;
+  int o_convw, o_bconv, o_a, o_b, o_u, o_v, w_bytes;  // resident weight blob offsets
+  int s_x, s_xc, s_ah, s_hs, s_aq, s_w, s_bar;
+  int t_c, t_e, t_z, tmem_cols;
+  const uint8_t* wpack;
+  __half* z;
+};
+
+template <int ACT>
+__global__ void __launch_bounds__(256, 1)
+    cf2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Cf2Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* s_x = smem + a.s_x;
+  __half* s_xc = reinterpret_cast<__half*>(smem + a.s_xc);
+  uint8_t* s_ah = smem + a.s_ah;
+  __half* s_hs = reinterpret_cast<__half*>(smem + a.s_hs);
+  uint8_t* s_aq = smem + a.s_aq;
+  uint8_t* s_w = smem + a.s_w;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // [0] load, [1] mma
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 2);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
+  const int q = warp % 4, half = warp / 4;
+  const int n = blockIdx.x / a.tiles_y, yo0 = (blockIdx.x % a.tiles_y) * a.R;
+  const int C = a.C, K = a.K, r = a.r, W = a.W, Wp = a.Wp;
+  const int planes = C / 8;
+  const int loaded = a.x_rows * Wp;
+
+  for (int i = tid; i < planes * (a.x_alloc - loaded); i += blockDim.x) {
+    const int pl = i / (a.x_alloc - loaded), f = loaded + i % (a.x_alloc - loaded);
+    *reinterpret_cast<uint4*>(s_x + ((size_t)pl * a.x_alloc + f) * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc_n(tbase, a.tmem_cols);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tbase;
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bars[0], planes * loaded * 16 + a.w_bytes);
+    for (int g = 0; g < planes; ++g)
+      tma_load_5d(s_x + (size_t)g * a.x_alloc * 16, &tmap_x, 0, -1, 2 * yo0 - 2, g, n, &bars[0]);
+    bulk_g2s(s_w, a.wpack, a.w_bytes, &bars[0]);
+  }
+  mbar_wait(&bars[0], 0);
+  uint32_t mma_phase = 0;
+  auto mma_wait = [&]() {
+    mbar_wait(&bars[1], mma_phase & 1);
+    ++mma_phase;
+    tc_fence_after();
+  };
+
+  // ---------------- grouped 3x3 conv (T = 8) over the flat x rows 1..2R+1
+  if (tid == 0) {
+    tc_fence_after();
+    const uint32_t idesc = make_idesc_f16(128, 16);
+    const uint32_t x0 = smem_u32(s_x), cw = smem_u32(s_w + a.o_convw);
+    for (int t = 0; t < a.n_ct; ++t)
+      for (int pr = 0; pr < C / 16; ++pr)
+        for (int tap = 0; tap < 9; ++tap) {
+          const int f = a.conv_base + t * 128 + (tap / 3 - 1) * Wp + (tap % 3 - 1);
+          const uint64_t ad = make_sdesc(x0 + (2 * pr * a.x_alloc + f) * 16, a.x_alloc * 16, 128);
+          const uint64_t bd = make_sdesc(cw + (pr * 9 + tap) * 512, 256, 128);
+          mma_ss(tmem + a.t_c + t * C + 16 * pr, ad, bd, idesc, tap > 0);
+        }
+    mma_commit(&bars[1]);
+  }
+  mma_wait();
+  {
+    const float* bconv = reinterpret_cast<const float*>(s_w + a.o_bconv);
+    for (int t = half; t < a.n_ct; t += 2) {
+      const int f = a.conv_base + t * 128 + q * 32 + lane;
+      const int row = f / Wp, col = f - row * Wp;  // row 1 .. 2R+1 <-> conv row 2*yo0 - 2 + row
+      const bool real = col >= 1 && col <= W && row >= 1 && row <= 2 * a.R + 1;
+      for (int c0 = 0; c0 < C; c0 += 16) {
+        uint32_t v[16];
+        WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C + c0), v);
+        tmem_ld_wait();
+        float fv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) fv[i] = __uint_as_float(v[i]) + bconv[c0 + i];
+        if (real) {
+          __half* dst = s_xc + ((size_t)(row - 1) * W + (col - 1)) * C + c0;
+          reinterpret_cast<uint4*>(dst)[0] = pack8(fv);
+          reinterpret_cast<uint4*>(dst)[1] = pack8(fv + 8);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  // ---------------- blur along H (stride 2, reflect) -> expansion operand
+  const int MH = a.n_eh * 128;
+  for (int p = tid; p < a.R * W; p += blockDim.x) {
+    const int ro = p / W, x = p - ro * W, yo = yo0 + ro;
+    int k0 = 2 * ro, k1 = 2 * ro + 1, k2 = 2 * ro + 2;  // staging rows of conv rows 2yo-1, 2yo, 2yo+1
+    if (yo == 0) k0 = k2;                               // reflect row -1 -> row 1
+    for (int c8 = 0; c8 < planes; ++c8) {
+      float fa[8], fb[8], fc[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k0 * W + x) * C + c8 * 8), fa);
+      unpack8(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k1 * W + x) * C + c8 * 8), fb);
+      unpack8(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k2 * W + x) * C + c8 * 8), fc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = 0.25f * fa[i] + 0.5f * fb[i] + 0.25f * fc[i];
+      *reinterpret_cast<uint4*>(s_ah + ((size_t)c8 * MH + p) * 16) = pack8(o);
+    }
+  }
+  fence_async_smem();
+  __syncthreads();
+
+  // ---------------- FFN over hidden chunks with the W blur between
+  const float* av = reinterpret_cast<const float*>(s_w + a.o_a);
+  const int MQ = a.n_pt * 128;
+  for (int j = 0; j < a.nch; ++j) {
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t idesc = make_idesc_f16(128, r);
+      const uint32_t ub = smem_u32(s_w + a.o_u) + j * (r * C * 2);
+      for (int t = 0; t < a.n_eh; ++t)
+        for (int kk = 0; kk < C / 16; ++kk) {
+          const uint64_t ad = make_sdesc(smem_u32(s_ah) + (kk * 2 * MH + t * 128) * 16, MH * 16, 128);
+          const uint64_t bd = make_sdesc(ub + kk * 2 * (r * 16), r * 16, 128);
+          mma_ss(tmem + a.t_e + t * r, ad, bd, idesc, kk > 0);
+        }
+      mma_commit(&bars[1]);
+    }
+    mma_wait();
+    for (int t = half; t < a.n_eh; t += 2) {
+      const int p = t * 128 + q * 32 + lane;
+      for (int c0 = 0; c0 < r; c0 += 16) {
+        uint32_t v[16];
+        WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + t * r + c0), v);
+        tmem_ld_wait();
+        if (p < a.R * W) {
+          float fv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) fv[i] = act<ACT>(__uint_as_float(v[i]) + av[j * r + c0 + i]);
+          __half* dst = s_hs + (size_t)p * r + c0;
+          reinterpret_cast<uint4*>(dst)[0] = pack8(fv);
+          reinterpret_cast<uint4*>(dst)[1] = pack8(fv + 8);
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    for (int qi = tid; qi < a.R * a.Wo; qi += blockDim.x) {
+      const int ro = qi / a.Wo, xo = qi - ro * a.Wo;
+      int x0 = 2 * xo - 1;
+      if (x0 < 0) x0 = 1;
+      const __half* r0 = s_hs + ((size_t)ro * W + x0) * r;
+      const __half* r1 = s_hs + ((size_t)ro * W + 2 * xo) * r;
+      const __half* r2 = s_hs + ((size_t)ro * W + 2 * xo + 1) * r;
+      for (int c8 = 0; c8 < r / 8; ++c8) {
+        float fa[8], fb[8], fc[8], o[8];
+        unpack8(*reinterpret_cast<const uint4*>(r0 + c8 * 8), fa);
+        unpack8(*reinterpret_cast<const uint4*>(r1 + c8 * 8), fb);
+        unpack8(*reinterpret_cast<const uint4*>(r2 + c8 * 8), fc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = 0.25f * fa[i] + 0.5f * fb[i] + 0.25f * fc[i];
+        *reinterpret_cast<uint4*>(s_aq + ((size_t)c8 * MQ + qi) * 16) = pack8(o);
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t idesc = make_idesc_f16(128, K);
+      const uint32_t vb = smem_u32(s_w + a.o_v) + j * (K * r * 2);
+      for (int t = 0; t < a.n_pt; ++t)
+        for (int kk = 0; kk < r / 16; ++kk) {
+          const uint64_t ad = make_sdesc(smem_u32(s_aq) + (kk * 2 * MQ + t * 128) * 16, MQ * 16, 128);
+          const uint64_t bd = make_sdesc(vb + kk * 2 * (K * 16), K * 16, 128);
+          mma_ss(tmem + a.t_z + t * K, ad, bd, idesc, (j > 0 || kk > 0));
+        }
+      mma_commit(&bars[1]);
+    }
+    mma_wait();
+  }
+  // ---------------- z = Z + b
+  const float* bv = reinterpret_cast<const float*>(s_w + a.o_b);
+  for (int t = half; t < a.n_pt; t += 2) {
+    const int qi = t * 128 + q * 32 + lane;
+    const int ro = qi / a.Wo, xo = qi - ro * a.Wo, yo = yo0 + ro;
+    const bool inside = qi < a.R * a.Wo && yo < a.Ho;
+    for (int c0 = 0; c0 < K; c0 += 16) {
+      uint32_t v[16];
+      WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * K + c0), v);
+      tmem_ld_wait();
+      if (!inside) continue;
+      float fv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) fv[i] = __uint_as_float(v[i]) + bv[c0 + i];
+      uint4* zp = reinterpret_cast<uint4*>(a.z + (((size_t)n * a.Ho + yo) * a.Wo + xo) * K + c0);
+      zp[0] = pack8(fv);
+      zp[1] = pack8(fv + 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc_n(tmem, a.tmem_cols);
+}
+
+}  // namespace wl
+
+// =================================================================== host
+#include <cstring>
+#include "launch.h"
+
+namespace wl {
+namespace {
+
+constexpr int kSmemMax2 = 232448;
+
+bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
+  memset(&a, 0, sizeof(a));
+  a.C = d.c;
+  a.K = d.k;
+  a.hid = d.expansion * d.c;
+  a.H = d.h;
+  a.W = d.w;
+  a.Ho = d.h / 2;
+  a.Wo = d.w / 2;
+  a.Wp = d.w + 1;
+  if (a.C % 16 || a.K % 16 || a.hid % 16 || a.K > 256) return false;
+  for (int R = 8; R >= 1; --R) {
+    if (R > a.Ho) continue;
+    a.R = R;
+    a.x_rows = 2 * R + 3;
+    a.conv_base = a.Wp + 1;
+    const int conv_end = (2 * R + 2) * a.Wp;
+    a.n_ct = (conv_end - a.conv_base + 127) / 128;
+    a.x_alloc = align_up(std::max(a.conv_base + a.n_ct * 128 + a.Wp + 2, a.x_rows * a.Wp), 8);
+    a.n_eh = (R * a.W + 127) / 128;
+    a.n_pt = (R * a.Wo + 127) / 128;
+    if (a.n_eh > 4) continue;
+    // hidden chunk
+    a.r = 0;
+    for (int rr = 128; rr >= 16; rr -= 16) {
+      if (a.hid % rr) continue;
+      const int cols = a.n_ct * a.C + a.n_eh * rr + a.n_pt * a.K;
+      if (cols <= 512) {
+        a.r = rr;
+        break;
+      }
+    }
+    if (!a.r) continue;
+    a.nch = a.hid / a.r;
+    int o = 0;
+    a.o_convw = o;
+    o += (a.C / 16) * 9 * 512;
+    a.o_bconv = o;
+    o = align_up(o + a.C * 4, 16);
+    a.o_a = o;
+    o = align_up(o + a.hid * 4, 16);
+    a.o_b = o;
+    o = align_up(o + a.K * 4, 16);
+    a.o_u = o;
+    o += a.hid * a.C * 2;
+    a.o_v = o;
+    o += a.K * a.hid * 2;
+    a.w_bytes = align_up(o, 16);
+    int s = 0;
+    a.s_x = s;
+    s = align_up(s + (a.C / 8) * a.x_alloc * 16, 128);
+    a.s_xc = s;
+    s = align_up(s + (2 * R + 1) * a.W * a.C * 2, 128);
+    a.s_ah = s;
+    s = align_up(s + a.n_eh * 128 * a.C * 2, 128);
+    a.s_hs = s;
+    s = align_up(s + R * a.W * a.r * 2, 128);
+    a.s_aq = s;
+    s = align_up(s + a.n_pt * 128 * a.r * 2, 128);
+    a.s_w = s;
+    s = align_up(s + a.w_bytes, 128);
+    a.s_bar = s;
+    s += 64;
+    if (s > kSmemMax2) continue;
+    a.tiles_y = (a.Ho + R - 1) / R;
+    a.t_c = 0;
+    a.t_e = a.n_ct * a.C;
+    a.t_z = a.t_e + a.n_eh * a.r;
+    const int cols = a.t_z + a.n_pt * a.K;
+    a.tmem_cols = 32;
+    while (a.tmem_cols < cols) a.tmem_cols *= 2;
+    return true;
+  }
+  return false;
+}
+
+using Cf2K = void (*)(const CUtensorMap, const Cf2Args);
+Cf2K cf2_kernel_for(int act) {
+  switch (act) {
+    case kRelu: return cf2_kernel<kRelu>;
+    case kSilu: return cf2_kernel<kSilu>;
+    case kGelu: return cf2_kernel<kGelu>;
+  }
+  return nullptr;
+}
+
+int cf2_validate(const wl_block_desc& d) {
+  if (d.h % 2 || d.w % 2) return set_error(WL_EINVAL, "stride 2 needs an even resolution");
+  if (d.group_width != 8 || d.ksize != 3)
+    return set_error(WL_EUNSUPPORTED, "downsampling ConvFirst supports T=8 3x3 (got T=%d k=%d)", d.group_width, d.ksize);
+  if (d.norm != WL_NORM_NONE) return set_error(WL_EUNSUPPORTED, "downsampling ConvFirst has no norm");
+  if (!cf2_kernel_for(d.act)) return set_error(WL_EUNSUPPORTED, "activation not supported");
+  Cf2Args a;
+  if (!cf2_plan(d, a)) return set_error(WL_EUNSUPPORTED, "no launch plan for downsampling ConvFirst C=%d K=%d", d.c, d.k);
+  return WL_OK;
+}
+int cf2_weight_count(const wl_block_desc&) { return 6; }
+int64_t cf2_weight_numel(const wl_block_desc& d, int i) {
+  const int64_t c = d.c, hid = (int64_t)d.expansion * d.c, k = d.k;
+  switch (i) {
+    case 0: return c * 9 * d.group_width;
+    case 1: return c;
+    case 2: return c * hid;
+    case 3: return hid;
+    case 4: return hid * k;
+    case 5: return k;
+  }
+  return set_error(WL_EINVAL, "weight index %d out of range", i);
+}
+int64_t cf2_packed_bytes(const wl_block_desc& d) {
+  Cf2Args a;
+  cf2_plan(d, a);
+  return a.w_bytes;
+}
+int cf2_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  Cf2Args a;
+  cf2_plan(d, a);
+  memset(out, 0, a.w_bytes);
+  const int C = a.C, hid = a.hid, K = a.K, r = a.r;
+  const float *wc = w[0], *bc = w[1], *u = w[2], *av = w[3], *v = w[4], *b = w[5];
+  for (int pr = 0; pr < C / 16; ++pr)
+    for (int t = 0; t < 9; ++t)
+      for (int nn = 0; nn < 16; ++nn)
+        for (int kk = 0; kk < 16; ++kk) {
+          if (nn / 8 != kk / 8) continue;
+          put_h(out + a.o_convw + (pr * 9 + t) * 512, core_off_h(nn, kk, 256), wc[((size_t)(16 * pr + nn) * 9 + t) * 8 + kk % 8]);
+        }
+  float* fb = reinterpret_cast<float*>(out + a.o_bconv);
+  float* fa = reinterpret_cast<float*>(out + a.o_a);
+  float* fbb = reinterpret_cast<float*>(out + a.o_b);
+  for (int i = 0; i < C; ++i) fb[i] = bc[i];
+  for (int i = 0; i < hid; ++i) fa[i] = av[i];
+  for (int i = 0; i < K; ++i) fbb[i] = b[i];
+  for (int j = 0; j < a.nch; ++j) {
+    uint8_t* ub = out + a.o_u + (size_t)j * r * C * 2;
+    for (int nn = 0; nn < r; ++nn)
+      for (int k = 0; k < C; ++k) put_h(ub, core_off_h(nn, k, r * 16), u[(size_t)k * hid + j * r + nn]);
+    uint8_t* vb = out + a.o_v + (size_t)j * K * r * 2;
+    for (int nn = 0; nn < K; ++nn)
+      for (int k = 0; k < r; ++k) put_h(vb, core_off_h(nn, k, K * 16), v[(size_t)(j * r + k) * K + nn]);
+  }
+  return WL_OK;
+}
+int64_t cf2_ws(const wl_block_desc&) { return 0; }
+int cf2_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void*, cudaStream_t st) {
+  Cf2Args a;
+  cf2_plan(d, a);
+  CUtensorMap tm;
+  const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)(d.c / 8), (uint64_t)d.n};
+  const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, 16, (uint64_t)d.h * d.w * d.c * 2};
+  const uint32_t box[5] = {8, (uint32_t)a.Wp, (uint32_t)a.x_rows, 1, 1};
+  if (int e = encode_tmap(&tm, x, 5, dims, strides, box)) return e;
+  a.wpack = reinterpret_cast<const uint8_t*>(packed);
+  a.z = reinterpret_cast<__half*>(z);
+  cf2_kernel_for(d.act)<<<d.n * a.tiles_y, 256, a.s_bar + 64, st>>>(tm, a);
+  return check_cuda(cudaGetLastError(), "cf2 launch");
+}
+int cf2_init() {
+  for (int act : {kRelu, kSilu, kGelu})
+    if (int e = check_cuda(cudaFuncSetAttribute(cf2_kernel_for(act), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax2),
+                           "cudaFuncSetAttribute(cf2)"))
+      return e;
+  return WL_OK;
+}
+
+}  // namespace
+
+const Family kCf2Family = {cf2_validate, cf2_weight_count, cf2_weight_numel, cf2_packed_bytes,
+                           cf2_pack,     cf2_ws,           cf2_forward,      cf2_init};
+
+}  // namespace wl
