@@ -1,0 +1,109 @@
+"""``torch.nn.Module`` wrappers around the fused kernels (the paper's
+TorchBlock pattern), plus the fan-in-scaled synthetic
+weight init used for whole-network runs.
+
+Each module owns its packed weights and workspace on the device and launches
+its block through the C ABI on the current torch stream. Inputs/outputs are
+NHWC fp16 CUDA tensors. No CPU fallback: construction raises without a GPU
+or without libwlfuse.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims
+from .machine import FusedSchedule, block_descriptor, build_schedule, random_inputs, weight_names
+
+
+def init_weights(s: FusedSchedule, rng: np.random.Generator, residual_gain: float = 0.5) -> dict:
+    """Fan-in-scaled weights N(0, 1/fan_in), biases 0.1 N(0, 1), LayerNorm
+    gamma 1 + 0.1 N, beta 0.1 N (documented in DESIGN.md: the reference's
+    0.5 N(0,1) init overflows fp16 after three chained blocks). Projections
+    feeding a residual are scaled by ``residual_gain``."""
+    out = {}
+    block = s.block
+    for t in s.tensors:
+        if t.role != "weights":
+            continue
+        name, dims = t.name, t.dims
+        if len(dims) == 1:
+            if name == "ln_gamma":
+                out[name] = (1.0 + 0.1 * rng.standard_normal(dims)).astype(np.float32)
+            else:
+                out[name] = (0.1 * rng.standard_normal(dims)).astype(np.float32)
+            continue
+        if len(dims) == 4:  # (K, R, S, T): fan-in R*S*T
+            fan_in = dims[1] * dims[2] * dims[3]
+        else:  # (in, out) matrices
+            fan_in = dims[0]
+        w = rng.standard_normal(dims) / np.sqrt(fan_in)
+        if name in ("v", "w_prj") and getattr(block, "stride", 1) == 1 and not isinstance(block, (Stem, Head)):
+            w = w * residual_gain
+        out[name] = w.astype(np.float32)
+    return out
+
+
+class FusedBlock(torch.nn.Module):
+    """One fused block bound to a batch geometry (the layer of the
+    model-level scheduler). ``weights`` uses the reference tensor names."""
+
+    def __init__(self, block, dims: TensorDims, out_channels: int | None = None, weights: dict | None = None,
+                 seed: int = 0, device: str | torch.device = "cuda"):
+        super().__init__()
+        if not torch.cuda.is_available():
+            raise RuntimeError("FusedBlock needs a CUDA device (there is no CPU fallback)")
+        self.schedule = build_schedule(block, dims, out_channels=out_channels)
+        self.desc = block_descriptor(block, dims, self.schedule.out_channels)
+        L = _lib.lib()
+        dev = torch.device(device)
+        _lib.check(L.wl_init(dev.index if dev.index is not None else torch.cuda.current_device()), "wl_init")
+        if weights is None:
+            weights = init_weights(self.schedule, np.random.default_rng(seed))
+        self.weights = {k: np.asarray(v, dtype=np.float32) for k, v in weights.items()}
+        packed = _lib.pack_weights(self.desc, [self.weights[n] for n in weight_names(self.schedule)])
+        self.register_buffer("packed", torch.from_numpy(packed).to(dev), persistent=False)
+        ws = _lib.check(L.wl_workspace_bytes(ctypes.byref(self.desc)))
+        self.register_buffer("workspace", torch.empty(max(ws, 256), dtype=torch.uint8, device=dev), persistent=False)
+        self.out_shape = tuple(self.schedule.out_dims)
+
+    def launch(self, x: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor | None = None, stream=None) -> None:
+        """Raw launch into a caller-owned output (graph-capturable)."""
+        ws = self.workspace if workspace is None else workspace
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _lib.check(
+            _lib.lib().wl_block_forward(
+                ctypes.byref(self.desc), x.data_ptr(), self.packed.data_ptr(), out.data_ptr(), ws.data_ptr(), st
+            ),
+            f"{self.schedule.label}",
+        )
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if x.dtype != torch.float16 or not x.is_cuda or not x.is_contiguous():
+            raise ValueError("FusedBlock expects a contiguous NHWC fp16 CUDA tensor")
+        want = (self.schedule.dims.n, self.schedule.dims.h, self.schedule.dims.w, self.schedule.dims.c)
+        if tuple(x.shape) != want:
+            raise ValueError(f"input shape {tuple(x.shape)} does not match the bound dims {want}")
+        out = torch.empty(self.out_shape, dtype=torch.float16, device=x.device)
+        self.launch(x, out)
+        return out
+
+
+def FusedConvFirst(dims: TensorDims, group_width=8, expansion=6, stride=1, activation="relu", out_channels=None, **kw):
+    return FusedBlock(ConvFirst(group_width, expansion, stride, activation), dims, out_channels, **kw)
+
+
+def FusedConvNeXtBlock(dims: TensorDims, kernel_size=7, expansion=4, activation="gelu", **kw):
+    return FusedBlock(ConvNeXtBlock(kernel_size, expansion, activation), dims, None, **kw)
+
+
+def FusedMBConv(dims: TensorDims, group_width=8, expansion=4, se_ratio=0.25, stride=1, activation="silu",
+                out_channels=None, **kw):
+    return FusedBlock(MBConv(group_width, expansion, se_ratio, stride, activation), dims, out_channels, **kw)
+
+
+__all__ = ["FusedBlock", "FusedConvFirst", "FusedConvNeXtBlock", "FusedMBConv", "init_weights", "random_inputs"]

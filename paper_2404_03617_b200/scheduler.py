@@ -1,0 +1,156 @@
+"""Model-level kernel scheduler: replaces the reference's per-layer path
+(``expand_network(..., LAYER_WISE)``, core.py:401-429) with one fused launch
+per ``plan_blocks`` unit (core.py:362-398), all stream-ordered on one CUDA
+stream and captured into a single CUDA graph.
+
+Memory plan (HBM): one fp16 NHWC activation buffer per unit boundary
+(the unit's output), one shared workspace sized to the largest unit
+(MBConv's L2-resident hidden + SE pool, the head's pooled embedding), packed
+weights per unit. Batch sharding across GPUs is by independent image shards
+(no collective on the path; see bench.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .blocks import FusedBlock, init_weights
+from .core import DeviceSpec, ExecutionScheme, NetworkSpec, TensorDims, expand_network, plan_blocks
+from .machine import build_schedule
+
+
+@dataclass
+class Unit:
+    label: str
+    block: object
+    module: FusedBlock
+    out: torch.Tensor
+
+
+class FusedNetwork:
+    """A NetworkSpec bound to a per-GPU batch, ready to launch.
+
+    ``weights`` (optional) maps unit labels (``stem``, ``s1b0`` ...,
+    ``head``) to reference-named float32 tensors; otherwise fan-in-scaled
+    synthetic weights are drawn with seed ``seed + unit index``.
+    """
+
+    def __init__(self, net: NetworkSpec, batch: int, device: str | torch.device = "cuda", seed: int = 0,
+                 weights: dict | None = None):
+        self.net = net
+        self.batch = batch
+        self.device = torch.device(device)
+        self.instances = plan_blocks(net)
+        h, w = net.input_resolution
+        c0 = self.instances[0].in_channels
+        self.x = torch.zeros((batch, h, w, c0), dtype=torch.float16, device=self.device)
+        self.units: list[Unit] = []
+        ws_bytes = 256
+        for i, inst in enumerate(self.instances):
+            dims = inst.dims(batch)
+            sched = build_schedule(inst.block, dims, out_channels=inst.out_channels)
+            wts = None
+            if weights is not None:
+                wts = weights[inst.label]
+            else:
+                wts = init_weights(sched, np.random.default_rng(seed + i))
+            mod = FusedBlock(inst.block, dims, inst.out_channels, weights=wts, device=self.device)
+            ws_bytes = max(ws_bytes, mod.workspace.numel())
+            out = torch.empty(mod.out_shape, dtype=torch.float16, device=self.device)
+            self.units.append(Unit(inst.label, inst.block, mod, out))
+        # one workspace shared by every unit (launches are stream-ordered)
+        self.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        for u in self.units:
+            u.module.workspace = self.workspace
+        self.graph: torch.cuda.CUDAGraph | None = None
+
+    # ----------------------------------------------------------- execution
+    @property
+    def output(self) -> torch.Tensor:
+        return self.units[-1].out
+
+    def launch_all(self, stream=None) -> None:
+        src = self.x
+        for u in self.units:
+            u.module.launch(src, u.out, self.workspace, stream)
+            src = u.out
+
+    def capture(self) -> torch.cuda.CUDAGraph:
+        """Capture the whole forward into one CUDA graph (warm-up first)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.launch_all(s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_all()
+        self.graph = g
+        return g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        """Forward on an NHWC fp16 batch (copied into the static input)."""
+        self.x.copy_(x, non_blocking=True)
+        self.replay()
+        return self.output
+
+    # ------------------------------------------------------- accounting
+    def workloads(self, device: DeviceSpec, scheme=ExecutionScheme.BLOCK_FUSION):
+        return expand_network(self.net, self.batch, scheme, device)
+
+    def launch_count(self) -> int:
+        """Kernels this forward launches (MBConv and head units launch two)."""
+        n = 0
+        for u in self.units:
+            kind = u.module.desc.kind
+            n += 2 if kind in (_lib.KIND_MBCONV, _lib.KIND_HEAD) else 1
+        return n
+
+    def weights(self) -> dict:
+        return {u.label: u.module.weights for u in self.units}
+
+    def time_units(self, iters: int = 20) -> list[float]:
+        """Per-unit device time (seconds, mean over ``iters``) with CUDA
+        events on the launching stream — the measured column beside the
+        waterline's attainable latency."""
+        torch.cuda.synchronize(self.device)
+        times = []
+        src = self.x
+        for u in self.units:
+            for _ in range(3):
+                u.module.launch(src, u.out, self.workspace)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(iters):
+                u.module.launch(src, u.out, self.workspace)
+            ev1.record()
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1) / iters / 1e3)
+            src = u.out
+        return times
+
+
+def ctypes_ref(x):
+    return ctypes.byref(x)
+
+
+def shard_range(global_batch: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous image shard of ``rank`` (near-equal split; images never
+    interact, so no collective is needed on the data path)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid rank / world size")
+    base, extra = divmod(global_batch, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)

@@ -1,0 +1,91 @@
+"""The C ABI (include/wlfuse.h) without a GPU: the library loads, exports
+every declared symbol, validates descriptors with the reference's error
+mapping, and packs weights deterministically."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2404_03617_b200 import _lib
+from paper_2404_03617_b200.core import ConvFirst, MBConv, Stem, Head, TensorDims
+from paper_2404_03617_b200.machine import ScheduleError, block_descriptor, build_schedule, random_inputs, weight_names
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "wlfuse.h")
+
+
+def declared_symbols():
+    return sorted(set(re.findall(r"WL_API\s+[\w\s\*]+?\b(wl_\w+)\s*\(", open(HEADER).read())))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    so = ctypes.CDLL(_lib.LIB_PATH)
+    for s in syms:
+        assert hasattr(so, s), s
+    assert sorted(_lib.EXPORTS) == syms
+    assert _lib.lib().wl_version() == 1
+
+
+def _desc(block, dims, k=None):
+    return block_descriptor(block, dims, k if k is not None else dims.c)
+
+
+def test_validate_maps_errors_like_the_reference():
+    L = _lib.lib()
+    d = _desc(ConvFirst(8, 6), TensorDims(1, 16, 16, 32))
+    assert L.wl_validate(ctypes.byref(d)) == 0
+    d.c = 36  # group width 8 does not divide 36 -> ValueError in the reference
+    with pytest.raises(ValueError):
+        _lib.check(L.wl_validate(ctypes.byref(d)))
+    d = _desc(ConvFirst(8, 6), TensorDims(1, 16, 16, 32))
+    d.group_width = 4  # valid block, no kernel -> ScheduleError (not executable)
+    with pytest.raises(ScheduleError):
+        _lib.check(L.wl_validate(ctypes.byref(d)))
+    d = _desc(ConvFirst(8, 6), TensorDims(1, 16, 16, 32))
+    d.k = 64  # stride-1 blocks keep their channel count
+    with pytest.raises(ValueError):
+        _lib.check(L.wl_validate(ctypes.byref(d)))
+    d.kind = 99
+    with pytest.raises(ValueError):
+        _lib.check(L.wl_validate(ctypes.byref(d)))
+
+
+@pytest.mark.parametrize(
+    "block,dims,k",
+    [
+        (ConvFirst(8, 6), TensorDims(2, 56, 56, 32), None),
+        (ConvFirst(8, 6, 2), TensorDims(2, 112, 112, 16), 32),
+        (MBConv(8, 4, 0.25), TensorDims(128, 14, 14, 128), None),
+        (MBConv(8, 4, 0.25, 2), TensorDims(128, 28, 28, 48), 128),
+        (MBConv(1, 4, 0.25), TensorDims(128, 28, 28, 80), None),
+        (Stem(16), TensorDims(128, 224, 224, 3), 16),
+        (Head(), TensorDims(128, 7, 7, 128), 1000),
+    ],
+)
+def test_pack_is_deterministic_and_sized(block, dims, k):
+    s = build_schedule(block, dims, out_channels=k)
+    d = block_descriptor(block, dims, s.out_channels)
+    ins = random_inputs(s, np.random.default_rng(0))
+    w = [ins[n] for n in weight_names(s)]
+    a = _lib.pack_weights(d, w)
+    b = _lib.pack_weights(d, w)
+    assert a.nbytes == _lib.lib().wl_packed_bytes(ctypes.byref(d)) and np.array_equal(a, b)
+    assert a.any()
+    with pytest.raises(ValueError):
+        _lib.pack_weights(d, w[:-1])
+    n, h, ww, c = _lib.output_dims(d)
+    assert (n, h, ww, c)[0] == dims.n
+
+
+def test_output_dims_and_workspace():
+    L = _lib.lib()
+    d = _desc(MBConv(8, 4, 0.25, 2), TensorDims(4, 28, 28, 48), 128)
+    assert _lib.output_dims(d) == (4, 14, 14, 128)
+    ws = L.wl_workspace_bytes(ctypes.byref(d))
+    assert ws >= 4 * 14 * 14 * 192 * 2 + 4 * 192 * 4  # L2-resident hidden + SE pool
+    d = _desc(ConvFirst(8, 6), TensorDims(4, 28, 28, 48))
+    assert L.wl_workspace_bytes(ctypes.byref(d)) == 0  # fully fused

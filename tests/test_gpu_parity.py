@@ -1,0 +1,153 @@
+"""Parity of the sm_100a kernels (through the C ABI) with the reference's
+golden vectors and the CPU oracle. Tolerance (fp16 storage, fp32
+accumulation): max|gpu - ref| / max|ref| <= 1e-2 and ||gpu - ref||_2 /
+||ref||_2 <= 2e-3."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import model as om  # noqa: E402
+from oracle.fixtures import golden_names, load_golden  # noqa: E402
+from paper_2404_03617_b200 import zoo  # noqa: E402
+from paper_2404_03617_b200.blocks import FusedBlock, init_weights  # noqa: E402
+from paper_2404_03617_b200.core import ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims  # noqa: E402
+from paper_2404_03617_b200.machine import ScheduleError, build_schedule, execute_numeric, random_inputs  # noqa: E402
+from paper_2404_03617_b200.scheduler import FusedNetwork  # noqa: E402
+
+MAX_REL, L2_REL = 1e-2, 2e-3
+
+
+def close(got, ref, max_rel=MAX_REL, l2_rel=L2_REL):
+    got = np.asarray(got, np.float64).reshape(np.shape(ref))
+    ref = np.asarray(ref, np.float64)
+    m = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-12)
+    l2 = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-12)
+    assert np.isfinite(got).all()
+    assert m <= max_rel and l2 <= l2_rel, (m, l2)
+
+
+def r16(rng, shape, scale=1.0):
+    return (scale * rng.standard_normal(shape)).astype(np.float16).astype(np.float32)
+
+
+def oracle_unit(block, w, x):
+    return om.unit_forward(block, w, x)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_vectors(name):
+    meta, ins, out_lw, _ = load_golden(name)
+    kinds = {"ConvFirst": ConvFirst, "MBConv": MBConv}
+    if meta["block"] not in kinds:
+        pytest.skip("FFN has no standalone kernel")
+    s = build_schedule(kinds[meta["block"]](**meta["params"]), TensorDims(*meta["dims"]))
+    if meta["dims"][3] % 16:
+        with pytest.raises(ScheduleError):  # fails loudly, never silently
+            execute_numeric(s, ins)
+        return
+    close(execute_numeric(s, ins), out_lw)
+
+
+def _block_case(block, dims, k=None, seed=0):
+    rng = np.random.default_rng(seed)
+    s = build_schedule(block, dims, out_channels=k)
+    w = init_weights(s, rng)
+    w = {n: v.astype(np.float16).astype(np.float32) for n, v in w.items()}
+    x = r16(rng, (dims.n, dims.h, dims.w, dims.c))
+    return s, w, x
+
+
+CASES = [
+    ("convfirst_pico_s1", ConvFirst(8, 3), TensorDims(2, 112, 112, 16), None),
+    ("convfirst_partial_tiles", ConvFirst(8, 6), TensorDims(3, 20, 12, 32), None),
+    ("convfirst_c96_ring", ConvFirst(8, 6), TensorDims(1, 28, 28, 96), None),
+    ("convfirst_dw3x3", ConvFirst(1, 4), TensorDims(2, 15, 9, 64), None),
+    ("convnext_c1_config", ConvNeXtBlock(7, 4, "gelu"), TensorDims(8, 56, 56, 96), None),
+    ("convfirst_s2_112", ConvFirst(8, 6, 2), TensorDims(2, 112, 112, 16), 32),
+    ("convfirst_s2_56", ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 32), 48),
+    ("mbconv_14", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 128), None),
+    ("mbconv_7_odd_batch", MBConv(8, 4, 0.25), TensorDims(3, 7, 7, 128), None),
+    ("mbconv_c2_config_shape", MBConv(1, 4, 0.25), TensorDims(4, 28, 28, 80), None),
+    ("mbconv_small_c256", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 256), None),
+    ("mbconv_s2_28", MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 48), 128),
+    ("mbconv_s2_14", MBConv(8, 4, 0.25, 2), TensorDims(2, 14, 14, 128), 128),
+    ("stem_224", Stem(16), TensorDims(2, 224, 224, 3), None),
+    ("stem_c32", Stem(32), TensorDims(1, 64, 48, 3), None),
+    ("head_pico", Head(1280, 1000), TensorDims(5, 7, 7, 128), None),
+    ("head_batch_over_128", Head(1280, 1000), TensorDims(130, 7, 7, 128), None),
+]
+
+
+@pytest.mark.parametrize("name,block,dims,k", CASES, ids=[c[0] for c in CASES])
+def test_block_vs_oracle(name, block, dims, k):
+    s, w, x = _block_case(block, dims, k)
+    got = execute_numeric(s, dict(w, x=x))
+    close(got, oracle_unit(block, w, x))
+
+
+def test_device_module_matches_host_abi():
+    s, w, x = _block_case(MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 128))
+    host = execute_numeric(s, dict(w, x=x))
+    mod = FusedBlock(s.block, s.dims, weights=w)
+    dev = mod(torch.from_numpy(x).half().cuda()).float().cpu().numpy()
+    close(dev, host, max_rel=2e-3, l2_rel=5e-4)
+
+
+def test_deterministic_and_graph_equals_eager():
+    net = zoo.at_resolution(zoo.from_name("convfirstnet-pico"), 224)
+    m = FusedNetwork(net, batch=4, seed=3)
+    m.x.normal_()
+    m.launch_all()
+    eager = m.output.clone()
+    m.capture()
+    m.replay()
+    a = m.output.clone()
+    m.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(eager, a) and torch.equal(a, m.output)
+
+
+@pytest.mark.parametrize("model", ["convfirstnet-pico", "convfirstnet-small"])
+def test_network_per_unit_and_logits(model):
+    net = zoo.at_resolution(zoo.from_name(model), 224)
+    m = FusedNetwork(net, batch=2, seed=11)
+    rng = np.random.default_rng(1)
+    x = r16(rng, (2, 224, 224, 3))
+    out = m(torch.from_numpy(x).half().cuda())
+    torch.cuda.synchronize()
+    src = x
+    for u, inst in zip(m.units, m.instances):
+        got = u.out.float().cpu().numpy()
+        ref = oracle_unit(inst.block, u.module.weights, src)
+        close(got, ref)
+        src = got.reshape(ref.shape)
+    ref = om.network_forward(m.instances, m.weights(), x)
+    close(out.float().cpu().numpy(), ref, max_rel=2e-2, l2_rel=1e-2)
+
+
+def test_full_size_pico_b128_sampled_images():
+    """BASELINE config 3 at full size: images 0 and 127 of the b128 forward
+    match the oracle unit by unit (the oracle runs on the two images)."""
+    net = zoo.at_resolution(zoo.from_name("convfirstnet-pico"), 224)
+    m = FusedNetwork(net, batch=128, seed=5)
+    m.x.normal_()
+    m.replay()
+    torch.cuda.synchronize()
+    pick = [0, 127]
+    src = m.x.float().cpu().numpy()[pick]
+    for u, inst in zip(m.units, m.instances):
+        got = u.out.float().cpu().numpy()[pick]
+        ref = oracle_unit(inst.block, u.module.weights, src)
+        close(got, ref)
+        src = got.reshape(ref.shape)
+
+
+def test_unsupported_configs_fail_loudly():
+    with pytest.raises(ScheduleError):
+        FusedBlock(ConvFirst(4, 6), TensorDims(1, 8, 8, 16))  # no T=4 kernel
+    with pytest.raises(ScheduleError):
+        FusedBlock(ConvFirst(8, 6), TensorDims(1, 8, 8, 24))  # C % 16 != 0
