@@ -96,7 +96,10 @@ WL_API int64_t wl_packed_bytes(const wl_block_desc* d);
  * copy it to the device once). Replaces the per-call weight handling of
  * machine._Executor.__init__ (machine.py:915-929). */
 WL_API int wl_pack_weights(const wl_block_desc* d, const float* const* weights, int count, void* packed_host);
-/* device workspace the forward needs (0 for fully fused blocks) */
+/* device workspace the forward needs (0 for fully fused blocks). The caller
+ * zeroes it once before the first forward; the library keeps its arrival-
+ * counter header zeroed across calls, so one workspace can serve many blocks
+ * launched in stream order. */
 WL_API int64_t wl_workspace_bytes(const wl_block_desc* d);
 
 /* forward: z = block(x). x, packed, z, workspace are DEVICE pointers.

@@ -68,7 +68,7 @@ class FusedBlock(torch.nn.Module):
         packed = _lib.pack_weights(self.desc, [self.weights[n] for n in weight_names(self.schedule)])
         self.register_buffer("packed", torch.from_numpy(packed).to(dev), persistent=False)
         ws = _lib.check(L.wl_workspace_bytes(ctypes.byref(self.desc)))
-        self.register_buffer("workspace", torch.empty(max(ws, 256), dtype=torch.uint8, device=dev), persistent=False)
+        self.register_buffer("workspace", torch.zeros(max(ws, 256), dtype=torch.uint8, device=dev), persistent=False)
         self.out_shape = tuple(self.schedule.out_dims)
 
     def launch(self, x: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor | None = None, stream=None) -> None:

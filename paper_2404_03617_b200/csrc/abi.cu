@@ -187,6 +187,7 @@ int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float*
     if ((rc = check_cuda(cudaMalloc(&dz, nz * 2), "cudaMalloc"))) break;
     if ((rc = check_cuda(cudaMalloc(&dp, pbytes), "cudaMalloc"))) break;
     if (wsb > 0 && (rc = check_cuda(cudaMalloc(&dws, wsb), "cudaMalloc"))) break;
+    if (wsb > 0 && (rc = check_cuda(cudaMemset(dws, 0, wsb), "cudaMemset"))) break;
     if ((rc = check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate"))) break;
     if ((rc = check_cuda(cudaMemcpyAsync(dx, xh.data(), nx * 2, cudaMemcpyHostToDevice, st), "H2D"))) break;
     if ((rc = check_cuda(cudaMemcpyAsync(dp, packed.data(), pbytes, cudaMemcpyHostToDevice, st), "H2D"))) break;

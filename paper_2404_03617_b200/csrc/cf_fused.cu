@@ -236,13 +236,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
           uint32_t v[16];
           WL_TMEM_LD16(tmem_lane_addr(tmem, q, pl.t_e + b * r + c0), v);
           tmem_ld_wait();
-          uint32_t o[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float x0 = act<ACT>(__uint_as_float(v[2 * i]) + aj[c0 + 2 * i]);
-            const float x1 = act<ACT>(__uint_as_float(v[2 * i + 1]) + aj[c0 + 2 * i + 1]);
-            o[i] = pack_h2(x0, x1);
-          }
+          uint4 o2[2];
+          o2[0] = bias_act8<ACT>(v, aj + c0);
+          o2[1] = bias_act8<ACT>(v + 8, aj + c0 + 8);
+          const uint32_t* o = reinterpret_cast<const uint32_t*>(o2);
           WL_TMEM_ST8(tmem_lane_addr(tmem, q, pl.t_h + b * pl.h_stride + c0 / 2), o);
         }
         tmem_st_wait();

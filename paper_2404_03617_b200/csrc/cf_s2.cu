@@ -27,8 +27,9 @@ struct Cf2Args {
   int C, K, hid, r, nch;
   int H, W, Ho, Wo, R, tiles_y, Wp;
   int n_ct, n_eh, n_pt, conv_base, x_alloc, x_rows;
-  int o_convw, o_bconv, o_a, o_b, o_u, o_v, w_bytes;  // resident weight blob offsets
-  int s_x, s_xc, s_ah, s_hs, s_aq, s_w, s_bar;
+  int o_convw, o_bconv, o_a, o_b, w_bytes;  // header: conv taps + fp32 vectors
+  int chunk_bytes, u_bytes;                 // chunk j = [U_j (r x C) | V_j (K x r)], 2-slot ring
+  int s_x, s_xc, s_ah, s_hs, s_aq, s_w, s_ring, s_bar;
   int t_c, t_e, t_z, tmem_cols;
   const uint8_t* wpack;
   __half* z;
@@ -44,8 +45,9 @@ __global__ void __launch_bounds__(256, 1)
   __half* s_hs = reinterpret_cast<__half*>(smem + a.s_hs);
   uint8_t* s_aq = smem + a.s_aq;
   uint8_t* s_w = smem + a.s_w;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // [0] load, [1] mma
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 2);
+  uint8_t* s_ring = smem + a.s_ring;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // [0] load, [1] mma, [2..3] chunk slots
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 4);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
   const int q = warp % 4, half = warp / 4;
   const int n = blockIdx.x / a.tiles_y, yo0 = (blockIdx.x % a.tiles_y) * a.R;
@@ -58,8 +60,7 @@ __global__ void __launch_bounds__(256, 1)
     *reinterpret_cast<uint4*>(s_x + ((size_t)pl * a.x_alloc + f) * 16) = make_uint4(0, 0, 0, 0);
   }
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc_n(tbase, a.tmem_cols);
@@ -73,6 +74,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int g = 0; g < planes; ++g)
       tma_load_5d(s_x + (size_t)g * a.x_alloc * 16, &tmap_x, 0, -1, 2 * yo0 - 2, g, n, &bars[0]);
     bulk_g2s(s_w, a.wpack, a.w_bytes, &bars[0]);
+    mbar_arrive_expect_tx(&bars[2], a.chunk_bytes);
+    bulk_g2s(s_ring, a.wpack + a.w_bytes, a.chunk_bytes, &bars[2]);
   }
   mbar_wait(&bars[0], 0);
   uint32_t mma_phase = 0;
@@ -145,9 +148,16 @@ __global__ void __launch_bounds__(256, 1)
   const int MQ = a.n_pt * 128;
   for (int j = 0; j < a.nch; ++j) {
     if (tid == 0) {
+      if (j + 1 < a.nch) {  // prefetch chunk j+1 (its slot's previous chunk finished last iteration)
+        const int sl = (j + 1) & 1;
+        mbar_arrive_expect_tx(&bars[2 + sl], a.chunk_bytes);
+        bulk_g2s(s_ring + sl * a.chunk_bytes, a.wpack + a.w_bytes + (size_t)(j + 1) * a.chunk_bytes, a.chunk_bytes,
+                 &bars[2 + sl]);
+      }
+      mbar_wait(&bars[2 + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t idesc = make_idesc_f16(128, r);
-      const uint32_t ub = smem_u32(s_w + a.o_u) + j * (r * C * 2);
+      const uint32_t ub = smem_u32(s_ring) + (j & 1) * a.chunk_bytes;
       for (int t = 0; t < a.n_eh; ++t)
         for (int kk = 0; kk < C / 16; ++kk) {
           const uint64_t ad = make_sdesc(smem_u32(s_ah) + (kk * 2 * MH + t * 128) * 16, MH * 16, 128);
@@ -197,7 +207,7 @@ __global__ void __launch_bounds__(256, 1)
     if (tid == 0) {
       tc_fence_after();
       const uint32_t idesc = make_idesc_f16(128, K);
-      const uint32_t vb = smem_u32(s_w + a.o_v) + j * (K * r * 2);
+      const uint32_t vb = smem_u32(s_ring) + (j & 1) * a.chunk_bytes + a.u_bytes;
       for (int t = 0; t < a.n_pt; ++t)
         for (int kk = 0; kk < r / 16; ++kk) {
           const uint64_t ad = make_sdesc(smem_u32(s_aq) + (kk * 2 * MQ + t * 128) * 16, MQ * 16, 128);
@@ -265,48 +275,46 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
     a.n_eh = (R * a.W + 127) / 128;
     a.n_pt = (R * a.Wo + 127) / 128;
     if (a.n_eh > 4) continue;
-    // hidden chunk
-    a.r = 0;
-    for (int rr = 128; rr >= 16; rr -= 16) {
+    // hidden chunk: widest that fits TMEM and shared memory
+    bool ok = false;
+    for (int rr = 128; rr >= 16 && !ok; rr -= 16) {
       if (a.hid % rr) continue;
       const int cols = a.n_ct * a.C + a.n_eh * rr + a.n_pt * a.K;
-      if (cols <= 512) {
-        a.r = rr;
-        break;
-      }
+      if (cols > 512) continue;
+      a.r = rr;
+      a.nch = a.hid / a.r;
+      int o = 0;
+      a.o_convw = o;
+      o += (a.C / 16) * 9 * 512;
+      a.o_bconv = o;
+      o = align_up(o + a.C * 4, 16);
+      a.o_a = o;
+      o = align_up(o + a.hid * 4, 16);
+      a.o_b = o;
+      o = align_up(o + a.K * 4, 16);
+      a.w_bytes = align_up(o, 128);
+      a.u_bytes = a.r * a.C * 2;
+      a.chunk_bytes = a.u_bytes + a.K * a.r * 2;
+      int s = 0;
+      a.s_x = s;
+      s = align_up(s + (a.C / 8) * a.x_alloc * 16, 128);
+      a.s_xc = s;
+      s = align_up(s + (2 * R + 1) * a.W * a.C * 2, 128);
+      a.s_ah = s;
+      s = align_up(s + a.n_eh * 128 * a.C * 2, 128);
+      a.s_hs = s;
+      s = align_up(s + R * a.W * a.r * 2, 128);
+      a.s_aq = s;
+      s = align_up(s + a.n_pt * 128 * a.r * 2, 128);
+      a.s_w = s;
+      s = align_up(s + a.w_bytes, 128);
+      a.s_ring = s;
+      s = align_up(s + 2 * a.chunk_bytes, 128);
+      a.s_bar = s;
+      s += 64;
+      ok = s <= kSmemMax2;
     }
-    if (!a.r) continue;
-    a.nch = a.hid / a.r;
-    int o = 0;
-    a.o_convw = o;
-    o += (a.C / 16) * 9 * 512;
-    a.o_bconv = o;
-    o = align_up(o + a.C * 4, 16);
-    a.o_a = o;
-    o = align_up(o + a.hid * 4, 16);
-    a.o_b = o;
-    o = align_up(o + a.K * 4, 16);
-    a.o_u = o;
-    o += a.hid * a.C * 2;
-    a.o_v = o;
-    o += a.K * a.hid * 2;
-    a.w_bytes = align_up(o, 16);
-    int s = 0;
-    a.s_x = s;
-    s = align_up(s + (a.C / 8) * a.x_alloc * 16, 128);
-    a.s_xc = s;
-    s = align_up(s + (2 * R + 1) * a.W * a.C * 2, 128);
-    a.s_ah = s;
-    s = align_up(s + a.n_eh * 128 * a.C * 2, 128);
-    a.s_hs = s;
-    s = align_up(s + R * a.W * a.r * 2, 128);
-    a.s_aq = s;
-    s = align_up(s + a.n_pt * 128 * a.r * 2, 128);
-    a.s_w = s;
-    s = align_up(s + a.w_bytes, 128);
-    a.s_bar = s;
-    s += 64;
-    if (s > kSmemMax2) continue;
+    if (!ok) continue;
     a.tiles_y = (a.Ho + R - 1) / R;
     a.t_c = 0;
     a.t_e = a.n_ct * a.C;
@@ -355,12 +363,12 @@ int64_t cf2_weight_numel(const wl_block_desc& d, int i) {
 int64_t cf2_packed_bytes(const wl_block_desc& d) {
   Cf2Args a;
   cf2_plan(d, a);
-  return a.w_bytes;
+  return a.w_bytes + (int64_t)a.nch * a.chunk_bytes;
 }
 int cf2_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   Cf2Args a;
   cf2_plan(d, a);
-  memset(out, 0, a.w_bytes);
+  memset(out, 0, (size_t)cf2_packed_bytes(d));
   const int C = a.C, hid = a.hid, K = a.K, r = a.r;
   const float *wc = w[0], *bc = w[1], *u = w[2], *av = w[3], *v = w[4], *b = w[5];
   for (int pr = 0; pr < C / 16; ++pr)
@@ -377,10 +385,10 @@ int cf2_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   for (int i = 0; i < hid; ++i) fa[i] = av[i];
   for (int i = 0; i < K; ++i) fbb[i] = b[i];
   for (int j = 0; j < a.nch; ++j) {
-    uint8_t* ub = out + a.o_u + (size_t)j * r * C * 2;
+    uint8_t* ub = out + a.w_bytes + (size_t)j * a.chunk_bytes;
     for (int nn = 0; nn < r; ++nn)
       for (int k = 0; k < C; ++k) put_h(ub, core_off_h(nn, k, r * 16), u[(size_t)k * hid + j * r + nn]);
-    uint8_t* vb = out + a.o_v + (size_t)j * K * r * 2;
+    uint8_t* vb = ub + a.u_bytes;
     for (int nn = 0; nn < K; ++nn)
       for (int k = 0; k < r; ++k) put_h(vb, core_off_h(nn, k, K * 16), v[(size_t)(j * r + k) * K + nn]);
   }

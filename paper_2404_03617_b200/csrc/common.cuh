@@ -18,6 +18,48 @@ __device__ __forceinline__ float act(float v) {
   return v;
 }
 
+// ---- packed-half activations (2 values per instruction; MUFU tanh.approx)
+// silu(x) = x/2 (1 + tanh(x/2)); sigmoid(x) = 1/2 + tanh(x/2)/2;
+// gelu(x) ~= x/2 (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))  (tanh form)
+__device__ __forceinline__ __half2 tanh_h2(__half2 x) {
+  uint32_t r, v = *reinterpret_cast<uint32_t*>(&x);
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(v));
+  return *reinterpret_cast<__half2*>(&r);
+}
+template <int ACT>
+__device__ __forceinline__ __half2 act_h2(__half2 x) {
+  if constexpr (ACT == kRelu) return __hmax2(x, __float2half2_rn(0.f));
+  if constexpr (ACT == kSilu) {
+    const __half2 h = __hmul2(x, __float2half2_rn(0.5f));
+    return __hfma2(h, tanh_h2(h), h);
+  }
+  if constexpr (ACT == kSigmoid) {
+    const __half2 h = __float2half2_rn(0.5f);
+    return __hfma2(h, tanh_h2(__hmul2(x, h)), h);
+  }
+  if constexpr (ACT == kGelu) {
+    const __half2 x2 = __hmul2(x, x);
+    const __half2 p = __hfma2(x2, __float2half2_rn(0.0356774081f), __float2half2_rn(0.7978845608f));
+    const __half2 h = __hmul2(x, __float2half2_rn(0.5f));
+    return __hfma2(h, tanh_h2(__hmul2(x, p)), h);
+  }
+  return x;
+}
+// fp32 accumulators (+ fp32 bias) -> packed-half activation: 8 values -> uint4
+template <int ACT>
+__device__ __forceinline__ uint4 bias_act8(const uint32_t* acc, const float* bias) {
+  uint4 q;
+  uint32_t* o = reinterpret_cast<uint32_t*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __half2 h = __floats2half2_rn(__uint_as_float(acc[2 * i]) + bias[2 * i],
+                                  __uint_as_float(acc[2 * i + 1]) + bias[2 * i + 1]);
+    h = act_h2<ACT>(h);
+    o[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return q;
+}
+
 __device__ __forceinline__ void unpack8(const uint4& q, float* f) {
   const __half2* h = reinterpret_cast<const __half2*>(&q);
 #pragma unroll

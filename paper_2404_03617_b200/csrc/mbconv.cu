@@ -1,23 +1,24 @@
 // mbconv.cu — MBConv + squeeze-excite on sm_100a (core.py:112-122; fused
 // schedule machine.py:649-733; layer-wise numerics machine.py:593-646).
 //
-// Two launches per block; the hidden activation is never materialised at
-// full width in HBM by design — it passes between the launches through the
+// Two launches per block; the expanded activation never reaches HBM by
+// design — the conv output h2 passes between the launches through the
 // 126 MB L2 (the tensor machine's GLOBAL tier, machine.py:667-687):
 //   front : one CTA per (image group, hidden range). Whole image(s) stacked in
-//           a flat padded layout (row width W+1: the left pad column of row
+//           a flat padded layout (row pitch >= W+1: the left pad column of row
 //           y+1 doubles as the right pad of row y), so every 3x3 tap is a
 //           constant shift of the flat index and an M=128 conv tile is 16
 //           consecutive 8-pixel core-matrix rows. Per hidden chunk:
-//             expand  (SS MMA, x smem x U_j)            -> TMEM E
-//             E + b_exp, phi, pads -> 0                 -> smem h1 planes
-//             grouped 3x3 conv (block-diagonal MMAs for T=8, CUDA cores T=1)
-//             + b_conv, phi [-> BlurPool 3x3 stride 2]  -> h2 (fp16, global)
-//             spatial sums of h2 reduced on chip        -> pool (fp32 mean)
-//   back  : one CTA per (128 consecutive output pixels, output-channel range).
-//           SE on CUDA cores: s = relu(pool W_sq + b_sq), e = sigmoid(s W_ex +
-//           b_ex); h2 tiles arrive by TMA, are gated in shared memory, the
-//           projection accumulates in TMEM; z = Z + b_prj (+ x for stride 1).
+//             expand (SS MMA, x smem x U_j)                 -> TMEM E (x2)
+//             E + b_exp, phi (packed half), pads -> 0       -> smem h1 planes
+//             grouped 3x3 conv (block-diagonal MMAs T=8, CUDA cores T=1)
+//             + b_conv, phi [-> BlurPool 3x3 stride 2]      -> smem staging
+//             staging -> h2 (TMA store), column sums -> pool (deterministic)
+//           The last CTA of an image group (threadfence + counter) runs the
+//           squeeze-excite once: gates = sigmoid(relu(pool W_sq + b_sq) W_ex + b_ex).
+//   back  : one CTA per (128 consecutive output pixels, output-channel range):
+//           h2 tiles arrive by TMA, are gated in shared memory (packed half),
+//           the projection accumulates in TMEM; z = Z + b_prj (+ x, stride 1).
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
@@ -27,33 +28,36 @@
 namespace wl {
 
 struct MbFrontArgs {
-  int C, hid, HR, HC, nch;  // nch: chunks per hidden range
+  int C, hid, sq, HR, HC, nch;  // nch: chunks per hidden range
   int T8, stride;
-  int H, W, Wp, imgs;
+  int H, W, Wp, imgs, groups;
   int total_rows, n_et, n_ct, conv_base, flat_h1, x_alloc;  // conv_base = Wp + 1
   int Ho, Wo, ranges;
-  int h1_bytes;
+  int P_out, P_full;       // dense output / full-res pixels per CTA
+  int st_rows, st_stores;  // TMA store box rows, stores per chunk
+  int e_bufs, c_bufs;
+  int h1_bytes, st_bytes, full_bytes;
   int hdr_bytes, chunk_bytes, u_bytes;  // per-range hdr = [b_exp | b_conv | (T1) convw fp32 [9][HR]]
   int o_bconv, o_convw;
-  int s_x, s_h1, s_stage, s_hdr, s_ring, s_pool, s_bar;
+  int o_wsq, o_bsq, o_wex, o_bex, se_bytes;  // SE section (fp32) at the front of the blob
+  int s_x, s_h1, s_st, s_full, s_hdr, s_ring, s_pool, s_bar, smem;
   int ring_stages;
   int t_e, t_c, tmem_cols;
-  const uint8_t* wpack;
-  __half* h2;   // (n, Ho*Wo, hid)
-  float* pool;  // (n, hid) spatial mean
+  const uint8_t* wpack;  // front blob: [SE][range hdrs][chunks]
+  float* pool;           // (n, hid) spatial mean
+  float* gates;          // (n, hid) SE gates
+  int* counters;         // (groups) zero-initialised arrival counters
 };
 
 struct MbBackArgs {
-  int hid, sq, K, KR, HCb, nchb, stride;
-  int P, pix_per_img, rows;  // total pixels, pixels per image, tile rows (128)
-  int kranges;
-  int residual;
-  int o_wsq, o_bsq, o_wex, o_bex, o_bprj, se_bytes;  // SE block in the back blob
-  int vchunk_bytes;
-  int s_a, s_gate, s_se, s_ring, s_bar, a_bytes, ring_stages;
+  int hid, K, KR, HCb, nchb, stride;
+  int P, pix_per_img;
+  int kranges, residual;
+  int vchunk_bytes, o_bprj;
+  int s_a, s_gate, s_ring, s_bar, smem, ring_stages;
   int t_z, tmem_cols;
-  const uint8_t* wpack;  // back blob: [SE fp32 ...][V chunks per (krange, j)]
-  const float* pool;
+  const uint8_t* wpack;  // back blob: [b_prj fp32][V chunks per (krange, j)]
+  const float* gates;
   const __half* x;  // residual (n, H, W, K)
   __half* z;        // (n, Ho, Wo, K)
 };
@@ -63,8 +67,10 @@ constexpr int kThreads = 384;
 struct FrontBars {
   uint64_t hdr_full, x_full;
   uint64_t w_full[4], w_empty[4];
-  uint64_t e_full, h1_full, h1_empty, c_full, c_empty;
+  uint64_t e_full[2], c_full[2], c_empty[2];
+  uint64_t h1_full, h1_empty;
   uint32_t tmem_base;
+  int last;
 };
 struct BackBars {
   uint64_t a_full[2], a_empty[2], a_ready[2];
@@ -80,22 +86,34 @@ __device__ __forceinline__ bool mb_real(int f, int Wp, int W, int H, int total_r
   return col >= 1 && col <= W && row < total_rows - 1 && (row % (H + 1)) != 0;
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-  return v;
-}
-
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__device__ __forceinline__ void tma_store_3d(const void* tmap, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// staging offset (bytes) of 8-channel group g of dense pixel p: stores of
+// st_rows rows, each [HC/8][st_rows][8] (the TMA store box)
+__device__ __forceinline__ int st_off(int p, int g, int st_rows, int groups8) {
+  const int k = p / st_rows, r = p - k * st_rows;
+  return ((k * groups8 + g) * st_rows + r) * 16;
+}
 
 template <int ACT>
 __global__ void __launch_bounds__(mbk::kThreads, 1)
-    mb_front_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ MbFrontArgs a) {
+    mb_front_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_h2,
+                    const __grid_constant__ MbFrontArgs a) {
   using namespace mbk;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* s_x = smem + a.s_x;
   uint8_t* s_h1 = smem + a.s_h1;
-  __half* s_stage = reinterpret_cast<__half*>(smem + a.s_stage);
+  uint8_t* s_st = smem + a.s_st;      // final h2 staging (dense output pixels)
+  uint8_t* s_full = smem + a.s_full;  // stride 2: full-resolution staging
   uint8_t* s_hdr = smem + a.s_hdr;
   uint8_t* s_ring = smem + a.s_ring;
   float* s_pool = reinterpret_cast<float*>(smem + a.s_pool);  // [imgs][HR]
@@ -104,9 +122,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int group = blockIdx.x / a.ranges, range = blockIdx.x % a.ranges;
   const int n0 = group * a.imgs;
   const int h0 = range * a.HR;
-  const int S = a.ring_stages, HC = a.HC, nch = a.nch;
+  const int S = a.ring_stages, HC = a.HC, nch = a.nch, G8 = HC / 8;
   const int img_flat = (a.H + 1) * a.Wp;
-  const int x_valid = a.imgs * img_flat;  // flat positions holding loaded x rows
+  const int x_valid = a.imgs * img_flat;
 
   for (int i = threadIdx.x; i < a.h1_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
@@ -125,11 +143,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_init(&B.w_full[i], 1);
       mbar_init(&B.w_empty[i], 1);
     }
-    mbar_init(&B.e_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.e_full[i], 1);
+      mbar_init(&B.c_full[i], 1);
+      mbar_init(&B.c_empty[i], 128);
+    }
     mbar_init(&B.h1_full, 128);
     mbar_init(&B.h1_empty, a.T8 ? 1 : 128);
-    mbar_init(&B.c_full, 1);
-    mbar_init(&B.c_empty, 128);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -143,14 +163,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (lane == 0) {
       prefetch_tmap(&tmap_x);
       mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
-      bulk_g2s(s_hdr, a.wpack + (size_t)range * a.hdr_bytes, a.hdr_bytes, &B.hdr_full);
+      bulk_g2s(s_hdr, a.wpack + a.se_bytes + (size_t)range * a.hdr_bytes, a.hdr_bytes, &B.hdr_full);
       const int planes = a.C / 8;
-      const int box_bytes = img_flat * 16;
-      mbar_arrive_expect_tx(&B.x_full, box_bytes * planes * a.imgs);
+      mbar_arrive_expect_tx(&B.x_full, img_flat * 16 * planes * a.imgs);
       for (int i = 0; i < a.imgs; ++i)
         for (int g = 0; g < planes; ++g)
           tma_load_5d(s_x + ((size_t)g * a.x_alloc + i * img_flat) * 16, &tmap_x, 0, -1, -1, g, n0 + i, &B.x_full);
-      const uint8_t* chunks = a.wpack + (size_t)a.ranges * a.hdr_bytes;
+      const uint8_t* chunks = a.wpack + a.se_bytes + (size_t)a.ranges * a.hdr_bytes;
       for (int j = 0; j < nch; ++j) {
         const int slot = j % S, use = j / S;
         mbar_wait(&B.w_empty[slot], (use & 1) ^ 1);
@@ -165,35 +184,39 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       const uint32_t idesc_c = make_idesc_f16(128, 16);
       const uint32_t x0 = smem_u32(s_x), h10 = smem_u32(s_h1), ring0 = smem_u32(s_ring);
       mbar_wait(&B.x_full, 0);
-      tc_fence_after();
-      for (int j = 0; j < nch; ++j) {
-        const int slot = j % S;
+      auto issue_expand = [&](int j) {
+        const int slot = j % S, eb = j % a.e_bufs;
         mbar_wait(&B.w_full[slot], (j / S) & 1);
-        if (j > 0) mbar_wait(&B.h1_full, (j - 1) & 1);  // expand epilogue done reading E
         tc_fence_after();
         const uint32_t ub = ring0 + slot * a.chunk_bytes;
         for (int t = 0; t < a.n_et; ++t)
           for (int kk = 0; kk < a.C / 16; ++kk) {
             const uint64_t ad = make_sdesc(x0 + (kk * 2 * a.x_alloc + t * 128) * 16, a.x_alloc * 16, 128);
             const uint64_t bd = make_sdesc(ub + kk * 2 * (HC * 16), HC * 16, 128);
-            mma_ss(tmem + a.t_e + t * HC, ad, bd, idesc_e, kk > 0);
+            mma_ss(tmem + a.t_e + (eb * a.n_et + t) * HC, ad, bd, idesc_e, kk > 0);
           }
-        mma_commit(&B.e_full);
+        mma_commit(&B.e_full[eb]);
+      };
+      issue_expand(0);
+      for (int j = 0; j < nch; ++j) {
+        const int slot = j % S;
+        if (a.e_bufs == 1) mbar_wait(&B.h1_full, j & 1);  // E of chunk j consumed
+        if (j + 1 < nch) issue_expand(j + 1);
         if (a.T8) {
-          mbar_wait(&B.h1_full, j & 1);
-          if (j > 0) mbar_wait(&B.c_empty, (j - 1) & 1);
+          const int cb = j % a.c_bufs;
+          if (a.e_bufs != 1) mbar_wait(&B.h1_full, j & 1);
+          if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t cw = ub + a.u_bytes;
+          const uint32_t cw = ring0 + slot * a.chunk_bytes + a.u_bytes;
           for (int t = 0; t < a.n_ct; ++t)
             for (int pr = 0; pr < HC / 16; ++pr)
               for (int tap = 0; tap < 9; ++tap) {
-                const int dy = tap / 3 - 1, dx = tap % 3 - 1;
-                const int f = a.conv_base + t * 128 + dy * a.Wp + dx;
+                const int f = a.conv_base + t * 128 + (tap / 3 - 1) * a.Wp + (tap % 3 - 1);
                 const uint64_t ad = make_sdesc(h10 + (2 * pr * a.flat_h1 + f) * 16, a.flat_h1 * 16, 128);
                 const uint64_t bd = make_sdesc(cw + (pr * 9 + tap) * 512, 256, 128);
-                mma_ss(tmem + a.t_c + t * HC + 16 * pr, ad, bd, idesc_c, tap > 0);
+                mma_ss(tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr, ad, bd, idesc_c, tap > 0);
               }
-          mma_commit(&B.c_full);
+          mma_commit(&B.c_full[cb]);
           mma_commit(&B.h1_empty);
         }
         mma_commit(&B.w_empty[slot]);
@@ -205,7 +228,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     const float* s_bexp = reinterpret_cast<const float*>(s_hdr);
     mbar_wait(&B.hdr_full, 0);
     for (int j = 0; j < nch; ++j) {
-      mbar_wait(&B.e_full, j & 1);
+      const int eb = j % a.e_bufs;
+      mbar_wait(&B.e_full[eb], (j / a.e_bufs) & 1);
       if (j > 0) mbar_wait(&B.h1_empty, (j - 1) & 1);
       tc_fence_after();
       for (int t = 0; t < a.n_et; ++t) {
@@ -213,14 +237,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const bool real = f < x_valid && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
         for (int c0 = 0; c0 < HC; c0 += 16) {
           uint32_t v[16];
-          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + t * HC + c0), v);
+          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + (eb * a.n_et + t) * HC + c0), v);
           tmem_ld_wait();
-          float fv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) fv[i] = real ? act<ACT>(__uint_as_float(v[i]) + s_bexp[j * HC + c0 + i]) : 0.f;
+          uint4 lo = bias_act8<ACT>(v, s_bexp + j * HC + c0);
+          uint4 hi = bias_act8<ACT>(v + 8, s_bexp + j * HC + c0 + 8);
+          if (!real) lo = hi = make_uint4(0, 0, 0, 0);
           if (f < a.flat_h1) {
-            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + f) * 16) = pack8(fv);
-            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + f) * 16) = pack8(fv + 8);
+            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + f) * 16) = lo;
+            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + f) * 16) = hi;
           }
         }
       }
@@ -229,34 +253,39 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_arrive(&B.h1_full);
     }
   } else if (warp >= 8 && warp < 12) {
-    // ------------- conv epilogue: (Cacc | stencil) + b_conv -> phi -> [blur] -> h2, pool
+    // ------------- conv epilogue -> staging -> h2 (TMA store) + pool
     const int q = warp - 8;
     const int tid = q * 32 + lane;
     const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
     const float* s_cw = reinterpret_cast<const float*>(s_hdr + a.o_convw);  // [9][HR] (T1)
     mbar_wait(&B.hdr_full, 0);
     const int conv_end = (a.total_rows - 1) * a.Wp;
+    uint8_t* dst_stage = a.stride == 1 ? s_st : s_full;
+    const int dst_rows = a.stride == 1 ? a.st_rows : a.P_full;
     for (int j = 0; j < nch; ++j) {
+      const int cb = j % a.c_bufs;
       if (a.T8) {
-        mbar_wait(&B.c_full, j & 1);
+        mbar_wait(&B.c_full[cb], (j / a.c_bufs) & 1);
         tc_fence_after();
       } else {
         mbar_wait(&B.h1_full, j & 1);
       }
+      // staging may still be read by the previous chunk's TMA store
+      if (tid == 0) bulk_wait_read0();
+      named_bar(1, 128);
       for (int t = 0; t < a.n_ct; ++t) {
         const int f = a.conv_base + t * 128 + tid;
         const bool real = f < conv_end && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
         const int row = f / a.Wp, img = row / (a.H + 1);
         const int y = row - img * (a.H + 1) - 1, x = f - row * a.Wp - 1;
+        const int p = (img * a.H + y) * a.W + x;  // dense full-resolution pixel
         for (int c0 = 0; c0 < HC; c0 += 16) {
-          float fv[16];
+          uint32_t v[16];
           if (a.T8) {
-            uint32_t v[16];
-            WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * HC + c0), v);
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + (cb * a.n_ct + t) * HC + c0), v);
             tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) fv[i] = __uint_as_float(v[i]);
           } else {
+            float fv[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) fv[i] = 0.f;
             if (real) {
@@ -265,80 +294,90 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
                 float hv[16];
                 unpack8(*reinterpret_cast<const uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + ff) * 16), hv);
                 unpack8(*reinterpret_cast<const uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + ff) * 16), hv + 8);
+                const float* w = s_cw + tap * a.HR + j * HC + c0;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) fv[i] += hv[i] * s_cw[tap * a.HR + j * HC + c0 + i];
+                for (int i = 0; i < 16; ++i) fv[i] += hv[i] * w[i];
               }
             }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(fv[i]);
           }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) fv[i] = real ? act<ACT>(fv[i] + s_bconv[j * HC + c0 + i]) : 0.f;
-          if (a.stride == 1) {
-            if (real) {
-              __half* dst = a.h2 + ((size_t)(n0 + img) * a.H * a.W + (size_t)y * a.W + x) * a.hid + h0 + j * HC + c0;
-              reinterpret_cast<uint4*>(dst)[0] = pack8(fv);
-              reinterpret_cast<uint4*>(dst)[1] = pack8(fv + 8);
-            }
-            // pool: per-image warp sums of the 16 channels
-            for (int im = 0; im < a.imgs; ++im) {
-              const unsigned m = __ballot_sync(0xffffffffu, real && img == im);
-              if (!m) continue;
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float s = warp_sum((real && img == im) ? fv[i] : 0.f);
-                if (lane == 0) atomicAdd(&s_pool[im * a.HR + j * HC + c0 + i], s);
-              }
-            }
-          } else {
-            // stage the full-resolution activation for the blur
-            if (real) {
-              const size_t o = ((size_t)(img * a.H + y) * a.W + x) * HC + c0;
-              reinterpret_cast<uint4*>(s_stage + o)[0] = pack8(fv);
-              reinterpret_cast<uint4*>(s_stage + o)[1] = pack8(fv + 8);
-            }
+          if (real) {
+            const uint4 lo = bias_act8<ACT>(v, s_bconv + j * HC + c0);
+            const uint4 hi = bias_act8<ACT>(v + 8, s_bconv + j * HC + c0 + 8);
+            *reinterpret_cast<uint4*>(dst_stage + st_off(p, c0 / 8, dst_rows, G8)) = lo;
+            *reinterpret_cast<uint4*>(dst_stage + st_off(p, c0 / 8 + 1, dst_rows, G8)) = hi;
           }
         }
       }
       if (a.T8) {
         tc_fence_before();
-        mbar_arrive(&B.c_empty);
+        mbar_arrive(&B.c_empty[cb]);
       } else {
         mbar_arrive(&B.h1_empty);
       }
+      named_bar(1, 128);
       if (a.stride == 2) {
-        named_bar(1, 128);
         // BlurPool Triangle-3 x Triangle-3 / 16, stride 2, reflect pad (-1 -> 1)
-        const int npix = a.imgs * a.Ho * a.Wo;
-        for (int pidx = tid; pidx < npix; pidx += 128) {
-          const int im = pidx / (a.Ho * a.Wo), rem = pidx % (a.Ho * a.Wo);
-          const int yo = rem / a.Wo, xo = rem % a.Wo;
-          int ys[3] = {2 * yo - 1, 2 * yo, 2 * yo + 1}, xs[3] = {2 * xo - 1, 2 * xo, 2 * xo + 1};
-          if (ys[0] < 0) ys[0] = 1;
-          if (xs[0] < 0) xs[0] = 1;
-          const float wt[3] = {0.25f, 0.5f, 0.25f};
-          for (int c0 = 0; c0 < HC; c0 += 8) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int dy = 0; dy < 3; ++dy)
-              for (int dx = 0; dx < 3; ++dx) {
-                float hv[8];
-                unpack8(*reinterpret_cast<const uint4*>(s_stage + ((size_t)(im * a.H + ys[dy]) * a.W + xs[dx]) * HC + c0),
-                        hv);
-                const float w = wt[dy] * wt[dx];
+        const int nq = a.P_out * G8;
+        for (int i = tid; i < nq; i += 128) {
+          const int g = i / a.P_out, qp = i - g * a.P_out;
+          const int im = qp / (a.Ho * a.Wo), rem = qp - im * (a.Ho * a.Wo);
+          const int yo = rem / a.Wo, xo = rem - yo * a.Wo;
+          const int ys[3] = {2 * yo - 1 < 0 ? 1 : 2 * yo - 1, 2 * yo, 2 * yo + 1};
+          const int xs[3] = {2 * xo - 1 < 0 ? 1 : 2 * xo - 1, 2 * xo, 2 * xo + 1};
+          float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] += w * hv[i];
-              }
-            __half* dst = a.h2 + ((size_t)(n0 + im) * a.Ho * a.Wo + rem) * a.hid + h0 + j * HC + c0;
-            *reinterpret_cast<uint4*>(dst) = pack8(acc);
-            // pool on the fp16-rounded values the projection will consume
-            float rv[8];
-            unpack8(pack8(acc), rv);
+          for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) atomicAdd(&s_pool[im * a.HR + j * HC + c0 + i], rv[i]);
-          }
+            for (int dx = 0; dx < 3; ++dx) {
+              float hv[8];
+              const int pf = (im * a.H + ys[dy]) * a.W + xs[dx];
+              unpack8(*reinterpret_cast<const uint4*>(s_full + st_off(pf, g, a.P_full, G8)), hv);
+              const float w = (dy == 1 ? 0.5f : 0.25f) * (dx == 1 ? 0.5f : 0.25f);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) acc[k] += w * hv[k];
+            }
+          *reinterpret_cast<uint4*>(s_st + st_off(qp, g, a.st_rows, G8)) = pack8(acc);
         }
         named_bar(1, 128);
       }
+      // h2 chunk -> global (TMA store of the dense staging)
+      fence_async_smem();
+      named_bar(1, 128);
+      if (tid == 0) {
+        for (int k = 0; k < a.st_stores; ++k)
+          tma_store_3d(&tmap_h2, s_st + (size_t)k * G8 * a.st_rows * 16, 0, group * a.P_out + k * a.st_rows,
+                       (h0 + j * HC) / 8);
+        bulk_commit();
+      }
+      // pool: deterministic column sums of the staged (fp16) h2 values.
+      // warp q sums channel groups g = q, q+4, ...; lane = (pixel offset i, word w)
+      const int pix_img = a.Ho * a.Wo;
+      for (int g = q; g < G8; g += 4) {
+        const int i = lane >> 2, w = lane & 3;
+        for (int im = 0; im < a.imgs; ++im) {
+          float s0 = 0.f, s1 = 0.f;
+          for (int p = im * pix_img + i; p < (im + 1) * pix_img; p += 8) {
+            const uint32_t hv = *reinterpret_cast<const uint32_t*>(s_st + st_off(p, g, a.st_rows, G8) + w * 4);
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&hv));
+            s0 += f2.x;
+            s1 += f2.y;
+          }
+#pragma unroll
+          for (int m = 4; m < 32; m <<= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, m);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, m);
+          }
+          if (i == 0) {
+            s_pool[im * a.HR + j * HC + g * 8 + w * 2] += s0;
+            s_pool[im * a.HR + j * HC + g * 8 + w * 2 + 1] += s1;
+          }
+        }
+      }
     }
     named_bar(1, 128);
+    if (tid == 0) bulk_wait0();
     const float inv = 1.f / (float)(a.Ho * a.Wo);
     for (int i = tid; i < a.imgs * a.HR; i += 128) {
       const int im = i / a.HR, c = i % a.HR;
@@ -346,7 +385,65 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     }
   }
 
+  // ---------------- squeeze-excite, once per image group (last CTA to arrive)
+  __threadfence();  // publish this CTA's pool slice before arriving
   tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(&a.counters[group], 1);
+    B.last = (old == a.ranges - 1);
+  }
+  __syncthreads();
+  if (B.last) {
+    __threadfence();
+    const float* wsq = reinterpret_cast<const float*>(a.wpack + a.o_wsq);  // [hid][sq]
+    const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
+    const float* wex = reinterpret_cast<const float*>(a.wpack + a.o_wex);  // [sq][hid]
+    const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_bex);
+    float* s_vec = reinterpret_cast<float*>(s_h1);  // scratch: pool[hid], partial[parts*sq], s[sq]
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int parts = nt / a.sq;
+    for (int im = 0; im < a.imgs; ++im) {
+      const float* pool = a.pool + (size_t)(n0 + im) * a.hid;
+      for (int i = tid; i < a.hid; i += nt) s_vec[i] = __ldcg(pool + i);
+      __syncthreads();
+      float* part = s_vec + a.hid;
+      if (tid < parts * a.sq) {
+        const int jj = tid % a.sq, pt = tid / a.sq;
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+        int i = pt;
+        for (; i + 3 * parts < a.hid; i += 4 * parts) {
+          acc0 += s_vec[i] * wsq[(size_t)i * a.sq + jj];
+          acc1 += s_vec[i + parts] * wsq[(size_t)(i + parts) * a.sq + jj];
+          acc2 += s_vec[i + 2 * parts] * wsq[(size_t)(i + 2 * parts) * a.sq + jj];
+          acc3 += s_vec[i + 3 * parts] * wsq[(size_t)(i + 3 * parts) * a.sq + jj];
+        }
+        for (; i < a.hid; i += parts) acc0 += s_vec[i] * wsq[(size_t)i * a.sq + jj];
+        part[tid] = (acc0 + acc1) + (acc2 + acc3);
+      }
+      __syncthreads();
+      float* sv = part + parts * a.sq;
+      if (tid < a.sq) {
+        float acc = bsq[tid];
+        for (int pt = 0; pt < parts; ++pt) acc += part[pt * a.sq + tid];
+        sv[tid] = fmaxf(acc, 0.f);
+      }
+      __syncthreads();
+      for (int i = tid; i < a.hid; i += nt) {
+        float acc0 = bex[i], acc1 = 0.f;
+        int jj = 0;
+        for (; jj + 1 < a.sq; jj += 2) {
+          acc0 += sv[jj] * wex[(size_t)jj * a.hid + i];
+          acc1 += sv[jj + 1] * wex[(size_t)(jj + 1) * a.hid + i];
+        }
+        if (jj < a.sq) acc0 += sv[jj] * wex[(size_t)jj * a.hid + i];
+        a.gates[(size_t)(n0 + im) * a.hid + i] = __fdividef(1.f, 1.f + __expf(-(acc0 + acc1)));
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.counters[group] = 0;  // self-cleaning for the next launch
+  }
   __syncthreads();
   if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
 }
@@ -354,15 +451,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
 // ----------------------------------------------------------------- back
 // CTA: 128 consecutive output pixels (any images) x output channels
 // [k0, k0 + KR). Threads: w0 producer, w1 MMA, w2 alloc, w3 idle, w4-7
-// SE + gating + epilogue.
-template <int dummy>
+// gating + epilogue.
 __global__ void __launch_bounds__(256, 1)
     mb_back_kernel(const __grid_constant__ CUtensorMap tmap_h2, const __grid_constant__ MbBackArgs a) {
   using namespace mbk;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* s_a = smem + a.s_a;          // 2 x [HCb/8][128][8] fp16
+  uint8_t* s_a = smem + a.s_a;                                // 2 x [HCb/8][128][8] fp16
   float* s_gate = reinterpret_cast<float*>(smem + a.s_gate);  // [4 imgs][hid]
-  float* s_se = reinterpret_cast<float*>(smem + a.s_se);      // [4][sq] scratch
   uint8_t* s_ring = smem + a.s_ring;
   BackBars& B = *reinterpret_cast<BackBars*>(smem + a.s_bar);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -397,12 +492,11 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     if (lane == 0) {
       prefetch_tmap(&tmap_h2);
-      const uint8_t* vchunks = a.wpack + a.se_bytes;
+      const uint8_t* vchunks = a.wpack + a.o_bprj + align_up(a.K * 4, 128);
       for (int j = 0; j < nch; ++j) {
         const int ab = j & 1;
         mbar_wait(&B.a_empty[ab], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&B.a_full[ab], a_stage_bytes);
-        // 3-D view of h2: (8, P, hid/8) -> smem [HCb/8][128][8]
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
             "%4}], [%5];" ::"r"(smem_u32(s_a + ab * a_stage_bytes)),
@@ -436,36 +530,8 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int q = warp - 4, tid = q * 32 + lane;
-    const float* wsq = reinterpret_cast<const float*>(a.wpack + a.o_wsq);  // [hid][sq]
-    const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
-    const float* wex = reinterpret_cast<const float*>(a.wpack + a.o_wex);  // [sq][hid]
-    const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_bex);
-    // ---- squeeze-excite for every image the tile touches
-    for (int im = 0; im < nimg; ++im) {
-      const float* pool = a.pool + (size_t)(img_first + im) * a.hid;
-      // s[j] = relu(sum_i pool[i] wsq[i][j] + bsq[j]); 128 threads: j = tid % sq, part = tid / sq
-      const int parts = 128 / a.sq;
-      if (tid < parts * a.sq) {
-        const int jj = tid % a.sq, part = tid / a.sq;
-        float acc = 0.f;
-        for (int i = part; i < a.hid; i += parts) acc += pool[i] * wsq[(size_t)i * a.sq + jj];
-        s_se[tid] = acc;
-      }
-      named_bar(1, 128);
-      if (tid < a.sq) {
-        float acc = bsq[tid];
-        for (int p = 0; p < parts; ++p) acc += s_se[p * a.sq + tid];
-        s_se[128 + tid] = fmaxf(acc, 0.f);
-      }
-      named_bar(1, 128);
-      for (int i = tid; i < a.hid; i += 128) {
-        float acc = bex[i];
-        for (int jj = 0; jj < a.sq; ++jj) acc += s_se[128 + jj] * wex[(size_t)jj * a.hid + i];
-        s_gate[im * a.hid + i] = __fdividef(1.f, 1.f + __expf(-acc));
-      }
-      named_bar(1, 128);
-    }
-    // ---- gate each h2 chunk in shared memory (row = pixel = TMEM lane)
+    for (int i = tid; i < nimg * a.hid; i += 128) s_gate[i] = a.gates[(size_t)img_first * a.hid + i];
+    named_bar(1, 128);
     const int p = p0 + tid;
     const int im = min(p, a.P - 1) / a.pix_per_img - img_first;
     for (int j = 0; j < nch; ++j) {
@@ -473,13 +539,14 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&B.a_full[ab], (j >> 1) & 1);
       uint8_t* base = s_a + ab * a_stage_bytes;
       const float* g = s_gate + im * a.hid + j * HCb;
+#pragma unroll 2
       for (int c8 = 0; c8 < HCb / 8; ++c8) {
         uint4* ptr = reinterpret_cast<uint4*>(base + (c8 * 128 + tid) * 16);
-        float f[8];
-        unpack8(*ptr, f);
+        uint4 v = *ptr;
+        __half2* h = reinterpret_cast<__half2*>(&v);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] *= g[c8 * 8 + i];
-        *ptr = pack8(f);
+        for (int i = 0; i < 4; ++i) h[i] = __hmul2(h[i], __floats2half2_rn(g[c8 * 8 + 2 * i], g[c8 * 8 + 2 * i + 1]));
+        *ptr = v;
       }
       fence_async_smem();
       mbar_arrive(&B.a_ready[ab]);
@@ -526,12 +593,13 @@ namespace wl {
 namespace {
 
 constexpr int kSmemMaxMb = 232448;
+constexpr int64_t kCounterBytes = 4096;  // workspace header: per-group arrival counters
 
 struct MbPlanH {
   MbFrontArgs f;
   MbBackArgs b;
   int64_t front_bytes, back_bytes;
-  int64_t h2_bytes, pool_bytes;
+  int64_t h2_bytes, pool_bytes, gate_bytes;
 };
 
 bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
@@ -542,13 +610,13 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   if (C % 16 || hid % 16 || K % 16) return false;
   f.C = C;
   f.hid = hid;
+  f.sq = d.se_sq;
   f.T8 = d.group_width == 8;
   f.stride = d.stride;
   f.H = d.h;
   f.W = d.w;
   f.imgs = (d.h * d.w <= 64 && d.n % 2 == 0) ? 2 : 1;
-  // row pitch: >= W + 1, and each stacked image must start 128-byte aligned (TMA)
-  f.Wp = d.w + 1;
+  f.Wp = d.w + 1;  // stacked images must start 128-byte aligned (TMA)
   while (f.imgs > 1 && ((d.h + 1) * f.Wp) % 8) ++f.Wp;
   f.Ho = d.h / d.stride;
   f.Wo = d.w / d.stride;
@@ -560,23 +628,30 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   const int conv_end = (f.total_rows - 1) * f.Wp;
   f.n_ct = (conv_end - f.conv_base + 127) / 128;
   f.flat_h1 = align_up(f.conv_base + f.n_ct * 128 + f.Wp + 2, 8);
-  const int groups = d.n / f.imgs;
-  // hidden ranges: enough CTAs to cover the SMs
+  f.groups = d.n / f.imgs;
+  f.P_out = f.imgs * f.Ho * f.Wo;
+  f.P_full = f.imgs * f.H * f.W;
+  f.st_stores = (f.P_out + 255) / 256;
+  while (f.P_out % f.st_stores) ++f.st_stores;
+  f.st_rows = f.P_out / f.st_stores;
+  if (f.groups > (int)(kCounterBytes / 4)) return false;
+  if (f.sq < 1 || f.sq > 128) return false;
   f.ranges = 1;
-  while (groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
+  while (f.groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
   f.HR = hid / f.ranges;
-  // hidden chunk: largest multiple of 16 dividing HR that fits TMEM and smem
-  const int tiles = f.T8 ? f.n_et + f.n_ct : f.n_et;
   f.HC = 0;
+  const int x_bytes = (C / 8) * f.x_alloc * 16;
+  const int se_scratch = align_up((hid + 384 + f.sq) * 4, 16);
   for (int hc = 128; hc >= 16; hc -= 16) {
-    if (f.HR % hc || tiles * hc > 512) continue;
-    // smem estimate
-    const int x_bytes = (C / 8) * f.x_alloc * 16;
-    const int h1_bytes = (hc / 8) * f.flat_h1 * 16;
-    const int stage = f.stride == 2 ? f.imgs * f.H * f.W * hc * 2 : 0;
+    if (f.HR % hc) continue;
+    const int tiles1 = f.T8 ? f.n_et + f.n_ct : f.n_et;
+    if (tiles1 * hc > 512) continue;
+    const int h1_bytes = std::max((hc / 8) * f.flat_h1 * 16, se_scratch);
+    const int st = f.P_out * hc * 2;
+    const int full = f.stride == 2 ? f.P_full * hc * 2 : 0;
     const int hdr = align_up(f.HR * 4, 16) * 2 + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
     const int chunk = hc * C * 2 + (f.T8 ? (hc / 16) * 9 * 512 : 0);
-    const int total = x_bytes + h1_bytes + stage + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048;
+    const int total = x_bytes + h1_bytes + st + full + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048;
     if (total <= kSmemMaxMb) {
       f.HC = hc;
       break;
@@ -584,20 +659,50 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   }
   if (!f.HC) return false;
   f.nch = f.HR / f.HC;
-  f.h1_bytes = (f.HC / 8) * f.flat_h1 * 16;
+  // double-buffer the expand / conv accumulators when TMEM allows
+  f.e_bufs = 1;
+  f.c_bufs = 1;
+  auto cols = [&]() { return (f.e_bufs * f.n_et + (f.T8 ? f.c_bufs * f.n_ct : 0)) * f.HC; };
+  if (f.nch > 1 && f.T8) {  // T=1: the MMA warp cannot observe E consumption early
+    f.e_bufs = 2;
+    if (cols() > 512) f.e_bufs = 1;
+    if (f.T8) {
+      f.c_bufs = 2;
+      if (cols() > 512) f.c_bufs = 1;
+    }
+  }
+  f.t_e = 0;
+  f.t_c = f.e_bufs * f.n_et * f.HC;
+  f.tmem_cols = 32;
+  while (f.tmem_cols < cols()) f.tmem_cols *= 2;
+  f.h1_bytes = std::max((f.HC / 8) * f.flat_h1 * 16, se_scratch);
+  f.st_bytes = f.P_out * f.HC * 2;
+  f.full_bytes = f.stride == 2 ? f.P_full * f.HC * 2 : 0;
   f.o_bconv = align_up(f.HR * 4, 16);
   f.o_convw = f.o_bconv + align_up(f.HR * 4, 16);
   f.hdr_bytes = f.o_convw + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
   f.u_bytes = f.HC * C * 2;
   f.chunk_bytes = f.u_bytes + (f.T8 ? (f.HC / 16) * 9 * 512 : 0);
   f.ring_stages = 2;
+  int so = 0;  // SE section (fp32) at the start of the front blob
+  f.o_wsq = so;
+  so = align_up(so + hid * f.sq * 4, 16);
+  f.o_bsq = so;
+  so = align_up(so + f.sq * 4, 16);
+  f.o_wex = so;
+  so = align_up(so + f.sq * hid * 4, 16);
+  f.o_bex = so;
+  so = align_up(so + hid * 4, 16);
+  f.se_bytes = align_up(so, 128);
   int o = 0;
   f.s_x = o;
-  o = align_up(o + (C / 8) * f.x_alloc * 16, 128);
+  o = align_up(o + x_bytes, 128);
   f.s_h1 = o;
   o = align_up(o + f.h1_bytes, 128);
-  f.s_stage = o;
-  o = align_up(o + (f.stride == 2 ? f.imgs * f.H * f.W * f.HC * 2 : 0), 128);
+  f.s_st = o;
+  o = align_up(o + f.st_bytes, 128);
+  f.s_full = o;
+  o = align_up(o + f.full_bytes, 128);
   f.s_hdr = o;
   o = align_up(o + f.hdr_bytes, 128);
   f.s_ring = o;
@@ -606,17 +711,12 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   o = align_up(o + f.imgs * f.HR * 4, 128);
   f.s_bar = o;
   o += 512;
+  f.smem = o;
   if (o > kSmemMaxMb) return false;
-  f.t_e = 0;
-  f.t_c = f.n_et * f.HC;
-  const int cols = tiles * f.HC;
-  f.tmem_cols = 32;
-  while (f.tmem_cols < cols) f.tmem_cols *= 2;
-  P.front_bytes = (int64_t)f.ranges * f.hdr_bytes + (int64_t)f.ranges * f.nch * f.chunk_bytes;
+  P.front_bytes = f.se_bytes + (int64_t)f.ranges * f.hdr_bytes + (int64_t)f.ranges * f.nch * f.chunk_bytes;
 
   // ---- back
   b.hid = hid;
-  b.sq = d.se_sq;
   b.K = K;
   b.stride = d.stride;
   b.P = d.n * f.Ho * f.Wo;
@@ -629,19 +729,7 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   b.kranges = K / b.KR;
   b.HCb = hid % 64 == 0 ? 64 : (hid % 32 == 0 ? 32 : 16);
   b.nchb = hid / b.HCb;
-  if (b.sq < 1 || b.sq > 128) return false;
-  int so = 0;
-  b.o_wsq = so;
-  so = align_up(so + hid * b.sq * 4, 16);
-  b.o_bsq = so;
-  so = align_up(so + b.sq * 4, 16);
-  b.o_wex = so;
-  so = align_up(so + b.sq * hid * 4, 16);
-  b.o_bex = so;
-  so = align_up(so + hid * 4, 16);
-  b.o_bprj = so;
-  so = align_up(so + K * 4, 16);
-  b.se_bytes = so;
+  b.o_bprj = 0;
   b.vchunk_bytes = b.KR * b.HCb * 2;
   b.ring_stages = 3;
   o = 0;
@@ -649,25 +737,23 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   o += 2 * 128 * b.HCb * 2;
   b.s_gate = o;
   o = align_up(o + 4 * hid * 4, 128);
-  b.s_se = o;
-  o = align_up(o + (128 + 128) * 4, 128);
   b.s_ring = o;
   o = align_up(o + b.ring_stages * b.vchunk_bytes, 128);
   b.s_bar = o;
   o += 512;
-  b.a_bytes = o;
+  b.smem = o;
   if (o > kSmemMaxMb) return false;
   b.t_z = 0;
   b.tmem_cols = 32;
   while (b.tmem_cols < b.KR) b.tmem_cols *= 2;
-  P.back_bytes = (int64_t)b.se_bytes + (int64_t)b.kranges * b.nchb * b.vchunk_bytes;
+  P.back_bytes = align_up(K * 4, 128) + (int64_t)b.kranges * b.nchb * b.vchunk_bytes;
   P.h2_bytes = (int64_t)d.n * f.Ho * f.Wo * hid * 2;
   P.pool_bytes = (int64_t)d.n * hid * 4;
+  P.gate_bytes = (int64_t)d.n * hid * 4;
   return true;
 }
 
-using FrontK = void (*)(const CUtensorMap, const MbFrontArgs);
-using BackK = void (*)(const CUtensorMap, const MbBackArgs);
+using FrontK = void (*)(const CUtensorMap, const CUtensorMap, const MbFrontArgs);
 
 FrontK front_kernel(int act) {
   switch (act) {
@@ -702,16 +788,16 @@ int mb_weight_count(const wl_block_desc&) { return 10; }
 int64_t mb_weight_numel(const wl_block_desc& d, int i) {
   const int64_t c = d.c, hid = (int64_t)d.expansion * d.c, sq = d.se_sq, k = d.k;
   switch (i) {
-    case 0: return c * hid;                      // w_exp (C, hid)
-    case 1: return hid;                          // b_exp
-    case 2: return hid * 9 * d.group_width;      // w_conv (hid, 3, 3, T)
-    case 3: return hid;                          // b_conv
-    case 4: return hid * sq;                     // w_sq (hid, sq)
-    case 5: return sq;                           // b_sq
-    case 6: return sq * hid;                     // w_ex (sq, hid)
-    case 7: return hid;                          // b_ex
-    case 8: return hid * k;                      // w_prj (hid, K)
-    case 9: return k;                            // b_prj
+    case 0: return c * hid;                  // w_exp (C, hid)
+    case 1: return hid;                      // b_exp
+    case 2: return hid * 9 * d.group_width;  // w_conv (hid, 3, 3, T)
+    case 3: return hid;                      // b_conv
+    case 4: return hid * sq;                 // w_sq (hid, sq)
+    case 5: return sq;                       // b_sq
+    case 6: return sq * hid;                 // w_ex (sq, hid)
+    case 7: return hid;                      // b_ex
+    case 8: return hid * k;                  // w_prj (hid, K)
+    case 9: return k;                        // b_prj
   }
   return set_error(WL_EINVAL, "weight index %d out of range", i);
 }
@@ -722,10 +808,11 @@ int64_t mb_packed_bytes(const wl_block_desc& d) {
   return P.front_bytes + P.back_bytes;
 }
 
+// workspace: [counters 4 KiB][h2][pool][gates]; zero it once before first use
 int64_t mb_workspace(const wl_block_desc& d) {
   MbPlanH P;
   mb_plan(d, P);
-  return align_up((int)0, 1) + ((P.h2_bytes + 255) / 256) * 256 + P.pool_bytes;
+  return kCounterBytes + ((P.h2_bytes + 255) / 256) * 256 + P.pool_bytes + P.gate_bytes;
 }
 
 int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
@@ -736,8 +823,12 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   memset(out, 0, (size_t)(P.front_bytes + P.back_bytes));
   const int C = d.c, hid = f.hid, T = d.group_width, K = d.k, sq = d.se_sq;
   const float *wexp = w[0], *bexp = w[1], *wconv = w[2], *bconv = w[3];
+  memcpy(out + f.o_wsq, w[4], sizeof(float) * hid * sq);
+  memcpy(out + f.o_bsq, w[5], sizeof(float) * sq);
+  memcpy(out + f.o_wex, w[6], sizeof(float) * sq * hid);
+  memcpy(out + f.o_bex, w[7], sizeof(float) * hid);
   for (int r = 0; r < f.ranges; ++r) {
-    uint8_t* hdr = out + (size_t)r * f.hdr_bytes;
+    uint8_t* hdr = out + f.se_bytes + (size_t)r * f.hdr_bytes;
     float* fb = reinterpret_cast<float*>(hdr);
     float* fc = reinterpret_cast<float*>(hdr + f.o_bconv);
     float* fw = reinterpret_cast<float*>(hdr + f.o_convw);
@@ -749,7 +840,7 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
         for (int t = 0; t < 9; ++t) fw[t * f.HR + i] = wconv[(size_t)h * 9 + t];
     }
     for (int j = 0; j < f.nch; ++j) {
-      uint8_t* ch = out + (size_t)f.ranges * f.hdr_bytes + (size_t)(r * f.nch + j) * f.chunk_bytes;
+      uint8_t* ch = out + f.se_bytes + (size_t)f.ranges * f.hdr_bytes + (size_t)(r * f.nch + j) * f.chunk_bytes;
       const int hb = r * f.HR + j * f.HC;
       for (int n = 0; n < f.HC; ++n)
         for (int k = 0; k < C; ++k) put_h(ch, core_off_h(n, k, f.HC * 16), wexp[(size_t)k * hid + hb + n]);
@@ -767,20 +858,12 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
     }
   }
   uint8_t* bk = out + P.front_bytes;
-  float* fsq = reinterpret_cast<float*>(bk + b.o_wsq);
-  float* fbsq = reinterpret_cast<float*>(bk + b.o_bsq);
-  float* fex = reinterpret_cast<float*>(bk + b.o_wex);
-  float* fbex = reinterpret_cast<float*>(bk + b.o_bex);
-  float* fbp = reinterpret_cast<float*>(bk + b.o_bprj);
-  memcpy(fsq, w[4], sizeof(float) * hid * sq);
-  memcpy(fbsq, w[5], sizeof(float) * sq);
-  memcpy(fex, w[6], sizeof(float) * sq * hid);
-  memcpy(fbex, w[7], sizeof(float) * hid);
-  memcpy(fbp, w[9], sizeof(float) * K);
+  memcpy(bk + b.o_bprj, w[9], sizeof(float) * K);
   const float* wprj = w[8];
+  uint8_t* vbase = bk + align_up(K * 4, 128);
   for (int kr = 0; kr < b.kranges; ++kr)
     for (int j = 0; j < b.nchb; ++j) {
-      uint8_t* vc = bk + b.se_bytes + (size_t)(kr * b.nchb + j) * b.vchunk_bytes;
+      uint8_t* vc = vbase + (size_t)(kr * b.nchb + j) * b.vchunk_bytes;
       for (int n = 0; n < b.KR; ++n)
         for (int k = 0; k < b.HCb; ++k)
           put_h(vc, core_off_h(n, k, b.KR * 16), wprj[(size_t)(j * b.HCb + k) * K + kr * b.KR + n]);
@@ -793,34 +876,36 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
   mb_plan(d, P);
   MbFrontArgs f = P.f;
   MbBackArgs b = P.b;
-  __half* h2 = reinterpret_cast<__half*>(ws);
-  float* pool = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((P.h2_bytes + 255) / 256) * 256);
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  __half* h2 = reinterpret_cast<__half*>(wsb + kCounterBytes);
+  float* pool = reinterpret_cast<float*>(wsb + kCounterBytes + ((P.h2_bytes + 255) / 256) * 256);
   f.wpack = reinterpret_cast<const uint8_t*>(packed);
-  f.h2 = h2;
   f.pool = pool;
-  CUtensorMap tx;
+  f.gates = pool + (size_t)d.n * f.hid;
+  f.counters = reinterpret_cast<int*>(wsb);
+  CUtensorMap tx, th_store, th_load;
   {
     const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)(d.c / 8), (uint64_t)d.n};
     const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, 16, (uint64_t)d.h * d.w * d.c * 2};
     const uint32_t box[5] = {8, (uint32_t)f.Wp, (uint32_t)(f.H + 1), 1, 1};
     if (int e = encode_tmap(&tx, x, 5, dims, strides, box)) return e;
   }
-  const int groups = d.n / f.imgs;
-  front_kernel(d.act)<<<groups * f.ranges, mbk::kThreads, f.s_bar + 512, st>>>(tx, f);
-  if (int e = check_cuda(cudaGetLastError(), "mb_front launch")) return e;
-  CUtensorMap th;
   {
-    const uint64_t dims[3] = {8, (uint64_t)b.P, (uint64_t)(b.hid / 8)};
-    const uint64_t strides[2] = {(uint64_t)b.hid * 2, 16};
-    const uint32_t box[3] = {8, 128, (uint32_t)(b.HCb / 8)};
-    if (int e = encode_tmap(&th, h2, 3, dims, strides, box)) return e;
+    const uint64_t dims[3] = {8, (uint64_t)b.P, (uint64_t)(f.hid / 8)};
+    const uint64_t strides[2] = {(uint64_t)f.hid * 2, 16};
+    const uint32_t box_s[3] = {8, (uint32_t)f.st_rows, (uint32_t)(f.HC / 8)};
+    if (int e = encode_tmap(&th_store, h2, 3, dims, strides, box_s)) return e;
+    const uint32_t box_l[3] = {8, 128, (uint32_t)(b.HCb / 8)};
+    if (int e = encode_tmap(&th_load, h2, 3, dims, strides, box_l)) return e;
   }
+  front_kernel(d.act)<<<f.groups * f.ranges, mbk::kThreads, f.smem, st>>>(tx, th_store, f);
+  if (int e = check_cuda(cudaGetLastError(), "mb_front launch")) return e;
   b.wpack = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
-  b.pool = pool;
+  b.gates = f.gates;
   b.x = reinterpret_cast<const __half*>(x);
   b.z = reinterpret_cast<__half*>(z);
   const int ntiles = (b.P + 127) / 128;
-  mb_back_kernel<0><<<ntiles * b.kranges, 256, b.a_bytes, st>>>(th, b);
+  mb_back_kernel<<<ntiles * b.kranges, 256, b.smem, st>>>(th_load, b);
   return check_cuda(cudaGetLastError(), "mb_back launch");
 }
 
@@ -829,7 +914,7 @@ int mb_init() {
     if (int e = check_cuda(cudaFuncSetAttribute(front_kernel(a), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
                            "cudaFuncSetAttribute(mb_front)"))
       return e;
-  return check_cuda(cudaFuncSetAttribute(mb_back_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
+  return check_cuda(cudaFuncSetAttribute(mb_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
                     "cudaFuncSetAttribute(mb_back)");
 }
 

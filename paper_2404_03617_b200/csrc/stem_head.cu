@@ -500,7 +500,8 @@ int head_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
     }
   return WL_OK;
 }
-int64_t head_ws(const wl_block_desc& d) { return align_up(d.n * d.embed * 2, 256); }
+// workspace: [4 KiB reserved counter header shared by all families][pooled embedding]
+int64_t head_ws(const wl_block_desc& d) { return 4096 + align_up(d.n * d.embed * 2, 256); }
 int head_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
   HeadPlan P;
   head_plan(d, P);
@@ -517,10 +518,10 @@ int head_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void
     const uint64_t dims[3] = {8, (uint64_t)d.n, (uint64_t)(h.E / 8)};
     const uint64_t strides[2] = {(uint64_t)h.E * 2, 16};
     const uint32_t box[3] = {8, 128, 8};
-    if (int e = encode_tmap(&tf, ws, 3, dims, strides, box)) return e;
+    if (int e = encode_tmap(&tf, reinterpret_cast<uint8_t*>(ws) + 4096, 3, dims, strides, box)) return e;
   }
   h.w1 = reinterpret_cast<const uint8_t*>(p);
-  h.feat = reinterpret_cast<__half*>(ws);
+  h.feat = reinterpret_cast<__half*>(reinterpret_cast<uint8_t*>(ws) + 4096);
   const int groups = (d.n + h.imgs - 1) / h.imgs;
   head_k(d.act)<<<groups, 256, h.s_bar + 64, st>>>(tx, h);
   if (int e = check_cuda(cudaGetLastError(), "head_pool launch")) return e;

@@ -64,7 +64,7 @@ class FusedNetwork:
             out = torch.empty(mod.out_shape, dtype=torch.float16, device=self.device)
             self.units.append(Unit(inst.label, inst.block, mod, out))
         # one workspace shared by every unit (launches are stream-ordered)
-        self.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device)
         for u in self.units:
             u.module.workspace = self.workspace
         self.graph: torch.cuda.CUDAGraph | None = None
