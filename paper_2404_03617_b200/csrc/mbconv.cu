@@ -40,7 +40,7 @@ struct MbFrontArgs {
   int hdr_bytes, chunk_bytes, u_bytes;  // per-range hdr = [b_exp | b_conv | (T1) convw fp32 [9][HR]]
   int o_bconv, o_convw;
   int o_wsq, o_bsq, o_wex, o_bex, se_bytes;  // SE section (fp32) at the front of the blob
-  int s_x, s_h1, s_st, s_full, s_hdr, s_ring, s_pool, s_bar, smem;
+  int s_x, s_h1, s_st, s_full, s_hdr, s_ring, s_pool, s_map, s_bar, smem;
   int ring_stages;
   int t_e, t_c, tmem_cols;
   const uint8_t* wpack;  // front blob: [SE][range hdrs][chunks]
@@ -63,7 +63,7 @@ struct MbBackArgs {
 };
 
 namespace mbk {
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 struct FrontBars {
   uint64_t hdr_full, x_full;
   uint64_t w_full[4], w_empty[4];
@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   uint8_t* s_hdr = smem + a.s_hdr;
   uint8_t* s_ring = smem + a.s_ring;
   float* s_pool = reinterpret_cast<float*>(smem + a.s_pool);  // [imgs][HR]
+  int* s_cmap = reinterpret_cast<int*>(smem + a.s_map);            // conv tile row -> dense pixel / -1
+  uint8_t* s_emap = smem + a.s_map + a.n_ct * 128 * 4;              // expand tile row -> real?
   FrontBars& B = *reinterpret_cast<FrontBars*>(smem + a.s_bar);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int group = blockIdx.x / a.ranges, range = blockIdx.x % a.ranges;
@@ -129,6 +131,20 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   for (int i = threadIdx.x; i < a.h1_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
   for (int i = threadIdx.x; i < a.imgs * a.HR; i += blockDim.x) s_pool[i] = 0.f;
+  {
+    const int conv_end = (a.total_rows - 1) * a.Wp;
+    for (int i = threadIdx.x; i < a.n_ct * 128; i += blockDim.x) {
+      const int f = a.conv_base + i;
+      int p = -1;
+      if (f < conv_end && mb_real(f, a.Wp, a.W, a.H, a.total_rows)) {
+        const int row = f / a.Wp, img = row / (a.H + 1);
+        p = (img * a.H + row - img * (a.H + 1) - 1) * a.W + (f - row * a.Wp - 1);
+      }
+      s_cmap[i] = p;
+    }
+    for (int f = threadIdx.x; f < a.n_et * 128; f += blockDim.x)
+      s_emap[f] = (f < x_valid && mb_real(f, a.Wp, a.W, a.H, a.total_rows)) ? 1 : 0;
+  }
   {
     const int tail = a.x_alloc - x_valid, planes = a.C / 8;
     for (int i = threadIdx.x; i < planes * tail; i += blockDim.x) {
@@ -146,10 +162,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.e_full[i], 1);
       mbar_init(&B.c_full[i], 1);
-      mbar_init(&B.c_empty[i], 128);
+      mbar_init(&B.c_empty[i], 256);
     }
     mbar_init(&B.h1_full, 128);
-    mbar_init(&B.h1_empty, a.T8 ? 1 : 128);
+    mbar_init(&B.h1_empty, a.T8 ? 1 : 256);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       tc_fence_after();
       for (int t = 0; t < a.n_et; ++t) {
         const int f = t * 128 + q * 32 + lane;
-        const bool real = f < x_valid && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
+        const bool real = s_emap[f] != 0;
         for (int c0 = 0; c0 < HC; c0 += 16) {
           uint32_t v[16];
           WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + (eb * a.n_et + t) * HC + c0), v);
@@ -252,16 +268,19 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       tc_fence_before();
       mbar_arrive(&B.h1_full);
     }
-  } else if (warp >= 8 && warp < 12) {
-    // ------------- conv epilogue -> staging -> h2 (TMA store) + pool
-    const int q = warp - 8;
-    const int tid = q * 32 + lane;
+  } else if (warp >= 8) {
+    // ------------- conv epilogue -> staging -> h2 (TMA store) + pool.
+    // 8 warps: TMEM quadrant q = warp % 4, 16-column blocks split by parity hh.
+    const int q = warp % 4, hh = (warp - 8) / 4;
+    const int tid = (warp - 8) * 32 + lane;  // 0..255
+    const int wi = warp - 8;
+    const int lrow = q * 32 + lane;
     const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
     const float* s_cw = reinterpret_cast<const float*>(s_hdr + a.o_convw);  // [9][HR] (T1)
     mbar_wait(&B.hdr_full, 0);
-    const int conv_end = (a.total_rows - 1) * a.Wp;
     uint8_t* dst_stage = a.stride == 1 ? s_st : s_full;
     const int dst_rows = a.stride == 1 ? a.st_rows : a.P_full;
+    const bool one_store = a.stride == 2 || a.st_stores == 1;
     for (int j = 0; j < nch; ++j) {
       const int cb = j % a.c_bufs;
       if (a.T8) {
@@ -272,14 +291,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       }
       // staging may still be read by the previous chunk's TMA store
       if (tid == 0) bulk_wait_read0();
-      named_bar(1, 128);
+      named_bar(1, 256);
       for (int t = 0; t < a.n_ct; ++t) {
-        const int f = a.conv_base + t * 128 + tid;
-        const bool real = f < conv_end && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
-        const int row = f / a.Wp, img = row / (a.H + 1);
-        const int y = row - img * (a.H + 1) - 1, x = f - row * a.Wp - 1;
-        const int p = (img * a.H + y) * a.W + x;  // dense full-resolution pixel
-        for (int c0 = 0; c0 < HC; c0 += 16) {
+        const int f = a.conv_base + t * 128 + lrow;
+        const int p = s_cmap[t * 128 + lrow];  // dense full-resolution pixel, -1 = pad
+        for (int c0 = hh * 16; c0 < HC; c0 += 32) {
           uint32_t v[16];
           if (a.T8) {
             WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + (cb * a.n_ct + t) * HC + c0), v);
@@ -288,7 +304,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             float fv[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) fv[i] = 0.f;
-            if (real) {
+            if (p >= 0) {
               for (int tap = 0; tap < 9; ++tap) {
                 const int ff = f + (tap / 3 - 1) * a.Wp + (tap % 3 - 1);
                 float hv[16];
@@ -302,11 +318,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(fv[i]);
           }
-          if (real) {
+          if (p >= 0) {
             const uint4 lo = bias_act8<ACT>(v, s_bconv + j * HC + c0);
             const uint4 hi = bias_act8<ACT>(v + 8, s_bconv + j * HC + c0 + 8);
-            *reinterpret_cast<uint4*>(dst_stage + st_off(p, c0 / 8, dst_rows, G8)) = lo;
-            *reinterpret_cast<uint4*>(dst_stage + st_off(p, c0 / 8 + 1, dst_rows, G8)) = hi;
+            if (one_store) {
+              *reinterpret_cast<uint4*>(dst_stage + ((c0 / 8) * dst_rows + p) * 16) = lo;
+              *reinterpret_cast<uint4*>(dst_stage + ((c0 / 8 + 1) * dst_rows + p) * 16) = hi;
+            } else {
+              *reinterpret_cast<uint4*>(dst_stage + st_off(p, c0 / 8, dst_rows, G8)) = lo;
+              *reinterpret_cast<uint4*>(dst_stage + st_off(p, c0 / 8 + 1, dst_rows, G8)) = hi;
+            }
           }
         }
       }
@@ -316,11 +337,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       } else {
         mbar_arrive(&B.h1_empty);
       }
-      named_bar(1, 128);
+      named_bar(1, 256);
       if (a.stride == 2) {
         // BlurPool Triangle-3 x Triangle-3 / 16, stride 2, reflect pad (-1 -> 1)
         const int nq = a.P_out * G8;
-        for (int i = tid; i < nq; i += 128) {
+        for (int i = tid; i < nq; i += 256) {
           const int g = i / a.P_out, qp = i - g * a.P_out;
           const int im = qp / (a.Ho * a.Wo), rem = qp - im * (a.Ho * a.Wo);
           const int yo = rem / a.Wo, xo = rem - yo * a.Wo;
@@ -333,18 +354,18 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             for (int dx = 0; dx < 3; ++dx) {
               float hv[8];
               const int pf = (im * a.H + ys[dy]) * a.W + xs[dx];
-              unpack8(*reinterpret_cast<const uint4*>(s_full + st_off(pf, g, a.P_full, G8)), hv);
+              unpack8(*reinterpret_cast<const uint4*>(s_full + (g * a.P_full + pf) * 16), hv);
               const float w = (dy == 1 ? 0.5f : 0.25f) * (dx == 1 ? 0.5f : 0.25f);
 #pragma unroll
               for (int k = 0; k < 8; ++k) acc[k] += w * hv[k];
             }
           *reinterpret_cast<uint4*>(s_st + st_off(qp, g, a.st_rows, G8)) = pack8(acc);
         }
-        named_bar(1, 128);
+        named_bar(1, 256);
       }
       // h2 chunk -> global (TMA store of the dense staging)
       fence_async_smem();
-      named_bar(1, 128);
+      named_bar(1, 256);
       if (tid == 0) {
         for (int k = 0; k < a.st_stores; ++k)
           tma_store_3d(&tmap_h2, s_st + (size_t)k * G8 * a.st_rows * 16, 0, group * a.P_out + k * a.st_rows,
@@ -352,18 +373,39 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         bulk_commit();
       }
       // pool: deterministic column sums of the staged (fp16) h2 values.
-      // warp q sums channel groups g = q, q+4, ...; lane = (pixel offset i, word w)
+      // warp wi sums channel groups g = wi, wi+8, ...; lane = (pixel offset i, word w)
       const int pix_img = a.Ho * a.Wo;
-      for (int g = q; g < G8; g += 4) {
+      for (int g = wi; g < G8; g += 8) {
         const int i = lane >> 2, w = lane & 3;
         for (int im = 0; im < a.imgs; ++im) {
-          float s0 = 0.f, s1 = 0.f;
-          for (int p = im * pix_img + i; p < (im + 1) * pix_img; p += 8) {
-            const uint32_t hv = *reinterpret_cast<const uint32_t*>(s_st + st_off(p, g, a.st_rows, G8) + w * 4);
-            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&hv));
-            s0 += f2.x;
-            s1 += f2.y;
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          int pp = im * pix_img + i;
+          const int pe = (im + 1) * pix_img;
+          if (a.st_stores == 1) {
+            const uint8_t* base = s_st + g * a.st_rows * 16 + w * 4;
+            for (; pp + 8 < pe; pp += 16) {
+              const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + pp * 16));
+              const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(base + (pp + 8) * 16));
+              s0 += f0.x;
+              s1 += f0.y;
+              s2 += f1.x;
+              s3 += f1.y;
+            }
+            if (pp < pe) {
+              const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + pp * 16));
+              s0 += f0.x;
+              s1 += f0.y;
+            }
+          } else {
+            for (; pp < pe; pp += 8) {
+              const uint32_t hv = *reinterpret_cast<const uint32_t*>(s_st + st_off(pp, g, a.st_rows, G8) + w * 4);
+              const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&hv));
+              s0 += f2.x;
+              s1 += f2.y;
+            }
           }
+          s0 += s2;
+          s1 += s3;
 #pragma unroll
           for (int m = 4; m < 32; m <<= 1) {
             s0 += __shfl_xor_sync(0xffffffffu, s0, m);
@@ -376,10 +418,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         }
       }
     }
-    named_bar(1, 128);
+    named_bar(1, 256);
     if (tid == 0) bulk_wait0();
     const float inv = 1.f / (float)(a.Ho * a.Wo);
-    for (int i = tid; i < a.imgs * a.HR; i += 128) {
+    for (int i = tid; i < a.imgs * a.HR; i += 256) {
       const int im = i / a.HR, c = i % a.HR;
       a.pool[(size_t)(n0 + im) * a.hid + h0 + c] = s_pool[i] * inv;
     }
@@ -641,7 +683,7 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   f.HR = hid / f.ranges;
   f.HC = 0;
   const int x_bytes = (C / 8) * f.x_alloc * 16;
-  const int se_scratch = align_up((hid + 384 + f.sq) * 4, 16);
+  const int se_scratch = align_up((hid + 512 + f.sq) * 4, 16);
   for (int hc = 128; hc >= 16; hc -= 16) {
     if (f.HR % hc) continue;
     const int tiles1 = f.T8 ? f.n_et + f.n_ct : f.n_et;
@@ -651,7 +693,8 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
     const int full = f.stride == 2 ? f.P_full * hc * 2 : 0;
     const int hdr = align_up(f.HR * 4, 16) * 2 + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
     const int chunk = hc * C * 2 + (f.T8 ? (hc / 16) * 9 * 512 : 0);
-    const int total = x_bytes + h1_bytes + st + full + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048;
+    const int total = x_bytes + h1_bytes + st + full + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048 +
+                      f.n_ct * 128 * 4 + f.n_et * 128;
     if (total <= kSmemMaxMb) {
       f.HC = hc;
       break;
@@ -709,6 +752,8 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   o = align_up(o + f.ring_stages * f.chunk_bytes, 128);
   f.s_pool = o;
   o = align_up(o + f.imgs * f.HR * 4, 128);
+  f.s_map = o;
+  o = align_up(o + f.n_ct * 128 * 4 + f.n_et * 128, 128);
   f.s_bar = o;
   o += 512;
   f.smem = o;
