@@ -125,6 +125,10 @@ WL_API int wl_head_fwd(const wl_block_desc* d, const void* x, const void* packed
 WL_API int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float* const* weights, int count,
                        float* z_host);
 
+/* debug only: when dev_ptr (>= 512 bytes of device memory) is non-null,
+ * CTA 0 of the MBConv front kernel records clock64() phase stamps there */
+WL_API void wl_debug_set_trace(void* dev_ptr);
+
 /* output geometry of a block */
 WL_API int wl_output_dims(const wl_block_desc* d, int32_t* n, int32_t* h, int32_t* w, int32_t* c);
 

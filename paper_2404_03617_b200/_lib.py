@@ -39,6 +39,7 @@ EXPORTS = (
     "wl_head_fwd",
     "wl_execute_numeric",
     "wl_output_dims",
+    "wl_debug_set_trace",
 )
 
 
@@ -107,6 +108,7 @@ def lib() -> ctypes.CDLL:
             [D, P(ctypes.c_float), P(P(ctypes.c_float)), ctypes.c_int, P(ctypes.c_float)],
         ),
         "wl_output_dims": (ctypes.c_int, [D] + [P(ctypes.c_int32)] * 4),
+        "wl_debug_set_trace": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(so, name)

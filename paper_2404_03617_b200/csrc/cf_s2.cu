@@ -35,6 +35,19 @@ struct Cf2Args {
   __half* z;
 };
 
+// Triangle-3 tap [1, 2, 1] / 4 on 8 packed halves
+__device__ __forceinline__ uint4 tri3(const uint4& a, const uint4& b, const uint4& c) {
+  uint4 o;
+  const __half2* ha = reinterpret_cast<const __half2*>(&a);
+  const __half2* hb = reinterpret_cast<const __half2*>(&b);
+  const __half2* hc = reinterpret_cast<const __half2*>(&c);
+  __half2* ho = reinterpret_cast<__half2*>(&o);
+  const __half2 q = __float2half2_rn(0.25f), h = __float2half2_rn(0.5f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ho[i] = __hfma2(hb[i], h, __hmul2(__hadd2(ha[i], hc[i]), q));
+  return o;
+}
+
 template <int ACT>
 __global__ void __launch_bounds__(256, 1)
     cf2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Cf2Args a) {
@@ -131,13 +144,10 @@ __global__ void __launch_bounds__(256, 1)
     int k0 = 2 * ro, k1 = 2 * ro + 1, k2 = 2 * ro + 2;  // staging rows of conv rows 2yo-1, 2yo, 2yo+1
     if (yo == 0) k0 = k2;                               // reflect row -1 -> row 1
     for (int c8 = 0; c8 < planes; ++c8) {
-      float fa[8], fb[8], fc[8], o[8];
-      unpack8(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k0 * W + x) * C + c8 * 8), fa);
-      unpack8(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k1 * W + x) * C + c8 * 8), fb);
-      unpack8(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k2 * W + x) * C + c8 * 8), fc);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = 0.25f * fa[i] + 0.5f * fb[i] + 0.25f * fc[i];
-      *reinterpret_cast<uint4*>(s_ah + ((size_t)c8 * MH + p) * 16) = pack8(o);
+      *reinterpret_cast<uint4*>(s_ah + ((size_t)c8 * MH + p) * 16) =
+          tri3(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k0 * W + x) * C + c8 * 8),
+               *reinterpret_cast<const uint4*>(s_xc + ((size_t)k1 * W + x) * C + c8 * 8),
+               *reinterpret_cast<const uint4*>(s_xc + ((size_t)k2 * W + x) * C + c8 * 8));
     }
   }
   fence_async_smem();
@@ -174,12 +184,9 @@ __global__ void __launch_bounds__(256, 1)
         WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + t * r + c0), v);
         tmem_ld_wait();
         if (p < a.R * W) {
-          float fv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) fv[i] = act<ACT>(__uint_as_float(v[i]) + av[j * r + c0 + i]);
           __half* dst = s_hs + (size_t)p * r + c0;
-          reinterpret_cast<uint4*>(dst)[0] = pack8(fv);
-          reinterpret_cast<uint4*>(dst)[1] = pack8(fv + 8);
+          reinterpret_cast<uint4*>(dst)[0] = bias_act8<ACT>(v, av + j * r + c0);
+          reinterpret_cast<uint4*>(dst)[1] = bias_act8<ACT>(v + 8, av + j * r + c0 + 8);
         }
       }
     }
@@ -193,13 +200,9 @@ __global__ void __launch_bounds__(256, 1)
       const __half* r1 = s_hs + ((size_t)ro * W + 2 * xo) * r;
       const __half* r2 = s_hs + ((size_t)ro * W + 2 * xo + 1) * r;
       for (int c8 = 0; c8 < r / 8; ++c8) {
-        float fa[8], fb[8], fc[8], o[8];
-        unpack8(*reinterpret_cast<const uint4*>(r0 + c8 * 8), fa);
-        unpack8(*reinterpret_cast<const uint4*>(r1 + c8 * 8), fb);
-        unpack8(*reinterpret_cast<const uint4*>(r2 + c8 * 8), fc);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = 0.25f * fa[i] + 0.5f * fb[i] + 0.25f * fc[i];
-        *reinterpret_cast<uint4*>(s_aq + ((size_t)c8 * MQ + qi) * 16) = pack8(o);
+        *reinterpret_cast<uint4*>(s_aq + ((size_t)c8 * MQ + qi) * 16) =
+            tri3(*reinterpret_cast<const uint4*>(r0 + c8 * 8), *reinterpret_cast<const uint4*>(r1 + c8 * 8),
+                 *reinterpret_cast<const uint4*>(r2 + c8 * 8));
       }
     }
     fence_async_smem();
@@ -264,6 +267,10 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   a.Wo = d.w / 2;
   a.Wp = d.w + 1;
   if (a.C % 16 || a.K % 16 || a.hid % 16 || a.K > 256) return false;
+  // pass 0: the largest R that lets two CTAs share an SM (TMEM <= 256 columns,
+  // <= 112 KB shared memory) so one CTA's serial phases overlap the other's;
+  // pass 1: any R that fits one CTA per SM
+  for (int pass = 0; pass < 2; ++pass)
   for (int R = 8; R >= 1; --R) {
     if (R > a.Ho) continue;
     a.R = R;
@@ -312,7 +319,7 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
       s = align_up(s + 2 * a.chunk_bytes, 128);
       a.s_bar = s;
       s += 64;
-      ok = s <= kSmemMax2;
+      ok = s <= (pass == 0 ? 112 * 1024 : kSmemMax2) && (pass == 1 || cols <= 256);
     }
     if (!ok) continue;
     a.tiles_y = (a.Ho + R - 1) / R;

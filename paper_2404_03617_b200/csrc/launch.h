@@ -43,5 +43,6 @@ extern const Family kCf2Family;
 extern const Family kMbFamily;
 extern const Family kStemFamily;
 extern const Family kHeadFamily;
+void mb_set_trace(void* p);
 
 }  // namespace wl

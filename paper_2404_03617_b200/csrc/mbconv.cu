@@ -35,18 +35,19 @@ struct MbFrontArgs {
   int Ho, Wo, ranges;
   int P_out, P_full;       // dense output / full-res pixels per CTA
   int st_rows, st_stores;  // TMA store box rows, stores per chunk
-  int e_bufs, c_bufs;
+  int e_bufs, c_bufs, h1_bufs, x_tmem;
   int h1_bytes, st_bytes, full_bytes;
   int hdr_bytes, chunk_bytes, u_bytes;  // per-range hdr = [b_exp | b_conv | (T1) convw fp32 [9][HR]]
   int o_bconv, o_convw;
   int o_wsq, o_bsq, o_wex, o_bex, se_bytes;  // SE section (fp32) at the front of the blob
   int s_x, s_h1, s_st, s_full, s_hdr, s_ring, s_pool, s_map, s_bar, smem;
   int ring_stages;
-  int t_e, t_c, tmem_cols;
+  int t_x, t_e, t_c, tmem_cols, s_h1b;
   const uint8_t* wpack;  // front blob: [SE][range hdrs][chunks]
   float* pool;           // (n, hid) spatial mean
   float* gates;          // (n, hid) SE gates
   int* counters;         // (groups) zero-initialised arrival counters
+  long long* trace;      // debug: per-phase clock64 stamps of CTA 0 (null = off)
 };
 
 struct MbBackArgs {
@@ -63,12 +64,12 @@ struct MbBackArgs {
 };
 
 namespace mbk {
-constexpr int kThreads = 512;
+constexpr int kThreads = 640;
 struct FrontBars {
   uint64_t hdr_full, x_full;
   uint64_t w_full[4], w_empty[4];
   uint64_t e_full[2], c_full[2], c_empty[2];
-  uint64_t h1_full, h1_empty;
+  uint64_t h1_full[2], h1_empty[2], x_ready;
   uint32_t tmem_base;
   int last;
 };
@@ -104,6 +105,11 @@ __device__ __forceinline__ int st_off(int p, int g, int st_rows, int groups8) {
   return ((k * groups8 + g) * st_rows + r) * 16;
 }
 
+#define WL_TRACE(slot)                                                  \
+  do {                                                                  \
+    if (a.trace && blockIdx.x == 0) a.trace[(slot)] = clock64();        \
+  } while (0)
+
 template <int ACT>
 __global__ void __launch_bounds__(mbk::kThreads, 1)
     mb_front_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_h2,
@@ -127,9 +133,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int S = a.ring_stages, HC = a.HC, nch = a.nch, G8 = HC / 8;
   const int img_flat = (a.H + 1) * a.Wp;
   const int x_valid = a.imgs * img_flat;
+  if (threadIdx.x == 0) WL_TRACE(0);
 
   for (int i = threadIdx.x; i < a.h1_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
+  if (a.h1_bufs > 1 && !a.x_tmem)
+    for (int i = threadIdx.x; i < G8 * a.flat_h1; i += blockDim.x)
+      reinterpret_cast<uint4*>(smem + a.s_h1b)[i] = make_uint4(0, 0, 0, 0);
   for (int i = threadIdx.x; i < a.imgs * a.HR; i += blockDim.x) s_pool[i] = 0.f;
   {
     const int conv_end = (a.total_rows - 1) * a.Wp;
@@ -164,8 +174,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_init(&B.c_full[i], 1);
       mbar_init(&B.c_empty[i], 256);
     }
-    mbar_init(&B.h1_full, 128);
-    mbar_init(&B.h1_empty, a.T8 ? 1 : 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.h1_full[i], 256);
+      mbar_init(&B.h1_empty[i], a.T8 ? 1 : 256);
+    }
+    mbar_init(&B.x_ready, 256);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -178,6 +191,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       prefetch_tmap(&tmap_x);
+      WL_TRACE(1);
       mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
       bulk_g2s(s_hdr, a.wpack + a.se_bytes + (size_t)range * a.hdr_bytes, a.hdr_bytes, &B.hdr_full);
       const int planes = a.C / 8;
@@ -198,60 +212,106 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc_e = make_idesc_f16(128, HC);
       const uint32_t idesc_c = make_idesc_f16(128, 16);
-      const uint32_t x0 = smem_u32(s_x), h10 = smem_u32(s_h1), ring0 = smem_u32(s_ring);
+      const uint32_t x0 = smem_u32(s_x), ring0 = smem_u32(s_ring);
       mbar_wait(&B.x_full, 0);
+      if (a.x_tmem) mbar_wait(&B.x_ready, 0);
+      WL_TRACE(2);
       auto issue_expand = [&](int j) {
         const int slot = j % S, eb = j % a.e_bufs;
         mbar_wait(&B.w_full[slot], (j / S) & 1);
+        WL_TRACE(16 + 8 * j + 0);
         tc_fence_after();
         const uint32_t ub = ring0 + slot * a.chunk_bytes;
-        for (int t = 0; t < a.n_et; ++t)
-          for (int kk = 0; kk < a.C / 16; ++kk) {
-            const uint64_t ad = make_sdesc(x0 + (kk * 2 * a.x_alloc + t * 128) * 16, a.x_alloc * 16, 128);
-            const uint64_t bd = make_sdesc(ub + kk * 2 * (HC * 16), HC * 16, 128);
-            mma_ss(tmem + a.t_e + (eb * a.n_et + t) * HC, ad, bd, idesc_e, kk > 0);
+        const uint64_t b_base = make_sdesc(ub, HC * 16, 128);
+        for (int t = 0; t < a.n_et; ++t) {
+          const uint32_t d = tmem + a.t_e + (eb * a.n_et + t) * HC;
+          if (a.x_tmem) {  // A = x tile in TMEM: only B streams from shared memory
+            for (int kk = 0; kk < a.C / 16; ++kk)
+              mma_ts(d, tmem + a.t_x + t * (a.C / 2) + kk * 8, b_base + (uint64_t)(kk * 2 * HC), idesc_e, kk > 0);
+          } else {
+            const uint64_t a_base = make_sdesc(x0 + t * 128 * 16, a.x_alloc * 16, 128);
+            for (int kk = 0; kk < a.C / 16; ++kk)
+              mma_ss(d, a_base + (uint64_t)(kk * 2 * a.x_alloc), b_base + (uint64_t)(kk * 2 * HC), idesc_e, kk > 0);
           }
+        }
         mma_commit(&B.e_full[eb]);
       };
       issue_expand(0);
       for (int j = 0; j < nch; ++j) {
-        const int slot = j % S;
-        if (a.e_bufs == 1) mbar_wait(&B.h1_full, j & 1);  // E of chunk j consumed
+        const int slot = j % S, hb = j % a.h1_bufs;
+        if (a.e_bufs == 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // E of chunk j consumed
         if (j + 1 < nch) issue_expand(j + 1);
         if (a.T8) {
           const int cb = j % a.c_bufs;
-          if (a.e_bufs != 1) mbar_wait(&B.h1_full, j & 1);
+          if (a.e_bufs != 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);
           if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
+          WL_TRACE(16 + 8 * j + 1);
           tc_fence_after();
-          const uint32_t cw = ring0 + slot * a.chunk_bytes + a.u_bytes;
+          // descriptors advance by constant 16-byte steps from the (dy, dx) = (-1, -1) tap
+          const uint32_t h1a = smem_u32(hb ? smem + a.s_h1b : s_h1);
+          const uint64_t a_base = make_sdesc(h1a + (a.conv_base - a.Wp - 1) * 16, a.flat_h1 * 16, 128);
+          // block-diagonal B tiles, compact: entry e = pr*9+tap keeps its two 8x8
+          // diagonal blocks at Z -/+ (e+1)*128 around one shared zero block Z,
+          // addressed with LBO = SBO = (e+1)*128 (both off-diagonal blocks hit Z)
+          const int E = (HC / 16) * 9;
+          const uint32_t zaddr = ring0 + slot * a.chunk_bytes + a.u_bytes + E * 128;
+          const uint64_t b_base = make_sdesc(zaddr - 128, 128, 128);
+          const uint64_t b_step = (8ull << 16) + (8ull << 32) - 8ull;
           for (int t = 0; t < a.n_ct; ++t)
-            for (int pr = 0; pr < HC / 16; ++pr)
-              for (int tap = 0; tap < 9; ++tap) {
-                const int f = a.conv_base + t * 128 + (tap / 3 - 1) * a.Wp + (tap % 3 - 1);
-                const uint64_t ad = make_sdesc(h10 + (2 * pr * a.flat_h1 + f) * 16, a.flat_h1 * 16, 128);
-                const uint64_t bd = make_sdesc(cw + (pr * 9 + tap) * 512, 256, 128);
-                mma_ss(tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr, ad, bd, idesc_c, tap > 0);
-              }
+            for (int pr = 0; pr < HC / 16; ++pr) {
+              const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
+              const uint64_t ap = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128);
+              const uint64_t bp = b_base + (uint64_t)(pr * 9) * b_step;
+#pragma unroll
+              for (int tap = 0; tap < 9; ++tap)
+                mma_ss(d, ap + (uint64_t)((tap / 3) * a.Wp + tap % 3), bp + (uint64_t)tap * b_step, idesc_c, tap > 0);
+            }
           mma_commit(&B.c_full[cb]);
-          mma_commit(&B.h1_empty);
+          mma_commit(&B.h1_empty[hb]);
+          WL_TRACE(16 + 8 * j + 2);
         }
         mma_commit(&B.w_empty[slot]);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 12) {
     // ------------- expand epilogue: E + b_exp -> phi -> pads 0 -> h1 planes
-    const int q = warp - 4;
+    const int q = warp % 4, eh = (warp - 4) / 4;  // TMEM quadrant, 16-column parity
     const float* s_bexp = reinterpret_cast<const float*>(s_hdr);
+    if (a.x_tmem) {
+      // move the x tile into TMEM (A operand of the expansion), then recycle
+      // its shared-memory region as the second h1 buffer
+      mbar_wait(&B.x_full, 0);
+      for (int t = 0; t < a.n_et; ++t) {
+        const int f = t * 128 + q * 32 + lane;
+        for (int pg = eh; pg < a.C / 16; pg += 2) {
+          const uint4 lo = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg) * a.x_alloc + f) * 16);
+          const uint4 hi = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg + 1) * a.x_alloc + f) * 16);
+          const uint32_t r8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+          WL_TMEM_ST8(tmem_lane_addr(tmem, q, a.t_x + t * (a.C / 2) + pg * 8), r8);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      named_bar(2, 256);
+      if (a.h1_bufs > 1) {
+        for (int i = (warp - 4) * 32 + lane; i < G8 * a.flat_h1; i += 256)
+          reinterpret_cast<uint4*>(smem + a.s_h1b)[i] = make_uint4(0, 0, 0, 0);
+        fence_async_smem();
+      }
+      mbar_arrive(&B.x_ready);
+    }
     mbar_wait(&B.hdr_full, 0);
     for (int j = 0; j < nch; ++j) {
-      const int eb = j % a.e_bufs;
+      const int eb = j % a.e_bufs, hb = j % a.h1_bufs;
+      uint8_t* h1 = hb ? smem + a.s_h1b : s_h1;
       mbar_wait(&B.e_full[eb], (j / a.e_bufs) & 1);
-      if (j > 0) mbar_wait(&B.h1_empty, (j - 1) & 1);
+      if (j >= a.h1_bufs) mbar_wait(&B.h1_empty[hb], ((j / a.h1_bufs) & 1) ^ 1);
+      if (warp == 4 && lane == 0) WL_TRACE(16 + 8 * j + 3);
       tc_fence_after();
       for (int t = 0; t < a.n_et; ++t) {
         const int f = t * 128 + q * 32 + lane;
         const bool real = s_emap[f] != 0;
-        for (int c0 = 0; c0 < HC; c0 += 16) {
+        for (int c0 = eh * 16; c0 < HC; c0 += 32) {
           uint32_t v[16];
           WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + (eb * a.n_et + t) * HC + c0), v);
           tmem_ld_wait();
@@ -259,21 +319,22 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           uint4 hi = bias_act8<ACT>(v + 8, s_bexp + j * HC + c0 + 8);
           if (!real) lo = hi = make_uint4(0, 0, 0, 0);
           if (f < a.flat_h1) {
-            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + f) * 16) = lo;
-            *reinterpret_cast<uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + f) * 16) = hi;
+            *reinterpret_cast<uint4*>(h1 + ((size_t)(c0 / 8) * a.flat_h1 + f) * 16) = lo;
+            *reinterpret_cast<uint4*>(h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + f) * 16) = hi;
           }
         }
       }
       fence_async_smem();
       tc_fence_before();
-      mbar_arrive(&B.h1_full);
+      mbar_arrive(&B.h1_full[hb]);
+      if (warp == 4 && lane == 0) WL_TRACE(16 + 8 * j + 4);
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ------------- conv epilogue -> staging -> h2 (TMA store) + pool.
     // 8 warps: TMEM quadrant q = warp % 4, 16-column blocks split by parity hh.
-    const int q = warp % 4, hh = (warp - 8) / 4;
-    const int tid = (warp - 8) * 32 + lane;  // 0..255
-    const int wi = warp - 8;
+    const int q = warp % 4, hh = (warp - 12) / 4;
+    const int tid = (warp - 12) * 32 + lane;  // 0..255
+    const int wi = warp - 12;
     const int lrow = q * 32 + lane;
     const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
     const float* s_cw = reinterpret_cast<const float*>(s_hdr + a.o_convw);  // [9][HR] (T1)
@@ -287,8 +348,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mbar_wait(&B.c_full[cb], (j / a.c_bufs) & 1);
         tc_fence_after();
       } else {
-        mbar_wait(&B.h1_full, j & 1);
+        mbar_wait(&B.h1_full[j % a.h1_bufs], (j / a.h1_bufs) & 1);
       }
+      const uint8_t* h1c = (j % a.h1_bufs) ? smem + a.s_h1b : s_h1;
+      if (tid == 0) WL_TRACE(16 + 8 * j + 5);
       // staging may still be read by the previous chunk's TMA store
       if (tid == 0) bulk_wait_read0();
       named_bar(1, 256);
@@ -308,8 +371,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
               for (int tap = 0; tap < 9; ++tap) {
                 const int ff = f + (tap / 3 - 1) * a.Wp + (tap % 3 - 1);
                 float hv[16];
-                unpack8(*reinterpret_cast<const uint4*>(s_h1 + ((size_t)(c0 / 8) * a.flat_h1 + ff) * 16), hv);
-                unpack8(*reinterpret_cast<const uint4*>(s_h1 + ((size_t)(c0 / 8 + 1) * a.flat_h1 + ff) * 16), hv + 8);
+                unpack8(*reinterpret_cast<const uint4*>(h1c + ((size_t)(c0 / 8) * a.flat_h1 + ff) * 16), hv);
+                unpack8(*reinterpret_cast<const uint4*>(h1c + ((size_t)(c0 / 8 + 1) * a.flat_h1 + ff) * 16), hv + 8);
                 const float* w = s_cw + tap * a.HR + j * HC + c0;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) fv[i] += hv[i] * w[i];
@@ -335,7 +398,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         tc_fence_before();
         mbar_arrive(&B.c_empty[cb]);
       } else {
-        mbar_arrive(&B.h1_empty);
+        mbar_arrive(&B.h1_empty[j % a.h1_bufs]);
       }
       named_bar(1, 256);
       if (a.stride == 2) {
@@ -366,6 +429,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       // h2 chunk -> global (TMA store of the dense staging)
       fence_async_smem();
       named_bar(1, 256);
+      if (tid == 0) WL_TRACE(16 + 8 * j + 6);
       if (tid == 0) {
         for (int k = 0; k < a.st_stores; ++k)
           tma_store_3d(&tmap_h2, s_st + (size_t)k * G8 * a.st_rows * 16, 0, group * a.P_out + k * a.st_rows,
@@ -419,6 +483,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       }
     }
     named_bar(1, 256);
+    if (tid == 0) WL_TRACE(8);
     if (tid == 0) bulk_wait0();
     const float inv = 1.f / (float)(a.Ho * a.Wo);
     for (int i = tid; i < a.imgs * a.HR; i += 256) {
@@ -437,6 +502,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     B.last = (old == a.ranges - 1);
   }
   __syncthreads();
+  if (threadIdx.x == 0) WL_TRACE(9);
   if (B.last) {
     __threadfence();
     const float* wsq = reinterpret_cast<const float*>(a.wpack + a.o_wsq);  // [hid][sq]
@@ -486,6 +552,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     }
     if (threadIdx.x == 0) a.counters[group] = 0;  // self-cleaning for the next launch
   }
+  if (threadIdx.x == 0) WL_TRACE(10);
   __syncthreads();
   if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
 }
@@ -635,6 +702,7 @@ namespace wl {
 namespace {
 
 constexpr int kSmemMaxMb = 232448;
+long long* g_mb_trace = nullptr;
 constexpr int64_t kCounterBytes = 4096;  // workspace header: per-group arrival counters
 
 struct MbPlanH {
@@ -683,7 +751,7 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   f.HR = hid / f.ranges;
   f.HC = 0;
   const int x_bytes = (C / 8) * f.x_alloc * 16;
-  const int se_scratch = align_up((hid + 512 + f.sq) * 4, 16);
+  const int se_scratch = align_up((hid + 640 + f.sq) * 4, 16);
   for (int hc = 128; hc >= 16; hc -= 16) {
     if (f.HR % hc) continue;
     const int tiles1 = f.T8 ? f.n_et + f.n_ct : f.n_et;
@@ -692,7 +760,7 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
     const int st = f.P_out * hc * 2;
     const int full = f.stride == 2 ? f.P_full * hc * 2 : 0;
     const int hdr = align_up(f.HR * 4, 16) * 2 + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
-    const int chunk = hc * C * 2 + (f.T8 ? (hc / 16) * 9 * 512 : 0);
+    const int chunk = hc * C * 2 + (f.T8 ? (2 * (hc / 16) * 9 + 1) * 128 : 0);
     const int total = x_bytes + h1_bytes + st + full + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048 +
                       f.n_ct * 128 * 4 + f.n_et * 128;
     if (total <= kSmemMaxMb) {
@@ -703,19 +771,29 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   if (!f.HC) return false;
   f.nch = f.HR / f.HC;
   // double-buffer the expand / conv accumulators when TMEM allows
-  f.e_bufs = 1;
-  f.c_bufs = 1;
-  auto cols = [&]() { return (f.e_bufs * f.n_et + (f.T8 ? f.c_bufs * f.n_ct : 0)) * f.HC; };
-  if (f.nch > 1 && f.T8) {  // T=1: the MMA warp cannot observe E consumption early
-    f.e_bufs = 2;
-    if (cols() > 512) f.e_bufs = 1;
-    if (f.T8) {
-      f.c_bufs = 2;
-      if (cols() > 512) f.c_bufs = 1;
+  // TMEM: x tile (A of a TS-mode expansion, T=8 only) + expand / conv
+  // accumulators, double-buffered when the 512 columns allow
+  const int x_cols = f.n_et * (C / 2);
+  auto cols = [&]() {
+    return (f.x_tmem ? x_cols : 0) + (f.e_bufs * f.n_et + (f.T8 ? f.c_bufs * f.n_ct : 0)) * f.HC;
+  };
+  bool placed = false;
+  for (int xt = f.T8 ? 1 : 0; xt >= 0 && !placed; --xt) {
+    const int combos[4][2] = {{2, 2}, {1, 2}, {2, 1}, {1, 1}};
+    for (auto& cb : combos) {
+      f.x_tmem = xt;
+      f.e_bufs = (f.T8 && f.nch > 1) ? cb[0] : 1;  // T=1: the MMA warp cannot observe E consumption early
+      f.c_bufs = (f.T8 && f.nch > 1) ? cb[1] : 1;
+      if (cols() <= 512) {
+        placed = true;
+        break;
+      }
     }
   }
-  f.t_e = 0;
-  f.t_c = f.e_bufs * f.n_et * f.HC;
+  if (!placed) return false;
+  f.t_x = 0;
+  f.t_e = f.x_tmem ? x_cols : 0;
+  f.t_c = f.t_e + f.e_bufs * f.n_et * f.HC;
   f.tmem_cols = 32;
   while (f.tmem_cols < cols()) f.tmem_cols *= 2;
   f.h1_bytes = std::max((f.HC / 8) * f.flat_h1 * 16, se_scratch);
@@ -725,8 +803,8 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   f.o_convw = f.o_bconv + align_up(f.HR * 4, 16);
   f.hdr_bytes = f.o_convw + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
   f.u_bytes = f.HC * C * 2;
-  f.chunk_bytes = f.u_bytes + (f.T8 ? (f.HC / 16) * 9 * 512 : 0);
-  f.ring_stages = 2;
+  f.chunk_bytes = f.u_bytes + (f.T8 ? (2 * (f.HC / 16) * 9 + 1) * 128 : 0);
+  f.ring_stages = 2;  // raised to 3 below when shared memory allows
   int so = 0;  // SE section (fp32) at the start of the front blob
   f.o_wsq = so;
   so = align_up(so + hid * f.sq * 4, 16);
@@ -754,6 +832,25 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   o = align_up(o + f.imgs * f.HR * 4, 128);
   f.s_map = o;
   o = align_up(o + f.n_ct * 128 * 4 + f.n_et * 128, 128);
+  if (o + f.chunk_bytes + 512 <= kSmemMaxMb && f.nch > 2) {  // third weight stage
+    // shift everything after the ring by one chunk
+    f.ring_stages = 3;
+    f.s_pool += f.chunk_bytes;
+    f.s_map += f.chunk_bytes;
+    o += f.chunk_bytes;
+  }
+  // second h1 buffer: the x region once x lives in TMEM, else a new region if it fits
+  const int h1_one = (f.HC / 8) * f.flat_h1 * 16;
+  f.h1_bufs = 1;
+  f.s_h1b = f.s_h1;
+  if (f.nch > 1 && f.x_tmem && x_bytes >= h1_one) {
+    f.h1_bufs = 2;
+    f.s_h1b = f.s_x;
+  } else if (f.nch > 1 && o + align_up(h1_one, 128) + 512 <= kSmemMaxMb) {
+    f.h1_bufs = 2;
+    f.s_h1b = o;
+    o = align_up(o + h1_one, 128);
+  }
   f.s_bar = o;
   o += 512;
   f.smem = o;
@@ -891,14 +988,20 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
         for (int k = 0; k < C; ++k) put_h(ch, core_off_h(n, k, f.HC * 16), wexp[(size_t)k * hid + hb + n]);
       if (f.T8) {
         uint8_t* cw = ch + f.u_bytes;
+        const int E = (f.HC / 16) * 9;
+        uint8_t* z = cw + E * 128;  // shared zero block
         for (int pr = 0; pr < f.HC / 16; ++pr)
-          for (int t = 0; t < 9; ++t)
-            for (int nn = 0; nn < 16; ++nn)
-              for (int kk = 0; kk < 16; ++kk) {
-                if (nn / 8 != kk / 8) continue;
-                const int oc = hb + 16 * pr + nn;
-                put_h(cw + (pr * 9 + t) * 512, core_off_h(nn, kk, 256), wconv[((size_t)oc * 9 + t) * T + kk % 8]);
-              }
+          for (int t = 0; t < 9; ++t) {
+            const int e = pr * 9 + t;
+            for (int half = 0; half < 2; ++half) {
+              uint8_t* blk = half ? z + (e + 1) * 128 : z - (e + 1) * 128;
+              for (int nn = 0; nn < 8; ++nn)
+                for (int kk = 0; kk < 8; ++kk) {
+                  const int oc = hb + 16 * pr + 8 * half + nn;
+                  put_h(blk, nn * 16 + kk * 2, wconv[((size_t)oc * 9 + t) * T + kk]);
+                }
+            }
+          }
       }
     }
   }
@@ -928,6 +1031,7 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
   f.pool = pool;
   f.gates = pool + (size_t)d.n * f.hid;
   f.counters = reinterpret_cast<int*>(wsb);
+  f.trace = g_mb_trace;
   CUtensorMap tx, th_store, th_load;
   {
     const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)(d.c / 8), (uint64_t)d.n};
@@ -964,6 +1068,8 @@ int mb_init() {
 }
 
 }  // namespace
+
+void mb_set_trace(void* p) { g_mb_trace = reinterpret_cast<long long*>(p); }
 
 const Family kMbFamily = {mb_validate, mb_weight_count, mb_weight_numel, mb_packed_bytes,
                           mb_pack,     mb_workspace,    mb_forward,      mb_init};

@@ -1,0 +1,29 @@
+"""Phase timeline of CTA 0 of the MBConv front kernel (clock64 stamps)."""
+import sys, os
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2404_03617_b200 import _lib
+from paper_2404_03617_b200.core import MBConv, TensorDims
+from paper_2404_03617_b200.blocks import FusedBlock
+cases = {"mb14": (MBConv(8, 4, 0.25), TensorDims(128, 14, 14, 128), None),
+         "mb7": (MBConv(8, 4, 0.25), TensorDims(128, 7, 7, 128), None),
+         "mbs2": (MBConv(8, 4, 0.25, 2), TensorDims(128, 28, 28, 48), 128)}
+for nm in sys.argv[1:]:
+    blk, dims, k = cases[nm]
+    m = FusedBlock(blk, dims, k)
+    x = torch.randn(dims.n, dims.h, dims.w, dims.c, device="cuda").half()
+    out = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
+    buf = torch.zeros(128, dtype=torch.int64, device="cuda")
+    for _ in range(3): m.launch(x, out)
+    _lib.lib().wl_debug_set_trace(buf.data_ptr())
+    m.launch(x, out)
+    torch.cuda.synchronize()
+    _lib.lib().wl_debug_set_trace(None)
+    t = buf.cpu().tolist()
+    t0 = t[0]
+    rel = lambda v: (v - t0) if v else -1
+    print(nm, "producer start", rel(t[1]), "x loaded", rel(t[2]), "pool done", rel(t[8]), "SE start", rel(t[9]), "end", rel(t[10]))
+    for j in range(12):
+        row = t[16 + 8 * j: 16 + 8 * j + 7]
+        if not any(row): break
+        print(f"  chunk {j}: expand@{rel(row[0])} conv@{rel(row[1])}..{rel(row[2])} Eepi {rel(row[3])}..{rel(row[4])} Cepi {rel(row[5])}..{rel(row[6])}")
