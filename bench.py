@@ -256,10 +256,17 @@ def run_gpu(args):
         value = world * B / (ms / 1e3)
         dev = DeviceSpec("b200", peak_sust, hbm)
         wl = model.workloads(dev, ExecutionScheme.BLOCK_FUSION)
-        # dominant unit by measured share
-        di = max(range(len(unit_s)), key=lambda i: unit_s[i])
+        # dominant kernel: identical units (same block, geometry) grouped, largest total share
+        sig = lambda i: (repr(model.instances[i].block), model.instances[i].in_h, model.instances[i].in_w,
+                         model.instances[i].in_channels, model.instances[i].out_channels)
+        groups = {}
+        for i in range(len(unit_s)):
+            groups.setdefault(sig(i), []).append(i)
+        members = max(groups.values(), key=lambda ix: sum(unit_s[i] for i in ix))
+        di = members[len(members) // 2]
         dom = model.units[di]
         inst = model.instances[di]
+        group_share = sum(unit_s[i] for i in members) / sum(unit_s)
         dom_ops = complexity.block_ops(inst.block, inst.dims(B), inst.out_channels)
         dom_bytes = wl[di].bytes
         intensity = dom_ops / dom_bytes
@@ -323,7 +330,8 @@ def run_gpu(args):
                 "traffic": traffic,
                 "algorithmic_flops_per_launch": dom_ops,
                 "algorithmic_bytes_per_launch": dom_bytes,
-                "share_of_step": unit_s[di] / sum(unit_s),
+                "share_of_step": group_share,
+                "launches_in_group": len(members),
             },
             "e2e": {
                 "value": world * B / (e2e / 1e3),
