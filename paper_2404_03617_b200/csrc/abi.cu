@@ -42,7 +42,7 @@ static PFN_encodeTiled_t g_encode = nullptr;
 static std::once_flag g_encode_once;
 
 int encode_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                const uint32_t* box) {
+                const uint32_t* box, bool swizzle128) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -61,7 +61,8 @@ int encode_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dim
     if (i + 1 < rank) s[i] = strides_bytes[i];
   }
   CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base), d, s, b, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(WL_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return WL_OK;

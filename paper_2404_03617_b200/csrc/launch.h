@@ -10,7 +10,7 @@ namespace wl {
 int set_error(int code, const char* fmt, ...);
 int check_cuda(cudaError_t e, const char* what);
 int encode_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                const uint32_t* box);
+                const uint32_t* box, bool swizzle128 = false);
 void put_h(uint8_t* base, size_t off, float v);
 static inline size_t core_off_h(int row, int k, int lbo) {
   return (size_t)(k / 8) * lbo + (size_t)(row / 8) * 128 + (size_t)(row % 8) * 16 + (size_t)(k % 8) * 2;

@@ -48,6 +48,12 @@ struct MbFrontArgs {
   float* gates;          // (n, hid) SE gates
   int* counters;         // (groups) zero-initialised arrival counters
   long long* trace;      // debug: per-phase clock64 stamps of CTA 0 (null = off)
+  // fused projection (one launch per block): gated h2 (re-read from L2) x W_prj
+  int fused, K, n_pt, HCb, nchb, vchunk_bytes, residual, sa, SQP;
+  int s_pa, s_pv, s_gate, t_z;
+  const uint8_t* wback;  // back blob: [b_prj fp32][V chunks]
+  const __half* x;       // residual source (n, H, W, C)
+  __half* z;             // (n, Ho, Wo, K)
 };
 
 struct MbBackArgs {
@@ -70,6 +76,7 @@ struct FrontBars {
   uint64_t w_full[4], w_empty[4];
   uint64_t e_full[2], c_full[2], c_empty[2];
   uint64_t h1_full[2], h1_empty[2], x_ready;
+  uint64_t pa_full[4], pa_ready[4], pa_empty[4], pv_full[3], pv_empty[3], z_full;
   uint32_t tmem_base;
   int last;
 };
@@ -113,7 +120,7 @@ __device__ __forceinline__ int st_off(int p, int g, int st_rows, int groups8) {
 template <int ACT>
 __global__ void __launch_bounds__(mbk::kThreads, 1)
     mb_front_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_h2,
-                    const __grid_constant__ MbFrontArgs a) {
+                    const __grid_constant__ CUtensorMap tmap_h2l, const __grid_constant__ MbFrontArgs a) {
   using namespace mbk;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* s_x = smem + a.s_x;
@@ -128,6 +135,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   FrontBars& B = *reinterpret_cast<FrontBars*>(smem + a.s_bar);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int group = blockIdx.x / a.ranges, range = blockIdx.x % a.ranges;
+  if ((smem_u32(smem) & 1023) != 0) __trap();  // swizzled tiles need 1024-byte alignment
   const int n0 = group * a.imgs;
   const int h0 = range * a.HR;
   const int S = a.ring_stages, HC = a.HC, nch = a.nch, G8 = HC / 8;
@@ -179,6 +187,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_init(&B.h1_empty[i], a.T8 ? 1 : 256);
     }
     mbar_init(&B.x_ready, 256);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&B.pa_full[i], 1);
+      mbar_init(&B.pa_ready[i], 256);
+      mbar_init(&B.pa_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&B.pv_full[i], 1);
+      mbar_init(&B.pv_empty[i], 1);
+    }
+    mbar_init(&B.z_full, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -496,64 +514,244 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   __threadfence();  // publish this CTA's pool slice before arriving
   tc_fence_before();
   __syncthreads();
+  const int a_tile = 128 * a.HCb * 2, a_stage = a.n_pt * a_tile;
+  uint8_t* s_pa = smem + a.s_pa;
+  uint8_t* s_pv = smem + a.s_pv;
+  const uint8_t* vch = a.wback + align_up(a.K * 4, 128);
+  auto load_a = [&](int j) {  // h2 rows of chunk j (re-read from L2) -> A stage
+    const int ab = j % a.sa;
+    mbar_arrive_expect_tx(&B.pa_full[ab], a_stage);
+    for (int t = 0; t < a.n_pt; ++t)  // 2-D box (64 channels x 128 rows), 128-byte swizzle
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+          "%3}], [%4];" ::"r"(smem_u32(s_pa + ab * a_stage + t * a_tile)),
+          "l"(&tmap_h2l), "r"(j * 64), "r"(group * a.P_out + t * 128), "r"(smem_u32(&B.pa_full[ab]))
+          : "memory");
+  };
+  auto load_v = [&](int j) {
+    const int vs = j % 3;
+    mbar_arrive_expect_tx(&B.pv_full[vs], a.vchunk_bytes);
+    bulk_g2s(s_pv + vs * a.vchunk_bytes, vch + (size_t)j * a.vchunk_bytes, a.vchunk_bytes, &B.pv_full[vs]);
+  };
   if (threadIdx.x == 0) {
     __threadfence();
     const int old = atomicAdd(&a.counters[group], 1);
     B.last = (old == a.ranges - 1);
+    if (a.fused) {  // the projection's first operand loads overlap the squeeze-excite
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // h2 TMA stores -> TMA loads
+      for (int j = 0; j < a.nchb && j < a.sa; ++j) load_a(j);
+      for (int j = 0; j < a.nchb && j < 3; ++j) load_v(j);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) WL_TRACE(9);
   if (B.last) {
     __threadfence();
-    const float* wsq = reinterpret_cast<const float*>(a.wpack + a.o_wsq);  // [hid][sq]
+    // fp16 weights: w_sq [hid][SQP], w_ex^T [hid][SQP] (SQP = sq padded to a power of two >= 8)
+    const __half* wsq = reinterpret_cast<const __half*>(a.wpack + a.o_wsq);
     const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
-    const float* wex = reinterpret_cast<const float*>(a.wpack + a.o_wex);  // [sq][hid]
+    const __half* wexT = reinterpret_cast<const __half*>(a.wpack + a.o_wex);
     const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_bex);
-    float* s_vec = reinterpret_cast<float*>(s_h1);  // scratch: pool[hid], partial[parts*sq], s[sq]
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int parts = nt / a.sq;
-    for (int im = 0; im < a.imgs; ++im) {
-      const float* pool = a.pool + (size_t)(n0 + im) * a.hid;
-      for (int i = tid; i < a.hid; i += nt) s_vec[i] = __ldcg(pool + i);
-      __syncthreads();
-      float* part = s_vec + a.hid;
-      if (tid < parts * a.sq) {
-        const int jj = tid % a.sq, pt = tid / a.sq;
-        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-        int i = pt;
-        for (; i + 3 * parts < a.hid; i += 4 * parts) {
-          acc0 += s_vec[i] * wsq[(size_t)i * a.sq + jj];
-          acc1 += s_vec[i + parts] * wsq[(size_t)(i + parts) * a.sq + jj];
-          acc2 += s_vec[i + 2 * parts] * wsq[(size_t)(i + 2 * parts) * a.sq + jj];
-          acc3 += s_vec[i + 3 * parts] * wsq[(size_t)(i + 3 * parts) * a.sq + jj];
+    float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;  // [imgs][hid] pool
+    float* s_red = s_vec + a.imgs * a.hid;                                       // [20 warps][imgs][SQP]
+    float* s_sq = s_red + 20 * a.imgs * a.SQP;                                   // [imgs][SQP]
+    float* s_gt = reinterpret_cast<float*>(smem + a.s_gate);
+    const int tid = threadIdx.x, nt = blockDim.x, nw = nt / 32;
+    for (int i = tid; i < a.imgs * a.hid; i += nt) {
+      const int im = i / a.hid;
+      s_vec[i] = __ldcg(a.pool + (size_t)(n0 + im) * a.hid + (i - im * a.hid));
+    }
+    __syncthreads();
+    // squeeze: lane = (row sub-index, 8-column block jb); each thread walks rows
+    const int JB = a.SQP / 8, sub = 32 / JB;
+    const int jb = lane % JB, isub = lane / JB;
+    float acc[2][8];
+#pragma unroll
+    for (int im = 0; im < 2; ++im)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[im][k] = 0.f;
+    for (int i0 = warp * sub + isub; i0 < a.hid; i0 += 4 * nw * sub) {
+      uint4 wq[4];  // four independent 16-byte loads in flight
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nw * sub;
+        wq[u] = i < a.hid ? *reinterpret_cast<const uint4*>(wsq + (size_t)i * a.SQP + jb * 8) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nw * sub;
+        if (i >= a.hid) break;
+        float wv[8];
+        unpack8(wq[u], wv);
+        const float p0 = s_vec[i], p1 = a.imgs > 1 ? s_vec[a.hid + i] : 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          acc[0][k] += p0 * wv[k];
+          acc[1][k] += p1 * wv[k];
         }
-        for (; i < a.hid; i += parts) acc0 += s_vec[i] * wsq[(size_t)i * a.sq + jj];
-        part[tid] = (acc0 + acc1) + (acc2 + acc3);
       }
-      __syncthreads();
-      float* sv = part + parts * a.sq;
-      if (tid < a.sq) {
-        float acc = bsq[tid];
-        for (int pt = 0; pt < parts; ++pt) acc += part[pt * a.sq + tid];
-        sv[tid] = fmaxf(acc, 0.f);
+    }
+#pragma unroll
+    for (int m = JB; m < 32; m <<= 1)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        acc[0][k] += __shfl_xor_sync(0xffffffffu, acc[0][k], m);
+        acc[1][k] += __shfl_xor_sync(0xffffffffu, acc[1][k], m);
       }
-      __syncthreads();
-      for (int i = tid; i < a.hid; i += nt) {
-        float acc0 = bex[i], acc1 = 0.f;
-        int jj = 0;
-        for (; jj + 1 < a.sq; jj += 2) {
-          acc0 += sv[jj] * wex[(size_t)jj * a.hid + i];
-          acc1 += sv[jj + 1] * wex[(size_t)(jj + 1) * a.hid + i];
+    if (isub == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_red[(warp * a.imgs) * a.SQP + jb * 8 + k] = acc[0][k];
+      if (a.imgs > 1)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s_red[(warp * a.imgs + 1) * a.SQP + jb * 8 + k] = acc[1][k];
+    }
+    __syncthreads();
+    for (int i = tid; i < a.imgs * a.SQP; i += nt) {
+      const int im = i / a.SQP, j = i - im * a.SQP;
+      float v = bsq[j];
+      for (int w2 = 0; w2 < nw; ++w2) v += s_red[(w2 * a.imgs + im) * a.SQP + j];
+      s_sq[i] = fmaxf(v, 0.f);
+    }
+    __syncthreads();
+    // excite: one hidden channel per thread, its SQP weights as 16-byte vectors
+    for (int i = tid; i < a.hid; i += nt) {
+      float e0 = bex[i], e1 = bex[i];
+      uint4 wq[8];
+#pragma unroll
+      for (int b8 = 0; b8 < 8; ++b8)
+        if (b8 < JB) wq[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8);
+      for (int b8 = 0; b8 < JB; ++b8) {
+        float wv[8];
+        unpack8(b8 < 8 ? wq[b8] : *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8), wv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          e0 += s_sq[b8 * 8 + k] * wv[k];
+          if (a.imgs > 1) e1 += s_sq[a.SQP + b8 * 8 + k] * wv[k];
         }
-        if (jj < a.sq) acc0 += sv[jj] * wex[(size_t)jj * a.hid + i];
-        a.gates[(size_t)(n0 + im) * a.hid + i] = __fdividef(1.f, 1.f + __expf(-(acc0 + acc1)));
       }
-      __syncthreads();
+      for (int im = 0; im < a.imgs; ++im) {
+        const float gv = __fdividef(1.f, 1.f + __expf(-(im ? e1 : e0)));
+        a.gates[(size_t)(n0 + im) * a.hid + i] = gv;
+        s_gt[im * a.hid + i] = gv;
+      }
     }
     if (threadIdx.x == 0) a.counters[group] = 0;  // self-cleaning for the next launch
   }
   if (threadIdx.x == 0) WL_TRACE(10);
   __syncthreads();
+  if (a.fused) {
+    // ---------------- projection: z = (h2 . gate) W_prj + b_prj (+ x). The
+    // phase-1 buffers are dead: A (h2 rows, re-read by TMA from L2) and V
+    // rings overlay them; Z accumulates in the expand/conv TMEM columns.
+    const float* s_gate = reinterpret_cast<const float*>(smem + a.s_gate);
+    const int pix_img = a.Ho * a.Wo;
+    if (threadIdx.x == 0) WL_TRACE(11);
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int j = 0; j < a.nchb; ++j) {
+          const int jn = j + a.sa, jv = j + 3;  // refill the stage chunk j frees
+          if (jn < a.nchb) {
+            mbar_wait(&B.pa_empty[j % a.sa], (j / a.sa) & 1);
+            load_a(jn);
+          }
+          if (jv < a.nchb) {
+            mbar_wait(&B.pv_empty[j % 3], (j / 3) & 1);
+            load_v(jv);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        const uint32_t idesc = make_idesc_f16(128, a.K);
+        for (int j = 0; j < a.nchb; ++j) {
+          const int ab = j % a.sa, vs = j % 3;
+          mbar_wait(&B.pa_ready[ab], (j / a.sa) & 1);
+          mbar_wait(&B.pv_full[vs], (j / 3) & 1);
+          tc_fence_after();
+          const uint64_t b_base = make_sdesc(smem_u32(s_pv + vs * a.vchunk_bytes), a.K * 16, 128);
+          for (int t = 0; t < a.n_pt; ++t) {
+            const uint64_t a_base = make_sdesc_sw128(smem_u32(s_pa + ab * a_stage + t * a_tile));
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ss(tmem + a.t_z + t * a.K, a_base + (uint64_t)(kk * 2), b_base + (uint64_t)(kk * 2 * a.K), idesc,
+                     (j > 0 || kk > 0));
+          }
+          mma_commit(&B.pa_empty[ab]);
+          mma_commit(&B.pv_empty[vs]);
+        }
+        mma_commit(&B.z_full);
+      }
+    } else if (warp >= 4 && warp < 12) {
+      // gate the staged h2 rows in place (packed half)
+      const int tid = (warp - 4) * 32 + lane;
+      for (int j = 0; j < a.nchb; ++j) {
+        const int ab = j % a.sa;
+        mbar_wait(&B.pa_full[ab], (j / a.sa) & 1);
+        for (int r = tid; r < a.n_pt * 128; r += 256) {
+          const int t = r >> 7, m = r & 127;
+          const int p = min(t * 128 + m, a.P_out - 1);
+          const float* g = s_gate + (p / pix_img) * a.hid + j * a.HCb;
+          uint8_t* base = s_pa + ab * a_stage + t * a_tile;
+          for (int c8 = 0; c8 < 8; ++c8) {
+            uint4* ptr = reinterpret_cast<uint4*>(base + sw128_off(m, c8));
+            uint4 v = *ptr;
+            __half2* h = reinterpret_cast<__half2*>(&v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              h[i] = __hmul2(h[i], __floats2half2_rn(g[c8 * 8 + 2 * i], g[c8 * 8 + 2 * i + 1]));
+            *ptr = v;
+          }
+        }
+        fence_async_smem();
+        mbar_arrive(&B.pa_ready[ab]);
+      }
+    } else if (warp >= 12) {
+      const int q = warp % 4, hh = (warp - 12) / 4;
+      const float* bprj = reinterpret_cast<const float*>(a.wback);
+      mbar_wait(&B.z_full, 0);
+      tc_fence_after();
+      for (int t = 0; t < a.n_pt; ++t) {
+        const int p = t * 128 + q * 32 + lane;
+        const bool inside = p < a.P_out;
+        const size_t gp = (size_t)group * a.P_out + (inside ? p : 0);  // dense (n, Ho*Wo) pixel
+        // residual rows are fetched up front (independent loads), then combined
+        uint4 res[16];
+        const int nblk = (a.K - hh * 16 + 31) / 32;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (b < nblk && a.residual) {
+            const uint4* xp = reinterpret_cast<const uint4*>(a.x + gp * a.K + hh * 16 + b * 32);
+            res[2 * b] = xp[0];
+            res[2 * b + 1] = xp[1];
+          }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (b >= nblk) break;
+          const int c0 = hh * 16 + b * 32;
+          uint32_t v[16];
+          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * a.K + c0), v);
+          tmem_ld_wait();
+          if (!inside) continue;
+          float f[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bprj[c0 + i];
+          if (a.residual) {
+            float r[16];
+            unpack8(res[2 * b], r);
+            unpack8(res[2 * b + 1], r + 8);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] += r[i];
+          }
+          uint4* zp = reinterpret_cast<uint4*>(a.z + gp * a.K + c0);
+          zp[0] = pack8(f);
+          zp[1] = pack8(f + 8);
+        }
+      }
+      tc_fence_before();
+      if (warp == 12 && lane == 0) WL_TRACE(12);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) WL_TRACE(13);
+  }
   if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
 }
 
@@ -712,7 +910,7 @@ struct MbPlanH {
   int64_t h2_bytes, pool_bytes, gate_bytes;
 };
 
-bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
+bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   memset(&P, 0, sizeof(P));
   MbFrontArgs& f = P.f;
   MbBackArgs& b = P.b;
@@ -746,8 +944,8 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   f.st_rows = f.P_out / f.st_stores;
   if (f.groups > (int)(kCounterBytes / 4)) return false;
   if (f.sq < 1 || f.sq > 128) return false;
-  f.ranges = 1;
-  while (f.groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
+  f.ranges = 1;  // fused mode: the CTA owns every hidden channel of its images
+  while (!want_fused && f.groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
   f.HR = hid / f.ranges;
   f.HC = 0;
   const int x_bytes = (C / 8) * f.x_alloc * 16;
@@ -805,13 +1003,19 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   f.u_bytes = f.HC * C * 2;
   f.chunk_bytes = f.u_bytes + (f.T8 ? (2 * (f.HC / 16) * 9 + 1) * 128 : 0);
   f.ring_stages = 2;  // raised to 3 below when shared memory allows
-  int so = 0;  // SE section (fp32) at the start of the front blob
+  // SE section at the start of the front blob: fp16 w_sq [hid][SQP] and
+  // w_ex^T [hid][SQP] (SQP = squeeze width padded to a power of two >= 8,
+  // zero-filled), fp32 biases
+  f.SQP = 8;
+  while (f.SQP < f.sq) f.SQP *= 2;
+  if (f.SQP > 256) return false;
+  int so = 0;
   f.o_wsq = so;
-  so = align_up(so + hid * f.sq * 4, 16);
+  so = align_up(so + hid * f.SQP * 2, 16);
   f.o_bsq = so;
-  so = align_up(so + f.sq * 4, 16);
+  so = align_up(so + f.SQP * 4, 16);
   f.o_wex = so;
-  so = align_up(so + f.sq * hid * 4, 16);
+  so = align_up(so + hid * f.SQP * 2, 16);
   f.o_bex = so;
   so = align_up(so + hid * 4, 16);
   f.se_bytes = align_up(so, 128);
@@ -851,11 +1055,36 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
     f.s_h1b = o;
     o = align_up(o + h1_one, 128);
   }
+  f.s_gate = o;  // SE gates (read by the fused projection) + squeeze-excite scratch
+  o = align_up(o + (2 * f.imgs * hid + 21 * f.imgs * f.SQP) * 4, 128);
   f.s_bar = o;
   o += 512;
   f.smem = o;
   if (o > kSmemMaxMb) return false;
   P.front_bytes = f.se_bytes + (int64_t)f.ranges * f.hdr_bytes + (int64_t)f.ranges * f.nch * f.chunk_bytes;
+  f.fused = 0;
+  if (want_fused) {
+    // projection overlays the dead phase-1 buffers: A ring (2 stages of the
+    // CTA's h2 rows), V ring (3 stages); Z in the expand/conv TMEM columns
+    f.K = K;
+    if (hid % 64) return false;  // 128-byte swizzled h2 tiles: 64-channel chunks
+    f.HCb = 64;
+    f.nchb = hid / f.HCb;
+    f.n_pt = (f.P_out + 127) / 128;
+    f.vchunk_bytes = K * f.HCb * 2;
+    f.residual = d.stride == 1;
+    f.t_z = f.t_e;
+    f.s_pa = 0;
+    if (K > 256 || f.t_z + f.n_pt * K > f.tmem_cols) return false;
+    const int a_stage = f.n_pt * 128 * f.HCb * 2;
+    f.sa = 0;
+    for (int sa = std::min(4, std::max(2, f.nchb)); sa >= 2 && !f.sa; --sa) {
+      f.s_pv = align_up(sa * a_stage, 128);
+      if (f.s_pv + 3 * f.vchunk_bytes <= f.s_gate) f.sa = sa;
+    }
+    if (!f.sa) return false;
+    f.fused = 1;
+  }
 
   // ---- back
   b.hid = hid;
@@ -866,7 +1095,7 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   b.residual = d.stride == 1;
   const int ntiles = (b.P + 127) / 128;
   b.KR = K;
-  while (b.KR > 256 || (ntiles * (K / b.KR) < kNumSMs && b.KR % 32 == 0 && b.KR >= 64)) b.KR /= 2;
+  while (!f.fused && (b.KR > 256 || (ntiles * (K / b.KR) < kNumSMs && b.KR % 32 == 0 && b.KR >= 64))) b.KR /= 2;
   if (K % b.KR || b.KR % 16) return false;
   b.kranges = K / b.KR;
   b.HCb = hid % 64 == 0 ? 64 : (hid % 32 == 0 ? 32 : 16);
@@ -895,7 +1124,10 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
   return true;
 }
 
-using FrontK = void (*)(const CUtensorMap, const CUtensorMap, const MbFrontArgs);
+// one launch per block when the projection fits (fused); else front + back
+bool mb_plan(const wl_block_desc& d, MbPlanH& P) { return mb_plan_try(d, P, true) || mb_plan_try(d, P, false); }
+
+using FrontK = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const MbFrontArgs);
 
 FrontK front_kernel(int act) {
   switch (act) {
@@ -965,9 +1197,12 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   memset(out, 0, (size_t)(P.front_bytes + P.back_bytes));
   const int C = d.c, hid = f.hid, T = d.group_width, K = d.k, sq = d.se_sq;
   const float *wexp = w[0], *bexp = w[1], *wconv = w[2], *bconv = w[3];
-  memcpy(out + f.o_wsq, w[4], sizeof(float) * hid * sq);
+  for (int i = 0; i < hid; ++i)
+    for (int j = 0; j < sq; ++j) {
+      put_h(out + f.o_wsq, ((size_t)i * f.SQP + j) * 2, w[4][(size_t)i * sq + j]);   // w_sq (hid, sq)
+      put_h(out + f.o_wex, ((size_t)i * f.SQP + j) * 2, w[6][(size_t)j * hid + i]);  // w_ex (sq, hid)^T
+    }
   memcpy(out + f.o_bsq, w[5], sizeof(float) * sq);
-  memcpy(out + f.o_wex, w[6], sizeof(float) * sq * hid);
   memcpy(out + f.o_bex, w[7], sizeof(float) * hid);
   for (int r = 0; r < f.ranges; ++r) {
     uint8_t* hdr = out + f.se_bytes + (size_t)r * f.hdr_bytes;
@@ -1047,8 +1282,19 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     const uint32_t box_l[3] = {8, 128, (uint32_t)(b.HCb / 8)};
     if (int e = encode_tmap(&th_load, h2, 3, dims, strides, box_l)) return e;
   }
-  front_kernel(d.act)<<<f.groups * f.ranges, mbk::kThreads, f.smem, st>>>(tx, th_store, f);
+  f.wback = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
+  f.x = reinterpret_cast<const __half*>(x);
+  f.z = reinterpret_cast<__half*>(z);
+  CUtensorMap th_fused = th_load;
+  if (f.fused) {
+    const uint64_t dims[2] = {(uint64_t)f.hid, (uint64_t)b.P};
+    const uint64_t strides[1] = {(uint64_t)f.hid * 2};
+    const uint32_t box[2] = {64, 128};
+    if (int e = encode_tmap(&th_fused, h2, 2, dims, strides, box, true)) return e;
+  }
+  front_kernel(d.act)<<<f.groups * f.ranges, mbk::kThreads, f.smem, st>>>(tx, th_store, th_fused, f);
   if (int e = check_cuda(cudaGetLastError(), "mb_front launch")) return e;
+  if (f.fused) return WL_OK;
   b.wpack = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
   b.gates = f.gates;
   b.x = reinterpret_cast<const __half*>(x);

@@ -111,6 +111,23 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)1 << 46;  // descriptor version for sm_100
   return d;                // base offset 0, legacy LBO mode, SWIZZLE_NONE
 }
+// K-major operand in the 128-byte-swizzle canonical layout: rows of 64 fp16
+// (128 B) in 1024-byte atoms of 8 rows, 16-byte chunk j of row r stored at
+// chunk (j ^ r % 8). TMA writes it with CU_TENSOR_MAP_SWIZZLE_128B; a K=16
+// step inside the atom advances the start address by 32 bytes (+2 units).
+__device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO: unused for swizzled K-major
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+// byte offset of 16-byte chunk c8 of row r in a 128B-swizzled tile
+__host__ __device__ __forceinline__ uint32_t sw128_off(int r, int c8) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4));
+}
 // kind::f16 instruction descriptor: fp16 A/B, fp32 accumulate, both K-major.
 __host__ __device__ constexpr uint32_t make_idesc_f16(uint32_t M, uint32_t N) {
   return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);

@@ -22,7 +22,8 @@ for nm in sys.argv[1:]:
     t = buf.cpu().tolist()
     t0 = t[0]
     rel = lambda v: (v - t0) if v else -1
-    print(nm, "producer start", rel(t[1]), "x loaded", rel(t[2]), "pool done", rel(t[8]), "SE start", rel(t[9]), "end", rel(t[10]))
+    print(nm, "producer start", rel(t[1]), "x loaded", rel(t[2]), "pool done", rel(t[8]), "SE start", rel(t[9]), "SE end", rel(t[10]),
+          "proj start", rel(t[11]), "z stored", rel(t[12]), "end", rel(t[13]))
     for j in range(12):
         row = t[16 + 8 * j: 16 + 8 * j + 7]
         if not any(row): break
