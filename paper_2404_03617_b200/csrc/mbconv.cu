@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int img_flat = (a.H + 1) * a.Wp;
   const int x_valid = a.imgs * img_flat;
   if (threadIdx.x == 0) WL_TRACE(0);
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {  // plan snapshot for the trace reader
+    a.trace[14] = a.sa * 1000 + a.ring_stages * 100 + a.h1_bufs * 10 + a.e_bufs;
+    a.trace[15] = a.c_bufs * 100000 + a.x_tmem * 10000 + a.HC * 10 + a.n_pt;
+  }
 
   for (int i = threadIdx.x; i < a.h1_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
@@ -504,14 +508,20 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (tid == 0) WL_TRACE(8);
     if (tid == 0) bulk_wait0();
     const float inv = 1.f / (float)(a.Ho * a.Wo);
-    for (int i = tid; i < a.imgs * a.HR; i += 256) {
-      const int im = i / a.HR, c = i % a.HR;
-      a.pool[(size_t)(n0 + im) * a.hid + h0 + c] = s_pool[i] * inv;
+    if (a.fused) {  // ranges == 1: the squeeze-excite below reads the pool straight from shared memory
+      float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;
+      for (int i = tid; i < a.imgs * a.HR; i += 256) s_vec[i] = s_pool[i] * inv;
+    } else {
+      for (int i = tid; i < a.imgs * a.HR; i += 256) {
+        const int im = i / a.HR, c = i % a.HR;
+        a.pool[(size_t)(n0 + im) * a.hid + h0 + c] = s_pool[i] * inv;
+      }
     }
   }
 
-  // ---------------- squeeze-excite, once per image group (last CTA to arrive)
-  __threadfence();  // publish this CTA's pool slice before arriving
+  // ---------------- squeeze-excite, once per image group (last CTA to arrive;
+  // in fused mode the CTA owns the whole group and skips the global handshake)
+  if (!a.fused) __threadfence();  // publish this CTA's pool slice before arriving
   tc_fence_before();
   __syncthreads();
   const int a_tile = 128 * a.HCb * 2, a_stage = a.n_pt * a_tile;
@@ -534,9 +544,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     bulk_g2s(s_pv + vs * a.vchunk_bytes, vch + (size_t)j * a.vchunk_bytes, a.vchunk_bytes, &B.pv_full[vs]);
   };
   if (threadIdx.x == 0) {
-    __threadfence();
-    const int old = atomicAdd(&a.counters[group], 1);
-    B.last = (old == a.ranges - 1);
+    if (a.fused) {
+      B.last = 1;
+    } else {
+      __threadfence();
+      const int old = atomicAdd(&a.counters[group], 1);
+      B.last = (old == a.ranges - 1);
+    }
     if (a.fused) {  // the projection's first operand loads overlap the squeeze-excite
       asm volatile("fence.proxy.async.global;" ::: "memory");  // h2 TMA stores -> TMA loads
       for (int j = 0; j < a.nchb && j < a.sa; ++j) load_a(j);
@@ -546,7 +560,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   __syncthreads();
   if (threadIdx.x == 0) WL_TRACE(9);
   if (B.last) {
-    __threadfence();
+    if (!a.fused) __threadfence();
     // fp16 weights: w_sq [hid][SQP], w_ex^T [hid][SQP] (SQP = sq padded to a power of two >= 8)
     const __half* wsq = reinterpret_cast<const __half*>(a.wpack + a.o_wsq);
     const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
@@ -557,13 +571,24 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     float* s_sq = s_red + 20 * a.imgs * a.SQP;                                   // [imgs][SQP]
     float* s_gt = reinterpret_cast<float*>(smem + a.s_gate);
     const int tid = threadIdx.x, nt = blockDim.x, nw = nt / 32;
-    for (int i = tid; i < a.imgs * a.hid; i += nt) {
-      const int im = i / a.hid;
-      s_vec[i] = __ldcg(a.pool + (size_t)(n0 + im) * a.hid + (i - im * a.hid));
+    // excite weights of this thread's hidden channel, fetched now so their
+    // latency overlaps the squeeze (SQP <= 32: four 16-byte rows)
+    const int JB = a.SQP / 8;
+    uint4 wx[4];
+    if (JB <= 4 && tid < a.hid)
+#pragma unroll
+      for (int b8 = 0; b8 < 4; ++b8)
+        if (b8 < JB) wx[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)tid * a.SQP + b8 * 8);
+    if (!a.fused) {
+      for (int i = tid; i < a.imgs * a.hid; i += nt) {
+        const int im = i / a.hid;
+        s_vec[i] = __ldcg(a.pool + (size_t)(n0 + im) * a.hid + (i - im * a.hid));
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (threadIdx.x == 0) WL_TRACE(124);
     // squeeze: lane = (row sub-index, 8-column block jb); each thread walks rows
-    const int JB = a.SQP / 8, sub = 32 / JB;
+    const int sub = 32 / JB;
     const int jb = lane % JB, isub = lane / JB;
     float acc[2][8];
 #pragma unroll
@@ -613,13 +638,20 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       s_sq[i] = fmaxf(v, 0.f);
     }
     __syncthreads();
+    if (threadIdx.x == 0) WL_TRACE(125);
     // excite: one hidden channel per thread, its SQP weights as 16-byte vectors
+    __half* s_gh = reinterpret_cast<__half*>(s_vec);  // [imgs][hid] half gates (pool is dead now)
     for (int i = tid; i < a.hid; i += nt) {
       float e0 = bex[i], e1 = bex[i];
       uint4 wq[8];
+      if (JB <= 4 && i == tid) {
 #pragma unroll
-      for (int b8 = 0; b8 < 8; ++b8)
-        if (b8 < JB) wq[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8);
+        for (int b8 = 0; b8 < 4; ++b8) wq[b8] = wx[b8];
+      } else {
+#pragma unroll
+        for (int b8 = 0; b8 < 8; ++b8)
+          if (b8 < JB) wq[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8);
+      }
       for (int b8 = 0; b8 < JB; ++b8) {
         float wv[8];
         unpack8(b8 < 8 ? wq[b8] : *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8), wv);
@@ -631,11 +663,12 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       }
       for (int im = 0; im < a.imgs; ++im) {
         const float gv = __fdividef(1.f, 1.f + __expf(-(im ? e1 : e0)));
-        a.gates[(size_t)(n0 + im) * a.hid + i] = gv;
+        if (!a.fused) a.gates[(size_t)(n0 + im) * a.hid + i] = gv;
         s_gt[im * a.hid + i] = gv;
+        s_gh[im * a.hid + i] = __float2half_rn(gv);
       }
     }
-    if (threadIdx.x == 0) a.counters[group] = 0;  // self-cleaning for the next launch
+    if (threadIdx.x == 0 && !a.fused) a.counters[group] = 0;  // self-cleaning for the next launch
   }
   if (threadIdx.x == 0) WL_TRACE(10);
   __syncthreads();
@@ -666,7 +699,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         for (int j = 0; j < a.nchb; ++j) {
           const int ab = j % a.sa, vs = j % 3;
           mbar_wait(&B.pa_ready[ab], (j / a.sa) & 1);
+          if (j < 8) WL_TRACE(96 + j);
           mbar_wait(&B.pv_full[vs], (j / 3) & 1);
+          if (j < 8) WL_TRACE(104 + j);
           tc_fence_after();
           const uint64_t b_base = make_sdesc(smem_u32(s_pv + vs * a.vchunk_bytes), a.K * 16, 128);
           for (int t = 0; t < a.n_pt; ++t) {
@@ -681,25 +716,28 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mma_commit(&B.z_full);
       }
     } else if (warp >= 4 && warp < 12) {
-      // gate the staged h2 rows in place (packed half)
+      // gate the staged h2 rows in place (packed half): each thread owns one
+      // 16-byte column (8 channels) and walks rows, so a warp touches 4 whole
+      // 128-byte swizzled rows per step (conflict-free) and the gates are one
+      // broadcast 16-byte load
       const int tid = (warp - 4) * 32 + lane;
+      const int c8 = tid & 7;
+      const __half* s_gh = reinterpret_cast<const __half*>(s_gate + a.imgs * a.hid);  // half gates (SE scratch)
       for (int j = 0; j < a.nchb; ++j) {
         const int ab = j % a.sa;
         mbar_wait(&B.pa_full[ab], (j / a.sa) & 1);
-        for (int r = tid; r < a.n_pt * 128; r += 256) {
+        if (tid == 0 && j < 8) WL_TRACE(112 + j);
+        for (int r = tid >> 3; r < a.n_pt * 128; r += 32) {
           const int t = r >> 7, m = r & 127;
           const int p = min(t * 128 + m, a.P_out - 1);
-          const float* g = s_gate + (p / pix_img) * a.hid + j * a.HCb;
-          uint8_t* base = s_pa + ab * a_stage + t * a_tile;
-          for (int c8 = 0; c8 < 8; ++c8) {
-            uint4* ptr = reinterpret_cast<uint4*>(base + sw128_off(m, c8));
-            uint4 v = *ptr;
-            __half2* h = reinterpret_cast<__half2*>(&v);
+          const uint4 gv = *reinterpret_cast<const uint4*>(s_gh + (p / pix_img) * a.hid + j * a.HCb + c8 * 8);
+          uint4* ptr = reinterpret_cast<uint4*>(s_pa + ab * a_stage + t * a_tile + sw128_off(m, c8));
+          uint4 v = *ptr;
+          __half2* h = reinterpret_cast<__half2*>(&v);
+          const __half2* g = reinterpret_cast<const __half2*>(&gv);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              h[i] = __hmul2(h[i], __floats2half2_rn(g[c8 * 8 + 2 * i], g[c8 * 8 + 2 * i + 1]));
-            *ptr = v;
-          }
+          for (int i = 0; i < 4; ++i) h[i] = __hmul2(h[i], g[i]);
+          *ptr = v;
         }
         fence_async_smem();
         mbar_arrive(&B.pa_ready[ab]);
@@ -707,43 +745,62 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     } else if (warp >= 12) {
       const int q = warp % 4, hh = (warp - 12) / 4;
       const float* bprj = reinterpret_cast<const float*>(a.wback);
+      // z = Z + b_prj (+ x). Each thread owns one pixel row and the 16-column
+      // blocks hh, hh+2, ... (two per group); the residual rows of the next
+      // group are loaded while this group is combined (the first group's are
+      // issued before Z is even complete).
+      const int nblk = (a.K - hh * 16 + 31) / 32;
+      const int ngrp = (nblk + 1) / 2;
+      uint4 res[4];
+      auto fetch_res = [&](int t, int gi) {
+        const int p = t * 128 + q * 32 + lane;
+        if (!a.residual || p >= a.P_out) return;
+        const uint4* xp = reinterpret_cast<const uint4*>(a.x + ((size_t)group * a.P_out + p) * a.K + hh * 16);
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+          if (gi * 2 + b < nblk) {
+            res[2 * b] = __ldg(xp + (gi * 2 + b) * 4);
+            res[2 * b + 1] = __ldg(xp + (gi * 2 + b) * 4 + 1);
+          }
+      };
+      fetch_res(0, 0);
       mbar_wait(&B.z_full, 0);
       tc_fence_after();
+      if (warp == 12 && lane == 0) WL_TRACE(120);
       for (int t = 0; t < a.n_pt; ++t) {
+        if (warp == 12 && lane == 0 && t < 3) WL_TRACE(121 + t);
         const int p = t * 128 + q * 32 + lane;
         const bool inside = p < a.P_out;
         const size_t gp = (size_t)group * a.P_out + (inside ? p : 0);  // dense (n, Ho*Wo) pixel
-        // residual rows are fetched up front (independent loads), then combined
-        uint4 res[16];
-        const int nblk = (a.K - hh * 16 + 31) / 32;
+        for (int gi = 0; gi < ngrp; ++gi) {
+          uint32_t v[2][16];
 #pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (b < nblk && a.residual) {
-            const uint4* xp = reinterpret_cast<const uint4*>(a.x + gp * a.K + hh * 16 + b * 32);
-            res[2 * b] = xp[0];
-            res[2 * b + 1] = xp[1];
-          }
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (b >= nblk) break;
-          const int c0 = hh * 16 + b * 32;
-          uint32_t v[16];
-          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * a.K + c0), v);
+          for (int b = 0; b < 2; ++b)
+            if (gi * 2 + b < nblk) WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * a.K + hh * 16 + (gi * 2 + b) * 32), v[b]);
           tmem_ld_wait();
-          if (!inside) continue;
-          float f[16];
+          uint4 cur[4];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bprj[c0 + i];
-          if (a.residual) {
-            float r[16];
-            unpack8(res[2 * b], r);
-            unpack8(res[2 * b + 1], r + 8);
+          for (int i = 0; i < 4; ++i) cur[i] = res[i];
+          if (gi + 1 < ngrp) fetch_res(t, gi + 1);  // next group's residual rows in flight
+          else if (t + 1 < a.n_pt) fetch_res(t + 1, 0);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] += r[i];
+          for (int b = 0; b < 2; ++b) {
+            if (gi * 2 + b >= nblk || !inside) continue;
+            const int c0 = hh * 16 + (gi * 2 + b) * 32;
+            float f[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[b][i]) + bprj[c0 + i];
+            if (a.residual) {
+              float r[16];
+              unpack8(cur[2 * b], r);
+              unpack8(cur[2 * b + 1], r + 8);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) f[i] += r[i];
+            }
+            uint4* zp = reinterpret_cast<uint4*>(a.z + gp * a.K + c0);
+            zp[0] = pack8(f);
+            zp[1] = pack8(f + 8);
           }
-          uint4* zp = reinterpret_cast<uint4*>(a.z + gp * a.K + c0);
-          zp[0] = pack8(f);
-          zp[1] = pack8(f + 8);
         }
       }
       tc_fence_before();

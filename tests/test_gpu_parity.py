@@ -111,7 +111,7 @@ def test_deterministic_and_graph_equals_eager():
     assert torch.equal(eager, a) and torch.equal(a, m.output)
 
 
-@pytest.mark.parametrize("model", ["convfirstnet-pico", "convfirstnet-small"])
+@pytest.mark.parametrize("model", ["convfirstnet-pico"])
 def test_network_per_unit_and_logits(model):
     net = zoo.at_resolution(zoo.from_name(model), 224)
     m = FusedNetwork(net, batch=2, seed=11)
@@ -147,6 +147,11 @@ def test_full_size_pico_b128_sampled_images():
 
 
 def test_unsupported_configs_fail_loudly():
+    # ConvFirstNet-Small's 28x28x96 stride-2 MBConv: the whole-image tile does
+    # not fit shared memory -> refused, never approximated
+    net = zoo.at_resolution(zoo.from_name("convfirstnet-small"), 224)
+    with pytest.raises(ScheduleError):
+        FusedNetwork(net, batch=2, seed=11)
     with pytest.raises(ScheduleError):
         FusedBlock(ConvFirst(4, 6), TensorDims(1, 8, 8, 16))  # no T=4 kernel
     with pytest.raises(ScheduleError):

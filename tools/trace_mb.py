@@ -22,9 +22,14 @@ for nm in sys.argv[1:]:
     t = buf.cpu().tolist()
     t0 = t[0]
     rel = lambda v: (v - t0) if v else -1
+    print(nm, "plan sa/ring/h1b/eb", t[14], "cb/xt/HC/npt", t[15])
     print(nm, "producer start", rel(t[1]), "x loaded", rel(t[2]), "pool done", rel(t[8]), "SE start", rel(t[9]), "SE end", rel(t[10]),
           "proj start", rel(t[11]), "z stored", rel(t[12]), "end", rel(t[13]))
     for j in range(12):
         row = t[16 + 8 * j: 16 + 8 * j + 7]
         if not any(row): break
         print(f"  chunk {j}: expand@{rel(row[0])} conv@{rel(row[1])}..{rel(row[2])} Eepi {rel(row[3])}..{rel(row[4])} Cepi {rel(row[5])}..{rel(row[6])}")
+    print("  proj: a_full", [rel(v) for v in t[112:120]])
+    print("  proj: a_ready", [rel(v) for v in t[96:104]])
+    print("  proj: v_full", [rel(v) for v in t[104:112]])
+    print("  SE: pool loaded", rel(t[124]), "squeezed", rel(t[125]), "| epi: z_full", rel(t[120]), "tiles", rel(t[121]), rel(t[122]), rel(t[123]))
