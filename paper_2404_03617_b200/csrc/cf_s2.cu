@@ -25,15 +25,22 @@ namespace wl {
 
 struct Cf2Args {
   int C, K, hid, r, nch;
-  int H, W, Ho, Wo, R, tiles_y, Wp;
-  int n_ct, n_eh, n_pt, conv_base, x_alloc, x_rows;
+  int H, W, Ho, Wo, R, tiles_y, Wp, nbands;
+  int n_ct, n_eh, n_pt, conv_base, x_alloc, x_rows, x_bufs;
   int o_convw, o_bconv, o_a, o_b, w_bytes;  // header: conv taps + fp32 vectors
-  int chunk_bytes, u_bytes;                 // chunk j = [U_j (r x C) | V_j (K x r)], 2-slot ring
-  int s_x, s_xc, s_ah, s_hs, s_aq, s_w, s_ring, s_bar;
+  int chunk_bytes, u_bytes;                 // chunk j = [U_j (r x C) | V_j (K x r)], all resident
+  int s_x, s_xc, s_ah, s_hs, s_zo, s_aq, s_w, s_bar, smem;
+  int ah_bytes, aq_bytes;
   int t_c, t_e, t_z, tmem_cols;
   const uint8_t* wpack;
   __half* z;
+  long long* trace;  // debug: clock64 stamps of CTA 0 (null = off)
 };
+
+#define CF2_TRACE(slot)                                                          \
+  do {                                                                           \
+    if (a.trace && blockIdx.x == 0 && (slot) < 256) a.trace[(slot)] = clock64(); \
+  } while (0)
 
 // Triangle-3 tap [1, 2, 1] / 4 on 8 packed halves
 __device__ __forceinline__ uint4 tri3(const uint4& a, const uint4& b, const uint4& c) {
@@ -48,206 +55,409 @@ __device__ __forceinline__ uint4 tri3(const uint4& a, const uint4& b, const uint
   return o;
 }
 
+namespace cf2k {
+constexpr int kThreads = 640;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 conv/blur_H,
+                               // w8-15 hidden (E -> phi), w16-19 output (Z -> blur_W)
+struct Bars {
+  uint64_t w_full, x_full[2], x_empty[2];
+  uint64_t conv_full, c_empty, xh_full[2], xh_empty[2];
+  uint64_t e_full[2], e_empty[2], q_full[2], q_empty[2];
+  uint64_t z_full, z_empty;
+  uint32_t tmem_base;
+};
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+}  // namespace cf2k
+__device__ __forceinline__ void tma_store_4d_cf2(const void* tmap, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_cf2() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0_cf2() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all_cf2() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+namespace cf2k {
+}  // namespace cf2k
+
+// Persistent CTA over bands of R output rows; the stages of consecutive bands
+// overlap: the tensor core runs the conv of band i+1 and the expand/project
+// chunks of band i while the CUDA-core warp groups drain the accumulators.
+// BlurPool along W commutes with the (linear) projection, so it is applied to
+// the K-channel projection output instead of the hidden activation:
+//   z = blur_W(y) V + b = blur_W(y V) + b     (y = phi(xh U + a))
+// which keeps the hidden-side CUDA-core work to one drain per chunk.
 template <int ACT>
-__global__ void __launch_bounds__(256, 1)
-    cf2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Cf2Args a) {
+__global__ void __launch_bounds__(cf2k::kThreads, 1)
+    cf2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_z,
+               const __grid_constant__ Cf2Args a) {
+  using namespace cf2k;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* s_x = smem + a.s_x;
   __half* s_xc = reinterpret_cast<__half*>(smem + a.s_xc);
   uint8_t* s_ah = smem + a.s_ah;
-  __half* s_hs = reinterpret_cast<__half*>(smem + a.s_hs);
+  __half* s_zs = reinterpret_cast<__half*>(smem + a.s_hs);
+  __half* s_zo = reinterpret_cast<__half*>(smem + a.s_zo);
   uint8_t* s_aq = smem + a.s_aq;
   uint8_t* s_w = smem + a.s_w;
-  uint8_t* s_ring = smem + a.s_ring;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // [0] load, [1] mma, [2..3] chunk slots
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 4);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
-  const int q = warp % 4, half = warp / 4;
-  const int n = blockIdx.x / a.tiles_y, yo0 = (blockIdx.x % a.tiles_y) * a.R;
-  const int C = a.C, K = a.K, r = a.r, W = a.W, Wp = a.Wp;
+  Bars& B = *reinterpret_cast<Bars*>(smem + a.s_bar);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int C = a.C, K = a.K, r = a.r, W = a.W, Wp = a.Wp, nch = a.nch;
   const int planes = C / 8;
   const int loaded = a.x_rows * Wp;
+  const int MH = a.n_eh * 128;
+  const int RW = a.R * W;
+  const int nb = a.nbands > (int)blockIdx.x ? (a.nbands - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto band_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
 
-  for (int i = tid; i < planes * (a.x_alloc - loaded); i += blockDim.x) {
-    const int pl = i / (a.x_alloc - loaded), f = loaded + i % (a.x_alloc - loaded);
-    *reinterpret_cast<uint4*>(s_x + ((size_t)pl * a.x_alloc + f) * 16) = make_uint4(0, 0, 0, 0);
-  }
-  if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+  // zero the conv-tile overrun past the loaded rows (TMA never writes it)
+  for (int xb = 0; xb < a.x_bufs; ++xb)
+    for (int i = threadIdx.x; i < planes * (a.x_alloc - loaded); i += blockDim.x) {
+      const int pl = i / (a.x_alloc - loaded), f = loaded + i % (a.x_alloc - loaded);
+      *reinterpret_cast<uint4*>(s_x + ((size_t)(xb * planes + pl) * a.x_alloc + f) * 16) = make_uint4(0, 0, 0, 0);
+    }
+  if (threadIdx.x == 0) {
+    mbar_init(&B.w_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.x_full[i], 1);
+      mbar_init(&B.x_empty[i], 1);
+      mbar_init(&B.xh_full[i], 128);
+      mbar_init(&B.xh_empty[i], 1);
+      mbar_init(&B.e_full[i], 1);
+      mbar_init(&B.e_empty[i], 256);
+      mbar_init(&B.q_full[i], 256);
+      mbar_init(&B.q_empty[i], 1);
+    }
+    mbar_init(&B.conv_full, 1);
+    mbar_init(&B.c_empty, 128);
+    mbar_init(&B.z_full, 1);
+    mbar_init(&B.z_empty, 128);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc_n(tbase, a.tmem_cols);
+  if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tbase;
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bars[0], planes * loaded * 16 + a.w_bytes);
-    for (int g = 0; g < planes; ++g)
-      tma_load_5d(s_x + (size_t)g * a.x_alloc * 16, &tmap_x, 0, -1, 2 * yo0 - 2, g, n, &bars[0]);
-    bulk_g2s(s_w, a.wpack, a.w_bytes, &bars[0]);
-    mbar_arrive_expect_tx(&bars[2], a.chunk_bytes);
-    bulk_g2s(s_ring, a.wpack + a.w_bytes, a.chunk_bytes, &bars[2]);
-  }
-  mbar_wait(&bars[0], 0);
-  uint32_t mma_phase = 0;
-  auto mma_wait = [&]() {
-    mbar_wait(&bars[1], mma_phase & 1);
-    ++mma_phase;
-    tc_fence_after();
-  };
+  const uint32_t tmem = B.tmem_base;
+  if (threadIdx.x == 0) CF2_TRACE(0);
 
-  // ---------------- grouped 3x3 conv (T = 8) over the flat x rows 1..2R+1
-  if (tid == 0) {
-    tc_fence_after();
-    const uint32_t idesc = make_idesc_f16(128, 16);
-    const uint32_t x0 = smem_u32(s_x), cw = smem_u32(s_w + a.o_convw);
-    for (int t = 0; t < a.n_ct; ++t)
-      for (int pr = 0; pr < C / 16; ++pr)
-        for (int tap = 0; tap < 9; ++tap) {
-          const int f = a.conv_base + t * 128 + (tap / 3 - 1) * Wp + (tap % 3 - 1);
-          const uint64_t ad = make_sdesc(x0 + (2 * pr * a.x_alloc + f) * 16, a.x_alloc * 16, 128);
-          const uint64_t bd = make_sdesc(cw + (pr * 9 + tap) * 512, 256, 128);
-          mma_ss(tmem + a.t_c + t * C + 16 * pr, ad, bd, idesc, tap > 0);
+  if (warp == 0) {
+    // ---------------- producer: resident weights once, x bands through a ring
+    if (lane == 0) {
+      prefetch_tmap(&tmap_x);
+      const int wtot = a.w_bytes + nch * a.chunk_bytes;
+      mbar_arrive_expect_tx(&B.w_full, wtot);
+      bulk_g2s(s_w, a.wpack, wtot, &B.w_full);
+      for (int i = 0; i < nb; ++i) {
+        const int xb = i % a.x_bufs, use = i / a.x_bufs;
+        mbar_wait_sleep(&B.x_empty[xb], (use & 1) ^ 1);
+        if (i < 8) CF2_TRACE(8 + i * 24 + 0);
+        const int band = band_of(i), n = band / a.tiles_y, yo0 = (band % a.tiles_y) * a.R;
+        mbar_arrive_expect_tx(&B.x_full[xb], planes * loaded * 16);
+        for (int g = 0; g < planes; ++g)
+          tma_load_5d(s_x + ((size_t)(xb * planes + g) * a.x_alloc) * 16, &tmap_x, 0, -1, 2 * yo0 - 2, g, n,
+                      &B.x_full[xb]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      mbar_wait(&B.w_full, 0);
+      const uint32_t cw = smem_u32(s_w + a.o_convw);
+      const uint32_t idesc_c = make_idesc_f16(128, 16);
+      const uint32_t idesc_e = make_idesc_f16(128, r);
+      const uint32_t idesc_z = make_idesc_f16(128, K);
+      auto conv_begin = [&](int i) {
+        if (i < 8) CF2_TRACE(8 + i * 24 + 1);
+        mbar_wait(&B.x_full[i % a.x_bufs], (i / a.x_bufs) & 1);
+        mbar_wait(&B.c_empty, (i & 1) ^ 1);  // previous band's conv accumulators drained
+        tc_fence_after();
+        if (i < 8) CF2_TRACE(8 + i * 24 + 2);
+      };
+      auto conv_tiles = [&](int i, int t0, int t1) {
+        const uint32_t x0 = smem_u32(s_x) + (i % a.x_bufs) * planes * a.x_alloc * 16;
+        for (int t = t0; t < t1; ++t)
+          for (int pr = 0; pr < C / 16; ++pr) {
+            const uint64_t ad = make_sdesc(x0 + (2 * pr * a.x_alloc + a.conv_base - Wp - 1 + t * 128) * 16,
+                                           a.x_alloc * 16, 128);
+            const uint64_t bd = make_sdesc(cw + pr * 9 * 512, 256, 128);
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap)
+              mma_ss(tmem + a.t_c + t * C + 16 * pr, ad + (uint64_t)((tap / 3) * Wp + tap % 3),
+                     bd + (uint64_t)(tap * 32), idesc_c, tap > 0);
+          }
+      };
+      auto conv_end = [&](int i) {
+        mma_commit(&B.conv_full);
+        mma_commit(&B.x_empty[i % a.x_bufs]);
+        if (i < 8) CF2_TRACE(8 + i * 24 + 3);
+      };
+      auto issue_project = [&](int i, int j) {
+        const int gq = i * nch + j, qs = gq & 1;
+        mbar_wait(&B.q_full[qs], (gq >> 1) & 1);
+        if (j == 0) mbar_wait(&B.z_empty, (i & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(s_w) + a.w_bytes + j * a.chunk_bytes + a.u_bytes;
+        const uint32_t aq = smem_u32(s_aq) + qs * a.aq_bytes;
+        for (int t = 0; t < a.n_eh; ++t)
+          for (int kk = 0; kk < r / 16; ++kk)
+            mma_ss(tmem + a.t_z + t * K, make_sdesc(aq + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
+                   make_sdesc(vb + kk * 2 * (K * 16), K * 16, 128), idesc_z, (j > 0 || kk > 0));
+        mma_commit(&B.q_empty[qs]);
+        if (j == nch - 1) mma_commit(&B.z_full);
+      };
+      // conv runs two bands ahead: conv(i+2) is issued tile by tile between
+      // the FFN chunks of band i (expand j, project j-1, conv tile(s)), so
+      // the tensor core works while the CUDA-core groups drain; G1 drains
+      // conv(i+1) and blurs it during FFN(i)
+      for (int i = 0; i < 2 && i < nb; ++i) {
+        conv_begin(i);
+        conv_tiles(i, 0, a.n_ct);
+        conv_end(i);
+      }
+      for (int i = 0; i < nb; ++i) {
+        const int hb = i & 1;
+        mbar_wait(&B.xh_full[hb], (i >> 1) & 1);
+        tc_fence_after();
+        if (i < 8) CF2_TRACE(8 + i * 24 + 4);
+        const uint32_t ah = smem_u32(s_ah) + hb * a.ah_bytes;
+        const bool conv_next = i + 2 < nb;
+        for (int j = 0; j < nch; ++j) {
+          const int gg = i * nch + j, es = gg & 1;
+          mbar_wait(&B.e_empty[es], ((gg >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ub = smem_u32(s_w) + a.w_bytes + j * a.chunk_bytes;
+          for (int t = 0; t < a.n_eh; ++t)
+            for (int kk = 0; kk < C / 16; ++kk)
+              mma_ss(tmem + a.t_e + (es * a.n_eh + t) * r, make_sdesc(ah + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
+                     make_sdesc(ub + kk * 2 * (r * 16), r * 16, 128), idesc_e, kk > 0);
+          mma_commit(&B.e_full[es]);
+          if (j == nch - 1) mma_commit(&B.xh_empty[hb]);
+          if (j > 0) issue_project(i, j - 1);
+          if (conv_next) {
+            if (j == 0) conv_begin(i + 2);
+            conv_tiles(i + 2, j * a.n_ct / nch, (j + 1) * a.n_ct / nch);
+            if (j == nch - 1) conv_end(i + 2);
+          }
         }
-    mma_commit(&bars[1]);
-  }
-  mma_wait();
-  {
+        issue_project(i, nch - 1);
+        if (i < 8) CF2_TRACE(8 + i * 24 + 5);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- conv drain (+ b_conv -> fp16 xc planes) and blur along H -> expand operand
+    const int q = warp % 4, tid = threadIdx.x - 128;
+    mbar_wait_sleep(&B.w_full, 0);
     const float* bconv = reinterpret_cast<const float*>(s_w + a.o_bconv);
-    for (int t = half; t < a.n_ct; t += 2) {
-      const int f = a.conv_base + t * 128 + q * 32 + lane;
-      const int row = f / Wp, col = f - row * Wp;  // row 1 .. 2R+1 <-> conv row 2*yo0 - 2 + row
-      const bool real = col >= 1 && col <= W && row >= 1 && row <= 2 * a.R + 1;
-      for (int c0 = 0; c0 < C; c0 += 16) {
-        uint32_t v[16];
-        WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C + c0), v);
-        tmem_ld_wait();
-        float fv[16];
+    const int XP = (2 * a.R + 1) * W;
+    const int cb = C / 16;  // 16-column blocks per conv tile (1 or 2)
+    float bc[2][16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) fv[i] = __uint_as_float(v[i]) + bconv[c0 + i];
-        if (real) {
-          __half* dst = s_xc + ((size_t)(row - 1) * W + (col - 1)) * C + c0;
-          reinterpret_cast<uint4*>(dst)[0] = pack8(fv);
-          reinterpret_cast<uint4*>(dst)[1] = pack8(fv + 8);
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) bc[b][k] = b < cb ? bconv[b * 16 + k] : 0.f;
+    for (int i = 0; i < nb; ++i) {
+      const int band = band_of(i), yo0 = (band % a.tiles_y) * a.R;
+      mbar_wait_sleep(&B.conv_full, i & 1);
+      tc_fence_after();
+      if (tid == 0 && i < 8) CF2_TRACE(8 + i * 24 + 6);
+      // lane row -> (flat row, col) walked incrementally (no integer division per tile)
+      int row = (a.conv_base + q * 32 + lane) / Wp, col = a.conv_base + q * 32 + lane - row * Wp;
+      for (int t = 0; t < a.n_ct; ++t) {
+        uint32_t v[2][16];
+        WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C), v[0]);
+        if (cb > 1) WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C + 16), v[1]);
+        tmem_ld_wait();
+        if (col >= 1 && col <= W && row >= 1 && row <= 2 * a.R + 1) {  // row 1 .. 2R+1 <-> conv row 2*yo0 - 2 + row
+          const int px = (row - 1) * W + (col - 1);
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            if (b >= cb) break;
+            float fv[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + bc[b][k];
+            *reinterpret_cast<uint4*>(s_xc + ((size_t)(2 * b) * XP + px) * 8) = pack8(fv);
+            *reinterpret_cast<uint4*>(s_xc + ((size_t)(2 * b + 1) * XP + px) * 8) = pack8(fv + 8);
+          }
+        }
+        col += 128;
+        while (col >= Wp) {
+          col -= Wp;
+          ++row;
         }
       }
+      tc_fence_before();
+      mbar_arrive(&B.c_empty);
+      if (tid == 0 && i < 8) CF2_TRACE(8 + i * 24 + 7);
+      const int hb = i & 1;
+      mbar_wait_sleep(&B.xh_empty[hb], ((i >> 1) & 1) ^ 1);
+      bar_sync(1, 128);  // all of xc written
+      uint8_t* ah = s_ah + hb * a.ah_bytes;
+      for (int c8 = 0; c8 < planes; ++c8) {
+        const __half* plc = s_xc + (size_t)c8 * XP * 8;
+        uint8_t* ahc = ah + (size_t)c8 * MH * 16;
+        int ro = tid / W, x = tid - ro * W;
+        for (int p = tid; p < RW; p += 128) {
+          const int k0 = (yo0 + ro == 0) ? 2 : 2 * ro;  // xc rows of conv rows 2yo-1 (reflect -1 -> 1), 2yo, 2yo+1
+          const __half* pl = plc + (size_t)x * 8;
+          *reinterpret_cast<uint4*>(ahc + (size_t)p * 16) =
+              tri3(*reinterpret_cast<const uint4*>(pl + (size_t)k0 * W * 8),
+                   *reinterpret_cast<const uint4*>(pl + (size_t)(2 * ro + 1) * W * 8),
+                   *reinterpret_cast<const uint4*>(pl + (size_t)(2 * ro + 2) * W * 8));
+          x += 128;
+          while (x >= W) {
+            x -= W;
+            ++ro;
+          }
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(&B.xh_full[hb]);
+      if (tid == 0 && i < 8) CF2_TRACE(8 + i * 24 + 8);
+      bar_sync(1, 128);  // xc free for the next band
+    }
+  } else if (warp >= 8 && warp < 16) {
+    // ---------------- hidden chunks: E + a -> phi -> fp16 project operand planes
+    // (two warps per TMEM quadrant, alternating 32-column blocks)
+    const int q = warp % 4, hh = (warp - 8) / 4, tid = threadIdx.x - 256;
+    mbar_wait_sleep(&B.w_full, 0);
+    const float* av = reinterpret_cast<const float*>(s_w + a.o_a);
+    for (int i = 0; i < nb; ++i) {
+      for (int j = 0; j < nch; ++j) {
+        const int gg = i * nch + j, es = gg & 1;
+        mbar_wait_sleep(&B.e_full[es], (gg >> 1) & 1);
+        mbar_wait_sleep(&B.q_empty[es], ((gg >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (tid == 0 && i < 8 && j < 4) CF2_TRACE(8 + i * 24 + 9 + 3 * j);
+        uint8_t* aq = s_aq + es * a.aq_bytes;
+        const float* avj = av + j * r;
+        for (int t = 0; t < a.n_eh; ++t) {
+          const int p = t * 128 + q * 32 + lane;
+          const uint32_t tcol = a.t_e + (es * a.n_eh + t) * r;
+          for (int c0 = hh * 32; c0 < r; c0 += 64) {
+            uint32_t v[2][16];
+            const bool two = c0 + 16 < r;
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, tcol + c0), v[0]);
+            if (two) WL_TMEM_LD16(tmem_lane_addr(tmem, q, tcol + c0 + 16), v[1]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              if (b == 1 && !two) break;
+              const int cc = c0 + 16 * b;
+              float bias[16];
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const float4 bb = *reinterpret_cast<const float4*>(avj + cc + 4 * k4);
+                bias[4 * k4] = bb.x;
+                bias[4 * k4 + 1] = bb.y;
+                bias[4 * k4 + 2] = bb.z;
+                bias[4 * k4 + 3] = bb.w;
+              }
+              *reinterpret_cast<uint4*>(aq + ((size_t)(cc / 8) * MH + p) * 16) = bias_act8<ACT>(v[b], bias);
+              *reinterpret_cast<uint4*>(aq + ((size_t)(cc / 8 + 1) * MH + p) * 16) = bias_act8<ACT>(v[b] + 8, bias + 8);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&B.e_empty[es]);
+        fence_async_smem();
+        mbar_arrive(&B.q_full[es]);
+        if (tid == 0 && i < 8 && j < 4) CF2_TRACE(8 + i * 24 + 11 + 3 * j);
+      }
+    }
+  } else if (warp >= 16) {
+    // ---------------- output: Z + b -> fp16 staging -> blur along W (stride 2) -> TMA store
+    const int q = warp % 4, tid = threadIdx.x - 512;
+    mbar_wait_sleep(&B.w_full, 0);
+    const float* bv = reinterpret_cast<const float*>(s_w + a.o_b);
+    const int k8 = K / 8, KP = K + 8;
+    const int RWo = a.R * a.Wo;
+    for (int i = 0; i < nb; ++i) {
+      const int band = band_of(i), n = band / a.tiles_y, yo0 = (band % a.tiles_y) * a.R;
+      mbar_wait_sleep(&B.z_full, i & 1);
+      tc_fence_after();
+      if (tid == 0 && i < 8) CF2_TRACE(8 + i * 24 + 21);
+      // staging: pixel-major rows of KP = K + 8 halves (the 16-byte pad spreads
+      // a warp's row-strided stores over the banks)
+      for (int t = 0; t < a.n_eh; ++t) {
+        const int p = t * 128 + q * 32 + lane;
+        for (int c0 = 0; c0 < K; c0 += 32) {
+          uint32_t v[2][16];
+          const bool two = c0 + 16 < K;
+          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * K + c0), v[0]);
+          if (two) WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * K + c0 + 16), v[1]);
+          tmem_ld_wait();
+          if (p >= RW) continue;
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            if (b == 1 && !two) break;
+            const int cc = c0 + 16 * b;
+            float fv[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + bv[cc + k];
+            *reinterpret_cast<uint4*>(s_zs + (size_t)p * KP + cc) = pack8(fv);
+            *reinterpret_cast<uint4*>(s_zs + (size_t)p * KP + cc + 8) = pack8(fv + 8);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&B.z_empty);
+      if (tid == 0) bulk_wait_read0_cf2();  // previous band's store has left the output staging
+      bar_sync(3, 128);                     // staging complete
+      // output pixel qi = (ro, xo), 8-channel group c8; items ordered c8-fastest
+      // so a warp writes contiguous 16-byte chunks of the dense [R][Wo][K] tile
+      {
+        int c8 = tid % k8, qi = tid / k8;
+        const int sq = 128 / k8, sc = 128 % k8;
+        int ro = qi / a.Wo, xo = qi - ro * a.Wo;
+        for (int idx = tid; idx < RWo * k8; idx += 128) {
+          const int x0 = xo == 0 ? 1 : 2 * xo - 1;  // reflect column -1 -> 1
+          const __half* rb = s_zs + (size_t)ro * W * KP + c8 * 8;
+          *reinterpret_cast<uint4*>(s_zo + ((size_t)qi * K + c8 * 8)) =
+              tri3(*reinterpret_cast<const uint4*>(rb + (size_t)x0 * KP),
+                   *reinterpret_cast<const uint4*>(rb + (size_t)(2 * xo) * KP),
+                   *reinterpret_cast<const uint4*>(rb + (size_t)(2 * xo + 1) * KP));
+          c8 += sc;
+          int dq = sq;
+          if (c8 >= k8) {
+            c8 -= k8;
+            ++dq;
+          }
+          qi += dq;
+          xo += dq;
+          while (xo >= a.Wo) {
+            xo -= a.Wo;
+            ++ro;
+          }
+        }
+      }
+      fence_async_smem();
+      bar_sync(3, 128);
+      if (tid == 0) {
+        tma_store_4d_cf2(&tmap_z, s_zo, 0, 0, yo0, n);
+        bulk_commit_cf2();
+      }
+      if (tid == 0 && i < 8) CF2_TRACE(8 + i * 24 + 22);
+      bar_sync(3, 128);  // staging free for the next band
     }
   }
   tc_fence_before();
   __syncthreads();
-  // ---------------- blur along H (stride 2, reflect) -> expansion operand
-  const int MH = a.n_eh * 128;
-  for (int p = tid; p < a.R * W; p += blockDim.x) {
-    const int ro = p / W, x = p - ro * W, yo = yo0 + ro;
-    int k0 = 2 * ro, k1 = 2 * ro + 1, k2 = 2 * ro + 2;  // staging rows of conv rows 2yo-1, 2yo, 2yo+1
-    if (yo == 0) k0 = k2;                               // reflect row -1 -> row 1
-    for (int c8 = 0; c8 < planes; ++c8) {
-      *reinterpret_cast<uint4*>(s_ah + ((size_t)c8 * MH + p) * 16) =
-          tri3(*reinterpret_cast<const uint4*>(s_xc + ((size_t)k0 * W + x) * C + c8 * 8),
-               *reinterpret_cast<const uint4*>(s_xc + ((size_t)k1 * W + x) * C + c8 * 8),
-               *reinterpret_cast<const uint4*>(s_xc + ((size_t)k2 * W + x) * C + c8 * 8));
+  if (threadIdx.x == 0) {
+    CF2_TRACE(1);
+    if (a.trace && blockIdx.x == 0) {
+      a.trace[2] = a.R * 1000 + a.r;
+      a.trace[3] = a.n_ct * 10000 + a.n_eh * 100 + a.n_pt;
+      a.trace[4] = nb * 10 + a.x_bufs;
     }
   }
-  fence_async_smem();
-  __syncthreads();
-
-  // ---------------- FFN over hidden chunks with the W blur between
-  const float* av = reinterpret_cast<const float*>(s_w + a.o_a);
-  const int MQ = a.n_pt * 128;
-  for (int j = 0; j < a.nch; ++j) {
-    if (tid == 0) {
-      if (j + 1 < a.nch) {  // prefetch chunk j+1 (its slot's previous chunk finished last iteration)
-        const int sl = (j + 1) & 1;
-        mbar_arrive_expect_tx(&bars[2 + sl], a.chunk_bytes);
-        bulk_g2s(s_ring + sl * a.chunk_bytes, a.wpack + a.w_bytes + (size_t)(j + 1) * a.chunk_bytes, a.chunk_bytes,
-                 &bars[2 + sl]);
-      }
-      mbar_wait(&bars[2 + (j & 1)], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t idesc = make_idesc_f16(128, r);
-      const uint32_t ub = smem_u32(s_ring) + (j & 1) * a.chunk_bytes;
-      for (int t = 0; t < a.n_eh; ++t)
-        for (int kk = 0; kk < C / 16; ++kk) {
-          const uint64_t ad = make_sdesc(smem_u32(s_ah) + (kk * 2 * MH + t * 128) * 16, MH * 16, 128);
-          const uint64_t bd = make_sdesc(ub + kk * 2 * (r * 16), r * 16, 128);
-          mma_ss(tmem + a.t_e + t * r, ad, bd, idesc, kk > 0);
-        }
-      mma_commit(&bars[1]);
-    }
-    mma_wait();
-    for (int t = half; t < a.n_eh; t += 2) {
-      const int p = t * 128 + q * 32 + lane;
-      for (int c0 = 0; c0 < r; c0 += 16) {
-        uint32_t v[16];
-        WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + t * r + c0), v);
-        tmem_ld_wait();
-        if (p < a.R * W) {
-          __half* dst = s_hs + (size_t)p * r + c0;
-          reinterpret_cast<uint4*>(dst)[0] = bias_act8<ACT>(v, av + j * r + c0);
-          reinterpret_cast<uint4*>(dst)[1] = bias_act8<ACT>(v + 8, av + j * r + c0 + 8);
-        }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();
-    for (int qi = tid; qi < a.R * a.Wo; qi += blockDim.x) {
-      const int ro = qi / a.Wo, xo = qi - ro * a.Wo;
-      int x0 = 2 * xo - 1;
-      if (x0 < 0) x0 = 1;
-      const __half* r0 = s_hs + ((size_t)ro * W + x0) * r;
-      const __half* r1 = s_hs + ((size_t)ro * W + 2 * xo) * r;
-      const __half* r2 = s_hs + ((size_t)ro * W + 2 * xo + 1) * r;
-      for (int c8 = 0; c8 < r / 8; ++c8) {
-        *reinterpret_cast<uint4*>(s_aq + ((size_t)c8 * MQ + qi) * 16) =
-            tri3(*reinterpret_cast<const uint4*>(r0 + c8 * 8), *reinterpret_cast<const uint4*>(r1 + c8 * 8),
-                 *reinterpret_cast<const uint4*>(r2 + c8 * 8));
-      }
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t idesc = make_idesc_f16(128, K);
-      const uint32_t vb = smem_u32(s_ring) + (j & 1) * a.chunk_bytes + a.u_bytes;
-      for (int t = 0; t < a.n_pt; ++t)
-        for (int kk = 0; kk < r / 16; ++kk) {
-          const uint64_t ad = make_sdesc(smem_u32(s_aq) + (kk * 2 * MQ + t * 128) * 16, MQ * 16, 128);
-          const uint64_t bd = make_sdesc(vb + kk * 2 * (K * 16), K * 16, 128);
-          mma_ss(tmem + a.t_z + t * K, ad, bd, idesc, (j > 0 || kk > 0));
-        }
-      mma_commit(&bars[1]);
-    }
-    mma_wait();
-  }
-  // ---------------- z = Z + b
-  const float* bv = reinterpret_cast<const float*>(s_w + a.o_b);
-  for (int t = half; t < a.n_pt; t += 2) {
-    const int qi = t * 128 + q * 32 + lane;
-    const int ro = qi / a.Wo, xo = qi - ro * a.Wo, yo = yo0 + ro;
-    const bool inside = qi < a.R * a.Wo && yo < a.Ho;
-    for (int c0 = 0; c0 < K; c0 += 16) {
-      uint32_t v[16];
-      WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * K + c0), v);
-      tmem_ld_wait();
-      if (!inside) continue;
-      float fv[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) fv[i] = __uint_as_float(v[i]) + bv[c0 + i];
-      uint4* zp = reinterpret_cast<uint4*>(a.z + (((size_t)n * a.Ho + yo) * a.Wo + xo) * K + c0);
-      zp[0] = pack8(fv);
-      zp[1] = pack8(fv + 8);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc_n(tmem, a.tmem_cols);
+  if (warp == 16 && lane == 0) bulk_wait_all_cf2();  // output stores complete before exit
+  if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
 }
 
 }  // namespace wl
 
 // =================================================================== host
+#include <algorithm>
 #include <cstring>
 #include "launch.h"
 
@@ -255,6 +465,7 @@ namespace wl {
 namespace {
 
 constexpr int kSmemMax2 = 232448;
+long long* g_cf2_trace = nullptr;
 
 bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   memset(&a, 0, sizeof(a));
@@ -267,74 +478,89 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   a.Wo = d.w / 2;
   a.Wp = d.w + 1;
   if (a.C % 16 || a.K % 16 || a.hid % 16 || a.K > 256) return false;
-  // pass 0: the largest R that lets two CTAs share an SM (TMEM <= 256 columns,
-  // <= 112 KB shared memory) so one CTA's serial phases overlap the other's;
-  // pass 1: any R that fits one CTA per SM
-  for (int pass = 0; pass < 2; ++pass)
-  for (int R = 8; R >= 1; --R) {
-    if (R > a.Ho) continue;
-    a.R = R;
-    a.x_rows = 2 * R + 3;
-    a.conv_base = a.Wp + 1;
-    const int conv_end = (2 * R + 2) * a.Wp;
-    a.n_ct = (conv_end - a.conv_base + 127) / 128;
-    a.x_alloc = align_up(std::max(a.conv_base + a.n_ct * 128 + a.Wp + 2, a.x_rows * a.Wp), 8);
-    a.n_eh = (R * a.W + 127) / 128;
-    a.n_pt = (R * a.Wo + 127) / 128;
-    if (a.n_eh > 4) continue;
-    // hidden chunk: widest that fits TMEM and shared memory
-    bool ok = false;
-    for (int rr = 128; rr >= 16 && !ok; rr -= 16) {
+  // choose (R output rows per band, hidden chunk r, x buffers) by the
+  // tcgen05 cost model (max(44, N/2) cycles per K=16 instruction) per output
+  // row, subject to TMEM (512 columns) and shared memory
+  double best = 1e30;
+  Cf2Args bestA{};
+  for (int R = 1; R <= 8; ++R) {
+    if (R > a.Ho) break;
+    for (int rr = 16; rr <= 256 && rr <= a.hid; rr += 16) {
       if (a.hid % rr) continue;
-      const int cols = a.n_ct * a.C + a.n_eh * rr + a.n_pt * a.K;
-      if (cols > 512) continue;
-      a.r = rr;
-      a.nch = a.hid / a.r;
-      int o = 0;
-      a.o_convw = o;
-      o += (a.C / 16) * 9 * 512;
-      a.o_bconv = o;
-      o = align_up(o + a.C * 4, 16);
-      a.o_a = o;
-      o = align_up(o + a.hid * 4, 16);
-      a.o_b = o;
-      o = align_up(o + a.K * 4, 16);
-      a.w_bytes = align_up(o, 128);
-      a.u_bytes = a.r * a.C * 2;
-      a.chunk_bytes = a.u_bytes + a.K * a.r * 2;
-      int s = 0;
-      a.s_x = s;
-      s = align_up(s + (a.C / 8) * a.x_alloc * 16, 128);
-      a.s_xc = s;
-      s = align_up(s + (2 * R + 1) * a.W * a.C * 2, 128);
-      a.s_ah = s;
-      s = align_up(s + a.n_eh * 128 * a.C * 2, 128);
-      a.s_hs = s;
-      s = align_up(s + R * a.W * a.r * 2, 128);
-      a.s_aq = s;
-      s = align_up(s + a.n_pt * 128 * a.r * 2, 128);
-      a.s_w = s;
-      s = align_up(s + a.w_bytes, 128);
-      a.s_ring = s;
-      s = align_up(s + 2 * a.chunk_bytes, 128);
-      a.s_bar = s;
-      s += 64;
-      ok = s <= (pass == 0 ? 112 * 1024 : kSmemMax2) && (pass == 1 || cols <= 256);
+      for (int xbufs = 2; xbufs >= 1; --xbufs) {
+        Cf2Args c = a;
+        c.R = R;
+        c.r = rr;
+        c.nch = c.hid / rr;
+        c.x_bufs = xbufs;
+        c.x_rows = 2 * R + 3;
+        c.conv_base = c.Wp + 1;
+        const int conv_end = (2 * R + 2) * c.Wp;
+        c.n_ct = (conv_end - c.conv_base + 127) / 128;
+        c.x_alloc = align_up(std::max(c.conv_base + c.n_ct * 128 + c.Wp + 2, c.x_rows * c.Wp), 8);
+        c.n_eh = (R * c.W + 127) / 128;
+        c.n_pt = c.n_eh;  // the projection runs at (R, W); BlurPool W follows it
+        c.t_c = 0;
+        c.t_e = c.n_ct * c.C;
+        c.t_z = c.t_e + 2 * c.n_eh * rr;
+        const int cols = c.t_z + c.n_pt * c.K;
+        if (cols > 512) continue;
+        int o = 0;
+        c.o_convw = o;
+        o += (c.C / 16) * 9 * 512;
+        c.o_bconv = o;
+        o = align_up(o + c.C * 4, 16);
+        c.o_a = o;
+        o = align_up(o + c.hid * 4, 16);
+        c.o_b = o;
+        o = align_up(o + c.K * 4, 16);
+        c.w_bytes = align_up(o, 128);
+        c.u_bytes = rr * c.C * 2;
+        c.chunk_bytes = c.u_bytes + c.K * rr * 2;
+        c.ah_bytes = c.n_eh * 128 * c.C * 2;
+        c.aq_bytes = c.n_eh * 128 * rr * 2;
+        int s = 0;
+        c.s_x = s;
+        s = align_up(s + xbufs * (c.C / 8) * c.x_alloc * 16, 128);
+        c.s_xc = s;
+        s = align_up(s + (2 * R + 1) * c.W * c.C * 2, 128);
+        c.s_ah = s;
+        s = align_up(s + 2 * c.ah_bytes, 128);
+        c.s_hs = s;  // projection staging (pixel-major rows of K + 8 halves) for BlurPool W
+        s = align_up(s + R * c.W * (c.K + 8) * 2, 128);
+        c.s_zo = s;  // dense output tile [R][Wo][K] for the TMA store
+        s = align_up(s + R * c.Wo * c.K * 2, 128);
+        c.s_aq = s;
+        s = align_up(s + 2 * c.aq_bytes, 128);
+        c.s_w = s;
+        s = align_up(s + c.w_bytes + c.nch * c.chunk_bytes, 128);
+        c.s_bar = s;
+        s += 256;
+        c.smem = s;
+        if (s > kSmemMax2) continue;
+        const double conv = (double)c.n_ct * (c.C / 16) * 9 * 44;
+        const double expand = (double)c.n_eh * (c.C / 16) * c.nch * std::max(44, rr / 2);
+        const double project = (double)c.n_pt * (c.hid / 16) * std::max(44, c.K / 2);
+        // TMEM reads of the accumulators (~128 B/cycle): conv, hidden, projection
+        const double tmem_rd = 4.0 * ((double)c.n_ct * c.C + (double)c.n_eh * c.hid + (double)c.n_pt * c.K);
+        const double cost = (std::max(conv + expand + project, tmem_rd) + 300.0) / R * (xbufs == 2 ? 1.0 : 1.15);
+        if (cost < best) {
+          best = cost;
+          bestA = c;
+        }
+      }
     }
-    if (!ok) continue;
-    a.tiles_y = (a.Ho + R - 1) / R;
-    a.t_c = 0;
-    a.t_e = a.n_ct * a.C;
-    a.t_z = a.t_e + a.n_eh * a.r;
-    const int cols = a.t_z + a.n_pt * a.K;
-    a.tmem_cols = 32;
-    while (a.tmem_cols < cols) a.tmem_cols *= 2;
-    return true;
   }
-  return false;
+  if (best >= 1e30) return false;
+  a = bestA;
+  a.tiles_y = (a.Ho + a.R - 1) / a.R;
+  a.nbands = d.n * a.tiles_y;
+  a.tmem_cols = 32;
+  while (a.tmem_cols < a.t_z + a.n_pt * a.K) a.tmem_cols *= 2;
+  return true;
 }
 
-using Cf2K = void (*)(const CUtensorMap, const Cf2Args);
+using Cf2K = void (*)(const CUtensorMap, const CUtensorMap, const Cf2Args);
 Cf2K cf2_kernel_for(int act) {
   switch (act) {
     case kRelu: return cf2_kernel<kRelu>;
@@ -410,9 +636,16 @@ int cf2_forward(const wl_block_desc& d, const void* x, const void* packed, void*
   const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, 16, (uint64_t)d.h * d.w * d.c * 2};
   const uint32_t box[5] = {8, (uint32_t)a.Wp, (uint32_t)a.x_rows, 1, 1};
   if (int e = encode_tmap(&tm, x, 5, dims, strides, box)) return e;
+  CUtensorMap tz;
+  const uint64_t zd[4] = {(uint64_t)d.k, (uint64_t)a.Wo, (uint64_t)a.Ho, (uint64_t)d.n};
+  const uint64_t zs[3] = {(uint64_t)d.k * 2, (uint64_t)a.Wo * d.k * 2, (uint64_t)a.Ho * a.Wo * d.k * 2};
+  const uint32_t zb[4] = {(uint32_t)d.k, (uint32_t)a.Wo, (uint32_t)a.R, 1};
+  if (int e = encode_tmap(&tz, z, 4, zd, zs, zb)) return e;
   a.wpack = reinterpret_cast<const uint8_t*>(packed);
   a.z = reinterpret_cast<__half*>(z);
-  cf2_kernel_for(d.act)<<<d.n * a.tiles_y, 256, a.s_bar + 64, st>>>(tm, a);
+  a.trace = g_cf2_trace;
+  const int grid = std::min(a.nbands, kNumSMs);
+  cf2_kernel_for(d.act)<<<grid, cf2k::kThreads, a.smem, st>>>(tm, tz, a);
   return check_cuda(cudaGetLastError(), "cf2 launch");
 }
 int cf2_init() {
@@ -424,6 +657,8 @@ int cf2_init() {
 }
 
 }  // namespace
+
+void cf2_set_trace(void* p) { g_cf2_trace = reinterpret_cast<long long*>(p); }
 
 const Family kCf2Family = {cf2_validate, cf2_weight_count, cf2_weight_numel, cf2_packed_bytes,
                            cf2_pack,     cf2_ws,           cf2_forward,      cf2_init};
