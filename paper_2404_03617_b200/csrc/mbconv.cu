@@ -50,6 +50,11 @@ struct MbFrontArgs {
   long long* trace;      // debug: per-phase clock64 stamps of CTA 0 (null = off)
   // fused projection (one launch per block): gated h2 (re-read from L2) x W_prj
   int fused, K, n_pt, HCb, nchb, vchunk_bytes, residual, sa, SQP;
+  // bulk mode (fused, single-store staging): h2 lives chunk-major in global,
+  // [group][hidden/8][P_out][8], so every conv chunk leaves and every
+  // projection chunk (HCb = lcm(HC, 64) channels) returns as ONE bulk copy
+  int bulk, a_stage_b;
+  __half* h2;
   int s_pa, s_pv, s_gate, t_z;
   const uint8_t* wback;  // back blob: [b_prj fp32][V chunks]
   const __half* x;       // residual source (n, H, W, C)
@@ -453,9 +458,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       named_bar(1, 256);
       if (tid == 0) WL_TRACE(16 + 8 * j + 6);
       if (tid == 0) {
-        for (int k = 0; k < a.st_stores; ++k)
-          tma_store_3d(&tmap_h2, s_st + (size_t)k * G8 * a.st_rows * 16, 0, group * a.P_out + k * a.st_rows,
-                       (h0 + j * HC) / 8);
+        if (a.bulk) {
+          const size_t off = ((size_t)group * a.hid + h0 + j * HC) * a.P_out;  // halves
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a.h2 + off),
+                       "r"(smem_u32(s_st)), "r"(a.P_out * HC * 2)
+                       : "memory");
+        } else {
+          for (int k = 0; k < a.st_stores; ++k)
+            tma_store_3d(&tmap_h2, s_st + (size_t)k * G8 * a.st_rows * 16, 0, group * a.P_out + k * a.st_rows,
+                         (h0 + j * HC) / 8);
+        }
         bulk_commit();
       }
       // pool: deterministic column sums of the staged (fp16) h2 values.
@@ -524,12 +536,18 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   if (!a.fused) __threadfence();  // publish this CTA's pool slice before arriving
   tc_fence_before();
   __syncthreads();
-  const int a_tile = 128 * a.HCb * 2, a_stage = a.n_pt * a_tile;
+  const int a_tile = 128 * a.HCb * 2, a_stage = a.bulk ? a.a_stage_b : a.n_pt * a_tile;
   uint8_t* s_pa = smem + a.s_pa;
   uint8_t* s_pv = smem + a.s_pv;
   const uint8_t* vch = a.wback + align_up(a.K * 4, 128);
   auto load_a = [&](int j) {  // h2 rows of chunk j (re-read from L2) -> A stage
     const int ab = j % a.sa;
+    if (a.bulk) {  // planes [HCb/8][P_out][8], contiguous in global
+      const uint32_t bytes = a.P_out * a.HCb * 2;
+      mbar_arrive_expect_tx(&B.pa_full[ab], bytes);
+      bulk_g2s(s_pa + ab * a_stage, a.h2 + ((size_t)group * a.hid + (size_t)j * a.HCb) * a.P_out, bytes, &B.pa_full[ab]);
+      return;
+    }
     mbar_arrive_expect_tx(&B.pa_full[ab], a_stage);
     for (int t = 0; t < a.n_pt; ++t)  // 2-D box (64 channels x 128 rows), 128-byte swizzle
       asm volatile(
@@ -703,12 +721,22 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           mbar_wait(&B.pv_full[vs], (j / 3) & 1);
           if (j < 8) WL_TRACE(104 + j);
           tc_fence_after();
-          const uint64_t b_base = make_sdesc(smem_u32(s_pv + vs * a.vchunk_bytes), a.K * 16, 128);
+          const uint32_t vbase = smem_u32(s_pv + vs * a.vchunk_bytes);
+          const int vsub = a.K * 64 * 2;  // one packed 64-row W_prj chunk
           for (int t = 0; t < a.n_pt; ++t) {
-            const uint64_t a_base = make_sdesc_sw128(smem_u32(s_pa + ab * a_stage + t * a_tile));
-            for (int kk = 0; kk < 4; ++kk)
-              mma_ss(tmem + a.t_z + t * a.K, a_base + (uint64_t)(kk * 2), b_base + (uint64_t)(kk * 2 * a.K), idesc,
-                     (j > 0 || kk > 0));
+            if (a.bulk) {
+              const uint64_t a_base = make_sdesc(smem_u32(s_pa + ab * a_stage) + t * 2048, a.P_out * 16, 128);
+              for (int kk = 0; kk < a.HCb / 16; ++kk) {
+                const uint64_t bd = make_sdesc(vbase + (kk / 4) * vsub + (kk % 4) * 2 * a.K * 16, a.K * 16, 128);
+                mma_ss(tmem + a.t_z + t * a.K, a_base + (uint64_t)(kk * 2 * a.P_out), bd, idesc, (j > 0 || kk > 0));
+              }
+            } else {
+              const uint64_t b_base = make_sdesc(vbase, a.K * 16, 128);
+              const uint64_t a_base = make_sdesc_sw128(smem_u32(s_pa + ab * a_stage + t * a_tile));
+              for (int kk = 0; kk < 4; ++kk)
+                mma_ss(tmem + a.t_z + t * a.K, a_base + (uint64_t)(kk * 2), b_base + (uint64_t)(kk * 2 * a.K), idesc,
+                       (j > 0 || kk > 0));
+            }
           }
           mma_commit(&B.pa_empty[ab]);
           mma_commit(&B.pv_empty[vs]);
@@ -727,6 +755,47 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const int ab = j % a.sa;
         mbar_wait(&B.pa_full[ab], (j / a.sa) & 1);
         if (tid == 0 && j < 8) WL_TRACE(112 + j);
+        if (a.bulk) {  // planes [HCb/8][P_out][8]: item = plane * P_out + pixel, 2 per step
+          uint8_t* base = s_pa + ab * a_stage;
+          const __half* gj = s_gh + j * a.HCb;
+          const int nitems = (a.HCb / 8) * a.P_out;
+          int c8p = tid / a.P_out, p = tid - c8p * a.P_out;  // walked incrementally
+          const int dq = 256 / a.P_out, dr = 256 - dq * a.P_out;
+          for (int idx = tid; idx < nitems; idx += 512) {
+            int c8b = c8p + dq, pb = p + dr;
+            if (pb >= a.P_out) {
+              pb -= a.P_out;
+              ++c8b;
+            }
+            const bool two = idx + 256 < nitems;
+            const int ia = (a.imgs == 1 || p < pix_img) ? 0 : 1, ib = (a.imgs == 1 || pb < pix_img) ? 0 : 1;
+            uint4* pa = reinterpret_cast<uint4*>(base + ((size_t)c8p * a.P_out + p) * 16);
+            uint4* pb2 = reinterpret_cast<uint4*>(base + ((size_t)c8b * a.P_out + pb) * 16);
+            uint4 va = *pa, vb = two ? *pb2 : va;
+            const uint4 ga = *reinterpret_cast<const uint4*>(gj + ia * a.hid + c8p * 8);
+            const uint4 gb = *reinterpret_cast<const uint4*>(gj + ib * a.hid + (two ? c8b : c8p) * 8);
+            __half2* ha = reinterpret_cast<__half2*>(&va);
+            __half2* hb = reinterpret_cast<__half2*>(&vb);
+            const __half2* g1 = reinterpret_cast<const __half2*>(&ga);
+            const __half2* g2 = reinterpret_cast<const __half2*>(&gb);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              ha[i] = __hmul2(ha[i], g1[i]);
+              hb[i] = __hmul2(hb[i], g2[i]);
+            }
+            *pa = va;
+            if (two) *pb2 = vb;
+            c8p = c8b + dq;
+            p = pb + dr;
+            if (p >= a.P_out) {
+              p -= a.P_out;
+              ++c8p;
+            }
+          }
+          fence_async_smem();
+          mbar_arrive(&B.pa_ready[ab]);
+          continue;
+        }
         for (int r = tid >> 3; r < a.n_pt * 128; r += 32) {
           const int t = r >> 7, m = r & 127;
           const int p = min(t * 128 + m, a.P_out - 1);
@@ -764,7 +833,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           }
       };
       fetch_res(0, 0);
-      mbar_wait(&B.z_full, 0);
+      mbar_wait_sleep(&B.z_full, 0);
       tc_fence_after();
       if (warp == 12 && lane == 0) WL_TRACE(120);
       for (int t = 0; t < a.n_pt; ++t) {
@@ -1124,8 +1193,15 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     // projection overlays the dead phase-1 buffers: A ring (2 stages of the
     // CTA's h2 rows), V ring (3 stages); Z in the expand/conv TMEM columns
     f.K = K;
-    if (hid % 64) return false;  // 128-byte swizzled h2 tiles: 64-channel chunks
+    if (hid % 64) return false;  // W_prj packed in 64-row chunks
     f.HCb = 64;
+    f.bulk = f.st_stores == 1;
+    if (f.bulk) {  // projection chunk = lcm(HC, 64) channels (whole conv chunks)
+      int pc = 64;
+      while (pc % f.HC) pc += 64;
+      if (hid % pc) f.bulk = 0;
+      else f.HCb = pc;
+    }
     f.nchb = hid / f.HCb;
     f.n_pt = (f.P_out + 127) / 128;
     f.vchunk_bytes = K * f.HCb * 2;
@@ -1133,7 +1209,10 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     f.t_z = f.t_e;
     f.s_pa = 0;
     if (K > 256 || f.t_z + f.n_pt * K > f.tmem_cols) return false;
-    const int a_stage = f.n_pt * 128 * f.HCb * 2;
+    // bulk stages hold [HCb/8][P_out][8] plus the slack the last plane's
+    // 128-row tiles read past P_out
+    f.a_stage_b = align_up((f.HCb / 8) * f.P_out * 16 + (f.n_pt * 128 - f.P_out) * 16, 128);
+    const int a_stage = f.bulk ? f.a_stage_b : f.n_pt * 128 * f.HCb * 2;
     f.sa = 0;
     for (int sa = std::min(4, std::max(2, f.nchb)); sa >= 2 && !f.sa; --sa) {
       f.s_pv = align_up(sa * a_stage, 128);
@@ -1340,6 +1419,7 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     if (int e = encode_tmap(&th_load, h2, 3, dims, strides, box_l)) return e;
   }
   f.wback = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
+  f.h2 = h2;
   f.x = reinterpret_cast<const __half*>(x);
   f.z = reinterpret_cast<__half*>(z);
   CUtensorMap th_fused = th_load;
