@@ -44,7 +44,7 @@ constexpr int kProducerWarp = 0, kMmaWarp = 1, kAllocWarp = 2, kHWarp0 = 4, kTWa
 
 struct Bars {
   uint64_t hdr_full, w_all;
-  uint64_t halo_full[2], halo_empty[2];
+  uint64_t halo_full[8], halo_empty[8];
   uint64_t conv_full, cacc_empty;
   uint64_t xc_full[2], xc_empty[2];
   uint64_t e_full[2], h_full[2], h_empty[2];
@@ -71,14 +71,16 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
   Bars& B = *reinterpret_cast<Bars*>(smem + pl.s_bar);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r = pl.r, nchunks = pl.nchunks, S = pl.ring_stages;
+  const int r = pl.r, nchunks = pl.nchunks, S = pl.ring_stages, NHB = pl.halo_bufs;
 
   if (threadIdx.x == 0) {
     mbar_init(&B.hdr_full, 1);
     mbar_init(&B.w_all, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < pl.halo_bufs; ++i) {
       mbar_init(&B.halo_full[i], 1);
       mbar_init(&B.halo_empty[i], 128);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&B.xc_full[i], 128);
       mbar_init(&B.xc_empty[i], 1);
       mbar_init(&B.e_full[i], 1);
@@ -124,14 +126,14 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       auto load_halo = [&](int it) {
         int n, y0, x0;
         tile_coords((int)blockIdx.x + it * (int)gridDim.x, n, y0, x0);
-        const int b = it & 1, use = it >> 1;
+        const int b = it % NHB, use = it / NHB;
         mbar_wait(&B.halo_empty[b], (use & 1) ^ 1);
         mbar_arrive_expect_tx(&B.halo_full[b], pl.halo_bytes);
         tma_load_5d(s_halo + b * pl.halo_bytes, &tmap_x, 0, x0 - P, y0 - P, 0, n, &B.halo_full[b]);
       };
-      if (my_tiles > 0) load_halo(0);
+      for (int it = 0; it < my_tiles && it < NHB - 1; ++it) load_halo(it);
       for (int it = 0; it < my_tiles; ++it) {
-        if (it + 1 < my_tiles) load_halo(it + 1);
+        if (it + NHB - 1 < my_tiles) load_halo(it + NHB - 1);
         if (!pl.resident) {
           for (int j = 0; j < nchunks; ++j) {
             const int g = it * nchunks + j, slot = g % S, use = g / S;
@@ -154,8 +156,8 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       if (pl.resident) mbar_wait(&B.w_all, 0);
       tc_fence_after();
       auto issue_conv = [&](int u) {  // grouped 3x3 conv of tile u into Cacc
-        const int b = u & 1;
-        mbar_wait(&B.halo_full[b], (u >> 1) & 1);
+        const int b = u % NHB;
+        mbar_wait(&B.halo_full[b], (u / NHB) & 1);
         if (u > 0) mbar_wait(&B.cacc_empty, (u - 1) & 1);
         tc_fence_after();
         const uint32_t hb = halo0 + b * pl.halo_bytes;
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         mbar_wait(&B.conv_full, u & 1);
         tc_fence_after();
       } else {
-        mbar_wait(&B.halo_full[xb], (u >> 1) & 1);
+        mbar_wait(&B.halo_full[u % NHB], (u / NHB) & 1);
       }
       mbar_wait(&B.xc_empty[xb], ((u >> 1) & 1) ^ 1);
       if constexpr (T8) {
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         mbar_arrive(&B.cacc_empty);
       } else {
         // depthwise k x k stencil on CUDA cores, fp32 accumulation
-        const uint8_t* hb = s_halo + xb * pl.halo_bytes;
+        const uint8_t* hb = s_halo + (u % NHB) * pl.halo_bytes;
         const float* s_w = reinterpret_cast<const float*>(s_hdr + pl.o_convw);  // [KS*KS][C]
 #pragma unroll 1
         for (int g = 0; g < G; ++g) {
@@ -339,9 +341,9 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
     auto final_epi = [&](int it) {
       int n, y0, x0;
       tile_coords((int)blockIdx.x + it * (int)gridDim.x, n, y0, x0);
-      const int hbuf = it & 1;
+      const int hbuf = it % NHB;
       mbar_wait(&B.z_full, it & 1);
-      mbar_wait(&B.halo_full[hbuf], (it >> 1) & 1);
+      mbar_wait(&B.halo_full[hbuf], (it / NHB) & 1);
       tc_fence_after();
       const uint8_t* hb = s_halo + hbuf * pl.halo_bytes;
       const int y = y0 + tr, x = x0 + tc;
@@ -449,30 +451,48 @@ bool cf_plan(const wl_block_desc& d, CfPlan& p) {
   p.halo_bytes = p.G * p.HH * p.HW * 16;
   p.xc_bytes = kTileM * p.C * 2;
   p.s_halo = 0;
-  p.s_xc = align_up(2 * p.halo_bytes, 128);
-  p.s_hdr = p.s_xc + 2 * p.xc_bytes;
-  p.s_ring = align_up(p.s_hdr + p.hdr_bytes, 128);
-  auto total = [&](int ring_bytes) { return align_up(p.s_ring + ring_bytes, 128) + 512; };
   const int all = p.nchunks * p.chunk_bytes;
-  if (total(all) <= kSmemTwoPerSm && p.tmem_cols <= 256) {
-    p.resident = 1;
-    p.ctas_per_sm = 2;
-    p.ring_stages = 1;
-  } else if (total(all) <= kSmemMax) {
-    p.resident = 1;
-    p.ctas_per_sm = 1;
-    p.ring_stages = 1;
-  } else {
+  // deepest halo ring (4..2) that keeps two CTAs per SM; else one CTA per SM
+  // with resident weights; else a streamed weight ring
+  auto layout = [&](int nb) {
+    p.halo_bufs = nb;
+    p.s_xc = align_up(nb * p.halo_bytes, 128);
+    p.s_hdr = p.s_xc + 2 * p.xc_bytes;
+    p.s_ring = align_up(p.s_hdr + p.hdr_bytes, 128);
+  };
+  auto total = [&](int ring_bytes) { return align_up(p.s_ring + ring_bytes, 128) + 512; };
+  bool placed = false;
+  for (int nb = 8; nb >= 2 && !placed; --nb) {
+    layout(nb);
+    if (total(all) <= kSmemTwoPerSm && p.tmem_cols <= 256) {
+      p.resident = 1;
+      p.ctas_per_sm = 2;
+      p.ring_stages = 1;
+      placed = true;
+    }
+  }
+  for (int nb = 8; nb >= 2 && !placed; --nb) {
+    layout(nb);
+    if (total(all) <= kSmemMax) {
+      p.resident = 1;
+      p.ctas_per_sm = 1;
+      p.ring_stages = 1;
+      placed = true;
+    }
+  }
+  for (int nb = 8; nb >= 2 && !placed; --nb) {
+    layout(nb);
     p.resident = 0;
     p.ctas_per_sm = 1;
     p.ring_stages = 0;
     for (int s = 8; s >= 2; --s)
       if (total(s * p.chunk_bytes) <= kSmemMax) {
         p.ring_stages = s;
+        placed = true;
         break;
       }
-    if (!p.ring_stages) return false;
   }
+  if (!placed) return false;
   const int ring = p.resident ? all : p.ring_stages * p.chunk_bytes;
   p.s_bar = align_up(p.s_ring + ring, 128);
   p.smem_bytes = p.s_bar + 512;

@@ -25,6 +25,7 @@ struct CfPlan {
   int s_halo, s_xc, s_hdr, s_ring, s_bar, smem_bytes;
   int t_z, t_cacc, t_e, t_h, h_stride, tmem_cols;
   int ctas_per_sm;
+  int halo_bufs;  // TMA halo ring depth (2..8)
 };
 
 // Stride-2 ConvFirst fused block (BlurPool along H then W).
