@@ -122,7 +122,9 @@ __device__ __forceinline__ int st_off(int p, int g, int st_rows, int groups8) {
     if (a.trace && blockIdx.x == 0) a.trace[(slot)] = clock64();        \
   } while (0)
 
-template <int ACT>
+// T8 / S2 / FUSED are compile-time so each instantiation carries only the
+// code its configuration executes (a smaller hot instruction footprint)
+template <int ACT, bool T8, bool S2, bool FUSED>
 __global__ void __launch_bounds__(mbk::kThreads, 1)
     mb_front_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_h2,
                     const __grid_constant__ CUtensorMap tmap_h2l, const __grid_constant__ MbFrontArgs a) {
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.h1_full[i], 256);
-      mbar_init(&B.h1_empty[i], a.T8 ? 1 : 256);
+      mbar_init(&B.h1_empty[i], T8 ? 1 : 256);
     }
     mbar_init(&B.x_ready, 256);
     for (int i = 0; i < 4; ++i) {
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const int slot = j % S, hb = j % a.h1_bufs;
         if (a.e_bufs == 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // E of chunk j consumed
         if (j + 1 < nch) issue_expand(j + 1);
-        if (a.T8) {
+        if (T8) {
           const int cb = j % a.c_bufs;
           if (a.e_bufs != 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);
           if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
@@ -366,12 +368,12 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
     const float* s_cw = reinterpret_cast<const float*>(s_hdr + a.o_convw);  // [9][HR] (T1)
     mbar_wait(&B.hdr_full, 0);
-    uint8_t* dst_stage = a.stride == 1 ? s_st : s_full;
-    const int dst_rows = a.stride == 1 ? a.st_rows : a.P_full;
-    const bool one_store = a.stride == 2 || a.st_stores == 1;
+    uint8_t* dst_stage = !S2 ? s_st : s_full;
+    const int dst_rows = !S2 ? a.st_rows : a.P_full;
+    const bool one_store = S2 || a.st_stores == 1;
     for (int j = 0; j < nch; ++j) {
       const int cb = j % a.c_bufs;
-      if (a.T8) {
+      if (T8) {
         mbar_wait(&B.c_full[cb], (j / a.c_bufs) & 1);
         tc_fence_after();
       } else {
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const int p = s_cmap[t * 128 + lrow];  // dense full-resolution pixel, -1 = pad
         for (int c0 = hh * 16; c0 < HC; c0 += 32) {
           uint32_t v[16];
-          if (a.T8) {
+          if (T8) {
             WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + (cb * a.n_ct + t) * HC + c0), v);
             tmem_ld_wait();
           } else {
@@ -421,14 +423,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           }
         }
       }
-      if (a.T8) {
+      if (T8) {
         tc_fence_before();
         mbar_arrive(&B.c_empty[cb]);
       } else {
         mbar_arrive(&B.h1_empty[j % a.h1_bufs]);
       }
       named_bar(1, 256);
-      if (a.stride == 2) {
+      if (S2) {
         // BlurPool Triangle-3 x Triangle-3 / 16, stride 2, reflect pad (-1 -> 1)
         const int nq = a.P_out * G8;
         for (int i = tid; i < nq; i += 256) {
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (tid == 0) WL_TRACE(8);
     if (tid == 0) bulk_wait0();
     const float inv = 1.f / (float)(a.Ho * a.Wo);
-    if (a.fused) {  // ranges == 1: the squeeze-excite below reads the pool straight from shared memory
+    if (FUSED) {  // ranges == 1: the squeeze-excite below reads the pool straight from shared memory
       float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;
       for (int i = tid; i < a.imgs * a.HR; i += 256) s_vec[i] = s_pool[i] * inv;
     } else {
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
 
   // ---------------- squeeze-excite, once per image group (last CTA to arrive;
   // in fused mode the CTA owns the whole group and skips the global handshake)
-  if (!a.fused) __threadfence();  // publish this CTA's pool slice before arriving
+  if (!FUSED) __threadfence();  // publish this CTA's pool slice before arriving
   tc_fence_before();
   __syncthreads();
   const int a_tile = 128 * a.HCb * 2, a_stage = a.bulk ? a.a_stage_b : a.n_pt * a_tile;
@@ -562,14 +564,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     bulk_g2s(s_pv + vs * a.vchunk_bytes, vch + (size_t)j * a.vchunk_bytes, a.vchunk_bytes, &B.pv_full[vs]);
   };
   if (threadIdx.x == 0) {
-    if (a.fused) {
+    if (FUSED) {
       B.last = 1;
     } else {
       __threadfence();
       const int old = atomicAdd(&a.counters[group], 1);
       B.last = (old == a.ranges - 1);
     }
-    if (a.fused) {  // the projection's first operand loads overlap the squeeze-excite
+    if (FUSED) {  // the projection's first operand loads overlap the squeeze-excite
       asm volatile("fence.proxy.async.global;" ::: "memory");  // h2 TMA stores -> TMA loads
       for (int j = 0; j < a.nchb && j < a.sa; ++j) load_a(j);
       for (int j = 0; j < a.nchb && j < 3; ++j) load_v(j);
@@ -578,7 +580,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   __syncthreads();
   if (threadIdx.x == 0) WL_TRACE(9);
   if (B.last) {
-    if (!a.fused) __threadfence();
+    if (!FUSED) __threadfence();
     // fp16 weights: w_sq [hid][SQP], w_ex^T [hid][SQP] (SQP = sq padded to a power of two >= 8)
     const __half* wsq = reinterpret_cast<const __half*>(a.wpack + a.o_wsq);
     const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
 #pragma unroll
       for (int b8 = 0; b8 < 4; ++b8)
         if (b8 < JB) wx[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)tid * a.SQP + b8 * 8);
-    if (!a.fused) {
+    if (!FUSED) {
       for (int i = tid; i < a.imgs * a.hid; i += nt) {
         const int im = i / a.hid;
         s_vec[i] = __ldcg(a.pool + (size_t)(n0 + im) * a.hid + (i - im * a.hid));
@@ -681,16 +683,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       }
       for (int im = 0; im < a.imgs; ++im) {
         const float gv = __fdividef(1.f, 1.f + __expf(-(im ? e1 : e0)));
-        if (!a.fused) a.gates[(size_t)(n0 + im) * a.hid + i] = gv;
+        if (!FUSED) a.gates[(size_t)(n0 + im) * a.hid + i] = gv;
         s_gt[im * a.hid + i] = gv;
         s_gh[im * a.hid + i] = __float2half_rn(gv);
       }
     }
-    if (threadIdx.x == 0 && !a.fused) a.counters[group] = 0;  // self-cleaning for the next launch
+    if (threadIdx.x == 0 && !FUSED) a.counters[group] = 0;  // self-cleaning for the next launch
   }
   if (threadIdx.x == 0) WL_TRACE(10);
   __syncthreads();
-  if (a.fused) {
+  if (FUSED) {
     // ---------------- projection: z = (h2 . gate) W_prj + b_prj (+ x). The
     // phase-1 buffers are dead: A (h2 rows, re-read by TMA from L2) and V
     // rings overlay them; Z accumulates in the expand/conv TMEM columns.
@@ -1265,11 +1267,21 @@ bool mb_plan(const wl_block_desc& d, MbPlanH& P) { return mb_plan_try(d, P, true
 
 using FrontK = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const MbFrontArgs);
 
-FrontK front_kernel(int act) {
+template <int ACT>
+FrontK front_kernel_act(bool t8, bool s2, bool fused) {
+  const int k = (t8 ? 4 : 0) + (s2 ? 2 : 0) + (fused ? 1 : 0);
+  static const FrontK tab[8] = {
+      mb_front_kernel<ACT, false, false, false>, mb_front_kernel<ACT, false, false, true>,
+      mb_front_kernel<ACT, false, true, false>,  mb_front_kernel<ACT, false, true, true>,
+      mb_front_kernel<ACT, true, false, false>,  mb_front_kernel<ACT, true, false, true>,
+      mb_front_kernel<ACT, true, true, false>,   mb_front_kernel<ACT, true, true, true>};
+  return tab[k];
+}
+FrontK front_kernel(int act, bool t8 = true, bool s2 = false, bool fused = true) {
   switch (act) {
-    case kRelu: return mb_front_kernel<kRelu>;
-    case kSilu: return mb_front_kernel<kSilu>;
-    case kGelu: return mb_front_kernel<kGelu>;
+    case kRelu: return front_kernel_act<kRelu>(t8, s2, fused);
+    case kSilu: return front_kernel_act<kSilu>(t8, s2, fused);
+    case kGelu: return front_kernel_act<kGelu>(t8, s2, fused);
   }
   return nullptr;
 }
@@ -1429,7 +1441,8 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     const uint32_t box[2] = {64, 128};
     if (int e = encode_tmap(&th_fused, h2, 2, dims, strides, box, true)) return e;
   }
-  front_kernel(d.act)<<<f.groups * f.ranges, mbk::kThreads, f.smem, st>>>(tx, th_store, th_fused, f);
+  front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0)<<<f.groups * f.ranges, mbk::kThreads, f.smem, st>>>(
+      tx, th_store, th_fused, f);
   if (int e = check_cuda(cudaGetLastError(), "mb_front launch")) return e;
   if (f.fused) return WL_OK;
   b.wpack = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
@@ -1443,9 +1456,11 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
 
 int mb_init() {
   for (int a : {kRelu, kSilu, kGelu})
-    if (int e = check_cuda(cudaFuncSetAttribute(front_kernel(a), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
-                           "cudaFuncSetAttribute(mb_front)"))
-      return e;
+    for (int k = 0; k < 8; ++k)
+      if (int e = check_cuda(cudaFuncSetAttribute(front_kernel(a, k & 4, k & 2, k & 1),
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
+                             "cudaFuncSetAttribute(mb_front)"))
+        return e;
   return check_cuda(cudaFuncSetAttribute(mb_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxMb),
                     "cudaFuncSetAttribute(mb_back)");
 }
