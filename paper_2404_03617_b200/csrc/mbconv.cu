@@ -337,10 +337,12 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       if (j >= a.h1_bufs) mbar_wait(&B.h1_empty[hb], ((j / a.h1_bufs) & 1) ^ 1);
       if (warp == 4 && lane == 0) WL_TRACE(16 + 8 * j + 3);
       tc_fence_after();
-      for (int t = 0; t < a.n_et; ++t) {
+      // (tile, 16-column block) items dealt round-robin to the two warps of a quadrant
+      for (int it = eh; it < a.n_et * (HC / 16); it += 2) {
+        const int t = it / (HC / 16), c0 = (it - t * (HC / 16)) * 16;
         const int f = t * 128 + q * 32 + lane;
         const bool real = s_emap[f] != 0;
-        for (int c0 = eh * 16; c0 < HC; c0 += 32) {
+        {
           uint32_t v[16];
           WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_e + (eb * a.n_et + t) * HC + c0), v);
           tmem_ld_wait();
@@ -384,10 +386,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       // staging may still be read by the previous chunk's TMA store
       if (tid == 0) bulk_wait_read0();
       named_bar(1, 256);
-      for (int t = 0; t < a.n_ct; ++t) {
+      for (int it = hh; it < a.n_ct * (HC / 16); it += 2) {  // (tile, 16-column block) round-robin
+        const int t = it / (HC / 16), c0 = (it - t * (HC / 16)) * 16;
         const int f = a.conv_base + t * 128 + lrow;
         const int p = s_cmap[t * 128 + lrow];  // dense full-resolution pixel, -1 = pad
-        for (int c0 = hh * 16; c0 < HC; c0 += 32) {
+        {
           uint32_t v[16];
           if (T8) {
             WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + (cb * a.n_ct + t) * HC + c0), v);
