@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // single-wave persistent grid: let the next kernel stage its prologue
+  pdl_wait();
   const uint32_t tmem = B.tmem_base;
 
   const int tiles_per_img = args.tiles_x * args.tiles_y;
@@ -670,8 +672,7 @@ int cf_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
   a.wpack = reinterpret_cast<const uint8_t*>(packed);
   a.z = reinterpret_cast<__half*>(z);
   const int grid = std::min(a.ntiles, kNumSMs * p.ctas_per_sm);
-  it->second<<<grid, cfk::kThreads, p.smem_bytes, st>>>(tm, a);
-  return check_cuda(cudaGetLastError(), "cf_fused launch");
+  return launch_pdl(it->second, grid, cfk::kThreads, p.smem_bytes, st, "cf_fused launch", tm, a);
 }
 
 int cf_init() {

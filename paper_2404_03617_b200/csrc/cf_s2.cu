@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // single-wave persistent grid: let the next kernel stage its prologue
+  pdl_wait();
   const uint32_t tmem = B.tmem_base;
   if (threadIdx.x == 0) CF2_TRACE(0);
 
@@ -645,8 +647,7 @@ int cf2_forward(const wl_block_desc& d, const void* x, const void* packed, void*
   a.z = reinterpret_cast<__half*>(z);
   a.trace = g_cf2_trace;
   const int grid = std::min(a.nbands, kNumSMs);
-  cf2_kernel_for(d.act)<<<grid, cf2k::kThreads, a.smem, st>>>(tm, tz, a);
-  return check_cuda(cudaGetLastError(), "cf2 launch");
+  return launch_pdl(cf2_kernel_for(d.act), grid, cf2k::kThreads, a.smem, st, "cf2 launch", tm, tz, a);
 }
 int cf2_init() {
   for (int act : {kRelu, kSilu, kGelu})

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(256, 1) head_pool_kernel(const __grid_constant
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = *tbase;
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar[0], 128 * a.C * 2 + a.w1_chunk);
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = *tbase;
   const uint8_t* wchunks = a.w2 + align_up(a.classes * 4, 128) + (size_t)cc * a.nkc * a.w_chunk;
   if (tid == 0) {
@@ -328,13 +330,11 @@ int head_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void
   h.w1 = reinterpret_cast<const uint8_t*>(p);
   h.feat = reinterpret_cast<__half*>(feat);
   const int groups = (d.n + h.imgs - 1) / h.imgs;
-  head_k(d.act)<<<groups * h.nce, 256, h.s_bar + 64, st>>>(tx, h);
-  if (int e = check_cuda(cudaGetLastError(), "head_pool launch")) return e;
+  if (int e = launch_pdl(head_k(d.act), groups * h.nce, 256, h.s_bar + 64, st, "head_pool launch", tx, h)) return e;
   f.w2 = reinterpret_cast<const uint8_t*>(p) + P.w1_bytes;
   f.z = reinterpret_cast<__half*>(z);
   const int rows = (d.n + 127) / 128;
-  head_fc_kernel<<<rows * f.N, 128, f.s_bar + 128, st>>>(tf, f);
-  return check_cuda(cudaGetLastError(), "head_fc launch");
+  return launch_pdl(head_fc_kernel, rows * f.N, 128, f.s_bar + 128, st, "head_fc launch", tf, f);
 }
 int head_init() {
   for (int act : {kRelu, kSilu, kGelu, kIdentity})

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 #include "../../include/wlfuse.h"
 
 namespace wl {
@@ -14,6 +15,25 @@ int encode_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dim
 void put_h(uint8_t* base, size_t off, float v);
 static inline size_t core_off_h(int row, int k, int lbo) {
   return (size_t)(k / 8) * lbo + (size_t)(row / 8) * 128 + (size_t)(row % 8) * 16 + (size_t)(k % 8) * 2;
+}
+
+// launch with programmatic stream serialization (PDL): the kernel's prologue
+// may overlap the previous kernel on the stream; kernels call pdl_wait()
+// before reading what that kernel produced (sm100.cuh)
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, const char* what,
+               Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return check_cuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), what);
 }
 
 // dispatch over block kinds (blocks.cu)

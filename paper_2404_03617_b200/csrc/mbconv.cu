@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (FUSED) pdl_trigger();  // single-wave persistent grid: let the next kernel stage its prologue
+  pdl_wait();
   const uint32_t tmem = B.tmem_base;
 
   if (warp == 0) {
@@ -924,6 +926,8 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // (multi-wave grid: dependents launch as CTAs retire)
+  pdl_wait();
   const uint32_t tmem = B.tmem_base;
   const int a_stage_bytes = 128 * HCb * 2;
 
@@ -1444,17 +1448,16 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     const uint32_t box[2] = {64, 128};
     if (int e = encode_tmap(&th_fused, h2, 2, dims, strides, box, true)) return e;
   }
-  front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0)<<<f.groups * f.ranges, mbk::kThreads, f.smem, st>>>(
-      tx, th_store, th_fused, f);
-  if (int e = check_cuda(cudaGetLastError(), "mb_front launch")) return e;
+  if (int e = launch_pdl(front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0), f.groups * f.ranges, mbk::kThreads,
+                         f.smem, st, "mb_front launch", tx, th_store, th_fused, f))
+    return e;
   if (f.fused) return WL_OK;
   b.wpack = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
   b.gates = f.gates;
   b.x = reinterpret_cast<const __half*>(x);
   b.z = reinterpret_cast<__half*>(z);
   const int ntiles = (b.P + 127) / 128;
-  mb_back_kernel<<<ntiles * b.kranges, 256, b.smem, st>>>(th_load, b);
-  return check_cuda(cudaGetLastError(), "mb_back launch");
+  return launch_pdl(mb_back_kernel, ntiles * b.kranges, 256, b.smem, st, "mb_back launch", th_load, b);
 }
 
 int mb_init() {

@@ -121,6 +121,14 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// ------------------------------------------------ programmatic dependent launch
+// Kernels are launched with programmatic stream serialization: the prologue
+// (barrier init, TMEM allocation, smem set-up) of kernel i+1 overlaps the tail
+// of kernel i; every thread waits for the previous grid before touching
+// global memory it produces (activations, the shared workspace).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------ descriptors
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;

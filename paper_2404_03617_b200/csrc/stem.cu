@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256, 1) stem_kernel(const __grid_constant__ St
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = *tbase;
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar[0], a.w_bytes);
@@ -199,8 +200,7 @@ int stem_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void
   a.x = reinterpret_cast<const __half*>(x);
   a.wpack = reinterpret_cast<const uint8_t*>(p);
   a.z = reinterpret_cast<__half*>(z);
-  stem_k(d.act)<<<d.n * a.tiles_y, 256, a.s_bar + 64, st>>>(a);
-  return check_cuda(cudaGetLastError(), "stem launch");
+  return launch_pdl(stem_k(d.act), d.n * a.tiles_y, 256, a.s_bar + 64, st, "stem launch", a);
 }
 int stem_init() {
   for (int act : {kRelu, kSilu, kGelu, kIdentity})
