@@ -166,12 +166,14 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         const uint32_t lbo = HH * HWD * 16, sbo = HWD * 16;
 #pragma unroll 1
         for (int pr = 0; pr < G / 2; ++pr) {
+          uint64_t ad = make_sdesc(hb + (2 * pr * HH * HWD) * 16, lbo, sbo);
+          uint64_t bd = make_sdesc(convw + (pr * KS * KS) * 512, 256, 128);
+          const uint32_t d = tmem + pl.t_cacc + 16 * pr;
 #pragma unroll
-          for (int t = 0; t < KS * KS; ++t) {
-            const int dy = t / KS, dx = t % KS;
-            const uint64_t ad = make_sdesc(hb + ((2 * pr * HH + dy) * HWD + dx) * 16, lbo, sbo);
-            const uint64_t bd = make_sdesc(convw + (pr * KS * KS + t) * 512, 256, 128);
-            mma_ss(tmem + pl.t_cacc + 16 * pr, ad, bd, idesc_conv, t > 0);
+          for (int t = 0; t < KS * KS; ++t) {  // incremental descriptors (cheap issue)
+            mma_ss(d, ad, bd, idesc_conv, t > 0);
+            ad += (t % KS == KS - 1) ? (uint64_t)(HWD - (KS - 1)) : 1ull;
+            bd += 32;
           }
         }
         mma_commit(&B.conv_full);

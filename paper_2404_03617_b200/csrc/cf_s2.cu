@@ -181,11 +181,14 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
           for (int pr = 0; pr < C / 16; ++pr) {
             const uint64_t ad = make_sdesc(x0 + (2 * pr * a.x_alloc + a.conv_base - Wp - 1 + t * 128) * 16,
                                            a.x_alloc * 16, 128);
-            const uint64_t bd = make_sdesc(cw + pr * 9 * 512, 256, 128);
+            uint64_t aa = ad, bd = make_sdesc(cw + pr * 9 * 512, 256, 128);
+            const uint32_t d = tmem + a.t_c + t * C + 16 * pr;
 #pragma unroll
-            for (int tap = 0; tap < 9; ++tap)
-              mma_ss(tmem + a.t_c + t * C + 16 * pr, ad + (uint64_t)((tap / 3) * Wp + tap % 3),
-                     bd + (uint64_t)(tap * 32), idesc_c, tap > 0);
+            for (int tap = 0; tap < 9; ++tap) {  // incremental descriptors (cheap issue)
+              mma_ss(d, aa, bd, idesc_c, tap > 0);
+              aa += (tap % 3 == 2) ? (uint64_t)(Wp - 2) : 1ull;
+              bd += 32;
+            }
           }
       };
       auto conv_end = [&](int i) {

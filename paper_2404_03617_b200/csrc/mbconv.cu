@@ -292,10 +292,15 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             for (int pr = 0; pr < HC / 16; ++pr) {
               const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
               const uint64_t ap = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128);
-              const uint64_t bp = b_base + (uint64_t)(pr * 9) * b_step;
+              // incremental descriptors: one 64-bit add each between MMAs keeps
+              // the single issuing thread off the critical path
+              uint64_t ad = ap, bd = b_base + (uint64_t)(pr * 9) * b_step;
 #pragma unroll
-              for (int tap = 0; tap < 9; ++tap)
-                mma_ss(d, ap + (uint64_t)((tap / 3) * a.Wp + tap % 3), bp + (uint64_t)tap * b_step, idesc_c, tap > 0);
+              for (int tap = 0; tap < 9; ++tap) {
+                mma_ss(d, ad, bd, idesc_c, tap > 0);
+                ad += (tap % 3 == 2) ? (uint64_t)(a.Wp - 2) : 1ull;
+                bd += b_step;
+              }
             }
           mma_commit(&B.c_full[cb]);
           mma_commit(&B.h1_empty[hb]);
