@@ -21,19 +21,28 @@ static inline size_t core_off_h(int row, int k, int lbo) {
 // may overlap the previous kernel on the stream; kernels call pdl_wait()
 // before reading what that kernel produced (sm100.cuh)
 template <typename... KArgs, typename... Args>
-int launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, const char* what,
-               Args&&... args) {
+int launch_pdl_cluster(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, const char* what,
+                       int cluster, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = cluster;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = cluster > 1 ? 2 : 1;
   return check_cuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), what);
+}
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, const char* what,
+               Args&&... args) {
+  return launch_pdl_cluster(kernel, grid, block, smem, st, what, 1, std::forward<Args>(args)...);
 }
 
 // dispatch over block kinds (blocks.cu)

@@ -100,6 +100,23 @@ __device__ __forceinline__ bool mb_real(int f, int Wp, int W, int H, int total_r
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+// thread-block-cluster pair (two CTAs split one image group's hidden channels)
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t peer_smem(const void* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void st_peer_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_peer_v4(uint32_t addr, const uint32_t* v) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3])
+               : "memory");
+}
 
 __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tmap),
@@ -551,13 +568,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int a_tile = 128 * a.HCb * 2, a_stage = a.bulk ? a.a_stage_b : a.n_pt * a_tile;
   uint8_t* s_pa = smem + a.s_pa;
   uint8_t* s_pv = smem + a.s_pv;
-  const uint8_t* vch = a.wback + align_up(a.K * 4, 128);
+  const uint8_t* vch = a.wback + align_up(a.K * 4, 128) + (FUSED ? (size_t)h0 * a.K * 2 : 0);  // this range's W_prj rows
   auto load_a = [&](int j) {  // h2 rows of chunk j (re-read from L2) -> A stage
     const int ab = j % a.sa;
     if (a.bulk) {  // planes [HCb/8][P_out][8], contiguous in global
       const uint32_t bytes = a.P_out * a.HCb * 2;
       mbar_arrive_expect_tx(&B.pa_full[ab], bytes);
-      bulk_g2s(s_pa + ab * a_stage, a.h2 + ((size_t)group * a.hid + (size_t)j * a.HCb) * a.P_out, bytes, &B.pa_full[ab]);
+      bulk_g2s(s_pa + ab * a_stage, a.h2 + ((size_t)group * a.hid + h0 + (size_t)j * a.HCb) * a.P_out, bytes,
+               &B.pa_full[ab]);
       return;
     }
     mbar_arrive_expect_tx(&B.pa_full[ab], a_stage);
@@ -599,16 +617,21 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;  // [imgs][hid] pool
     float* s_red = s_vec + a.imgs * a.hid;                                       // [20 warps][imgs][SQP]
     float* s_sq = s_red + 20 * a.imgs * a.SQP;                                   // [imgs][SQP]
+    float* s_sqx = s_sq + a.imgs * a.SQP;  // the pair peer's partial squeeze (cluster mode)
     float* s_gt = reinterpret_cast<float*>(smem + a.s_gate);
     const int tid = threadIdx.x, nt = blockDim.x, nw = nt / 32;
+    // fused: this CTA's hidden range [h0, h0 + HR) (all of hid unless paired);
+    // the split CTAs exchange partial squeezes through distributed shared memory
+    const int SEH = FUSED ? a.HR : a.hid, seh0 = FUSED ? h0 : 0;
+    const bool paired = FUSED && a.ranges == 2;
     // excite weights of this thread's hidden channel, fetched now so their
     // latency overlaps the squeeze (SQP <= 32: four 16-byte rows)
     const int JB = a.SQP / 8;
     uint4 wx[4];
-    if (JB <= 4 && tid < a.hid)
+    if (JB <= 4 && tid < SEH)
 #pragma unroll
       for (int b8 = 0; b8 < 4; ++b8)
-        if (b8 < JB) wx[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)tid * a.SQP + b8 * 8);
+        if (b8 < JB) wx[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)(seh0 + tid) * a.SQP + b8 * 8);
     if (!FUSED) {
       for (int i = tid; i < a.imgs * a.hid; i += nt) {
         const int im = i / a.hid;
@@ -625,20 +648,21 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     for (int im = 0; im < 2; ++im)
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[im][k] = 0.f;
-    for (int i0 = warp * sub + isub; i0 < a.hid; i0 += 4 * nw * sub) {
+    for (int i0 = warp * sub + isub; i0 < SEH; i0 += 4 * nw * sub) {
       uint4 wq[4];  // four independent 16-byte loads in flight
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * nw * sub;
-        wq[u] = i < a.hid ? *reinterpret_cast<const uint4*>(wsq + (size_t)i * a.SQP + jb * 8) : make_uint4(0, 0, 0, 0);
+        wq[u] = i < SEH ? *reinterpret_cast<const uint4*>(wsq + (size_t)(seh0 + i) * a.SQP + jb * 8)
+                        : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * nw * sub;
-        if (i >= a.hid) break;
+        if (i >= SEH) break;
         float wv[8];
         unpack8(wq[u], wv);
-        const float p0 = s_vec[i], p1 = a.imgs > 1 ? s_vec[a.hid + i] : 0.f;
+        const float p0 = s_vec[i], p1 = a.imgs > 1 ? s_vec[SEH + i] : 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           acc[0][k] += p0 * wv[k];
@@ -661,18 +685,32 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         for (int k = 0; k < 8; ++k) s_red[(warp * a.imgs + 1) * a.SQP + jb * 8 + k] = acc[1][k];
     }
     __syncthreads();
-    for (int i = tid; i < a.imgs * a.SQP; i += nt) {
-      const int im = i / a.SQP, j = i - im * a.SQP;
-      float v = bsq[j];
-      for (int w2 = 0; w2 < nw; ++w2) v += s_red[(w2 * a.imgs + im) * a.SQP + j];
-      s_sq[i] = fmaxf(v, 0.f);
+    if (paired) {  // partial squeezes of the two hidden halves meet in both CTAs
+      const uint32_t peer = blockIdx.x & 1 ? 0u : 1u;
+      for (int i = tid; i < a.imgs * a.SQP; i += nt) {
+        const int im = i / a.SQP, j = i - im * a.SQP;
+        float v = 0.f;
+        for (int w2 = 0; w2 < nw; ++w2) v += s_red[(w2 * a.imgs + im) * a.SQP + j];
+        s_sq[i] = v;
+        st_peer_f32(peer_smem(s_sqx + i, peer), v);
+      }
+      cluster_sync_all();
+      for (int i = tid; i < a.imgs * a.SQP; i += nt) s_sq[i] = fmaxf(s_sq[i] + s_sqx[i] + bsq[i % a.SQP], 0.f);
+    } else {
+      for (int i = tid; i < a.imgs * a.SQP; i += nt) {
+        const int im = i / a.SQP, j = i - im * a.SQP;
+        float v = bsq[j];
+        for (int w2 = 0; w2 < nw; ++w2) v += s_red[(w2 * a.imgs + im) * a.SQP + j];
+        s_sq[i] = fmaxf(v, 0.f);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) WL_TRACE(125);
     // excite: one hidden channel per thread, its SQP weights as 16-byte vectors
     __half* s_gh = reinterpret_cast<__half*>(s_vec);  // [imgs][hid] half gates (pool is dead now)
-    for (int i = tid; i < a.hid; i += nt) {
-      float e0 = bex[i], e1 = bex[i];
+    for (int i = tid; i < SEH; i += nt) {
+      const int hch = seh0 + i;
+      float e0 = bex[hch], e1 = bex[hch];
       uint4 wq[8];
       if (JB <= 4 && i == tid) {
 #pragma unroll
@@ -680,11 +718,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       } else {
 #pragma unroll
         for (int b8 = 0; b8 < 8; ++b8)
-          if (b8 < JB) wq[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8);
+          if (b8 < JB) wq[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)hch * a.SQP + b8 * 8);
       }
       for (int b8 = 0; b8 < JB; ++b8) {
         float wv[8];
-        unpack8(b8 < 8 ? wq[b8] : *reinterpret_cast<const uint4*>(wexT + (size_t)i * a.SQP + b8 * 8), wv);
+        unpack8(b8 < 8 ? wq[b8] : *reinterpret_cast<const uint4*>(wexT + (size_t)hch * a.SQP + b8 * 8), wv);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           e0 += s_sq[b8 * 8 + k] * wv[k];
@@ -694,8 +732,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       for (int im = 0; im < a.imgs; ++im) {
         const float gv = __fdividef(1.f, 1.f + __expf(-(im ? e1 : e0)));
         if (!FUSED) a.gates[(size_t)(n0 + im) * a.hid + i] = gv;
-        s_gt[im * a.hid + i] = gv;
-        s_gh[im * a.hid + i] = __float2half_rn(gv);
+        s_gt[im * SEH + i] = gv;
+        s_gh[im * SEH + i] = __float2half_rn(gv);
       }
     }
     if (threadIdx.x == 0 && !FUSED) a.counters[group] = 0;  // self-cleaning for the next launch
@@ -762,14 +800,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       // broadcast 16-byte load
       const int tid = (warp - 4) * 32 + lane;
       const int c8 = tid & 7;
-      const __half* s_gh = reinterpret_cast<const __half*>(s_gate + a.imgs * a.hid);  // half gates (SE scratch)
+      const __half* s_gh = reinterpret_cast<const __half*>(s_gate + a.imgs * a.hid);  // half gates [imgs][HR] (SE scratch)
       for (int j = 0; j < a.nchb; ++j) {
         const int ab = j % a.sa;
         mbar_wait(&B.pa_full[ab], (j / a.sa) & 1);
         if (tid == 0 && j < 8) WL_TRACE(112 + j);
         if (a.bulk) {  // planes [HCb/8][P_out][8]: item = plane * P_out + pixel, 2 per step
           uint8_t* base = s_pa + ab * a_stage;
-          const __half* gj = s_gh + j * a.HCb;
+          const __half* gj = s_gh + j * a.HCb;  // [imgs][HR] gates of this hidden range
           const int nitems = (a.HCb / 8) * a.P_out;
           int c8p = tid / a.P_out, p = tid - c8p * a.P_out;  // walked incrementally
           const int dq = 256 / a.P_out, dr = 256 - dq * a.P_out;
@@ -784,8 +822,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             uint4* pa = reinterpret_cast<uint4*>(base + ((size_t)c8p * a.P_out + p) * 16);
             uint4* pb2 = reinterpret_cast<uint4*>(base + ((size_t)c8b * a.P_out + pb) * 16);
             uint4 va = *pa, vb = two ? *pb2 : va;
-            const uint4 ga = *reinterpret_cast<const uint4*>(gj + ia * a.hid + c8p * 8);
-            const uint4 gb = *reinterpret_cast<const uint4*>(gj + ib * a.hid + (two ? c8b : c8p) * 8);
+            const uint4 ga = *reinterpret_cast<const uint4*>(gj + ia * a.HR + c8p * 8);
+            const uint4 gb = *reinterpret_cast<const uint4*>(gj + ib * a.HR + (two ? c8b : c8p) * 8);
             __half2* ha = reinterpret_cast<__half2*>(&va);
             __half2* hb = reinterpret_cast<__half2*>(&vb);
             const __half2* g1 = reinterpret_cast<const __half2*>(&ga);
@@ -811,7 +849,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         for (int r = tid >> 3; r < a.n_pt * 128; r += 32) {
           const int t = r >> 7, m = r & 127;
           const int p = min(t * 128 + m, a.P_out - 1);
-          const uint4 gv = *reinterpret_cast<const uint4*>(s_gh + (p / pix_img) * a.hid + j * a.HCb + c8 * 8);
+          const uint4 gv = *reinterpret_cast<const uint4*>(s_gh + (p / pix_img) * a.HR + j * a.HCb + c8 * 8);
           uint4* ptr = reinterpret_cast<uint4*>(s_pa + ab * a_stage + t * a_tile + sw128_off(m, c8));
           uint4 v = *ptr;
           __half2* h = reinterpret_cast<__half2*>(&v);
@@ -826,6 +864,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     } else if (warp >= 12) {
       const int q = warp % 4, hh = (warp - 12) / 4;
       const float* bprj = reinterpret_cast<const float*>(a.wback);
+      if (a.ranges == 2) {  // paired: the two partial Z meet after the projection (below)
+        mbar_wait_sleep(&B.z_full, 0);
+        tc_fence_after();
+      } else {
       // z = Z + b_prj (+ x). Each thread owns one pixel row and the 16-column
       // blocks hh, hh+2, ... (two per group); the residual rows of the next
       // group are loaded while this group is combined (the first group's are
@@ -885,10 +927,66 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         }
       }
       tc_fence_before();
+      }
       if (warp == 12 && lane == 0) WL_TRACE(12);
     }
     __syncthreads();
     if (threadIdx.x == 0) WL_TRACE(13);
+    if (a.ranges == 2) {
+      // ---- paired CTAs: each holds Z over its hidden half. CTA r finishes the
+      // output channels [r K/2, (r+1) K/2): it receives the peer's partial for
+      // them (fp32, distributed shared memory, rows padded by 16 bytes) into
+      // the dead projection-operand region, then adds its own, b_prj and x.
+      const int rank = blockIdx.x & 1, KH = a.K / 2, RS = KH + 4;
+      float* s_zr = reinterpret_cast<float*>(smem);  // [n_pt * 128][RS]
+      cluster_sync_all();                            // both projections done: operand regions free
+      if (warp >= 12) {
+        const int q = warp % 4, hh = (warp - 12) / 4, m = q * 32 + lane;
+        const int pc0 = (1 - rank) * KH;
+        for (int t = 0; t < a.n_pt; ++t)
+          for (int c0 = hh * 16; c0 < KH; c0 += 32) {
+            uint32_t v[16];
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * a.K + pc0 + c0), v);
+            tmem_ld_wait();
+            const uint32_t dst = peer_smem(s_zr + (size_t)(t * 128 + m) * RS + c0, 1u - rank);
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) st_peer_v4(dst + 16 * k4, v + 4 * k4);
+          }
+      }
+      cluster_sync_all();  // partials delivered
+      if (warp >= 12) {
+        const int q = warp % 4, hh = (warp - 12) / 4, m = q * 32 + lane;
+        const int oc0 = rank * KH;
+        const float* bprj = reinterpret_cast<const float*>(a.wback);
+        for (int t = 0; t < a.n_pt; ++t) {
+          const int p = t * 128 + m;
+          const bool inside = p < a.P_out;
+          const size_t gp = (size_t)group * a.P_out + (inside ? p : 0);
+          for (int c0 = hh * 16; c0 < KH; c0 += 32) {
+            uint32_t v[16];
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * a.K + oc0 + c0), v);
+            tmem_ld_wait();
+            if (!inside) continue;
+            float f[16], r[16];
+            const float* zr = s_zr + (size_t)(t * 128 + m) * RS + c0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + zr[i] + bprj[oc0 + c0 + i];
+            if (a.residual) {
+              const uint4* xp = reinterpret_cast<const uint4*>(a.x + gp * a.K + oc0 + c0);
+              unpack8(__ldg(xp), r);
+              unpack8(__ldg(xp + 1), r + 8);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) f[i] += r[i];
+            }
+            uint4* zp = reinterpret_cast<uint4*>(a.z + gp * a.K + oc0 + c0);
+            zp[0] = pack8(f);
+            zp[1] = pack8(f + 8);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncthreads();
+    }
   }
   if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
 }
@@ -1084,7 +1182,9 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   f.st_rows = f.P_out / f.st_stores;
   if (f.groups > (int)(kCounterBytes / 4)) return false;
   if (f.sq < 1 || f.sq > 128) return false;
-  f.ranges = 1;  // fused mode: the CTA owns every hidden channel of its images
+  // fused mode: the CTA owns every hidden channel of its images, or - when the
+  // image groups would leave over half the SMs idle - a cluster pair splits them
+  f.ranges = (want_fused && 2 * f.groups <= kNumSMs && hid % 128 == 0 && K % 64 == 0 && K <= 256) ? 2 : 1;
   while (!want_fused && f.groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
   f.HR = hid / f.ranges;
   f.HC = 0;
@@ -1196,7 +1296,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     o = align_up(o + h1_one, 128);
   }
   f.s_gate = o;  // SE gates (read by the fused projection) + squeeze-excite scratch
-  o = align_up(o + (2 * f.imgs * hid + 21 * f.imgs * f.SQP) * 4, 128);
+  o = align_up(o + (2 * f.imgs * hid + 22 * f.imgs * f.SQP) * 4, 128);
   f.s_bar = o;
   o += 512;
   f.smem = o;
@@ -1213,10 +1313,11 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     if (f.bulk) {  // projection chunk = lcm(HC, 64) channels (whole conv chunks)
       int pc = 64;
       while (pc % f.HC) pc += 64;
-      if (hid % pc) f.bulk = 0;
+      if (f.HR % pc) f.bulk = 0;
       else f.HCb = pc;
     }
-    f.nchb = hid / f.HCb;
+    if (f.HR % f.HCb || (f.ranges > 1 && !f.bulk)) return false;
+    f.nchb = f.HR / f.HCb;
     f.n_pt = (f.P_out + 127) / 128;
     f.vchunk_bytes = K * f.HCb * 2;
     f.residual = d.stride == 1;
@@ -1453,8 +1554,9 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     const uint32_t box[2] = {64, 128};
     if (int e = encode_tmap(&th_fused, h2, 2, dims, strides, box, true)) return e;
   }
-  if (int e = launch_pdl(front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0), f.groups * f.ranges, mbk::kThreads,
-                         f.smem, st, "mb_front launch", tx, th_store, th_fused, f))
+  if (int e = launch_pdl_cluster(front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0), f.groups * f.ranges,
+                                 mbk::kThreads, f.smem, st, "mb_front launch", (f.fused && f.ranges == 2) ? 2 : 1, tx,
+                                 th_store, th_fused, f))
     return e;
   if (f.fused) return WL_OK;
   b.wpack = reinterpret_cast<const uint8_t*>(packed) + P.front_bytes;
