@@ -74,25 +74,54 @@ class FusedNetwork:
     def output(self) -> torch.Tensor:
         return self.units[-1].out
 
-    def launch_all(self, stream=None) -> None:
-        src = self.x
+    def launch_all(self, stream=None, x: torch.Tensor | None = None) -> None:
+        src = self.x if x is None else x
         for u in self.units:
             u.module.launch(src, u.out, self.workspace, stream)
             src = u.out
 
-    def capture(self) -> torch.cuda.CUDAGraph:
-        """Capture the whole forward into one CUDA graph (warm-up first)."""
+    def _capture_on(self, x: torch.Tensor) -> torch.cuda.CUDAGraph:
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            self.launch_all(s)
+            self.launch_all(s, x)
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.launch_all()
-        self.graph = g
+            self.launch_all(x=x)
         return g
+
+    def capture(self) -> torch.cuda.CUDAGraph:
+        """Capture the whole forward into one CUDA graph (warm-up first)."""
+        self.graph = self._capture_on(self.x)
+        return self.graph
+
+    def run_host_batches(self, batches, outs) -> None:
+        """Serve a sequence of host batches (pinned NHWC fp16) into host logit
+        buffers (pinned). Two input slots, each with its own captured graph:
+        the host->device copy of batch i+1 runs on a copy stream while the
+        forward of batch i runs, and each batch's logits are read back right
+        behind its forward on the compute stream."""
+        if not hasattr(self, "_slots"):
+            self._slots = [self.x, torch.empty_like(self.x)]
+            self._graphs = [self.graph or self.capture(), self._capture_on(self._slots[1])]
+            self._copy = torch.cuda.Stream(device=self.device)
+            self._h2d = [torch.cuda.Event(), torch.cuda.Event()]
+            self._free = [torch.cuda.Event(), torch.cuda.Event()]
+        comp = torch.cuda.current_stream(self.device)
+        for b in range(2):
+            self._free[b].record(comp)
+        for i, (hb, ho) in enumerate(zip(batches, outs)):
+            b = i & 1
+            with torch.cuda.stream(self._copy):
+                self._copy.wait_event(self._free[b])  # slot's previous forward has read it
+                self._slots[b].copy_(hb, non_blocking=True)
+                self._h2d[b].record(self._copy)
+            comp.wait_event(self._h2d[b])
+            self._graphs[b].replay()
+            self._free[b].record(comp)
+            ho.copy_(self.output, non_blocking=True)
 
     def replay(self) -> None:
         if self.graph is None:

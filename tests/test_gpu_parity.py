@@ -156,3 +156,20 @@ def test_unsupported_configs_fail_loudly():
         FusedBlock(ConvFirst(4, 6), TensorDims(1, 8, 8, 16))  # no T=4 kernel
     with pytest.raises(ScheduleError):
         FusedBlock(ConvFirst(8, 6), TensorDims(1, 8, 8, 24))  # C % 16 != 0
+
+
+def test_pipelined_host_batches_match_single_calls():
+    """run_host_batches (double-buffered H2D / forward overlap, the e2e path of
+    bench.py) returns exactly the logits of one-at-a-time calls."""
+    net = zoo.at_resolution(zoo.from_name("convfirstnet-pico"), 224)
+    m = FusedNetwork(net, batch=4, seed=9)
+    rng = np.random.default_rng(4)
+    hosts = [torch.from_numpy(r16(rng, (4, 224, 224, 3))).half().pin_memory() for _ in range(3)]
+    ref = []
+    for h in hosts:
+        ref.append(m(h.cuda()).clone())
+    outs = [torch.empty(m.output.shape, dtype=torch.float16).pin_memory() for _ in hosts]
+    m.run_host_batches(hosts, outs)
+    torch.cuda.synchronize()
+    for r, o in zip(ref, outs):
+        assert torch.equal(r.cpu(), o)
