@@ -281,7 +281,9 @@ def run_gpu(args):
         traffic = None
         try:
             with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as fh:
-                traffic = json.load(fh).get(f"{args.model}:{dom.label}")
+                tkey = (f"{args.model}:{type(inst.block).__name__}:{inst.in_h}x{inst.in_w}x{inst.in_channels}"
+                        f"->{inst.out_channels}")
+                traffic = json.load(fh).get(tkey)
         except Exception:
             pass
         cpu = None
