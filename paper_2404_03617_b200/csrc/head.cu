@@ -120,12 +120,12 @@ __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__
   uint8_t* s_a = smem + a.s_a;  // stages x [8][128][8] (K chunk 64)
   uint8_t* s_w = smem + a.s_w;  // stages x NC x 64
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // full[4], empty[4], mma
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 9);
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 2 * a.stages + 1);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row0 = (blockIdx.x / a.N) * 128, cc = blockIdx.x % a.N;
   const int S = a.stages;
   if (tid == 0) {
-    for (int i = 0; i < 9; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 2 * S + 1; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc_n(tbase, a.tmem_cols);
@@ -161,9 +161,9 @@ __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__
       }
       mma_commit(&bar[S + b]);
     }
-    mma_commit(&bar[8]);
+    mma_commit(&bar[2 * S]);
   }
-  mbar_wait(&bar[8], 0);
+  mbar_wait(&bar[2 * S], 0);
   tc_fence_after();
   const float* b2 = reinterpret_cast<const float*>(a.w2);
   const int row = row0 + warp * 32 + lane;
@@ -213,7 +213,7 @@ bool head_plan(const wl_block_desc& d, HeadPlan& P) {
   if (h.C % 16 || h.E % 64 || h.HW > 128 || h.C > 512) return false;
   h.imgs = std::max(1, 128 / h.HW);
   h.P = d.n * h.HW;
-  h.NE = h.E % 256 == 0 ? 256 : (h.E % 128 == 0 ? 128 : 64);
+  h.NE = h.E % 128 == 0 ? 128 : 64;  // 96 KB per CTA: two CTAs per SM
   h.nce = h.E / h.NE;
   h.o_b1 = 0;
   h.w1_chunk = h.NE * h.C * 2;
@@ -230,11 +230,11 @@ bool head_plan(const wl_block_desc& d, HeadPlan& P) {
   h.tmem_cols = std::max(32, h.NE);
   f.E = h.E;
   f.classes = h.M;
-  f.NC = 32;
+  f.NC = 16;  // 63 class chunks: more CTAs share the K stream
   f.N = (h.M + f.NC - 1) / f.NC;
   f.nkc = h.E / 64;
   f.nrows = d.n;
-  f.stages = 4;
+  f.stages = 8;
   f.w_chunk = f.NC * 64 * 2;
   P.w2_bytes = align_up(h.M * 4, 128) + (int64_t)f.N * f.nkc * f.w_chunk;
   f.s_a = 0;
@@ -334,7 +334,7 @@ int head_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void
   f.w2 = reinterpret_cast<const uint8_t*>(p) + P.w1_bytes;
   f.z = reinterpret_cast<__half*>(z);
   const int rows = (d.n + 127) / 128;
-  return launch_pdl(head_fc_kernel, rows * f.N, 128, f.s_bar + 128, st, "head_fc launch", tf, f);
+  return launch_pdl(head_fc_kernel, rows * f.N, 128, f.s_bar + 256, st, "head_fc launch", tf, f);
 }
 int head_init() {
   for (int act : {kRelu, kSilu, kGelu, kIdentity})

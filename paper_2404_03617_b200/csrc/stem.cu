@@ -136,7 +136,7 @@ bool stem_plan(const wl_block_desc& d, StemArgs& a) {
   a.Cs = d.k;
   a.Np = align_up(d.k, 16);
   if (a.Wo > 128 || a.Np > 256 || d.k % 8 || (d.w * 3 * 2) % 16) return false;
-  a.R = 4;
+  a.R = 4;  // measured: R = 2 and R = 8 are both slower (54-55 us vs 40 us at 224x224x16, b128)
   while (a.R * a.Np > 512) --a.R;
   a.tiles_y = (a.Ho + a.R - 1) / a.R;
   a.o_bias = a.Np * 32 * 2;
