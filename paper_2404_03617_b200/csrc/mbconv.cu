@@ -54,6 +54,7 @@ struct MbFrontArgs {
   // [group][hidden/8][P_out][8], so every conv chunk leaves and every
   // projection chunk (HCb = lcm(HC, 64) channels) returns as ONE bulk copy
   int bulk, a_stage_b;
+  int xsw;  // x staged as 128-byte-swizzled pixel rows of 64 channels (one 128 B TMA row per pixel)
   __half* h2;
   int s_pa, s_pv, s_gate, t_z;
   const uint8_t* wback;  // back blob: [b_prj fp32][V chunks]
@@ -243,10 +244,22 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
       bulk_g2s(s_hdr, a.wpack + a.se_bytes + (size_t)range * a.hdr_bytes, a.hdr_bytes, &B.hdr_full);
       const int planes = a.C / 8;
-      mbar_arrive_expect_tx(&B.x_full, img_flat * 16 * planes * a.imgs);
-      for (int i = 0; i < a.imgs; ++i)
-        for (int g = 0; g < planes; ++g)
-          tma_load_5d(s_x + ((size_t)g * a.x_alloc + i * img_flat) * 16, &tmap_x, 0, -1, -1, g, n0 + i, &B.x_full);
+      if (a.xsw) {
+        // 64-channel blocks, box {64 ch, Wp, H+1, imgs}: 128-byte rows per
+        // pixel (SWIZZLE_128B) — 8x fewer TMA rows than 16-byte planes
+        mbar_arrive_expect_tx(&B.x_full, img_flat * 128 * (a.C / 64) * a.imgs);
+        for (int cb = 0; cb < a.C / 64; ++cb)
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+              "%4, %5}], [%6];" ::"r"(smem_u32(s_x + (size_t)cb * a.n_et * 128 * 128)),
+              "l"(&tmap_x), "r"(cb * 64), "r"(-1), "r"(-1), "r"(n0), "r"(smem_u32(&B.x_full))
+              : "memory");
+      } else {
+        // the whole x tile in ONE tensor-map load: box {8 ch, Wp, H+1, imgs, C/8}
+        // lands as [plane][image][row][col][8] (plane stride = x_alloc rows)
+        mbar_arrive_expect_tx(&B.x_full, img_flat * 16 * planes * a.imgs);
+        tma_load_5d(s_x, &tmap_x, 0, -1, -1, n0, 0, &B.x_full);
+      }
       const uint8_t* chunks = a.wpack + a.se_bytes + (size_t)a.ranges * a.hdr_bytes;
       for (int j = 0; j < nch; ++j) {
         const int slot = j % S, use = j / S;
@@ -337,8 +350,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       for (int t = 0; t < a.n_et; ++t) {
         const int f = t * 128 + q * 32 + lane;
         for (int pg = eh; pg < a.C / 16; pg += 2) {
-          const uint4 lo = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg) * a.x_alloc + f) * 16);
-          const uint4 hi = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg + 1) * a.x_alloc + f) * 16);
+          uint4 lo, hi;
+          if (a.xsw) {  // pixel row f of 64-channel block pg/4, 16-byte chunk c at (c ^ f%8)
+            const uint8_t* row = s_x + ((size_t)(pg / 4) * a.n_et * 128 + f) * 128;
+            const int c = (pg % 4) * 2;
+            lo = *reinterpret_cast<const uint4*>(row + ((c ^ (f & 7)) << 4));
+            hi = *reinterpret_cast<const uint4*>(row + (((c + 1) ^ (f & 7)) << 4));
+          } else {
+            lo = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg) * a.x_alloc + f) * 16);
+            hi = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg + 1) * a.x_alloc + f) * 16);
+          }
           const uint32_t r8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
           WL_TMEM_ST8(tmem_lane_addr(tmem, q, a.t_x + t * (a.C / 2) + pg * 8), r8);
         }
@@ -1169,7 +1190,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   f.total_rows = f.imgs * (f.H + 1) + 1;
   const int x_valid = f.imgs * (f.H + 1) * f.Wp;
   f.n_et = (x_valid + 127) / 128;
-  f.x_alloc = f.n_et * 128;
+  f.x_alloc = x_valid;  // plane stride = the loaded rows (one TMA box); tile overrun reads are masked
   f.conv_base = f.Wp + 1;
   const int conv_end = (f.total_rows - 1) * f.Wp;
   f.n_ct = (conv_end - f.conv_base + 127) / 128;
@@ -1188,7 +1209,10 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   while (!want_fused && f.groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
   f.HR = hid / f.ranges;
   f.HC = 0;
-  const int x_bytes = (C / 8) * f.x_alloc * 16;
+  // room for either staging: [C/8 planes][x_valid rows] (+ tile overrun) or
+  // [C/64 blocks][n_et * 128 rows][128 B] (swizzled pixel rows)
+  const int x_bytes = std::max(align_up((C / 8) * f.x_alloc * 16 + (f.n_et * 128 - x_valid) * 16, 128),
+                               (C % 64 == 0) ? C * 2 * f.n_et * 128 : 0);
   const int se_scratch = align_up((hid + 640 + f.sq) * 4, 16);
   for (int hc = 128; hc >= 16; hc -= 16) {
     if (f.HR % hc) continue;
@@ -1229,6 +1253,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     }
   }
   if (!placed) return false;
+  f.xsw = f.x_tmem && C % 64 == 0;
   f.t_x = 0;
   f.t_e = f.x_tmem ? x_cols : 0;
   f.t_c = f.t_e + f.e_bufs * f.n_et * f.HC;
@@ -1530,10 +1555,18 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
   f.trace = g_mb_trace;
   CUtensorMap tx, th_store, th_load;
   {
-    const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)(d.c / 8), (uint64_t)d.n};
-    const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, 16, (uint64_t)d.h * d.w * d.c * 2};
-    const uint32_t box[5] = {8, (uint32_t)f.Wp, (uint32_t)(f.H + 1), 1, 1};
-    if (int e = encode_tmap(&tx, x, 5, dims, strides, box)) return e;
+    // dims (8 ch, W, H, image, channel group): one box = every plane of the CTA's images
+    if (f.xsw) {
+      const uint64_t dims[4] = {(uint64_t)d.c, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n};
+      const uint64_t strides[3] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2};
+      const uint32_t box[4] = {64, (uint32_t)f.Wp, (uint32_t)(f.H + 1), (uint32_t)f.imgs};
+      if (int e = encode_tmap(&tx, x, 4, dims, strides, box, true)) return e;
+    } else {
+      const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n, (uint64_t)(d.c / 8)};
+      const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2, 16};
+      const uint32_t box[5] = {8, (uint32_t)f.Wp, (uint32_t)(f.H + 1), (uint32_t)f.imgs, (uint32_t)(d.c / 8)};
+      if (int e = encode_tmap(&tx, x, 5, dims, strides, box)) return e;
+    }
   }
   {
     const uint64_t dims[3] = {8, (uint64_t)b.P, (uint64_t)(f.hid / 8)};
