@@ -7,7 +7,7 @@
 #include "../paper_2404_03617_b200/csrc/sm100.cuh"
 using namespace wl;
 
-template <int MODE, int NW>
+template <int MODE, int NW, bool MMA = true>
 __global__ void k(long long* out, float* sink, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -22,7 +22,13 @@ __global__ void k(long long* out, float* sink, int iters) {
   tc_fence_after();
   const uint32_t tmem = tb;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !MMA) {
+    long long t0 = clock64();
+    while (clock64() - t0 < 200000) {
+    }
+    out[0] = clock64() - t0;
+    done = 1;
+  } else if (threadIdx.x == 0) {
     const uint32_t idesc = make_idesc_f16(128, 16);
     const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 65536);
     uint64_t ad[8], bd[8];
@@ -39,7 +45,9 @@ __global__ void k(long long* out, float* sink, int iters) {
     float acc = 0.f;
     uint8_t* buf = smem + 98304 + (warp - 4) * 4096;
     const int q = warp % 4;
+    long long nit = 0;
     while (!done) {
+      ++nit;
       if (MODE == 1) {
         for (int r = 0; r < 16; ++r) {
           uint4 v = reinterpret_cast<uint4*>(buf)[(lane + r * 32) & 255];
@@ -54,29 +62,32 @@ __global__ void k(long long* out, float* sink, int iters) {
       }
     }
     sink[threadIdx.x] = acc;
+    if (lane == 0) reinterpret_cast<long long*>(sink + 1024)[warp] = nit;
   }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
-template <int MODE, int NW>
+template <int MODE, int NW, bool MMA = true>
 void run(const char* what) {
   long long* d; float* s;
-  cudaMalloc(&d, 8); cudaMalloc(&s, 8192);
-  auto kk = k<MODE, NW>;
+  cudaMalloc(&d, 8); cudaMalloc(&s, 16384);
+  auto kk = k<MODE, NW, MMA>;
   cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, 164 * 1024);
   kk<<<1, 640, 164 * 1024>>>(d, s, 10);
   kk<<<1, 640, 164 * 1024>>>(d, s, 500);
   long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("%-40s %6.2f cycles/MMA  %s\n", what, (double)h / 4000, cudaGetErrorString(cudaGetLastError()));
+  long long nit[32];
+  cudaMemcpy(nit, s + 1024, sizeof(nit), cudaMemcpyDeviceToHost);
+  const double bytes = (double)nit[4] * 16 * 32 * 32;  // warp 4: 16 x (LDS.128 + STS.128) per iteration
+  printf("%-40s %6.2f cycles/MMA | warp4 smem %.1f B/cycle  %s\n", what, (double)h / 4000, bytes / h,
+         cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
-  run<0, 8>("N16 SS, others idle");
-  run<1, 4>("N16 SS, 4 warps LDS/STS.128");
-  run<1, 8>("N16 SS, 8 warps LDS/STS.128");
-  run<1, 16>("N16 SS, 16 warps LDS/STS.128");
-  run<2, 4>("N16 SS, 4 warps tcgen05.ld");
-  run<2, 8>("N16 SS, 8 warps tcgen05.ld");
+  run<1, 8, false>("no MMA, 8 warps LDS/STS.128");
+  run<1, 8, true>("N16 SS MMA + 8 warps LDS/STS.128");
+  run<1, 16, false>("no MMA, 16 warps LDS/STS.128");
+  run<1, 16, true>("N16 SS MMA + 16 warps LDS/STS.128");
   return 0;
 }
