@@ -164,6 +164,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int n0 = group * a.imgs;
   const int h0 = range * a.HR;
   const int S = a.ring_stages, HC = a.HC, nch = a.nch, G8 = HC / 8;
+  // T=8 with two or more conv tiles: warp 3 issues the odd tiles' conv MMAs so
+  // the single issuing thread (which shares its SMSP with busy epilogue warps)
+  // is not the bottleneck of the 16-wide grouped-conv instructions
+  const bool dual = T8 && a.n_ct >= 2;
   const int img_flat = (a.H + 1) * a.Wp;
   const int x_valid = a.imgs * img_flat;
   if (threadIdx.x == 0) WL_TRACE(0);
@@ -204,16 +208,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     mbar_init(&B.x_full, 1);
     for (int i = 0; i < S; ++i) {
       mbar_init(&B.w_full[i], 1);
-      mbar_init(&B.w_empty[i], 1);
+      mbar_init(&B.w_empty[i], dual ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.e_full[i], 1);
-      mbar_init(&B.c_full[i], 1);
+      mbar_init(&B.c_full[i], dual ? 2 : 1);
       mbar_init(&B.c_empty[i], 256);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.h1_full[i], 256);
-      mbar_init(&B.h1_empty[i], T8 ? 1 : 256);
+      mbar_init(&B.h1_empty[i], T8 ? (dual ? 2 : 1) : 256);
     }
     mbar_init(&B.x_ready, 256);
     for (int i = 0; i < 4; ++i) {
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           const uint32_t zaddr = ring0 + slot * a.chunk_bytes + a.u_bytes + E * 128;
           const uint64_t b_base = make_sdesc(zaddr - 128, 128, 128);
           const uint64_t b_step = (8ull << 16) + (8ull << 32) - 8ull;
-          for (int t = 0; t < a.n_ct; ++t)
+          for (int t = 0; t < a.n_ct; t += dual ? 2 : 1)
             for (int pr = 0; pr < HC / 16; ++pr) {
               const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
               const uint64_t ap = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128);
@@ -336,6 +340,37 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           mma_commit(&B.h1_empty[hb]);
           WL_TRACE(16 + 8 * j + 2);
         }
+        mma_commit(&B.w_empty[slot]);
+      }
+    }
+  } else if (warp == 3) {
+    if (dual && lane == 0) {
+      const uint32_t idesc_c = make_idesc_f16(128, 16);
+      const uint32_t ring0 = smem_u32(s_ring);
+      for (int j = 0; j < nch; ++j) {
+        const int slot = j % S, hb = j % a.h1_bufs, cb = j % a.c_bufs;
+        mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // h1 ready implies the chunk's weights landed
+        if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t h1a = smem_u32(hb ? smem + a.s_h1b : s_h1);
+        const uint64_t a_base = make_sdesc(h1a + (a.conv_base - a.Wp - 1) * 16, a.flat_h1 * 16, 128);
+        const int E = (HC / 16) * 9;
+        const uint32_t zaddr = ring0 + slot * a.chunk_bytes + a.u_bytes + E * 128;
+        const uint64_t b_base = make_sdesc(zaddr - 128, 128, 128);
+        const uint64_t b_step = (8ull << 16) + (8ull << 32) - 8ull;
+        for (int t = 1; t < a.n_ct; t += 2)
+          for (int pr = 0; pr < HC / 16; ++pr) {
+            const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
+            uint64_t ad = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128), bd = b_base + (uint64_t)(pr * 9) * b_step;
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+              mma_ss(d, ad, bd, idesc_c, tap > 0);
+              ad += (tap % 3 == 2) ? (uint64_t)(a.Wp - 2) : 1ull;
+              bd += b_step;
+            }
+          }
+        mma_commit(&B.c_full[cb]);
+        mma_commit(&B.h1_empty[hb]);
         mma_commit(&B.w_empty[slot]);
       }
     }
