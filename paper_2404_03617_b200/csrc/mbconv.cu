@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   // T=8 with two or more conv tiles: warp 3 issues the odd tiles' conv MMAs so
   // the single issuing thread (which shares its SMSP with busy epilogue warps)
   // is not the bottleneck of the 16-wide grouped-conv instructions
-  const bool dual = T8 && a.n_ct >= 2;
+  // conv (tile, pair) items are dealt round-robin to NIS issuing threads
+  // (warps 1, 3, 2): warp 1 also issues the expansions
+  const int NIS = T8 ? min(3, a.n_ct * (HC / 16)) : 1;
+  const bool dual = NIS > 1;
   const int img_flat = (a.H + 1) * a.Wp;
   const int x_valid = a.imgs * img_flat;
   if (threadIdx.x == 0) WL_TRACE(0);
@@ -208,16 +211,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     mbar_init(&B.x_full, 1);
     for (int i = 0; i < S; ++i) {
       mbar_init(&B.w_full[i], 1);
-      mbar_init(&B.w_empty[i], dual ? 2 : 1);
+      mbar_init(&B.w_empty[i], NIS);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.e_full[i], 1);
-      mbar_init(&B.c_full[i], dual ? 2 : 1);
+      mbar_init(&B.c_full[i], NIS);
       mbar_init(&B.c_empty[i], 256);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.h1_full[i], 256);
-      mbar_init(&B.h1_empty[i], T8 ? (dual ? 2 : 1) : 256);
+      mbar_init(&B.h1_empty[i], T8 ? NIS : 256);
     }
     mbar_init(&B.x_ready, 256);
     for (int i = 0; i < 4; ++i) {
@@ -322,8 +325,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           const uint32_t zaddr = ring0 + slot * a.chunk_bytes + a.u_bytes + E * 128;
           const uint64_t b_base = make_sdesc(zaddr - 128, 128, 128);
           const uint64_t b_step = (8ull << 16) + (8ull << 32) - 8ull;
-          for (int t = 0; t < a.n_ct; t += dual ? 2 : 1)
-            for (int pr = 0; pr < HC / 16; ++pr) {
+          for (int k = 0; k < a.n_ct * (HC / 16); k += NIS) {
+            const int t = k / (HC / 16), pr = k - t * (HC / 16);
+            {
               const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
               const uint64_t ap = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128);
               // incremental descriptors: one 64-bit add each between MMAs keeps
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
                 bd += b_step;
               }
             }
+          }
           mma_commit(&B.c_full[cb]);
           mma_commit(&B.h1_empty[hb]);
           WL_TRACE(16 + 8 * j + 2);
@@ -343,8 +348,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mma_commit(&B.w_empty[slot]);
       }
     }
-  } else if (warp == 3) {
-    if (dual && lane == 0) {
+  } else if (warp == 3 || warp == 2) {
+    const int isx = warp == 3 ? 1 : 2;  // issuer index
+    if (isx < NIS && lane == 0) {
       const uint32_t idesc_c = make_idesc_f16(128, 16);
       const uint32_t ring0 = smem_u32(s_ring);
       for (int j = 0; j < nch; ++j) {
@@ -358,8 +364,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const uint32_t zaddr = ring0 + slot * a.chunk_bytes + a.u_bytes + E * 128;
         const uint64_t b_base = make_sdesc(zaddr - 128, 128, 128);
         const uint64_t b_step = (8ull << 16) + (8ull << 32) - 8ull;
-        for (int t = 1; t < a.n_ct; t += 2)
-          for (int pr = 0; pr < HC / 16; ++pr) {
+        for (int k = isx; k < a.n_ct * (HC / 16); k += NIS) {
+          const int t = k / (HC / 16), pr = k - t * (HC / 16);
+          {
             const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
             uint64_t ad = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128), bd = b_base + (uint64_t)(pr * 9) * b_step;
 #pragma unroll
@@ -369,6 +376,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
               bd += b_step;
             }
           }
+        }
         mma_commit(&B.c_full[cb]);
         mma_commit(&B.h1_empty[hb]);
         mma_commit(&B.w_empty[slot]);
