@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
     mbar_init(&B.w_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.x_full[i], 1);
-      mbar_init(&B.x_empty[i], 1);
+      mbar_init(&B.x_empty[i], 2);
       mbar_init(&B.xh_full[i], 128);
       mbar_init(&B.xh_empty[i], 1);
       mbar_init(&B.e_full[i], 1);
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
       mbar_init(&B.q_full[i], 256);
       mbar_init(&B.q_empty[i], 1);
     }
-    mbar_init(&B.conv_full, 1);
+    mbar_init(&B.conv_full, 2);
     mbar_init(&B.c_empty, 128);
     mbar_init(&B.z_full, 1);
     mbar_init(&B.z_empty, 128);
@@ -210,22 +210,15 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         mma_commit(&B.q_empty[qs]);
         if (j == nch - 1) mma_commit(&B.z_full);
       };
-      // conv runs two bands ahead: conv(i+2) is issued tile by tile between
-      // the FFN chunks of band i (expand j, project j-1, conv tile(s)), so
-      // the tensor core works while the CUDA-core groups drain; G1 drains
-      // conv(i+1) and blurs it during FFN(i)
-      for (int i = 0; i < 2 && i < nb; ++i) {
-        conv_begin(i);
-        conv_tiles(i, 0, a.n_ct);
-        conv_end(i);
-      }
+      // warp 1 issues the FFN (expand / project chunks); the grouped conv is
+      // issued by warps 3 and 2 (below) and runs ahead as far as G1's drain
+      // of the single conv accumulator allows
       for (int i = 0; i < nb; ++i) {
         const int hb = i & 1;
         mbar_wait(&B.xh_full[hb], (i >> 1) & 1);
         tc_fence_after();
         if (i < 8) CF2_TRACE(8 + i * 24 + 4);
         const uint32_t ah = smem_u32(s_ah) + hb * a.ah_bytes;
-        const bool conv_next = i + 2 < nb;
         for (int j = 0; j < nch; ++j) {
           const int gg = i * nch + j, es = gg & 1;
           mbar_wait(&B.e_empty[es], ((gg >> 1) & 1) ^ 1);
@@ -238,14 +231,40 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
           mma_commit(&B.e_full[es]);
           if (j == nch - 1) mma_commit(&B.xh_empty[hb]);
           if (j > 0) issue_project(i, j - 1);
-          if (conv_next) {
-            if (j == 0) conv_begin(i + 2);
-            conv_tiles(i + 2, j * a.n_ct / nch, (j + 1) * a.n_ct / nch);
-            if (j == nch - 1) conv_end(i + 2);
-          }
         }
         issue_project(i, nch - 1);
         if (i < 8) CF2_TRACE(8 + i * 24 + 5);
+      }
+    }
+  } else if (warp == 3 || warp == 2) {
+    // ---------------- grouped-conv issuers: conv tiles split between two threads
+    if (lane == 0) {
+      const int ci = warp == 3 ? 0 : 1;
+      mbar_wait(&B.w_full, 0);
+      const uint32_t cw = smem_u32(s_w + a.o_convw);
+      const uint32_t idesc_c = make_idesc_f16(128, 16);
+      for (int i = 0; i < nb; ++i) {
+        const int xb = i % a.x_bufs;
+        mbar_wait(&B.x_full[xb], (i / a.x_bufs) & 1);
+        mbar_wait(&B.c_empty, (i & 1) ^ 1);  // previous band's conv accumulators drained
+        tc_fence_after();
+        if (ci == 0 && i < 8) CF2_TRACE(8 + i * 24 + 2);
+        const uint32_t x0 = smem_u32(s_x) + xb * planes * a.x_alloc * 16;
+        for (int t = ci; t < a.n_ct; t += 2)
+          for (int pr = 0; pr < C / 16; ++pr) {
+            uint64_t aa = make_sdesc(x0 + (2 * pr * a.x_alloc + a.conv_base - Wp - 1 + t * 128) * 16, a.x_alloc * 16, 128);
+            uint64_t bd = make_sdesc(cw + pr * 9 * 512, 256, 128);
+            const uint32_t d = tmem + a.t_c + t * C + 16 * pr;
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+              mma_ss(d, aa, bd, idesc_c, tap > 0);
+              aa += (tap % 3 == 2) ? (uint64_t)(Wp - 2) : 1ull;
+              bd += 32;
+            }
+          }
+        mma_commit(&B.conv_full);
+        mma_commit(&B.x_empty[xb]);
+        if (ci == 0 && i < 8) CF2_TRACE(8 + i * 24 + 3);
       }
     }
   } else if (warp >= 4 && warp < 8) {
