@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r = pl.r, nchunks = pl.nchunks, S = pl.ring_stages, NHB = pl.halo_bufs;
+  // T=8: the grouped conv is issued by its own thread(s) (warps 3, 2), one
+  // channel pair each, so the FFN issuer never waits behind the conv
+  constexpr int NCI = T8 ? (G / 2 >= 2 ? 2 : 1) : 1;
 
   if (threadIdx.x == 0) {
     mbar_init(&B.hdr_full, 1);
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       mbar_init(&B.h_full[i], 128);
       mbar_init(&B.h_empty[i], 1);
     }
-    mbar_init(&B.conv_full, 1);
+    mbar_init(&B.conv_full, NCI);
     mbar_init(&B.cacc_empty, 128);
     mbar_init(&B.z_full, 1);
     mbar_init(&B.z_empty, 128);
@@ -157,34 +160,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       mbar_wait(&B.hdr_full, 0);
       if (pl.resident) mbar_wait(&B.w_all, 0);
       tc_fence_after();
-      auto issue_conv = [&](int u) {  // grouped 3x3 conv of tile u into Cacc
-        const int b = u % NHB;
-        mbar_wait(&B.halo_full[b], (u / NHB) & 1);
-        if (u > 0) mbar_wait(&B.cacc_empty, (u - 1) & 1);
-        tc_fence_after();
-        const uint32_t hb = halo0 + b * pl.halo_bytes;
-        const uint32_t lbo = HH * HWD * 16, sbo = HWD * 16;
-#pragma unroll 1
-        for (int pr = 0; pr < G / 2; ++pr) {
-          uint64_t ad = make_sdesc(hb + (2 * pr * HH * HWD) * 16, lbo, sbo);
-          uint64_t bd = make_sdesc(convw + (pr * KS * KS) * 512, 256, 128);
-          const uint32_t d = tmem + pl.t_cacc + 16 * pr;
-#pragma unroll
-          for (int t = 0; t < KS * KS; ++t) {  // incremental descriptors (cheap issue)
-            mma_ss(d, ad, bd, idesc_conv, t > 0);
-            ad += (t % KS == KS - 1) ? (uint64_t)(HWD - (KS - 1)) : 1ull;
-            bd += 32;
-          }
-        }
-        mma_commit(&B.conv_full);
-      };
-      if constexpr (T8) {
-        if (my_tiles > 0) issue_conv(0);
-      }
+
+
       for (int it = 0; it < my_tiles; ++it) {
-        if constexpr (T8) {
-          if (it + 1 < my_tiles) issue_conv(it + 1);
-        }
+
         const int xb = it & 1;
         mbar_wait(&B.xc_full[xb], (it >> 1) & 1);
         tc_fence_after();
@@ -223,6 +202,36 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         }
         issue_project(nchunks - 1);
         mma_commit(&B.z_full);
+      }
+    }
+  } else if (T8 && (warp == 3 || (NCI > 1 && warp == kAllocWarp))) {
+    // ---------------- grouped 3x3 conv issuers: pairs pr = ci, ci + NCI, ...
+    if (lane == 0) {
+      const int ci = warp == 3 ? 0 : 1;
+      const uint32_t idesc_conv = make_idesc_f16(128, 16);
+      const uint32_t halo0 = smem_u32(s_halo);
+      const uint32_t convw = smem_u32(s_hdr + pl.o_convw);
+      mbar_wait(&B.hdr_full, 0);
+      for (int u = 0; u < my_tiles; ++u) {
+        const int b = u % NHB;
+        mbar_wait(&B.halo_full[b], (u / NHB) & 1);
+        if (u > 0) mbar_wait(&B.cacc_empty, (u - 1) & 1);
+        tc_fence_after();
+        const uint32_t hb = halo0 + b * pl.halo_bytes;
+        const uint32_t lbo = HH * HWD * 16, sbo = HWD * 16;
+#pragma unroll 1
+        for (int pr = ci; pr < G / 2; pr += NCI) {
+          uint64_t ad = make_sdesc(hb + (2 * pr * HH * HWD) * 16, lbo, sbo);
+          uint64_t bd = make_sdesc(convw + (pr * KS * KS) * 512, 256, 128);
+          const uint32_t d = tmem + pl.t_cacc + 16 * pr;
+#pragma unroll
+          for (int t = 0; t < KS * KS; ++t) {  // incremental descriptors (cheap issue)
+            mma_ss(d, ad, bd, idesc_conv, t > 0);
+            ad += (t % KS == KS - 1) ? (uint64_t)(HWD - (KS - 1)) : 1ull;
+            bd += 32;
+          }
+        }
+        mma_commit(&B.conv_full);
       }
     }
   } else if (warp >= kHWarp0 && warp < kHWarp0 + 4) {
