@@ -169,8 +169,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   // is not the bottleneck of the 16-wide grouped-conv instructions
   // conv (tile, pair) items are dealt round-robin to NIS issuing threads
   // (warps 1, 3, 2): warp 1 also issues the expansions
-  const int NIS = T8 ? min(3, a.n_ct * (HC / 16)) : 1;
-  const bool dual = NIS > 1;
+  // T=8: warp 1 issues only the expansions; the grouped conv's (tile, pair)
+  // items go round-robin to NIS dedicated issuing threads (warps 3, 2), so the
+  // conv never queues behind an expansion waiting for its weight chunk
+  const int NIS = T8 ? min(2, a.n_ct * (HC / 16)) : 1;
   const int img_flat = (a.H + 1) * a.Wp;
   const int x_valid = a.imgs * img_flat;
   if (threadIdx.x == 0) WL_TRACE(0);
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     mbar_init(&B.x_full, 1);
     for (int i = 0; i < S; ++i) {
       mbar_init(&B.w_full[i], 1);
-      mbar_init(&B.w_empty[i], NIS);
+      mbar_init(&B.w_empty[i], T8 ? NIS + 1 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.e_full[i], 1);
@@ -307,6 +309,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       issue_expand(0);
       for (int j = 0; j < nch; ++j) {
         const int slot = j % S, hb = j % a.h1_bufs;
+        if (T8) {
+          // expansion j+1 reuses the E buffer of chunk j+1-e_bufs: wait for its drain
+          const int jd = j + 1 - a.e_bufs;
+          if (j + 1 < nch) {
+            if (jd >= 0) mbar_wait(&B.h1_full[jd % a.h1_bufs], (jd / a.h1_bufs) & 1);
+            issue_expand(j + 1);
+          }
+          mma_commit(&B.w_empty[slot]);
+          continue;
+        }
         if (a.e_bufs == 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // E of chunk j consumed
         if (j + 1 < nch) issue_expand(j + 1);
         if (T8) {
@@ -349,8 +361,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       }
     }
   } else if (warp == 3 || warp == 2) {
-    const int isx = warp == 3 ? 1 : 2;  // issuer index
-    if (isx < NIS && lane == 0) {
+    const int isx = warp == 3 ? 0 : 1;  // conv issuer index
+    if (T8 && isx < NIS && lane == 0) {
       const uint32_t idesc_c = make_idesc_f16(128, 16);
       const uint32_t ring0 = smem_u32(s_ring);
       for (int j = 0; j < nch; ++j) {
