@@ -55,6 +55,7 @@ struct MbFrontArgs {
   // projection chunk (HCb = lcm(HC, 64) channels) returns as ONE bulk copy
   int bulk, a_stage_b;
   int xsw;  // x staged as 128-byte-swizzled pixel rows of 64 channels (one 128 B TMA row per pixel)
+  int se_pref, se_off;  // squeeze-excite weights prefetched into the tail of the (then idle) weight ring
   __half* h2;
   int s_pa, s_pv, s_gate, t_z;
   const uint8_t* wback;  // back blob: [b_prj fp32][V chunks]
@@ -83,6 +84,7 @@ struct FrontBars {
   uint64_t e_full[2], c_full[2], c_empty[2];
   uint64_t h1_full[2], h1_empty[2], x_ready;
   uint64_t pa_full[4], pa_ready[4], pa_empty[4], pv_full[3], pv_empty[3], z_full;
+  uint64_t se_full;
   uint32_t tmem_base;
   int last;
 };
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int x_valid = a.imgs * img_flat;
   if (threadIdx.x == 0) WL_TRACE(0);
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {  // plan snapshot for the trace reader
-    a.trace[14] = a.sa * 1000 + a.ring_stages * 100 + a.h1_bufs * 10 + a.e_bufs;
+    a.trace[14] = a.se_pref * 10000 + a.sa * 1000 + a.ring_stages * 100 + a.h1_bufs * 10 + a.e_bufs;
     a.trace[15] = a.c_bufs * 100000 + a.x_tmem * 10000 + a.HC * 10 + a.n_pt;
   }
 
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_init(&B.pv_empty[i], 1);
     }
     mbar_init(&B.z_full, 1);
+    mbar_init(&B.se_full, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -276,6 +279,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mbar_arrive_expect_tx(&B.w_full[slot], a.chunk_bytes);
         bulk_g2s(s_ring + slot * a.chunk_bytes, chunks + (size_t)(range * nch + j) * a.chunk_bytes, a.chunk_bytes,
                  &B.w_full[slot]);
+      }
+      if (FUSED && a.se_pref) {
+        // squeeze-excite weights into the weight ring once its last chunks
+        // are consumed: they land while the final conv epilogue runs
+        for (int j = nch - S; j < nch; ++j)
+          if (j >= 0) mbar_wait(&B.w_empty[j % S], (j / S) & 1);
+        mbar_arrive_expect_tx(&B.se_full, a.se_bytes);
+        bulk_g2s(smem + a.se_off, a.wpack, a.se_bytes, &B.se_full);
       }
     }
   } else if (warp == 1) {
@@ -686,10 +697,15 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   if (B.last) {
     if (!FUSED) __threadfence();
     // fp16 weights: w_sq [hid][SQP], w_ex^T [hid][SQP] (SQP = sq padded to a power of two >= 8)
-    const __half* wsq = reinterpret_cast<const __half*>(a.wpack + a.o_wsq);
-    const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_bsq);
-    const __half* wexT = reinterpret_cast<const __half*>(a.wpack + a.o_wex);
-    const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_bex);
+    const uint8_t* seb = a.wpack;
+    if (FUSED && a.se_pref) {  // prefetched into the weight ring
+      mbar_wait(&B.se_full, 0);
+      seb = smem + a.se_off;
+    }
+    const __half* wsq = reinterpret_cast<const __half*>(seb + a.o_wsq);
+    const float* bsq = reinterpret_cast<const float*>(seb + a.o_bsq);
+    const __half* wexT = reinterpret_cast<const __half*>(seb + a.o_wex);
+    const float* bex = reinterpret_cast<const float*>(seb + a.o_bex);
     float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;  // [imgs][hid] pool
     float* s_red = s_vec + a.imgs * a.hid;                                       // [20 warps][imgs][SQP]
     float* s_sq = s_red + 20 * a.imgs * a.SQP;                                   // [imgs][SQP]
@@ -1415,6 +1431,19 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     }
     if (!f.sa) return false;
     f.fused = 1;
+    // SE weights at the tail of the weight ring, clear of the projection's A / V
+    // rings (give up A stages for it, down to two)
+    f.se_off = (f.s_ring + f.ring_stages * f.chunk_bytes - f.se_bytes) / 128 * 128;
+    f.se_pref = 0;
+    if (f.se_off >= f.s_ring)
+      for (int sa = f.sa; sa >= 2 && !f.se_pref; --sa) {
+        const int spv = align_up(sa * a_stage, 128);
+        if (f.se_off >= spv + 3 * f.vchunk_bytes) {
+          f.sa = sa;
+          f.s_pv = spv;
+          f.se_pref = 1;
+        }
+      }
   }
 
   // ---- back
