@@ -56,6 +56,9 @@ struct MbFrontArgs {
   int bulk, a_stage_b;
   int xsw;  // x staged as 128-byte-swizzled pixel rows of 64 channels (one 128 B TMA row per pixel)
   int se_pref, se_off;  // squeeze-excite weights prefetched into the tail of the (then idle) weight ring
+  // z staged in shared memory (128B-swizzled 64-channel rows, over the dead SE
+  // weights): residual rows arrive by TMA during the projection, z leaves by TMA
+  int zst, zst_rows;
   __half* h2;
   int s_pa, s_pv, s_gate, t_z;
   const uint8_t* wback;  // back blob: [b_prj fp32][V chunks]
@@ -84,7 +87,7 @@ struct FrontBars {
   uint64_t e_full[2], c_full[2], c_empty[2];
   uint64_t h1_full[2], h1_empty[2], x_ready;
   uint64_t pa_full[4], pa_ready[4], pa_empty[4], pv_full[3], pv_empty[3], z_full;
-  uint64_t se_full;
+  uint64_t se_full, res_full;
   uint32_t tmem_base;
   int last;
 };
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     }
     mbar_init(&B.z_full, 1);
     mbar_init(&B.se_full, 1);
+    mbar_init(&B.res_full, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -841,6 +845,15 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (threadIdx.x == 0) WL_TRACE(11);
     if (warp == 0) {
       if (lane == 0) {
+        if (a.zst && a.residual) {  // residual rows (the SE weights there are dead now)
+          mbar_arrive_expect_tx(&B.res_full, (a.K / 64) * a.P_out * 128);
+          for (int cb = 0; cb < a.K / 64; ++cb)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3}], [%4];" ::"r"(smem_u32(smem + a.se_off + cb * a.zst_rows * 128)),
+                "l"(&tmap_h2l), "r"(cb * 64), "r"(group * a.P_out), "r"(smem_u32(&B.res_full))
+                : "memory");
+        }
         for (int j = 0; j < a.nchb; ++j) {
           const int jn = j + a.sa, jv = j + 3;  // refill the stage chunk j frees
           if (jn < a.nchb) {
@@ -959,6 +972,52 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       if (a.ranges == 2) {  // paired: the two partial Z meet after the projection (below)
         mbar_wait_sleep(&B.z_full, 0);
         tc_fence_after();
+      } else if (a.zst) {
+        // z = Z + b_prj (+ x) in shared memory: pixel p, 16-byte chunk c of the
+        // 64-channel block cb at (p/8)*1024 + (p%8)*128 + (c ^ p%8)*16
+        uint8_t* zs = smem + a.se_off;
+        mbar_wait_sleep(&B.z_full, 0);
+        if (a.residual) mbar_wait_sleep(&B.res_full, 0);
+        tc_fence_after();
+        if (warp == 12 && lane == 0) WL_TRACE(120);
+        for (int t = 0; t < a.n_pt; ++t) {
+          const int p = t * 128 + q * 32 + lane;
+          const bool inside = p < a.P_out;
+          uint8_t* rowb = zs + (p >> 3) * 1024 + (p & 7) * 128;
+          for (int c0 = hh * 16; c0 < a.K; c0 += 32) {
+            uint32_t v[16];
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_z + t * a.K + c0), v);
+            tmem_ld_wait();
+            if (!inside) continue;
+            uint8_t* rb = rowb + (c0 / 64) * a.zst_rows * 128;
+            const int ch = (c0 % 64) / 8;
+            uint4* p0 = reinterpret_cast<uint4*>(rb + ((ch ^ (p & 7)) << 4));
+            uint4* p1 = reinterpret_cast<uint4*>(rb + (((ch + 1) ^ (p & 7)) << 4));
+            float f[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bprj[c0 + i];
+            if (a.residual) {
+              float r[16];
+              unpack8(*p0, r);
+              unpack8(*p1, r + 8);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) f[i] += r[i];
+            }
+            *p0 = pack8(f);
+            *p1 = pack8(f + 8);
+          }
+        }
+        fence_async_smem();
+        named_bar(1, 256);
+        if (warp == 12 && lane == 0) {
+          for (int cb = 0; cb < a.K / 64; ++cb)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap_h2),
+                         "r"(smem_u32(zs + cb * a.zst_rows * 128)), "r"(cb * 64), "r"(group * a.P_out)
+                         : "memory");
+          bulk_commit();
+          bulk_wait0();
+        }
+        tc_fence_before();
       } else {
       // z = Z + b_prj (+ x). Each thread owns one pixel row and the 16-column
       // blocks hh, hh+2, ... (two per group); the residual rows of the next
@@ -1433,7 +1492,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     f.fused = 1;
     // SE weights at the tail of the weight ring, clear of the projection's A / V
     // rings (give up A stages for it, down to two)
-    f.se_off = (f.s_ring + f.ring_stages * f.chunk_bytes - f.se_bytes) / 128 * 128;
+    f.se_off = (f.s_ring + f.ring_stages * f.chunk_bytes - f.se_bytes) / 1024 * 1024;
     f.se_pref = 0;
     if (f.se_off >= f.s_ring)
       for (int sa = f.sa; sa >= 2 && !f.se_pref; --sa) {
@@ -1444,6 +1503,9 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
           f.se_pref = 1;
         }
       }
+    f.zst_rows = align_up(f.P_out, 8);
+    f.zst = f.se_pref && f.bulk && f.ranges == 1 && f.imgs == 1 && K % 64 == 0 && f.P_out <= 256 &&
+            f.se_off + (K / 64) * f.zst_rows * 128 <= f.s_ring + f.ring_stages * f.chunk_bytes;
   }
 
   // ---- back
@@ -1670,6 +1732,14 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     const uint64_t strides[1] = {(uint64_t)f.hid * 2};
     const uint32_t box[2] = {64, 128};
     if (int e = encode_tmap(&th_fused, h2, 2, dims, strides, box, true)) return e;
+  }
+  if (f.zst) {  // [pixels][K] rows of z and of the residual x, 64-channel 128B-swizzled boxes
+    const uint64_t dims[2] = {(uint64_t)d.k, (uint64_t)d.n * f.Ho * f.Wo};
+    const uint64_t strides[1] = {(uint64_t)d.k * 2};
+    const uint32_t box[2] = {64, (uint32_t)f.P_out};
+    if (int e = encode_tmap(&th_store, z, 2, dims, strides, box, true)) return e;
+    if (f.residual)
+      if (int e = encode_tmap(&th_fused, x, 2, dims, strides, box, true)) return e;
   }
   if (int e = launch_pdl_cluster(front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0), f.groups * f.ranges,
                                  mbk::kThreads, f.smem, st, "mb_front launch", (f.fused && f.ranges == 2) ? 2 : 1, tx,
