@@ -13,7 +13,7 @@ for nm in sys.argv[1:]:
     m = FusedBlock(blk, dims, k)
     x = torch.randn(dims.n, dims.h, dims.w, dims.c, device="cuda").half()
     out = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
-    buf = torch.zeros(128, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(256, dtype=torch.int64, device="cuda")
     for _ in range(3): m.launch(x, out)
     _lib.lib().wl_debug_set_trace(buf.data_ptr())
     m.launch(x, out)
@@ -33,3 +33,5 @@ for nm in sys.argv[1:]:
     print("  proj: a_ready", [rel(v) for v in t[96:104]])
     print("  proj: v_full", [rel(v) for v in t[104:112]])
     print("  SE: pool loaded", rel(t[124]), "squeezed", rel(t[125]), "| epi: z_full", rel(t[120]), "tiles", rel(t[121]), rel(t[122]), rel(t[123]))
+    print("  proj: load issue", [rel(v) for v in t[88:96]])
+    print("  gating chunk 3 per warp (pa_full ok, pt_empty ok, loop done, st done):", [[rel(t[200 + 4 * w + i]) for i in (3, 0, 1, 2)] for w in range(8)])
