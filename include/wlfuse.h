@@ -102,6 +102,11 @@ WL_API int wl_pack_weights(const wl_block_desc* d, const float* const* weights, 
  * launched in stream order. */
 WL_API int64_t wl_workspace_bytes(const wl_block_desc* d);
 
+/* number of kernels one wl_block_forward launches for this descriptor (1 for
+ * every fused block; 2 for the head, and for MBConv when it falls back to its
+ * two-launch form); negative status on an invalid descriptor. */
+WL_API int wl_kernel_launches(const wl_block_desc* d);
+
 /* forward: z = block(x). x, packed, z, workspace are DEVICE pointers.
  * Replaces execute_numeric(build_schedule(block, dims, BLOCK_FUSION), ...)
  * (machine.py:1053) for one block. */

@@ -32,6 +32,7 @@ EXPORTS = (
     "wl_packed_bytes",
     "wl_pack_weights",
     "wl_workspace_bytes",
+    "wl_kernel_launches",
     "wl_block_forward",
     "wl_convfirst_fwd",
     "wl_mbconv_fwd",
@@ -98,6 +99,7 @@ def lib() -> ctypes.CDLL:
         "wl_packed_bytes": (ctypes.c_int64, [D]),
         "wl_pack_weights": (ctypes.c_int, [D, P(P(ctypes.c_float)), ctypes.c_int, vp]),
         "wl_workspace_bytes": (ctypes.c_int64, [D]),
+        "wl_kernel_launches": (ctypes.c_int, [D]),
         "wl_block_forward": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
         "wl_convfirst_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
         "wl_mbconv_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),

@@ -138,6 +138,11 @@ int64_t wl_workspace_bytes(const wl_block_desc* d) {
   return workspace_bytes(*d);
 }
 
+int wl_kernel_launches(const wl_block_desc* d) {
+  if (int e = wl_validate(d)) return e;
+  return kernel_launches(*d);
+}
+
 int wl_output_dims(const wl_block_desc* d, int32_t* n, int32_t* h, int32_t* w, int32_t* c) {
   if (int e = wl_validate(d)) return e;
   output_dims(*d, n, h, w, c);

@@ -33,6 +33,11 @@ int64_t weight_numel(const wl_block_desc& d, int i) { return family_of(d)->weigh
 int64_t packed_bytes(const wl_block_desc& d) { return family_of(d)->packed_bytes(d); }
 int pack_weights(const wl_block_desc& d, const float* const* w, uint8_t* out) { return family_of(d)->pack(d, w, out); }
 int64_t workspace_bytes(const wl_block_desc& d) { return family_of(d)->workspace_bytes(d); }
+int kernel_launches(const wl_block_desc& d) {
+  if (d.kind == WL_KIND_HEAD) return 2;
+  if (d.kind == WL_KIND_MBCONV) return mb_kernel_launches(d);
+  return 1;
+}
 int forward(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
   return family_of(d)->forward(d, x, p, z, ws, st);
 }

@@ -53,6 +53,8 @@ int64_t weight_numel(const wl_block_desc& d, int i);
 int64_t packed_bytes(const wl_block_desc& d);
 int pack_weights(const wl_block_desc& d, const float* const* w, uint8_t* out);
 int64_t workspace_bytes(const wl_block_desc& d);
+int kernel_launches(const wl_block_desc& d);
+int mb_kernel_launches(const wl_block_desc& d);
 void output_dims(const wl_block_desc& d, int32_t* n, int32_t* h, int32_t* w, int32_t* c);
 int forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st);
 

@@ -1767,6 +1767,12 @@ int mb_init() {
 
 }  // namespace
 
+int mb_kernel_launches(const wl_block_desc& d) {
+  MbPlanH P;
+  if (!mb_plan(d, P)) return set_error(WL_EUNSUPPORTED, "no MBConv launch plan");
+  return P.f.fused ? 1 : 2;
+}
+
 void mb_set_trace(void* p) { g_mb_trace = reinterpret_cast<long long*>(p); }
 
 const Family kMbFamily = {mb_validate, mb_weight_count, mb_weight_numel, mb_packed_bytes,

@@ -139,11 +139,13 @@ class FusedNetwork:
         return expand_network(self.net, self.batch, scheme, device)
 
     def launch_count(self) -> int:
-        """Kernels this forward launches (MBConv and head units launch two)."""
+        """Kernels this forward launches, as the library plans them
+        (``wl_kernel_launches``: 1 per fused block, 2 for the head)."""
         n = 0
         for u in self.units:
-            kind = u.module.desc.kind
-            n += 2 if kind in (_lib.KIND_MBCONV, _lib.KIND_HEAD) else 1
+            k = _lib.lib().wl_kernel_launches(ctypes.byref(u.module.desc))
+            _lib.check(k if k < 0 else 0, "wl_kernel_launches")
+            n += k
         return n
 
     def weights(self) -> dict:

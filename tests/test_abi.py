@@ -89,3 +89,18 @@ def test_output_dims_and_workspace():
     assert ws >= 4 * 14 * 14 * 192 * 2 + 4 * 192 * 4  # L2-resident hidden + SE pool
     d = _desc(ConvFirst(8, 6), TensorDims(4, 28, 28, 48))
     assert L.wl_workspace_bytes(ctypes.byref(d)) == 0  # fully fused
+
+
+def test_kernel_launches_per_block():
+    """wl_kernel_launches reports the planned launches (host-side, no GPU):
+    one per fused block, two for the head (pool, classifier)."""
+    L = _lib.lib()
+    for blk, dims, k in ((MBConv(8, 4, 0.25), TensorDims(128, 14, 14, 128), None),
+                         (MBConv(8, 4, 0.25), TensorDims(128, 7, 7, 128), None),
+                         (MBConv(8, 4, 0.25, 2), TensorDims(128, 28, 28, 48), 128),
+                         (ConvFirst(8, 6), TensorDims(8, 28, 28, 48), None),
+                         (ConvFirst(8, 6, 2), TensorDims(8, 56, 56, 32), 48)):
+        d = _desc(blk, dims, k)
+        assert L.wl_kernel_launches(ctypes.byref(d)) == 1
+    d = _desc(Head(1280, 1000), TensorDims(128, 7, 7, 128))
+    assert L.wl_kernel_launches(ctypes.byref(d)) == 2
