@@ -14,7 +14,7 @@ from functools import lru_cache
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwlfuse.so")
+LIB_PATH = os.environ.get("WLFUSE_LIB_AB") or os.path.join(HERE, "libwlfuse.so")  # A/B timing override (tools/ab_build.sh)
 
 WL_OK, WL_EINVAL, WL_EUNSUPPORTED, WL_ECUDA = 0, -1, -2, -3
 KIND_CONVFIRST, KIND_MBCONV, KIND_STEM, KIND_HEAD = 1, 2, 4, 5

@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from .core import ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims
-from .machine import FusedSchedule, block_descriptor, build_schedule, random_inputs, weight_names
+from .machine import FusedSchedule, build_schedule, device_binding, random_inputs
 
 
 def init_weights(s: FusedSchedule, rng: np.random.Generator, residual_gain: float = 0.5) -> dict:
@@ -58,21 +58,25 @@ class FusedBlock(torch.nn.Module):
         if not torch.cuda.is_available():
             raise RuntimeError("FusedBlock needs a CUDA device (there is no CPU fallback)")
         self.schedule = build_schedule(block, dims, out_channels=out_channels)
-        self.desc = block_descriptor(block, dims, self.schedule.out_channels)
+        self.binding = device_binding(self.schedule)  # zero-padded channels where C % 16 != 0
+        self.desc = self.binding.desc
         L = _lib.lib()
         dev = torch.device(device)
         _lib.check(L.wl_init(dev.index if dev.index is not None else torch.cuda.current_device()), "wl_init")
         if weights is None:
             weights = init_weights(self.schedule, np.random.default_rng(seed))
         self.weights = {k: np.asarray(v, dtype=np.float32) for k, v in weights.items()}
-        packed = _lib.pack_weights(self.desc, [self.weights[n] for n in weight_names(self.schedule)])
+        packed = _lib.pack_weights(self.desc, self.binding.device_weights(self.weights))
         self.register_buffer("packed", torch.from_numpy(packed).to(dev), persistent=False)
         ws = _lib.check(L.wl_workspace_bytes(ctypes.byref(self.desc)))
         self.register_buffer("workspace", torch.zeros(max(ws, 256), dtype=torch.uint8, device=dev), persistent=False)
-        self.out_shape = tuple(self.schedule.out_dims)
+        self.out_shape = tuple(self.binding.out_dims)  # device shape (padded channels)
+        self.in_shape = (dims.n, dims.h, dims.w, self.binding.dims.c)
 
     def launch(self, x: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor | None = None, stream=None) -> None:
-        """Raw launch into a caller-owned output (graph-capturable)."""
+        """Raw launch into a caller-owned output (graph-capturable). ``x``
+        and ``out`` carry the device channel counts (``in_shape`` /
+        ``out_shape``; padded channels are zero)."""
         ws = self.workspace if workspace is None else workspace
         st = (stream or torch.cuda.current_stream()).cuda_stream
         _lib.check(
@@ -88,9 +92,11 @@ class FusedBlock(torch.nn.Module):
         want = (self.schedule.dims.n, self.schedule.dims.h, self.schedule.dims.w, self.schedule.dims.c)
         if tuple(x.shape) != want:
             raise ValueError(f"input shape {tuple(x.shape)} does not match the bound dims {want}")
+        if self.in_shape != want:
+            x = torch.nn.functional.pad(x, (0, self.in_shape[3] - want[3]))
         out = torch.empty(self.out_shape, dtype=torch.float16, device=x.device)
         self.launch(x, out)
-        return out
+        return self.binding.real_output(out).contiguous() if self.binding.padded else out
 
 
 def FusedConvFirst(dims: TensorDims, group_width=8, expansion=6, stride=1, activation="relu", out_channels=None, **kw):

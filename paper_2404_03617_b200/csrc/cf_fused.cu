@@ -540,6 +540,7 @@ void cf_register() {
   reg_c<32>();
   reg_c<48>();
   reg_c<64>();
+  reg_c<80>();  // ConvFirstNet-Tiny's 72 channels, padded to a whole channel pair
   reg_c<96>();
   reg_c<128>();
 }

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
     mbar_wait_sleep(&B.w_full, 0);
     const float* bconv = reinterpret_cast<const float*>(s_w + a.o_bconv);
     const int XP = (2 * a.R + 1) * W;
-    const int cb = C / 16;  // 16-column blocks per conv tile (1 or 2)
+    const int cb = C / 16;  // 16-column blocks per conv tile
     float bc[2][16];
 #pragma unroll
     for (int b = 0; b < 2; ++b)
@@ -287,20 +287,29 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
       // lane row -> (flat row, col) walked incrementally (no integer division per tile)
       int row = (a.conv_base + q * 32 + lane) / Wp, col = a.conv_base + q * 32 + lane - row * Wp;
       for (int t = 0; t < a.n_ct; ++t) {
-        uint32_t v[2][16];
-        WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C), v[0]);
-        if (cb > 1) WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C + 16), v[1]);
-        tmem_ld_wait();
-        if (col >= 1 && col <= W && row >= 1 && row <= 2 * a.R + 1) {  // row 1 .. 2R+1 <-> conv row 2*yo0 - 2 + row
-          const int px = (row - 1) * W + (col - 1);
+        const bool inside = col >= 1 && col <= W && row >= 1 && row <= 2 * a.R + 1;  // row 1 .. 2R+1 <-> conv row 2*yo0 - 2 + row
+        const int px = (row - 1) * W + (col - 1);
+        for (int b0 = 0; b0 < cb; b0 += 2) {  // 32 columns per TMEM round trip
+          uint32_t v[2][16];
+          WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C + 16 * b0), v[0]);
+          if (b0 + 1 < cb) WL_TMEM_LD16(tmem_lane_addr(tmem, q, a.t_c + t * C + 16 * b0 + 16), v[1]);
+          tmem_ld_wait();
+          if (inside) {
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            if (b >= cb) break;
-            float fv[16];
+            for (int b = 0; b < 2; ++b) {
+              if (b0 + b >= cb) break;
+              float fv[16];
+              if (b0 == 0) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + bc[b][k];
-            *reinterpret_cast<uint4*>(s_xc + ((size_t)(2 * b) * XP + px) * 8) = pack8(fv);
-            *reinterpret_cast<uint4*>(s_xc + ((size_t)(2 * b + 1) * XP + px) * 8) = pack8(fv + 8);
+                for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + bc[b][k];
+              } else {  // C > 32: the other channel blocks' biases come from shared memory
+#pragma unroll
+                for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + bconv[(b0 + b) * 16 + k];
+              }
+              const int pl = 2 * (b0 + b);
+              *reinterpret_cast<uint4*>(s_xc + ((size_t)pl * XP + px) * 8) = pack8(fv);
+              *reinterpret_cast<uint4*>(s_xc + ((size_t)(pl + 1) * XP + px) * 8) = pack8(fv + 8);
+            }
           }
         }
         col += 128;

@@ -1463,32 +1463,37 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     // CTA's h2 rows), V ring (3 stages); Z in the expand/conv TMEM columns
     f.K = K;
     if (hid % 64) return false;  // W_prj packed in 64-row chunks
-    f.HCb = 64;
     f.bulk = f.st_stores == 1;
-    if (f.bulk) {  // projection chunk = lcm(HC, 64) channels (whole conv chunks)
-      int pc = 64;
-      while (pc % f.HC) pc += 64;
-      if (f.HR % pc) f.bulk = 0;
-      else f.HCb = pc;
-    }
-    if (f.HR % f.HCb || (f.ranges > 1 && !f.bulk)) return false;
-    f.nchb = f.HR / f.HCb;
+    if (f.ranges > 1 && !f.bulk) return false;
     f.n_pt = (f.P_out + 127) / 128;
-    f.vchunk_bytes = K * f.HCb * 2;
     f.residual = d.stride == 1;
-    f.t_z = f.t_e;
+    f.t_z = 0;  // x tile, expand and conv accumulators are all dead by the projection
     f.s_pa = 0;
-    if (K > 256 || f.t_z + f.n_pt * K > f.tmem_cols) return false;
-    // bulk stages hold [HCb/8][P_out][8] plus the slack the last plane's
-    // 128-row tiles read past P_out
-    f.a_stage_b = align_up((f.HCb / 8) * f.P_out * 16 + (f.n_pt * 128 - f.P_out) * 16, 128);
-    const int a_stage = f.bulk ? f.a_stage_b : f.n_pt * 128 * f.HCb * 2;
+    if (K > 256 || f.n_pt * K > 512) return false;
+    while (f.tmem_cols < f.n_pt * K) f.tmem_cols *= 2;
+    // projection chunk width: whole conv chunks (lcm(HC, 64)) when its A / V
+    // rings fit, else 64 channels (bulk h2 is plane-contiguous, [hidden/8][P_out][8],
+    // so any 64-channel range is one copy whatever the conv chunk width)
+    int pc = 64;
+    if (f.bulk)
+      while (pc % f.HC) pc += 64;
     f.sa = 0;
-    for (int sa = std::min(4, std::max(2, f.nchb)); sa >= 2 && !f.sa; --sa) {
-      f.s_pv = align_up(sa * a_stage, 128);
-      if (f.s_pv + 3 * f.vchunk_bytes <= f.s_gate) f.sa = sa;
+    for (int hcb : {pc, 64}) {
+      if (f.sa || f.HR % hcb || (hcb != 64 && !f.bulk)) continue;
+      f.HCb = hcb;
+      f.nchb = f.HR / f.HCb;
+      f.vchunk_bytes = K * f.HCb * 2;
+      // bulk stages hold [HCb/8][P_out][8] plus the slack the last plane's
+      // 128-row tiles read past P_out
+      f.a_stage_b = align_up((f.HCb / 8) * f.P_out * 16 + (f.n_pt * 128 - f.P_out) * 16, 128);
+      const int a_stage = f.bulk ? f.a_stage_b : f.n_pt * 128 * f.HCb * 2;
+      for (int sa = std::min(4, std::max(2, f.nchb)); sa >= 2 && !f.sa; --sa) {
+        f.s_pv = align_up(sa * a_stage, 128);
+        if (f.s_pv + 3 * f.vchunk_bytes <= f.s_gate) f.sa = sa;
+      }
     }
     if (!f.sa) return false;
+    const int a_stage = f.bulk ? f.a_stage_b : f.n_pt * 128 * f.HCb * 2;
     f.fused = 1;
     // SE weights at the tail of the weight ring, clear of the projection's A / V
     // rings (give up A stages for it, down to two)

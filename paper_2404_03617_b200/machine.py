@@ -10,7 +10,7 @@ There is no CPU path: without the library or a GPU every call raises.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
@@ -238,6 +238,86 @@ def block_descriptor(block, dims: TensorDims, k: int):
     return d
 
 
+def device_channels(c: int) -> int:
+    """Channel count a block boundary runs at on the device: the kernels'
+    K-steps and channel-pair tiles need C % 16 == 0, so ConvFirstNet-Nano's
+    24 and Tiny's 72 run as 32 and 80. The extra channels are exact zeros
+    end to end (zero weights and biases; ReLU/SiLU/GELU(0) = 0; the SE gate
+    of a zero channel multiplies zero), so the real channels are unchanged."""
+    return c if c % 16 == 0 else -(-c // 16) * 16
+
+
+_SQ_AXIS = {"w_sq": 1, "b_sq": 0, "w_ex": 0}  # SE squeeze width stays the real int(se_ratio * C)
+
+
+@dataclass(frozen=True)
+class DeviceBinding:
+    """A schedule (reference shapes) bound to its device channel counts:
+    the C-ABI descriptor plus the zero-embedding of reference-shaped
+    weights and activations into the padded device tensors."""
+
+    schedule: FusedSchedule
+    block: object  # the block as the device runs it (a Stem carries its padded width)
+    dims: TensorDims  # device input dims
+    k: int  # device output channels
+    desc: object
+
+    @property
+    def padded(self) -> bool:
+        return self.dims.c != self.schedule.dims.c or self.k != self.schedule.out_channels
+
+    @property
+    def out_dims(self) -> tuple[int, ...]:
+        d = self.schedule.out_dims
+        return d if len(d) == 2 else (*d[:3], self.k)
+
+    def device_weights(self, weights: dict) -> list[np.ndarray]:
+        """Reference-named float32 weights -> the device list (padded)."""
+        dev = build_schedule(self.block, self.dims, out_channels=self.k)
+        out = []
+        for t in self.schedule.tensors:
+            if t.role != "weights":
+                continue
+            w = np.asarray(weights[t.name], dtype=np.float32)
+            if w.shape != t.dims:
+                raise ScheduleError(f"weight {t.name!r} has shape {w.shape}, expected {t.dims}")
+            if not self.padded:
+                out.append(w)
+                continue
+            shape = list(dev.tensor(t.name).dims)
+            if t.name in _SQ_AXIS:
+                shape[_SQ_AXIS[t.name]] = t.dims[_SQ_AXIS[t.name]]
+            z = np.zeros(shape, dtype=np.float32)
+            z[tuple(slice(0, n) for n in w.shape)] = w
+            out.append(z)
+        return out
+
+    def device_input(self, x: np.ndarray) -> np.ndarray:
+        if x.shape[-1] == self.dims.c:
+            return x
+        z = np.zeros((*x.shape[:-1], self.dims.c), dtype=x.dtype)
+        z[..., : x.shape[-1]] = x
+        return z
+
+    def real_output(self, z):
+        """Device output -> the reference's channel count (a view)."""
+        return z if len(self.schedule.out_dims) == 2 else z[..., : self.schedule.out_channels]
+
+
+def device_binding(s: FusedSchedule) -> DeviceBinding:
+    block, dims = s.block, s.dims
+    cin = dims.c if isinstance(block, Stem) else device_channels(dims.c)
+    k = s.out_channels if isinstance(block, Head) else device_channels(s.out_channels)
+    if isinstance(block, ConvNeXtBlock) and cin != dims.c:
+        raise ScheduleError("LayerNorm blocks cannot be zero-padded (the padding would enter the channel mean)")
+    ddims = TensorDims(dims.n, dims.h, dims.w, cin)
+    dblock = replace(block, out_channels=k) if isinstance(block, Stem) else block
+    desc = block_descriptor(dblock, ddims, k)
+    if isinstance(block, MBConv):
+        desc.se_sq = int(block.se_ratio * dims.c)
+    return DeviceBinding(s, dblock, ddims, k, desc)
+
+
 def _act(name: str) -> int:
     from . import _lib
 
@@ -270,9 +350,9 @@ def execute_numeric(s: FusedSchedule, inputs: dict) -> np.ndarray:
         arrays[t.name] = arr
     from . import _lib
 
-    desc = block_descriptor(s.block, s.dims, s.out_channels)
-    out = _lib.execute_numeric_host(desc, arrays["x"], [arrays[nm] for nm in weight_names(s)])
-    return out.reshape(s.out_dims)
+    b = device_binding(s)
+    out = _lib.execute_numeric_host(b.desc, b.device_input(arrays["x"]), b.device_weights(arrays))
+    return np.ascontiguousarray(b.real_output(out.reshape(b.out_dims)))
 
 
 def fused_dram_bytes(s: FusedSchedule, element_bytes: int = 2) -> int:

@@ -32,6 +32,6 @@ for nm in a.names:
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(10): m.launch(x, out)
+    for _ in range(50): m.launch(x, out)
     e1.record(); e1.synchronize()
-    print(nm, "%.1f us" % (e0.elapsed_time(e1) / 10 * 1e3), flush=True)
+    print(nm, "%.1f us" % (e0.elapsed_time(e1) / 50 * 1e3), flush=True)
