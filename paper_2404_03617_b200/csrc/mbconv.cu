@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       for (int j = 0; j < nch; ++j) {
         const int slot = j % S, use = j / S;
         mbar_wait(&B.w_empty[slot], (use & 1) ^ 1);
+        if (j < 10) WL_TRACE(16 + 8 * j + 7);
         mbar_arrive_expect_tx(&B.w_full[slot], a.chunk_bytes);
         bulk_g2s(s_ring + slot * a.chunk_bytes, chunks + (size_t)(range * nch + j) * a.chunk_bytes, a.chunk_bytes,
                  &B.w_full[slot]);
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       WL_TRACE(2);
       auto issue_expand = [&](int j) {
         const int slot = j % S, eb = j % a.e_bufs;
+        if (j < 20) WL_TRACE(232 + j);
         mbar_wait(&B.w_full[slot], (j / S) & 1);
         WL_TRACE(16 + 8 * j + 0);
         tc_fence_after();
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const int slot = j % S, hb = j % a.h1_bufs, cb = j % a.c_bufs;
         mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // h1 ready implies the chunk's weights landed
         if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
+        if (isx == 0) WL_TRACE(16 + 8 * j + 1);
         tc_fence_after();
         const uint32_t h1a = smem_u32(hb ? smem + a.s_h1b : s_h1);
         const uint64_t a_base = make_sdesc(h1a + (a.conv_base - a.Wp - 1) * 16, a.flat_h1 * 16, 128);
@@ -407,6 +410,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mma_commit(&B.c_full[cb]);
         mma_commit(&B.h1_empty[hb]);
         mma_commit(&B.w_empty[slot]);
+        if (isx == 0) WL_TRACE(16 + 8 * j + 2);
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -1283,6 +1287,8 @@ __global__ void __launch_bounds__(256, 1)
 // =================================================================== host
 #include <algorithm>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include "launch.h"
 
 namespace wl {
@@ -1344,8 +1350,11 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   const int x_bytes = std::max(align_up((C / 8) * f.x_alloc * 16 + (f.n_et * 128 - x_valid) * 16, 128),
                                (C % 64 == 0) ? C * 2 * f.n_et * 128 : 0);
   const int se_scratch = align_up((hid + 640 + f.sq) * 4, 16);
+  // planner experiments: WL_MB_FORCE="xt,eb,cb,hc" pins the TMEM / chunk choice
+  int force[4] = {-1, -1, -1, -1};
+  if (const char* e = getenv("WL_MB_FORCE")) sscanf(e, "%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3]);
   for (int hc = 128; hc >= 16; hc -= 16) {
-    if (f.HR % hc) continue;
+    if (f.HR % hc || (force[3] > 0 && hc != force[3])) continue;
     const int tiles1 = f.T8 ? f.n_et + f.n_ct : f.n_et;
     if (tiles1 * hc > 512) continue;
     const int h1_bytes = std::max((hc / 8) * f.flat_h1 * 16, se_scratch);
@@ -1373,6 +1382,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   for (int xt = f.T8 ? 1 : 0; xt >= 0 && !placed; --xt) {
     const int combos[4][2] = {{2, 2}, {1, 2}, {2, 1}, {1, 1}};
     for (auto& cb : combos) {
+      if (force[0] >= 0 && (xt != force[0] || cb[0] != force[1] || cb[1] != force[2])) continue;
       f.x_tmem = xt;
       f.e_bufs = (f.T8 && f.nch > 1) ? cb[0] : 1;  // T=1: the MMA warp cannot observe E consumption early
       f.c_bufs = (f.T8 && f.nch > 1) ? cb[1] : 1;
