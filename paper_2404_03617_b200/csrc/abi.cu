@@ -92,6 +92,7 @@ int wl_version(void) { return WL_ABI_VERSION; }
 void wl_debug_set_trace(void* dev_ptr) {
   wl::mb_set_trace(dev_ptr);
   wl::cf2_set_trace(dev_ptr);
+  wl::cf_set_trace(dev_ptr);
 }
 
 const char* wl_last_error(void) { return g_last_error.c_str(); }

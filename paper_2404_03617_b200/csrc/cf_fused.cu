@@ -36,6 +36,7 @@ struct CfArgs {
   int norm;
   const uint8_t* wpack;
   __half* z;
+  long long* trace;  // debug: clock64 stamps of CTA 0 (tools/trace_cf.py), null in production
 };
 
 namespace cfk {
@@ -53,6 +54,11 @@ struct Bars {
   uint32_t tmem_base;
 };
 }  // namespace cfk
+
+#define CF_TRACE(it, k)                                                                 \
+  do {                                                                                  \
+    if (args.trace && blockIdx.x == 0 && (it) < 16) args.trace[8 + 12 * (it) + (k)] = clock64(); \
+  } while (0)
 
 template <int C, int KS, bool T8, int ACT>
 __global__ void __launch_bounds__(cfk::kThreads, 2)
@@ -107,6 +113,11 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
   pdl_trigger();  // single-wave persistent grid: let the next kernel stage its prologue
   pdl_wait();
   const uint32_t tmem = B.tmem_base;
+  if (args.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    args.trace[0] = clock64();
+    args.trace[2] = pl.halo_bufs * 100 + nchunks;
+    args.trace[3] = r;
+  }
 
   const int tiles_per_img = args.tiles_x * args.tiles_y;
   auto tile_coords = [&](int t, int& n, int& y0, int& x0) {
@@ -133,6 +144,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         tile_coords((int)blockIdx.x + it * (int)gridDim.x, n, y0, x0);
         const int b = it % NHB, use = it / NHB;
         mbar_wait(&B.halo_empty[b], (use & 1) ^ 1);
+        CF_TRACE(it, 0);
         mbar_arrive_expect_tx(&B.halo_full[b], pl.halo_bytes);
         tma_load_5d(s_halo + b * pl.halo_bytes, &tmap_x, 0, x0 - P, y0 - P, 0, n, &B.halo_full[b]);
       };
@@ -160,12 +172,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       mbar_wait(&B.hdr_full, 0);
       if (pl.resident) mbar_wait(&B.w_all, 0);
       tc_fence_after();
-
-
       for (int it = 0; it < my_tiles; ++it) {
-
         const int xb = it & 1;
         mbar_wait(&B.xc_full[xb], (it >> 1) & 1);
+        CF_TRACE(it, 5);
         tc_fence_after();
         const uint32_t xcb = xc0 + xb * pl.xc_bytes;
         auto slot_addr = [&](int j, int g) -> uint32_t {
@@ -202,6 +212,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         }
         issue_project(nchunks - 1);
         mma_commit(&B.z_full);
+        CF_TRACE(it, 8);
       }
     }
   } else if (T8 && (warp == 3 || (NCI > 1 && warp == kAllocWarp))) {
@@ -216,6 +227,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         const int b = u % NHB;
         mbar_wait(&B.halo_full[b], (u / NHB) & 1);
         if (u > 0) mbar_wait(&B.cacc_empty, (u - 1) & 1);
+        if (ci == 0) CF_TRACE(u, 1);
         tc_fence_after();
         const uint32_t hb = halo0 + b * pl.halo_bytes;
         const uint32_t lbo = HH * HWD * 16, sbo = HWD * 16;
@@ -232,6 +244,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
           }
         }
         mma_commit(&B.conv_full);
+        if (ci == 0) CF_TRACE(u, 2);
       }
     }
   } else if (warp >= kHWarp0 && warp < kHWarp0 + 4) {
@@ -244,6 +257,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         const int g = it * nchunks + j, b = g & 1;
         mbar_wait(&B.e_full[b], (g >> 1) & 1);
         mbar_wait(&B.h_empty[b], ((g >> 1) & 1) ^ 1);
+        if (q == 0 && lane == 0 && j == 0) CF_TRACE(it, 6);
         tc_fence_after();
         const float* aj = s_a + j * r;
 #pragma unroll 1
@@ -260,6 +274,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&B.h_full[b]);
+        if (q == 0 && lane == 0 && j == nchunks - 1) CF_TRACE(it, 7);
       }
     }
   } else if (warp >= kTWarp0 && warp < kTWarp0 + 4) {
@@ -284,6 +299,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         mbar_wait(&B.halo_full[u % NHB], (u / NHB) & 1);
       }
       mbar_wait(&B.xc_empty[xb], ((u >> 1) & 1) ^ 1);
+      if (q == 0 && lane == 0) CF_TRACE(u, 3);
       if constexpr (T8) {
 #pragma unroll 1
         for (int c0 = 0; c0 < C; c0 += 16) {
@@ -349,6 +365,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       }
       fence_async_smem();
       mbar_arrive(&B.xc_full[xb]);
+      if (q == 0 && lane == 0) CF_TRACE(u, 4);
     };
 
     auto final_epi = [&](int it) {
@@ -357,6 +374,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       const int hbuf = it % NHB;
       mbar_wait(&B.z_full, it & 1);
       mbar_wait(&B.halo_full[hbuf], (it / NHB) & 1);
+      if (q == 0 && lane == 0) CF_TRACE(it, 9);
       tc_fence_after();
       const uint8_t* hb = s_halo + hbuf * pl.halo_bytes;
       const int y = y0 + tr, x = x0 + tc;
@@ -380,6 +398,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       tc_fence_before();
       mbar_arrive(&B.z_empty);
       mbar_arrive(&B.halo_empty[hbuf]);
+      if (q == 0 && lane == 0) CF_TRACE(it, 10);
     };
 
     if (my_tiles > 0) conv_epi(0);
@@ -403,6 +422,9 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
 #include "launch.h"
 
 namespace wl {
+long long* g_cf_trace = nullptr;
+void cf_set_trace(void* p) { g_cf_trace = reinterpret_cast<long long*>(p); }
+
 namespace {
 
 constexpr int kSmemMax = 232448;          // 227 KB per CTA
@@ -683,6 +705,7 @@ int cf_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
   a.norm = d.norm;
   a.wpack = reinterpret_cast<const uint8_t*>(packed);
   a.z = reinterpret_cast<__half*>(z);
+  a.trace = g_cf_trace;
   const int grid = std::min(a.ntiles, kNumSMs * p.ctas_per_sm);
   return launch_pdl(it->second, grid, cfk::kThreads, p.smem_bytes, st, "cf_fused launch", tm, a);
 }

@@ -76,5 +76,6 @@ extern const Family kStemFamily;
 extern const Family kHeadFamily;
 void mb_set_trace(void* p);
 void cf2_set_trace(void* p);
+void cf_set_trace(void* p);
 
 }  // namespace wl
