@@ -28,7 +28,8 @@ struct Cf2Args {
   int H, W, Ho, Wo, R, tiles_y, Wp, nbands;
   int n_ct, n_eh, n_pt, conv_base, x_alloc, x_rows, x_bufs;
   int o_convw, o_bconv, o_a, o_b, w_bytes;  // header: conv taps + fp32 vectors
-  int chunk_bytes, u_bytes;                 // chunk j = [U_j (r x C) | V_j (K x r)], all resident
+  int chunk_bytes, u_bytes;                 // chunk j = [U_j (r x C) | V_j (K x r)]
+  int ws;                                   // 0: every chunk resident; else a ring of ws chunk stages
   int s_x, s_xc, s_ah, s_hs, s_zo, s_aq, s_w, s_bar, smem;
   int ah_bytes, aq_bytes;
   int t_c, t_e, t_z, tmem_cols;
@@ -56,13 +57,15 @@ __device__ __forceinline__ uint4 tri3(const uint4& a, const uint4& b, const uint
 }
 
 namespace cf2k {
-constexpr int kThreads = 640;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 conv/blur_H,
-                               // w8-15 hidden (E -> phi), w16-19 output (Z -> blur_W)
+constexpr int kThreads = 640;  // w0 TMA (x bands, weights), w1 FFN MMA, w2/w3 conv MMA (w2 allocates
+                               // TMEM), w4-7 conv/blur_H, w8-15 hidden (E -> phi), w16-19 output
+                               // (Z -> blur_W)
 struct Bars {
   uint64_t w_full, x_full[2], x_empty[2];
   uint64_t conv_full, c_empty, xh_full[2], xh_empty[2];
   uint64_t e_full[2], e_empty[2], q_full[2], q_empty[2];
   uint64_t z_full, z_empty;
+  uint64_t wr_full[4], wr_empty[4];
   uint32_t tmem_base;
 };
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -130,6 +133,10 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
     mbar_init(&B.c_empty, 128);
     mbar_init(&B.z_full, 1);
     mbar_init(&B.z_empty, 128);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&B.wr_full[i], 1);
+      mbar_init(&B.wr_empty[i], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -146,18 +153,45 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
     // ---------------- producer: resident weights once, x bands through a ring
     if (lane == 0) {
       prefetch_tmap(&tmap_x);
-      const int wtot = a.w_bytes + nch * a.chunk_bytes;
+      const int wtot = a.w_bytes + (a.ws ? 0 : nch * a.chunk_bytes);
       mbar_arrive_expect_tx(&B.w_full, wtot);
       bulk_g2s(s_w, a.wpack, wtot, &B.w_full);
-      for (int i = 0; i < nb; ++i) {
-        const int xb = i % a.x_bufs, use = i / a.x_bufs;
-        mbar_wait_sleep(&B.x_empty[xb], (use & 1) ^ 1);
+      auto load_x = [&](int i) {
+        const int xb = i % a.x_bufs;
         if (i < 8) CF2_TRACE(8 + i * 24 + 0);
         const int band = band_of(i), n = band / a.tiles_y, yo0 = (band % a.tiles_y) * a.R;
         mbar_arrive_expect_tx(&B.x_full[xb], planes * loaded * 16);
         for (int g = 0; g < planes; ++g)
           tma_load_5d(s_x + ((size_t)(xb * planes + g) * a.x_alloc) * 16, &tmap_x, 0, -1, 2 * yo0 - 2, g, n,
                       &B.x_full[xb]);
+      };
+      if (!a.ws) {
+        for (int i = 0; i < nb; ++i) {
+          mbar_wait_sleep(&B.x_empty[i % a.x_bufs], ((i / a.x_bufs) & 1) ^ 1);
+          load_x(i);
+        }
+      } else {
+        // streamed FFN weights: x bands and weight chunks from one thread,
+        // each issued as soon as its ring slot frees (neither waits behind the other)
+        const uint8_t* chunks = a.wpack + a.w_bytes;
+        const int total = nb * nch;
+        int i = 0, g = 0;
+        while (i < nb || g < total) {
+          bool moved = false;
+          if (i < nb && mbar_test(&B.x_empty[i % a.x_bufs], ((i / a.x_bufs) & 1) ^ 1)) {
+            load_x(i++);
+            moved = true;
+          }
+          if (g < total && mbar_test(&B.wr_empty[g % a.ws], ((g / a.ws) & 1) ^ 1)) {
+            const int slot = g % a.ws;
+            mbar_arrive_expect_tx(&B.wr_full[slot], a.chunk_bytes);
+            bulk_g2s(s_w + a.w_bytes + slot * a.chunk_bytes, chunks + (size_t)(g % nch) * a.chunk_bytes,
+                     a.chunk_bytes, &B.wr_full[slot]);
+            ++g;
+            moved = true;
+          }
+          if (!moved) __nanosleep(32);
+        }
       }
     }
   } else if (warp == 1) {
@@ -196,18 +230,23 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         mma_commit(&B.x_empty[i % a.x_bufs]);
         if (i < 8) CF2_TRACE(8 + i * 24 + 3);
       };
+      // chunk j of band i (global index g): resident slot j, or ring stage g % ws
+      auto chunk_addr = [&](int g, int j) -> uint32_t {
+        return smem_u32(s_w) + a.w_bytes + (a.ws ? g % a.ws : j) * a.chunk_bytes;
+      };
       auto issue_project = [&](int i, int j) {
         const int gq = i * nch + j, qs = gq & 1;
         mbar_wait(&B.q_full[qs], (gq >> 1) & 1);
         if (j == 0) mbar_wait(&B.z_empty, (i & 1) ^ 1);
         tc_fence_after();
-        const uint32_t vb = smem_u32(s_w) + a.w_bytes + j * a.chunk_bytes + a.u_bytes;
+        const uint32_t vb = chunk_addr(gq, j) + a.u_bytes;
         const uint32_t aq = smem_u32(s_aq) + qs * a.aq_bytes;
         for (int t = 0; t < a.n_eh; ++t)
           for (int kk = 0; kk < r / 16; ++kk)
             mma_ss(tmem + a.t_z + t * K, make_sdesc(aq + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
                    make_sdesc(vb + kk * 2 * (K * 16), K * 16, 128), idesc_z, (j > 0 || kk > 0));
         mma_commit(&B.q_empty[qs]);
+        if (a.ws) mma_commit(&B.wr_empty[gq % a.ws]);
         if (j == nch - 1) mma_commit(&B.z_full);
       };
       // warp 1 issues the FFN (expand / project chunks); the grouped conv is
@@ -222,8 +261,9 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         for (int j = 0; j < nch; ++j) {
           const int gg = i * nch + j, es = gg & 1;
           mbar_wait(&B.e_empty[es], ((gg >> 1) & 1) ^ 1);
+          if (a.ws) mbar_wait(&B.wr_full[gg % a.ws], (gg / a.ws) & 1);
           tc_fence_after();
-          const uint32_t ub = smem_u32(s_w) + a.w_bytes + j * a.chunk_bytes;
+          const uint32_t ub = chunk_addr(gg, j);
           for (int t = 0; t < a.n_eh; ++t)
             for (int kk = 0; kk < C / 16; ++kk)
               mma_ss(tmem + a.t_e + (es * a.n_eh + t) * r, make_sdesc(ah + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
@@ -520,8 +560,10 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
     if (R > a.Ho) break;
     for (int rr = 16; rr <= 256 && rr <= a.hid; rr += 16) {
       if (a.hid % rr) continue;
-      for (int xbufs = 2; xbufs >= 1; --xbufs) {
+      for (int xbufs = 2; xbufs >= 1; --xbufs)
+      for (int ws : {0, 3, 2}) {
         Cf2Args c = a;
+        c.ws = ws;
         c.R = R;
         c.r = rr;
         c.nch = c.hid / rr;
@@ -566,7 +608,8 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
         c.s_aq = s;
         s = align_up(s + 2 * c.aq_bytes, 128);
         c.s_w = s;
-        s = align_up(s + c.w_bytes + c.nch * c.chunk_bytes, 128);
+        s = align_up(s + c.w_bytes + (ws ? std::min(ws, c.nch) : c.nch) * c.chunk_bytes, 128);
+        if (ws > c.nch) continue;
         c.s_bar = s;
         s += 256;
         c.smem = s;
@@ -576,7 +619,10 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
         const double project = (double)c.n_pt * (c.hid / 16) * std::max(44, c.K / 2);
         // TMEM reads of the accumulators (~128 B/cycle): conv, hidden, projection
         const double tmem_rd = 4.0 * ((double)c.n_ct * c.C + (double)c.n_eh * c.hid + (double)c.n_pt * c.K);
-        const double cost = (std::max(conv + expand + project, tmem_rd) + 300.0) / R * (xbufs == 2 ? 1.0 : 1.15);
+        // streamed plans re-read every chunk per band from L2 (~50 B/cycle)
+        const double l2 = ws ? (double)c.nch * c.chunk_bytes / 50.0 : 0.0;
+        const double cost = (std::max(std::max(conv + expand + project, tmem_rd), l2) + 300.0 + (ws ? 200.0 : 0.0)) / R *
+                            (xbufs == 2 ? 1.0 : 1.15);
         if (cost < best) {
           best = cost;
           bestA = c;

@@ -84,6 +84,8 @@ CASES = [
     ("mbconv_s2_72_192_padded_in", MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 72), 192),
     ("mbconv_c192_hc48", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 192), None),
     ("mbconv_c160", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 160), None),
+    # ConvFirstNet-Small s3b0: FFN weights streamed through a chunk ring
+    ("convfirst_s2_64_96_streamed", ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 64), 96),
 ]
 
 
