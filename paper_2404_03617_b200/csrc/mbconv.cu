@@ -1305,12 +1305,17 @@ struct MbPlanH {
   int64_t h2_bytes, pool_bytes, gate_bytes;
 };
 
+// WL_MB_DEBUG=1 names the planner check that rejected a configuration
+static bool mb_plan_fail(int id, int line) {
+  if (getenv("WL_MB_DEBUG")) fprintf(stderr, "mb plan: rejected at check %d (mbconv.cu:%d)\n", id, line);
+  return false;
+}
 bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   memset(&P, 0, sizeof(P));
   MbFrontArgs& f = P.f;
   MbBackArgs& b = P.b;
   const int C = d.c, hid = d.expansion * d.c, K = d.k;
-  if (C % 16 || hid % 16 || K % 16) return false;
+  if (C % 16 || hid % 16 || K % 16) return mb_plan_fail(1, __LINE__);
   f.C = C;
   f.hid = hid;
   f.sq = d.se_sq;
@@ -1337,8 +1342,8 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   f.st_stores = (f.P_out + 255) / 256;
   while (f.P_out % f.st_stores) ++f.st_stores;
   f.st_rows = f.P_out / f.st_stores;
-  if (f.groups > (int)(kCounterBytes / 4)) return false;
-  if (f.sq < 1 || f.sq > 128) return false;
+  if (f.groups > (int)(kCounterBytes / 4)) return mb_plan_fail(2, __LINE__);
+  if (f.sq < 1 || f.sq > 128) return mb_plan_fail(3, __LINE__);
   // fused mode: the CTA owns every hidden channel of its images, or - when the
   // image groups would leave over half the SMs idle - a cluster pair splits them
   f.ranges = (want_fused && 2 * f.groups <= kNumSMs && hid % 128 == 0 && K % 64 == 0 && K <= 256) ? 2 : 1;
@@ -1362,14 +1367,17 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     const int full = f.stride == 2 ? f.P_full * hc * 2 : 0;
     const int hdr = align_up(f.HR * 4, 16) * 2 + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
     const int chunk = hc * C * 2 + (f.T8 ? (2 * (hc / 16) * 9 + 1) * 128 : 0);
+    int sqp = 8;
+    while (sqp < f.sq) sqp *= 2;
+    const int gate = (2 * f.imgs * hid + 22 * f.imgs * sqp) * 4;  // SE gates + squeeze-excite scratch
     const int total = x_bytes + h1_bytes + st + full + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048 +
-                      f.n_ct * 128 * 4 + f.n_et * 128;
+                      f.n_ct * 128 * 4 + f.n_et * 128 + gate;
     if (total <= kSmemMaxMb) {
       f.HC = hc;
       break;
     }
   }
-  if (!f.HC) return false;
+  if (!f.HC) return mb_plan_fail(4, __LINE__);
   f.nch = f.HR / f.HC;
   // double-buffer the expand / conv accumulators when TMEM allows
   // TMEM: x tile (A of a TS-mode expansion, T=8 only) + expand / conv
@@ -1392,7 +1400,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
       }
     }
   }
-  if (!placed) return false;
+  if (!placed) return mb_plan_fail(5, __LINE__);
   f.xsw = f.x_tmem && C % 64 == 0;
   f.t_x = 0;
   f.t_e = f.x_tmem ? x_cols : 0;
@@ -1413,7 +1421,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   // zero-filled), fp32 biases
   f.SQP = 8;
   while (f.SQP < f.sq) f.SQP *= 2;
-  if (f.SQP > 256) return false;
+  if (f.SQP > 256) return mb_plan_fail(6, __LINE__);
   int so = 0;
   f.o_wsq = so;
   so = align_up(so + hid * f.SQP * 2, 16);
@@ -1465,21 +1473,21 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   f.s_bar = o;
   o += 512;
   f.smem = o;
-  if (o > kSmemMaxMb) return false;
+  if (o > kSmemMaxMb) return mb_plan_fail(7, __LINE__);
   P.front_bytes = f.se_bytes + (int64_t)f.ranges * f.hdr_bytes + (int64_t)f.ranges * f.nch * f.chunk_bytes;
   f.fused = 0;
   if (want_fused) {
     // projection overlays the dead phase-1 buffers: A ring (2 stages of the
     // CTA's h2 rows), V ring (3 stages); Z in the expand/conv TMEM columns
     f.K = K;
-    if (hid % 64) return false;  // W_prj packed in 64-row chunks
+    if (hid % 64) return mb_plan_fail(8, __LINE__);  // W_prj packed in 64-row chunks
     f.bulk = f.st_stores == 1;
-    if (f.ranges > 1 && !f.bulk) return false;
+    if (f.ranges > 1 && !f.bulk) return mb_plan_fail(9, __LINE__);
     f.n_pt = (f.P_out + 127) / 128;
     f.residual = d.stride == 1;
     f.t_z = 0;  // x tile, expand and conv accumulators are all dead by the projection
     f.s_pa = 0;
-    if (K > 256 || f.n_pt * K > 512) return false;
+    if (K > 256 || f.n_pt * K > 512) return mb_plan_fail(10, __LINE__);
     while (f.tmem_cols < f.n_pt * K) f.tmem_cols *= 2;
     // projection chunk width: whole conv chunks (lcm(HC, 64)) when its A / V
     // rings fit, else 64 channels (bulk h2 is plane-contiguous, [hidden/8][P_out][8],
@@ -1502,7 +1510,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
         if (f.s_pv + 3 * f.vchunk_bytes <= f.s_gate) f.sa = sa;
       }
     }
-    if (!f.sa) return false;
+    if (!f.sa) return mb_plan_fail(11, __LINE__);
     const int a_stage = f.bulk ? f.a_stage_b : f.n_pt * 128 * f.HCb * 2;
     f.fused = 1;
     // SE weights at the tail of the weight ring, clear of the projection's A / V
@@ -1533,7 +1541,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   const int ntiles = (b.P + 127) / 128;
   b.KR = K;
   while (!f.fused && (b.KR > 256 || (ntiles * (K / b.KR) < kNumSMs && b.KR % 32 == 0 && b.KR >= 64))) b.KR /= 2;
-  if (K % b.KR || b.KR % 16) return false;
+  if (K % b.KR || b.KR % 16) return mb_plan_fail(12, __LINE__);
   b.kranges = K / b.KR;
   b.HCb = hid % 64 == 0 ? 64 : (hid % 32 == 0 ? 32 : 16);
   b.nchb = hid / b.HCb;
@@ -1550,7 +1558,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   b.s_bar = o;
   o += 512;
   b.smem = o;
-  if (o > kSmemMaxMb) return false;
+  if (o > kSmemMaxMb) return mb_plan_fail(13, __LINE__);
   b.t_z = 0;
   b.tmem_cols = 32;
   while (b.tmem_cols < b.KR) b.tmem_cols *= 2;

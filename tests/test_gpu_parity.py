@@ -84,6 +84,8 @@ CASES = [
     ("mbconv_s2_72_192_padded_in", MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 72), 192),
     ("mbconv_c192_hc48", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 192), None),
     ("mbconv_c160", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 160), None),
+    # ConvFirstNet-Pico at the reference's native 256: 8x8 stage, two images per CTA pair
+    ("mbconv_8x8_c128", MBConv(8, 4, 0.25), TensorDims(4, 8, 8, 128), None),
     # ConvFirstNet-Small s3b0: FFN weights streamed through a chunk ring
     ("convfirst_s2_64_96_streamed", ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 64), 96),
 ]
@@ -118,12 +120,13 @@ def test_deterministic_and_graph_equals_eager():
     assert torch.equal(eager, a) and torch.equal(a, m.output)
 
 
-@pytest.mark.parametrize("model", ["convfirstnet-pico", "convfirstnet-nano", "convfirstnet-tiny"])
-def test_network_per_unit_and_logits(model):
-    net = zoo.at_resolution(zoo.from_name(model), 224)
+@pytest.mark.parametrize("model,res", [("convfirstnet-pico", 224), ("convfirstnet-nano", 224),
+                                       ("convfirstnet-tiny", 224), ("convfirstnet-pico", 256)])
+def test_network_per_unit_and_logits(model, res):
+    net = zoo.at_resolution(zoo.from_name(model), res)
     m = FusedNetwork(net, batch=2, seed=11)
     rng = np.random.default_rng(1)
-    x = r16(rng, (2, 224, 224, 3))
+    x = r16(rng, (2, res, res, 3))
     out = m(torch.from_numpy(x).half().cuda())
     torch.cuda.synchronize()
     src = x
