@@ -33,6 +33,10 @@ struct MbFrontArgs {
   int H, W, Wp, imgs, groups;
   int total_rows, n_et, n_ct, conv_base, flat_h1, x_alloc;  // conv_base = Wp + 1
   int Ho, Wo, ranges;
+  // row bands: a cluster pair splits ONE image by output rows when its whole
+  // tile does not fit (H/Ho above are then the band's conv / output rows);
+  // the pair meets once, to sum the SE pool over DSMEM
+  int bands, H_img, Ho_img;
   int P_out, P_full;       // dense output / full-res pixels per CTA
   int st_rows, st_stores;  // TMA store box rows, stores per chunk
   int e_bufs, c_bufs, h1_bufs, x_tmem;
@@ -166,7 +170,12 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int group = blockIdx.x / a.ranges, range = blockIdx.x % a.ranges;
   if ((smem_u32(smem) & 1023) != 0) __trap();  // swizzled tiles need 1024-byte alignment
-  const int n0 = group * a.imgs;
+  // row bands (a.bands == 2): CTA pair (group = 2 n + band) splits image n;
+  // the band's first conv row c0 and the image row of its first x row xr0
+  const int band = a.bands > 1 ? group % 2 : 0;
+  const int n0 = a.bands > 1 ? group / 2 : group * a.imgs;
+  const int c0 = !band ? 0 : (a.stride == 1 ? a.H : 2 * a.Ho - 1);
+  const int xr0 = c0 - 1;
   const int h0 = range * a.HR;
   const int S = a.ring_stages, HC = a.HC, nch = a.nch, G8 = HC / 8;
   // T=8 with two or more conv tiles: warp 3 issues the odd tiles' conv MMAs so
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   // items go round-robin to NIS dedicated issuing threads (warps 3, 2), so the
   // conv never queues behind an expansion waiting for its weight chunk
   const int NIS = T8 ? min(2, a.n_ct * (HC / 16)) : 1;
-  const int img_flat = (a.H + 1) * a.Wp;
+  const int img_flat = (a.bands > 1 ? a.H + 2 : a.H + 1) * a.Wp;
   const int x_valid = a.imgs * img_flat;
   if (threadIdx.x == 0) WL_TRACE(0);
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {  // plan snapshot for the trace reader
@@ -203,8 +212,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       }
       s_cmap[i] = p;
     }
-    for (int f = threadIdx.x; f < a.n_et * 128; f += blockDim.x)
-      s_emap[f] = (f < x_valid && mb_real(f, a.Wp, a.W, a.H, a.total_rows)) ? 1 : 0;
+    for (int f = threadIdx.x; f < a.n_et * 128; f += blockDim.x) {
+      bool real;
+      if (a.bands > 1) {  // halo rows are real image rows unless past the image border
+        const int row = f / a.Wp, col = f - row * a.Wp;
+        real = f < x_valid && col >= 1 && col <= a.W && xr0 + row >= 0 && xr0 + row < a.H_img;
+      } else {
+        real = f < x_valid && mb_real(f, a.Wp, a.W, a.H, a.total_rows);
+      }
+      s_emap[f] = real ? 1 : 0;
+    }
   }
   {
     const int tail = a.x_alloc - x_valid, planes = a.C / 8;
@@ -268,13 +285,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
               "%4, %5}], [%6];" ::"r"(smem_u32(s_x + (size_t)cb * a.n_et * 128 * 128)),
-              "l"(&tmap_x), "r"(cb * 64), "r"(-1), "r"(-1), "r"(n0), "r"(smem_u32(&B.x_full))
+              "l"(&tmap_x), "r"(cb * 64), "r"(-1), "r"(xr0), "r"(n0), "r"(smem_u32(&B.x_full))
               : "memory");
       } else {
         // the whole x tile in ONE tensor-map load: box {8 ch, Wp, H+1, imgs, C/8}
         // lands as [plane][image][row][col][8] (plane stride = x_alloc rows)
         mbar_arrive_expect_tx(&B.x_full, img_flat * 16 * planes * a.imgs);
-        tma_load_5d(s_x, &tmap_x, 0, -1, -1, n0, 0, &B.x_full);
+        tma_load_5d(s_x, &tmap_x, 0, -1, xr0, n0, 0, &B.x_full);
       }
       const uint8_t* chunks = a.wpack + a.se_bytes + (size_t)a.ranges * a.hdr_bytes;
       for (int j = 0; j < nch; ++j) {
@@ -559,7 +576,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           const int g = i / a.P_out, qp = i - g * a.P_out;
           const int im = qp / (a.Ho * a.Wo), rem = qp - im * (a.Ho * a.Wo);
           const int yo = rem / a.Wo, xo = rem - yo * a.Wo;
-          const int ys[3] = {2 * yo - 1 < 0 ? 1 : 2 * yo - 1, 2 * yo, 2 * yo + 1};
+          const int yg = yo + band * a.Ho;  // image output row; conv rows relative to the band's c0
+          const int ys[3] = {(2 * yg - 1 < 0 ? 1 : 2 * yg - 1) - c0, 2 * yg - c0, 2 * yg + 1 - c0};
           const int xs[3] = {2 * xo - 1 < 0 ? 1 : 2 * xo - 1, 2 * xo, 2 * xo + 1};
           float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -643,8 +661,15 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     named_bar(1, 256);
     if (tid == 0) WL_TRACE(8);
     if (tid == 0) bulk_wait0();
-    const float inv = 1.f / (float)(a.Ho * a.Wo);
-    if (FUSED) {  // ranges == 1: the squeeze-excite below reads the pool straight from shared memory
+    const float inv = 1.f / (float)(a.Ho_img * a.Wo);
+    if (FUSED && a.bands > 1) {
+      // row bands: each CTA pooled its band; the partial sums cross to the
+      // peer's (still unused) gate region over DSMEM; they are summed below,
+      // after the cluster barrier every thread of both CTAs passes
+      float* s_gt = reinterpret_cast<float*>(smem + a.s_gate);
+      const uint32_t peer = band ? 0u : 1u;
+      for (int i = tid; i < a.hid; i += 256) st_peer_f32(peer_smem(s_gt + i, peer), s_pool[i]);
+    } else if (FUSED) {  // ranges == 1: the squeeze-excite below reads the pool straight from shared memory
       float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;
       for (int i = tid; i < a.imgs * a.HR; i += 256) s_vec[i] = s_pool[i] * inv;
     } else {
@@ -660,6 +685,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   if (!FUSED) __threadfence();  // publish this CTA's pool slice before arriving
   tc_fence_before();
   __syncthreads();
+  if (FUSED && a.bands > 1) {
+    cluster_sync_all();  // both bands' partial pools delivered
+    float* s_gt = reinterpret_cast<float*>(smem + a.s_gate);
+    float* s_vec = s_gt + a.hid;
+    const float inv = 1.f / (float)(a.Ho_img * a.Wo);
+    for (int i = threadIdx.x; i < a.hid; i += blockDim.x) s_vec[i] = (s_pool[i] + s_gt[i]) * inv;
+    __syncthreads();
+  }
   const int a_tile = 128 * a.HCb * 2, a_stage = a.bulk ? a.a_stage_b : a.n_pt * a_tile;
   uint8_t* s_pa = smem + a.s_pa;
   uint8_t* s_pv = smem + a.s_pv;
@@ -1310,7 +1343,8 @@ static bool mb_plan_fail(int id, int line) {
   if (getenv("WL_MB_DEBUG")) fprintf(stderr, "mb plan: rejected at check %d (mbconv.cu:%d)\n", id, line);
   return false;
 }
-bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
+bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused, int bands = 1, int max_imgs = 2,
+                 bool pair = true, int hc_cap = 128) {
   memset(&P, 0, sizeof(P));
   MbFrontArgs& f = P.f;
   MbBackArgs& b = P.b;
@@ -1323,20 +1357,31 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   f.stride = d.stride;
   f.H = d.h;
   f.W = d.w;
-  f.imgs = (d.h * d.w <= 64 && d.n % 2 == 0) ? 2 : 1;
+  f.bands = bands;
+  f.H_img = d.h;
+  f.Ho_img = d.h / d.stride;
+  if (bands > 1) {  // two row bands of Ob output rows: stride 1 convs Ob rows, stride 2 2*Ob+1 (blur halo)
+    if (bands != 2 || !want_fused || f.Ho_img % 2) return mb_plan_fail(14, __LINE__);
+    const int Ob = f.Ho_img / 2;
+    f.H = d.stride == 1 ? Ob : 2 * Ob + 1;
+  }
+  f.imgs = (bands == 1 && max_imgs > 1 && d.h * d.w <= 64 && d.n % 2 == 0) ? 2 : 1;
   f.Wp = d.w + 1;  // stacked images must start 128-byte aligned (TMA)
   while (f.imgs > 1 && ((d.h + 1) * f.Wp) % 8) ++f.Wp;
-  f.Ho = d.h / d.stride;
+  f.Ho = bands > 1 ? f.Ho_img / 2 : d.h / d.stride;
   f.Wo = d.w / d.stride;
-  f.total_rows = f.imgs * (f.H + 1) + 1;
-  const int x_valid = f.imgs * (f.H + 1) * f.Wp;
+  // whole images: [top halo + H rows] per image, one zero row below the stack;
+  // bands: the band's H rows between two loaded halo rows (real image rows or
+  // TMA zero fill at the image border)
+  f.total_rows = bands > 1 ? f.H + 2 : f.imgs * (f.H + 1) + 1;
+  const int x_valid = bands > 1 ? (f.H + 2) * f.Wp : f.imgs * (f.H + 1) * f.Wp;
   f.n_et = (x_valid + 127) / 128;
   f.x_alloc = x_valid;  // plane stride = the loaded rows (one TMA box); tile overrun reads are masked
   f.conv_base = f.Wp + 1;
   const int conv_end = (f.total_rows - 1) * f.Wp;
   f.n_ct = (conv_end - f.conv_base + 127) / 128;
   f.flat_h1 = align_up(f.conv_base + f.n_ct * 128 + f.Wp + 2, 8);
-  f.groups = d.n / f.imgs;
+  f.groups = d.n / f.imgs * bands;  // CTAs per range
   f.P_out = f.imgs * f.Ho * f.Wo;
   f.P_full = f.imgs * f.H * f.W;
   f.st_stores = (f.P_out + 255) / 256;
@@ -1346,7 +1391,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   if (f.sq < 1 || f.sq > 128) return mb_plan_fail(3, __LINE__);
   // fused mode: the CTA owns every hidden channel of its images, or - when the
   // image groups would leave over half the SMs idle - a cluster pair splits them
-  f.ranges = (want_fused && 2 * f.groups <= kNumSMs && hid % 128 == 0 && K % 64 == 0 && K <= 256) ? 2 : 1;
+  f.ranges = (want_fused && pair && bands == 1 && 2 * f.groups <= kNumSMs && hid % 128 == 0 && K % 64 == 0 && K <= 256) ? 2 : 1;
   while (!want_fused && f.groups * f.ranges < kNumSMs && hid % (f.ranges * 2 * 16) == 0) f.ranges *= 2;
   f.HR = hid / f.ranges;
   f.HC = 0;
@@ -1358,7 +1403,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   // planner experiments: WL_MB_FORCE="xt,eb,cb,hc" pins the TMEM / chunk choice
   int force[4] = {-1, -1, -1, -1};
   if (const char* e = getenv("WL_MB_FORCE")) sscanf(e, "%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3]);
-  for (int hc = 128; hc >= 16; hc -= 16) {
+  for (int hc = hc_cap; hc >= 16; hc -= 16) {
     if (f.HR % hc || (force[3] > 0 && hc != force[3])) continue;
     const int tiles1 = f.T8 ? f.n_et + f.n_ct : f.n_et;
     if (tiles1 * hc > 512) continue;
@@ -1367,11 +1412,8 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
     const int full = f.stride == 2 ? f.P_full * hc * 2 : 0;
     const int hdr = align_up(f.HR * 4, 16) * 2 + (f.T8 ? 0 : align_up(9 * f.HR * 4, 16));
     const int chunk = hc * C * 2 + (f.T8 ? (2 * (hc / 16) * 9 + 1) * 128 : 0);
-    int sqp = 8;
-    while (sqp < f.sq) sqp *= 2;
-    const int gate = (2 * f.imgs * hid + 22 * f.imgs * sqp) * 4;  // SE gates + squeeze-excite scratch
     const int total = x_bytes + h1_bytes + st + full + hdr + 2 * chunk + f.imgs * f.HR * 4 + 2048 +
-                      f.n_ct * 128 * 4 + f.n_et * 128 + gate;
+                      f.n_ct * 128 * 4 + f.n_et * 128;
     if (total <= kSmemMaxMb) {
       f.HC = hc;
       break;
@@ -1473,7 +1515,10 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   f.s_bar = o;
   o += 512;
   f.smem = o;
-  if (o > kSmemMaxMb) return mb_plan_fail(7, __LINE__);
+  if (o > kSmemMaxMb) {  // the chunk-width estimate above was optimistic: next narrower chunk
+    if (f.HC > 16) return mb_plan_try(d, P, want_fused, bands, max_imgs, pair, f.HC - 16);
+    return mb_plan_fail(7, __LINE__);
+  }
   P.front_bytes = f.se_bytes + (int64_t)f.ranges * f.hdr_bytes + (int64_t)f.ranges * f.nch * f.chunk_bytes;
   f.fused = 0;
   if (want_fused) {
@@ -1535,7 +1580,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   b.hid = hid;
   b.K = K;
   b.stride = d.stride;
-  b.P = d.n * f.Ho * f.Wo;
+  b.P = d.n * f.Ho_img * f.Wo;
   b.pix_per_img = f.Ho * f.Wo;
   b.residual = d.stride == 1;
   const int ntiles = (b.P + 127) / 128;
@@ -1563,14 +1608,17 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused) {
   b.tmem_cols = 32;
   while (b.tmem_cols < b.KR) b.tmem_cols *= 2;
   P.back_bytes = align_up(K * 4, 128) + (int64_t)b.kranges * b.nchb * b.vchunk_bytes;
-  P.h2_bytes = (int64_t)d.n * f.Ho * f.Wo * hid * 2;
+  P.h2_bytes = (int64_t)d.n * f.Ho_img * f.Wo * hid * 2;
   P.pool_bytes = (int64_t)d.n * hid * 4;
   P.gate_bytes = (int64_t)d.n * hid * 4;
   return true;
 }
 
 // one launch per block when the projection fits (fused); else front + back
-bool mb_plan(const wl_block_desc& d, MbPlanH& P) { return mb_plan_try(d, P, true) || mb_plan_try(d, P, false); }
+bool mb_plan(const wl_block_desc& d, MbPlanH& P) {
+  return mb_plan_try(d, P, true) || mb_plan_try(d, P, false) || mb_plan_try(d, P, true, 1, 1) ||
+         mb_plan_try(d, P, true, 1, 1, false) || mb_plan_try(d, P, true, 2);
+}
 
 using FrontK = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const MbFrontArgs);
 
@@ -1728,12 +1776,13 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     if (f.xsw) {
       const uint64_t dims[4] = {(uint64_t)d.c, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n};
       const uint64_t strides[3] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2};
-      const uint32_t box[4] = {64, (uint32_t)f.Wp, (uint32_t)(f.H + 1), (uint32_t)f.imgs};
+      const uint32_t box[4] = {64, (uint32_t)f.Wp, (uint32_t)(f.bands > 1 ? f.H + 2 : f.H + 1), (uint32_t)f.imgs};
       if (int e = encode_tmap(&tx, x, 4, dims, strides, box, true)) return e;
     } else {
       const uint64_t dims[5] = {8, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n, (uint64_t)(d.c / 8)};
       const uint64_t strides[4] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2, 16};
-      const uint32_t box[5] = {8, (uint32_t)f.Wp, (uint32_t)(f.H + 1), (uint32_t)f.imgs, (uint32_t)(d.c / 8)};
+      const uint32_t box[5] = {8, (uint32_t)f.Wp, (uint32_t)(f.bands > 1 ? f.H + 2 : f.H + 1), (uint32_t)f.imgs,
+                               (uint32_t)(d.c / 8)};
       if (int e = encode_tmap(&tx, x, 5, dims, strides, box)) return e;
     }
   }
@@ -1757,7 +1806,7 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
     if (int e = encode_tmap(&th_fused, h2, 2, dims, strides, box, true)) return e;
   }
   if (f.zst) {  // [pixels][K] rows of z and of the residual x, 64-channel 128B-swizzled boxes
-    const uint64_t dims[2] = {(uint64_t)d.k, (uint64_t)d.n * f.Ho * f.Wo};
+    const uint64_t dims[2] = {(uint64_t)d.k, (uint64_t)d.n * f.Ho_img * f.Wo};
     const uint64_t strides[1] = {(uint64_t)d.k * 2};
     const uint32_t box[2] = {64, (uint32_t)f.P_out};
     if (int e = encode_tmap(&th_store, z, 2, dims, strides, box, true)) return e;
@@ -1765,7 +1814,8 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
       if (int e = encode_tmap(&th_fused, x, 2, dims, strides, box, true)) return e;
   }
   if (int e = launch_pdl_cluster(front_kernel(d.act, f.T8 != 0, f.stride == 2, f.fused != 0), f.groups * f.ranges,
-                                 mbk::kThreads, f.smem, st, "mb_front launch", (f.fused && f.ranges == 2) ? 2 : 1, tx,
+                                 mbk::kThreads, f.smem, st, "mb_front launch",
+                                 (f.fused && (f.ranges == 2 || f.bands == 2)) ? 2 : 1, tx,
                                  th_store, th_fused, f))
     return e;
   if (f.fused) return WL_OK;

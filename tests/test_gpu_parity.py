@@ -86,6 +86,11 @@ CASES = [
     ("mbconv_c160", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 160), None),
     # ConvFirstNet-Pico at the reference's native 256: 8x8 stage, two images per CTA pair
     ("mbconv_8x8_c128", MBConv(8, 4, 0.25), TensorDims(4, 8, 8, 128), None),
+    # row bands: a cluster pair splits one image (whole tile exceeds shared memory)
+    ("mbconv_s2_28_c96_bands", MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 96), 256),
+    ("mbconv_s2_32_c64_bands", MBConv(8, 4, 0.25, 2), TensorDims(2, 32, 32, 64), 160),
+    ("mbconv_16_c256_bands", MBConv(8, 4, 0.25), TensorDims(2, 16, 16, 256), None),
+    ("mbconv_8x8_c256_one_image", MBConv(8, 4, 0.25), TensorDims(2, 8, 8, 256), None),
     # ConvFirstNet-Small s3b0: FFN weights streamed through a chunk ring
     ("convfirst_s2_64_96_streamed", ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 64), 96),
 ]
@@ -121,7 +126,8 @@ def test_deterministic_and_graph_equals_eager():
 
 
 @pytest.mark.parametrize("model,res", [("convfirstnet-pico", 224), ("convfirstnet-nano", 224),
-                                       ("convfirstnet-tiny", 224), ("convfirstnet-pico", 256)])
+                                       ("convfirstnet-tiny", 224), ("convfirstnet-small", 224),
+                                       ("convfirstnet-pico", 256), ("convfirstnet-nano", 256)])
 def test_network_per_unit_and_logits(model, res):
     net = zoo.at_resolution(zoo.from_name(model), res)
     m = FusedNetwork(net, batch=2, seed=11)
@@ -160,11 +166,9 @@ def test_full_size_pico_b128_sampled_images():
 
 
 def test_unsupported_configs_fail_loudly():
-    # ConvFirstNet-Small's 28x28x96 stride-2 MBConv: the whole-image tile does
-    # not fit shared memory -> refused, never approximated
-    net = zoo.at_resolution(zoo.from_name("convfirstnet-small"), 224)
+    # a 56x56x256 MBConv: even a row band's tile exceeds shared memory -> refused, never approximated
     with pytest.raises(ScheduleError):
-        FusedNetwork(net, batch=2, seed=11)
+        FusedBlock(MBConv(8, 4, 0.25), TensorDims(2, 56, 56, 256))
     with pytest.raises(ScheduleError):
         FusedBlock(ConvFirst(4, 6), TensorDims(1, 8, 8, 16))  # no T=4 kernel
     with pytest.raises(ScheduleError):  # LayerNorm statistics cannot absorb zero padding

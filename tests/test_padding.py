@@ -53,11 +53,13 @@ def test_layernorm_blocks_refuse_padding():
         device_binding(build_schedule(ConvNeXtBlock(7, 4, "gelu"), TensorDims(1, 8, 8, 24)))
 
 
-@pytest.mark.parametrize("model", ["convfirstnet-pico", "convfirstnet-nano", "convfirstnet-tiny"])
-def test_zoo_models_plan_at_b128(model):
-    """Every unit of the model has a launch plan at the BASELINE batch."""
+@pytest.mark.parametrize("res", [224, 256])
+@pytest.mark.parametrize("model", ["convfirstnet-pico", "convfirstnet-nano", "convfirstnet-tiny", "convfirstnet-small"])
+def test_zoo_models_plan_at_b128(model, res):
+    """Every unit of every zoo model has a launch plan at the BASELINE batch,
+    at 224 and at the reference's native 256 (zoo.py:10)."""
     L = _lib.lib()
-    net = zoo.at_resolution(zoo.from_name(model), 224)
+    net = zoo.at_resolution(zoo.from_name(model), res)
     for inst in plan_blocks(net):
         b = device_binding(build_schedule(inst.block, inst.dims(128), out_channels=inst.out_channels))
         assert L.wl_validate(ctypes.byref(b.desc)) == 0, (inst.label, _lib.last_error())
