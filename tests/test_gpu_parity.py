@@ -127,7 +127,8 @@ def test_deterministic_and_graph_equals_eager():
 
 @pytest.mark.parametrize("model,res", [("convfirstnet-pico", 224), ("convfirstnet-nano", 224),
                                        ("convfirstnet-tiny", 224), ("convfirstnet-small", 224),
-                                       ("convfirstnet-pico", 256), ("convfirstnet-nano", 256)])
+                                       ("convfirstnet-pico", 256), ("convfirstnet-nano", 256),
+                                       ("convfirstnet-tiny", 256), ("convfirstnet-small", 256)])
 def test_network_per_unit_and_logits(model, res):
     net = zoo.at_resolution(zoo.from_name(model), res)
     m = FusedNetwork(net, batch=2, seed=11)
