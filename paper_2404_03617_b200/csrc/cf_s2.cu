@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
 // =================================================================== host
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include "launch.h"
 
 namespace wl {
@@ -556,8 +557,10 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   // row, subject to TMEM (512 columns) and shared memory
   double best = 1e30;
   Cf2Args bestA{};
+  const char* force_r = getenv("WL_CF2_R");  // planner experiments: pin the band height
   for (int R = 1; R <= 8; ++R) {
     if (R > a.Ho) break;
+    if (force_r ? R != atoi(force_r) : R > 1 && R * a.W > 256) continue;  // measured: wider bands lengthen each band's chain
     for (int rr = 16; rr <= 256 && rr <= a.hid; rr += 16) {
       if (a.hid % rr) continue;
       for (int xbufs = 2; xbufs >= 1; --xbufs)

@@ -19,6 +19,7 @@ namespace wl {
 
 struct HeadArgs {
   int C, E, M, HW, imgs, P, NE, nce;
+  int xsw;  // C % 64 == 0: x rows staged as 128-byte swizzled 64-channel blocks (one TMA row per pixel)
   int s_a, s_w, s_st, s_bar, tmem_cols, w1_chunk, o_b1;
   const uint8_t* w1;  // [b1 fp32 E (padded to 128 B)][chunks: NE x C core layout]
   __half* feat;       // (n, E) pooled embedding
@@ -49,18 +50,28 @@ __global__ void __launch_bounds__(256, 1) head_pool_kernel(const __grid_constant
   const uint32_t tmem = *tbase;
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar[0], 128 * a.C * 2 + a.w1_chunk);
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(s_a)),
-        "l"(&tmap_x), "r"(0), "r"(p0), "r"(0), "r"(smem_u32(&bar[0]))
-        : "memory");
+    if (a.xsw) {
+      for (int cb = 0; cb < a.C / 64; ++cb)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(smem_u32(s_a + cb * 16384)),
+            "l"(&tmap_x), "r"(cb * 64), "r"(p0), "r"(smem_u32(&bar[0]))
+            : "memory");
+    } else {
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(smem_u32(s_a)),
+          "l"(&tmap_x), "r"(0), "r"(p0), "r"(0), "r"(smem_u32(&bar[0]))
+          : "memory");
+    }
     const uint8_t* chunk = a.w1 + align_up(a.E * 4, 128) + (size_t)j * a.w1_chunk;
     bulk_g2s(s_w, chunk, a.w1_chunk, &bar[0]);
     mbar_wait(&bar[0], 0);
     tc_fence_after();
     const uint32_t idesc = make_idesc_f16(128, a.NE);
     for (int kk = 0; kk < a.C / 16; ++kk) {
-      const uint64_t ad = make_sdesc(smem_u32(s_a) + kk * 2 * 2048, 2048, 128);
+      const uint64_t ad = a.xsw ? make_sdesc_sw128(smem_u32(s_a) + (kk / 4) * 16384) + (uint64_t)((kk % 4) * 2)
+                                : make_sdesc(smem_u32(s_a) + kk * 2 * 2048, 2048, 128);
       const uint64_t bd = make_sdesc(smem_u32(s_w) + kk * 2 * (a.NE * 16), a.NE * 16, 128);
       mma_ss(tmem, ad, bd, idesc, kk > 0);
     }
@@ -117,7 +128,7 @@ struct FcArgs {
 __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__ CUtensorMap tmap_f,
                                                          const __grid_constant__ FcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* s_a = smem + a.s_a;  // stages x [8][128][8] (K chunk 64)
+  uint8_t* s_a = smem + a.s_a;  // stages x [128 rows][64 features], 128B-swizzled (K chunk 64)
   uint8_t* s_w = smem + a.s_w;  // stages x NC x 64
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // full[4], empty[4], mma
   uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 2 * a.stages + 1);
@@ -141,10 +152,11 @@ __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__
       const int b = k % S;
       if (k >= S) mbar_wait(&bar[S + b], ((k / S) - 1) & 1);
       mbar_arrive_expect_tx(&bar[b], 128 * 64 * 2 + a.w_chunk);
+      // 64 features x 128 rows as 128-byte swizzled rows (one TMA row per batch row)
       asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-          "%4}], [%5];" ::"r"(smem_u32(s_a + b * 16384)),
-          "l"(&tmap_f), "r"(0), "r"(row0), "r"(k * 8), "r"(smem_u32(&bar[b]))
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+          "[%4];" ::"r"(smem_u32(s_a + b * 16384)),
+          "l"(&tmap_f), "r"(k * 64), "r"(row0), "r"(smem_u32(&bar[b]))
           : "memory");
       bulk_g2s(s_w + b * a.w_chunk, wchunks + (size_t)k * a.w_chunk, a.w_chunk, &bar[b]);
     };
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__
       mbar_wait(&bar[b], (k / S) & 1);
       tc_fence_after();
       for (int s = 0; s < 4; ++s) {
-        const uint64_t ad = make_sdesc(smem_u32(s_a + b * 16384) + s * 2 * 2048, 2048, 128);
+        const uint64_t ad = make_sdesc_sw128(smem_u32(s_a + b * 16384)) + (uint64_t)(s * 2);
         const uint64_t bd = make_sdesc(smem_u32(s_w + b * a.w_chunk) + s * 2 * (a.NC * 16), a.NC * 16, 128);
         mma_ss(tmem, ad, bd, idesc, (k > 0 || s > 0));
       }
@@ -212,6 +224,7 @@ bool head_plan(const wl_block_desc& d, HeadPlan& P) {
   h.HW = d.h * d.w;
   if (h.C % 16 || h.E % 64 || h.HW > 128 || h.C > 512) return false;
   h.imgs = std::max(1, 128 / h.HW);
+  h.xsw = h.C % 64 == 0;
   h.P = d.n * h.HW;
   h.NE = h.E % 128 == 0 ? 128 : 64;  // 96 KB per CTA: two CTAs per SM
   h.nce = h.E / h.NE;
@@ -316,16 +329,23 @@ int head_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void
   uint8_t* feat = reinterpret_cast<uint8_t*>(ws) + kWsHeader;
   CUtensorMap tx, tf;
   {
-    const uint64_t dims[3] = {8, (uint64_t)h.P, (uint64_t)(h.C / 8)};
-    const uint64_t strides[2] = {(uint64_t)h.C * 2, 16};
-    const uint32_t box[3] = {8, 128, (uint32_t)(h.C / 8)};
-    if (int e = encode_tmap(&tx, x, 3, dims, strides, box)) return e;
+    if (h.xsw) {
+      const uint64_t dims[2] = {(uint64_t)h.C, (uint64_t)h.P};
+      const uint64_t strides[1] = {(uint64_t)h.C * 2};
+      const uint32_t box[2] = {64, 128};
+      if (int e = encode_tmap(&tx, x, 2, dims, strides, box, true)) return e;
+    } else {
+      const uint64_t dims[3] = {8, (uint64_t)h.P, (uint64_t)(h.C / 8)};
+      const uint64_t strides[2] = {(uint64_t)h.C * 2, 16};
+      const uint32_t box[3] = {8, 128, (uint32_t)(h.C / 8)};
+      if (int e = encode_tmap(&tx, x, 3, dims, strides, box)) return e;
+    }
   }
   {
-    const uint64_t dims[3] = {8, (uint64_t)d.n, (uint64_t)(h.E / 8)};
-    const uint64_t strides[2] = {(uint64_t)h.E * 2, 16};
-    const uint32_t box[3] = {8, 128, 8};
-    if (int e = encode_tmap(&tf, feat, 3, dims, strides, box)) return e;
+    const uint64_t dims[2] = {(uint64_t)h.E, (uint64_t)d.n};
+    const uint64_t strides[1] = {(uint64_t)h.E * 2};
+    const uint32_t box[2] = {64, 128};
+    if (int e = encode_tmap(&tf, feat, 2, dims, strides, box, true)) return e;
   }
   h.w1 = reinterpret_cast<const uint8_t*>(p);
   h.feat = reinterpret_cast<__half*>(feat);

@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           }
         }
       }
+      if (tid == 0 && j < 20) WL_TRACE(160 + j);
     }
     named_bar(1, 256);
     if (tid == 0) WL_TRACE(8);
