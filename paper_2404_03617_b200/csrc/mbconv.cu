@@ -1354,7 +1354,9 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused, int bands 
   f.C = C;
   f.hid = hid;
   f.sq = d.se_sq;
-  f.T8 = d.group_width == 8;
+  // depthwise (T=1) convs run on the same tensor-core path as T=8: each 8x8
+  // block of the block-diagonal B is itself diagonal (exact, zeros elsewhere)
+  f.T8 = d.group_width == 8 || (d.group_width == 1 && !getenv("WL_MB_DW_CUDA"));
   f.stride = d.stride;
   f.H = d.h;
   f.W = d.w;
@@ -1737,7 +1739,8 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
               for (int nn = 0; nn < 8; ++nn)
                 for (int kk = 0; kk < 8; ++kk) {
                   const int oc = hb + 16 * pr + 8 * half + nn;
-                  put_h(blk, nn * 16 + kk * 2, wconv[((size_t)oc * 9 + t) * T + kk]);
+                  const float wv = T == 8 ? wconv[((size_t)oc * 9 + t) * T + kk] : (kk == nn ? wconv[(size_t)oc * 9 + t] : 0.f);
+                  put_h(blk, nn * 16 + kk * 2, wv);
                 }
             }
           }

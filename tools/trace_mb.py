@@ -7,7 +7,8 @@ from paper_2404_03617_b200.core import MBConv, TensorDims
 from paper_2404_03617_b200.blocks import FusedBlock
 cases = {"mb14": (MBConv(8, 4, 0.25), TensorDims(128, 14, 14, 128), None),
          "mb7": (MBConv(8, 4, 0.25), TensorDims(128, 7, 7, 128), None),
-         "mbs2": (MBConv(8, 4, 0.25, 2), TensorDims(128, 28, 28, 48), 128)}
+         "mbs2": (MBConv(8, 4, 0.25, 2), TensorDims(128, 28, 28, 48), 128),
+         "c2": (MBConv(1, 4, 0.25), TensorDims(128, 28, 28, 80), None)}
 for nm in sys.argv[1:]:
     blk, dims, k = cases[nm]
     m = FusedBlock(blk, dims, k)
