@@ -636,6 +636,26 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
               s0 += f0.x;
               s1 += f0.y;
             }
+          } else if (a.imgs == 1) {
+            // one image split over st_stores row blocks [k][G8][st_rows][8]:
+            // walk each block's contiguous rows (no per-pixel division)
+            for (int k = 0; k < a.st_stores; ++k) {
+              const uint8_t* base = s_st + ((size_t)(k * G8 + g) * a.st_rows) * 16 + w * 4;
+              int r = i;
+              for (; r + 8 < a.st_rows; r += 16) {
+                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + r * 16));
+                const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(base + (r + 8) * 16));
+                s0 += f0.x;
+                s1 += f0.y;
+                s2 += f1.x;
+                s3 += f1.y;
+              }
+              if (r < a.st_rows) {
+                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + r * 16));
+                s0 += f0.x;
+                s1 += f0.y;
+              }
+            }
           } else {
             for (; pp < pe; pp += 8) {
               const uint32_t hv = *reinterpret_cast<const uint32_t*>(s_st + st_off(pp, g, a.st_rows, G8) + w * 4);
