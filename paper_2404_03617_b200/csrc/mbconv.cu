@@ -149,6 +149,53 @@ __device__ __forceinline__ int st_off(int p, int g, int st_rows, int groups8) {
     if (a.trace && blockIdx.x == 0) a.trace[(slot)] = clock64();        \
   } while (0)
 
+// SE pool of one chunk when a single image's h2 staging spans several store
+// blocks [k][G8][st_rows][8]: warps take (channel group, block) pairs and walk
+// contiguous rows; the per-block partials meet in the (idle until the squeeze)
+// pool-vector scratch in a fixed order. Out of line: the common single-block
+// path keeps its register allocation.
+__device__ __noinline__ void mb_pool_split_stores(const MbFrontArgs& a, uint8_t* smem, const uint8_t* s_st, float* s_pool,
+                                                   int j, int HC, int G8, int wi, int lane, int tid) {
+  float* scr = reinterpret_cast<float*>(smem + a.s_gate) + a.hid;
+  const int i = lane >> 2, w = lane & 3;
+  for (int pr = wi; pr < G8 * a.st_stores; pr += 8) {
+    const int g = pr % G8, k = pr / G8;
+    const uint8_t* base = s_st + ((size_t)(k * G8 + g) * a.st_rows) * 16 + w * 4;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int r = i;
+    for (; r + 8 < a.st_rows; r += 16) {
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + r * 16));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(base + (r + 8) * 16));
+      s0 += f0.x;
+      s1 += f0.y;
+      s2 += f1.x;
+      s3 += f1.y;
+    }
+    if (r < a.st_rows) {
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + r * 16));
+      s0 += f0.x;
+      s1 += f0.y;
+    }
+    s0 += s2;
+    s1 += s3;
+#pragma unroll
+    for (int m = 4; m < 32; m <<= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, m);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, m);
+    }
+    if (i == 0) {
+      scr[k * HC + g * 8 + w * 2] = s0;
+      scr[k * HC + g * 8 + w * 2 + 1] = s1;
+    }
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  for (int c = tid; c < HC; c += 256) {
+    float acc = 0.f;
+    for (int k = 0; k < a.st_stores; ++k) acc += scr[k * HC + c];
+    s_pool[j * HC + c] += acc;
+  }
+}
+
 // T8 / S2 / FUSED are compile-time so each instantiation carries only the
 // code its configuration executes (a smaller hot instruction footprint)
 template <int ACT, bool T8, bool S2, bool FUSED>
@@ -615,7 +662,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       // pool: deterministic column sums of the staged (fp16) h2 values.
       // warp wi sums channel groups g = wi, wi+8, ...; lane = (pixel offset i, word w)
       const int pix_img = a.Ho * a.Wo;
-      for (int g = wi; g < G8; g += 8) {
+      constexpr bool kSplitPool = !S2;  // stride-2 pools read the single-store blurred staging
+      if (kSplitPool && a.imgs == 1 && a.st_stores > 1 && a.st_stores * HC <= a.hid)
+        mb_pool_split_stores(a, smem, s_st, s_pool, j, HC, G8, wi, lane, tid);
+      for (int g = wi; g < G8 && !(kSplitPool && a.imgs == 1 && a.st_stores > 1 && a.st_stores * HC <= a.hid); g += 8) {
         const int i = lane >> 2, w = lane & 3;
         for (int im = 0; im < a.imgs; ++im) {
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -635,26 +685,6 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
               const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + pp * 16));
               s0 += f0.x;
               s1 += f0.y;
-            }
-          } else if (a.imgs == 1) {
-            // one image split over st_stores row blocks [k][G8][st_rows][8]:
-            // walk each block's contiguous rows (no per-pixel division)
-            for (int k = 0; k < a.st_stores; ++k) {
-              const uint8_t* base = s_st + ((size_t)(k * G8 + g) * a.st_rows) * 16 + w * 4;
-              int r = i;
-              for (; r + 8 < a.st_rows; r += 16) {
-                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + r * 16));
-                const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(base + (r + 8) * 16));
-                s0 += f0.x;
-                s1 += f0.y;
-                s2 += f1.x;
-                s3 += f1.y;
-              }
-              if (r < a.st_rows) {
-                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(base + r * 16));
-                s0 += f0.x;
-                s1 += f0.y;
-              }
             }
           } else {
             for (; pp < pe; pp += 8) {
