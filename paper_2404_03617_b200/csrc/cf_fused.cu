@@ -40,7 +40,7 @@ struct CfArgs {
 };
 
 namespace cfk {
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;  // warps 12-15: second hidden-epilogue group (odd 16-column blocks)
 constexpr int kProducerWarp = 0, kMmaWarp = 1, kAllocWarp = 2, kHWarp0 = 4, kTWarp0 = 8;
 
 struct Bars {
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       mbar_init(&B.xc_full[i], 128);
       mbar_init(&B.xc_empty[i], 1);
       mbar_init(&B.e_full[i], 1);
-      mbar_init(&B.h_full[i], 128);
+      mbar_init(&B.h_full[i], 256);
       mbar_init(&B.h_empty[i], 1);
     }
     mbar_init(&B.conv_full, NCI);
@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         if (ci == 0) CF_TRACE(u, 2);
       }
     }
-  } else if (warp >= kHWarp0 && warp < kHWarp0 + 4) {
+  } else if ((warp >= kHWarp0 && warp < kHWarp0 + 4) || warp >= 12) {
     // ---------------- hidden epilogue: E -> +a, phi -> fp16 -> TMEM H
-    const int q = warp - kHWarp0;
+    // (two warp groups per TMEM quadrant, alternating 16-column blocks)
+    const int q = warp % 4, hsub = warp >= 12 ? 1 : 0;
     const float* s_a = reinterpret_cast<const float*>(s_hdr + pl.o_a);
     mbar_wait(&B.hdr_full, 0);
     for (int it = 0; it < my_tiles; ++it) {
@@ -257,11 +258,11 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         const int g = it * nchunks + j, b = g & 1;
         mbar_wait(&B.e_full[b], (g >> 1) & 1);
         mbar_wait(&B.h_empty[b], ((g >> 1) & 1) ^ 1);
-        if (q == 0 && lane == 0 && j == 0) CF_TRACE(it, 6);
+        if (q == 0 && lane == 0 && j == 0 && !hsub) CF_TRACE(it, 6);
         tc_fence_after();
         const float* aj = s_a + j * r;
 #pragma unroll 1
-        for (int c0 = 0; c0 < r; c0 += 16) {
+        for (int c0 = hsub * 16; c0 < r; c0 += 32) {
           uint32_t v[16];
           WL_TMEM_LD16(tmem_lane_addr(tmem, q, pl.t_e + b * r + c0), v);
           tmem_ld_wait();
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&B.h_full[b]);
-        if (q == 0 && lane == 0 && j == nchunks - 1) CF_TRACE(it, 7);
+        if (q == 0 && lane == 0 && j == nchunks - 1 && !hsub) CF_TRACE(it, 7);
       }
     }
   } else if (warp >= kTWarp0 && warp < kTWarp0 + 4) {
