@@ -316,6 +316,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   if (FUSED) pdl_trigger();  // single-wave persistent grid: let the next kernel stage its prologue
   pdl_wait();
   const uint32_t tmem = B.tmem_base;
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // per-CTA span (global ns): start
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[512 + 2 * blockIdx.x] = (long long)gt;
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1226,6 +1231,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       tc_fence_before();
       __syncthreads();
     }
+  }
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // per-CTA span: end
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[512 + 2 * blockIdx.x + 1] = (long long)gt;
   }
   if (warp == 2) tmem_dealloc_n(tmem, a.tmem_cols);
 }

@@ -14,13 +14,21 @@ for nm in sys.argv[1:]:
     m = FusedBlock(blk, dims, k)
     x = torch.randn(dims.n, dims.h, dims.w, dims.c, device="cuda").half()
     out = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
-    buf = torch.zeros(256, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(512 + 2048, dtype=torch.int64, device="cuda")
     for _ in range(3): m.launch(x, out)
     _lib.lib().wl_debug_set_trace(buf.data_ptr())
     m.launch(x, out)
     torch.cuda.synchronize()
     _lib.lib().wl_debug_set_trace(None)
     t = buf.cpu().tolist()
+    spans = [(t[512 + 2 * b], t[512 + 2 * b + 1]) for b in range(1024) if t[512 + 2 * b]]
+    if spans:
+        s0 = min(a for a, _ in spans)
+        starts = sorted((a - s0) / 1e3 for a, _ in spans)
+        ends = sorted((b - s0) / 1e3 for _, b in spans)
+        durs = sorted((b - a) / 1e3 for a, b in spans)
+        print(nm, f"CTAs {len(spans)}: start spread {starts[0]:.1f}..{starts[-1]:.1f} us, end {ends[0]:.1f}..{ends[-1]:.1f} us, "
+              f"span min/med/max {durs[0]:.1f}/{durs[len(durs)//2]:.1f}/{durs[-1]:.1f} us")
     t0 = t[0]
     rel = lambda v: (v - t0) if v else -1
     print(nm, "plan sa/ring/h1b/eb", t[14], "cb/xt/HC/npt", t[15])
