@@ -621,31 +621,57 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mbar_arrive(&B.h1_empty[j % a.h1_bufs]);
       }
       named_bar(1, 256);
+      if (tid == 0 && j < 20) WL_TRACE(300 + j);
       if (S2) {
-        // BlurPool Triangle-3 x Triangle-3 / 16, stride 2, reflect pad (-1 -> 1)
-        const int nq = a.P_out * G8;
-        for (int i = tid; i < nq; i += 256) {
-          const int g = i / a.P_out, qp = i - g * a.P_out;
-          const int im = qp / (a.Ho * a.Wo), rem = qp - im * (a.Ho * a.Wo);
-          const int yo = rem / a.Wo, xo = rem - yo * a.Wo;
-          const int yg = yo + band * a.Ho;  // image output row; conv rows relative to the band's c0
-          const int ys[3] = {(2 * yg - 1 < 0 ? 1 : 2 * yg - 1) - c0, 2 * yg - c0, 2 * yg + 1 - c0};
-          const int xs[3] = {2 * xo - 1 < 0 ? 1 : 2 * xo - 1, 2 * xo, 2 * xo + 1};
-          float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        // BlurPool Triangle-3 x Triangle-3 / 16, stride 2, reflect pad (-1 -> 1),
+        // separable: a thread owns (image, channel group, output column, segment
+        // of kRB output rows) and slides down it, so each output row costs two
+        // horizontal row-blurs (6 loads) and the row above is reused
+        constexpr int kRB = 4;
+        const int nseg = (a.Ho + kRB - 1) / kRB;
+        const int nitems = a.imgs * G8 * a.Wo * nseg;
+        for (int it = tid; it < nitems; it += 256) {
+          int r = it;
+          const int xo = r % a.Wo;
+          r /= a.Wo;
+          const int g = r % G8;
+          r /= G8;
+          const int seg = r % nseg, im = r / nseg;
+          const int x0 = 2 * xo - 1 < 0 ? 1 : 2 * xo - 1;
+          const uint8_t* plane = s_full + ((size_t)g * a.P_full + (size_t)im * a.H * a.W + 2 * xo) * 16;
+          const int dxm = (x0 - 2 * xo) * 16;  // -16, or +16 at the reflected left edge
+          auto hrow = [&](int cr, float (&o)[8]) {  // horizontal [1 2 1]/4 of band conv row cr
+            const uint8_t* p0 = plane + (size_t)cr * a.W * 16;
+            float h0[8], h1[8], h2[8];
+            unpack8(*reinterpret_cast<const uint4*>(p0 + dxm), h0);
+            unpack8(*reinterpret_cast<const uint4*>(p0), h1);
+            unpack8(*reinterpret_cast<const uint4*>(p0 + 16), h2);
 #pragma unroll
-          for (int dy = 0; dy < 3; ++dy)
+            for (int k = 0; k < 8; ++k) o[k] = 0.25f * (h0[k] + h2[k]) + 0.5f * h1[k];
+          };
+          const int yo0 = seg * kRB, yo1 = min(yo0 + kRB, a.Ho);
+          float prev[8];
+          {
+            const int yg = yo0 + band * a.Ho;
+            hrow((2 * yg - 1 < 0 ? 1 : 2 * yg - 1) - c0, prev);
+          }
+          for (int yo = yo0; yo < yo1; ++yo) {
+            const int yg = yo + band * a.Ho;
+            float mid[8], nxt[8], acc[8];
+            hrow(2 * yg - c0, mid);
+            hrow(2 * yg + 1 - c0, nxt);
 #pragma unroll
-            for (int dx = 0; dx < 3; ++dx) {
-              float hv[8];
-              const int pf = (im * a.H + ys[dy]) * a.W + xs[dx];
-              unpack8(*reinterpret_cast<const uint4*>(s_full + (g * a.P_full + pf) * 16), hv);
-              const float w = (dy == 1 ? 0.5f : 0.25f) * (dx == 1 ? 0.5f : 0.25f);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) acc[k] += w * hv[k];
+            for (int k = 0; k < 8; ++k) {
+              acc[k] = 0.25f * (prev[k] + nxt[k]) + 0.5f * mid[k];
+              prev[k] = nxt[k];
             }
-          *reinterpret_cast<uint4*>(s_st + st_off(qp, g, a.st_rows, G8)) = pack8(acc);
+            const int qp = (im * a.Ho + yo) * a.Wo + xo;
+            const int off = a.st_stores == 1 ? (g * a.st_rows + qp) * 16 : st_off(qp, g, a.st_rows, G8);
+            *reinterpret_cast<uint4*>(s_st + off) = pack8(acc);
+          }
         }
         named_bar(1, 256);
+        if (tid == 0 && j < 20) WL_TRACE(320 + j);
       }
       // h2 chunk -> global (TMA store of the dense staging)
       fence_async_smem();

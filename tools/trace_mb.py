@@ -37,7 +37,7 @@ for nm in sys.argv[1:]:
     for j in range(12):
         row = t[16 + 8 * j: 16 + 8 * j + 7]
         if not any(row): break
-        print(f"  chunk {j}: wload@{rel(t[16 + 8 * j + 7])} xwait@{rel(t[232 + j])} expand@{rel(row[0])} conv@{rel(row[1])}..{rel(row[2])} Eepi {rel(row[3])}..{rel(row[4])} Cepi {rel(row[5])}..{rel(row[6])} pool@{rel(t[160 + j])}")
+        print(f"  chunk {j}: wload@{rel(t[16 + 8 * j + 7])} xwait@{rel(t[232 + j])} expand@{rel(row[0])} conv@{rel(row[1])}..{rel(row[2])} Eepi {rel(row[3])}..{rel(row[4])} Cepi {rel(row[5])}..{rel(row[6])} pool@{rel(t[160 + j])} drain_end@{rel(t[300 + j])} blur_end@{rel(t[320 + j])}")
     print("  proj: a_full", [rel(v) for v in t[112:120]])
     print("  proj: a_ready", [rel(v) for v in t[96:104]])
     print("  proj: v_full", [rel(v) for v in t[104:112]])
