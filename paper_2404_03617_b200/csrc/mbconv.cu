@@ -693,7 +693,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       // pool: deterministic column sums of the staged (fp16) h2 values.
       // warp wi sums channel groups g = wi, wi+8, ...; lane = (pixel offset i, word w)
       const int pix_img = a.Ho * a.Wo;
-      constexpr bool kSplitPool = !S2;  // stride-2 pools read the single-store blurred staging
+      // multi-block staging (P_out > 256) only arises in the two-launch plans of
+      // large stride-1 images; compiled out of the fused kernels so their
+      // register allocation is untouched
+      constexpr bool kSplitPool = !S2 && !FUSED;
       if (kSplitPool && a.imgs == 1 && a.st_stores > 1 && a.st_stores * HC <= a.hid)
         mb_pool_split_stores(a, smem, s_st, s_pool, j, HC, G8, wi, lane, tid);
       for (int g = wi; g < G8 && !(kSplitPool && a.imgs == 1 && a.st_stores > 1 && a.st_stores * HC <= a.hid); g += 8) {
