@@ -149,21 +149,24 @@ def test_network_per_unit_and_logits(model, res):
     close(out.float().cpu().numpy(), ref, max_rel=2e-2, l2_rel=1e-2)
 
 
-def test_full_size_pico_b128_sampled_images():
-    """BASELINE config 3 at full size: images 0 and 127 of the b128 forward
-    match the oracle unit by unit (the oracle runs on the two images)."""
-    net = zoo.at_resolution(zoo.from_name("convfirstnet-pico"), 224)
+@pytest.mark.parametrize("model,res", [("convfirstnet-pico", 224), ("convfirstnet-small", 224),
+                                       ("convfirstnet-tiny", 256)])
+def test_full_size_b128_sampled_images(model, res):
+    """BASELINE config 3 at full size (and the padded / row-band plans at the
+    same batch): images 0, 63 and 127 of the b128 forward match the oracle
+    unit by unit (the oracle runs on the three images)."""
+    net = zoo.at_resolution(zoo.from_name(model), res)
     m = FusedNetwork(net, batch=128, seed=5)
     m.x.normal_()
     m.replay()
     torch.cuda.synchronize()
-    pick = [0, 127]
+    pick = [0, 63, 127]
     src = m.x.float().cpu().numpy()[pick]
     for u, inst in zip(m.units, m.instances):
-        got = u.out.float().cpu().numpy()[pick]
+        got = u.module.binding.real_output(u.out.float().cpu().numpy()[pick])
         ref = oracle_unit(inst.block, u.module.weights, src)
         close(got, ref)
-        src = got.reshape(ref.shape)
+        src = np.ascontiguousarray(got).reshape(ref.shape)
 
 
 def test_unsupported_configs_fail_loudly():

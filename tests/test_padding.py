@@ -63,3 +63,17 @@ def test_zoo_models_plan_at_b128(model, res):
     for inst in plan_blocks(net):
         b = device_binding(build_schedule(inst.block, inst.dims(128), out_channels=inst.out_channels))
         assert L.wl_validate(ctypes.byref(b.desc)) == 0, (inst.label, _lib.last_error())
+
+
+@pytest.mark.parametrize("model", ["convfirstnet-pico", "convfirstnet-small"])
+def test_zoo_launch_plan_is_one_kernel_per_block(model):
+    """The model-level scheduler's promise (one fused launch per block, two
+    for the head) holds for the plans the library picks at b128."""
+    L = _lib.lib()
+    net = zoo.at_resolution(zoo.from_name(model), 224)
+    counts = {}
+    for inst in plan_blocks(net):
+        b = device_binding(build_schedule(inst.block, inst.dims(128), out_channels=inst.out_channels))
+        counts[inst.label] = L.wl_kernel_launches(ctypes.byref(b.desc))
+    assert counts.pop("head") == 2
+    assert set(counts.values()) == {1}, counts
