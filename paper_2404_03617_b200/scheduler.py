@@ -107,11 +107,15 @@ class FusedNetwork:
             self._slots = [self.x, torch.empty_like(self.x)]
             self._graphs = [self.graph or self.capture(), self._capture_on(self._slots[1])]
             self._copy = torch.cuda.Stream(device=self.device)
+            self._d2h = torch.cuda.Stream(device=self.device)
             self._h2d = [torch.cuda.Event(), torch.cuda.Event()]
             self._free = [torch.cuda.Event(), torch.cuda.Event()]
+            self._done = [torch.cuda.Event(), torch.cuda.Event()]
+            self._logits = [torch.empty_like(self.output), torch.empty_like(self.output)]
         comp = torch.cuda.current_stream(self.device)
         for b in range(2):
             self._free[b].record(comp)
+            self._done[b].record(comp)
         for i, (hb, ho) in enumerate(zip(batches, outs)):
             b = i & 1
             with torch.cuda.stream(self._copy):
@@ -119,9 +123,20 @@ class FusedNetwork:
                 self._slots[b].copy_(hb, non_blocking=True)
                 self._h2d[b].record(self._copy)
             comp.wait_event(self._h2d[b])
+            comp.wait_event(self._done[b])  # the slot's logits of batch i-2 have left the device
             self._graphs[b].replay()
             self._free[b].record(comp)
-            ho.copy_(self.output, non_blocking=True)
+            # logits to a per-slot buffer (on device), read back on a third
+            # stream so neither the next forward nor the next upload queues
+            # behind the PCIe transfer
+            self._logits[b].copy_(self.output, non_blocking=True)
+            fwd = torch.cuda.Event()
+            fwd.record(comp)
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(fwd)
+                ho.copy_(self._logits[b], non_blocking=True)
+                self._done[b].record(self._d2h)
+        comp.wait_stream(self._d2h)  # every read-back complete before the caller syncs
 
     def replay(self) -> None:
         if self.graph is None:
