@@ -560,7 +560,9 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   const char* force_r = getenv("WL_CF2_R");  // planner experiments: pin the band height
   for (int R = 1; R <= 8; ++R) {
     if (R > a.Ho) break;
-    if (force_r ? R != atoi(force_r) : R > 1 && R * a.W > 256) continue;  // measured: wider bands lengthen each band's chain
+    // measured: bands wider than 256 pixels lengthen each band's chain, and odd
+    // heights above 1 run 1.4-2x slower than their even neighbours (W = 56 and 112)
+    if (force_r ? R != atoi(force_r) : R > 1 && (R * a.W > 256 || R % 2)) continue;
     for (int rr = 16; rr <= 256 && rr <= a.hid; rr += 16) {
       if (a.hid % rr) continue;
       for (int xbufs = 2; xbufs >= 1; --xbufs)

@@ -15,6 +15,9 @@ CASES = {
     "cf28": (ConvFirst(8, 6), TensorDims(128, 28, 28, 48), None),
     "cfs2_112": (ConvFirst(8, 6, 2), TensorDims(128, 112, 112, 16), 32),
     "cfs2_56": (ConvFirst(8, 6, 2), TensorDims(128, 56, 56, 32), 48),
+    "nano_s2b0": (ConvFirst(8, 6, 2), TensorDims(128, 112, 112, 32), 48),
+    "nano_s3b0": (ConvFirst(8, 6, 2), TensorDims(128, 56, 56, 48), 64),
+    "small_s3b0": (ConvFirst(8, 6, 2), TensorDims(128, 56, 56, 64), 96),
     "stem": (Stem(16), TensorDims(128, 224, 224, 3), None),
     "head": (Head(), TensorDims(128, 7, 7, 128), None),
     "cnx": (ConvNeXtBlock(), TensorDims(8, 56, 56, 96), None),
