@@ -60,6 +60,7 @@ class FusedSchedule:
     tensors: tuple[TensorEntry, ...]
     output: str = "z"
     executable: bool = True
+    processors: int | None = None  # the reference's partitioned schedules (same values, machine.py:528-569, 649-660)
 
     def tensor(self, name: str) -> TensorEntry:
         for t in self.tensors:
@@ -183,6 +184,18 @@ def build_schedule(
         hid = getattr(block, "expansion", 1) * dims.c
         if not 1 <= chunk <= hid or hid % chunk:
             raise ValueError(f"chunk {chunk} does not divide {hid} hidden channels")
+    if processors is not None and scheme == ExecutionScheme.BLOCK_FUSION:
+        # the reference's partition rules; the B200 kernel computes the same
+        # values whatever the partition (its CTA split is planned on chip)
+        if isinstance(block, ConvFirst) and processors > 1:  # machine.py:469-474
+            if getattr(block, "stride", 1) == 2:
+                raise ValueError("the scaling variant models stride-1 blocks only")
+            if dims.c % processors or (dims.c // processors) % block.group_width or k != dims.c:
+                raise ValueError(f"cannot partition {dims.c} channels across {processors} processors")
+        if isinstance(block, MBConv):  # machine.py:655-657
+            hid = block.expansion * dims.c
+            if processors < 1 or hid % processors or (hid // processors) % block.group_width:
+                raise ValueError(f"cannot partition {hid} hidden channels across {processors} processors")
     return FusedSchedule(
         label=f"{block.kind}-{scheme.value}",
         scheme=scheme,
@@ -190,6 +203,7 @@ def build_schedule(
         dims=dims,
         out_channels=k,
         tensors=tensor_table(block, dims, k),
+        processors=processors,
     )
 
 

@@ -40,16 +40,26 @@ def main() -> None:
         ("mbconv_t8_a4_se25_14", MBConv(8, 4, 0.25, 1, "silu"), (1, 14, 14, 48), 7),
         ("mbconv_t8_a4_se25_c128_7", MBConv(8, 4, 0.25, 1, "silu"), (2, 7, 7, 128), 8),
         ("ffn_a4_relu", FFN(4, "relu"), (1, 8, 8, 16), 9),
+        # processors > 1: the channel-partitioned ConvFirst scaling schedule
+        # (machine.py:528-569) and the explicitly partitioned MBConv (machine.py:649-660)
+        ("convfirst_t8_a6_relu_scaling_p2", ConvFirst(8, 6, 1, "relu"), (1, 8, 8, 32), 10, 2),
+        ("convfirst_t8_a4_relu_scaling_p4", ConvFirst(8, 4, 1, "relu"), (2, 6, 6, 64), 11, 4),
+        ("mbconv_t8_a4_se25_p2", MBConv(8, 4, 0.25, 1, "silu"), (2, 7, 7, 32), 12, 2),
     ]
     index = {}
-    for name, block, dims, seed in cases:
+    for case in cases:
+        name, block, dims, seed = case[:4]
+        procs = case[4] if len(case) > 4 else None
         td = TensorDims(*dims)
         lw = build_schedule(block, td, ExecutionScheme.LAYER_WISE)
         bf = build_schedule(block, td, ExecutionScheme.BLOCK_FUSION)
         inputs = random_inputs(lw, np.random.default_rng(seed))
         inputs = {k: v.astype(np.float16).astype(np.float32) for k, v in inputs.items()}
         out_lw = execute_numeric(lw, inputs)
-        out_bf = execute_numeric(bf, inputs)
+        if procs:  # the partitioned schedule is the one evaluated as "fused"
+            out_bf = execute_numeric(build_schedule(block, td, ExecutionScheme.BLOCK_FUSION, processors=procs), inputs)
+        else:
+            out_bf = execute_numeric(bf, inputs)
         traffic = simulate_traffic(bf)
         meta = {
             "block": type(block).__name__,
@@ -60,6 +70,8 @@ def main() -> None:
             "macs": traffic.mac_ops,
             "fused_vs_layerwise_max_abs": float(np.max(np.abs(out_lw - out_bf))),
         }
+        if procs:
+            meta["processors"] = procs
         np.savez_compressed(
             os.path.join(HERE, f"{name}.npz"),
             out_layerwise=out_lw,

@@ -44,7 +44,8 @@ def test_golden_vectors(name):
     kinds = {"ConvFirst": ConvFirst, "MBConv": MBConv}
     if meta["block"] not in kinds:
         pytest.skip("FFN has no standalone kernel")
-    s = build_schedule(kinds[meta["block"]](**meta["params"]), TensorDims(*meta["dims"]))
+    s = build_schedule(kinds[meta["block"]](**meta["params"]), TensorDims(*meta["dims"]),
+                       processors=meta.get("processors"))
     close(execute_numeric(s, ins), out_lw)
 
 

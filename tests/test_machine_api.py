@@ -33,6 +33,16 @@ def test_build_schedule_errors_match_reference():
         build_schedule(ConvFirst(8, 6), TensorDims(1, 4, 4, 16), out_channels=32)
     with pytest.raises(ValueError):
         build_schedule(ConvFirst(8, 6), TensorDims(1, 4, 4, 16), chunk=7)
+    # partitioned schedules follow the reference's rules (machine.py:469-474, 655-657)
+    assert build_schedule(ConvFirst(8, 6), TensorDims(1, 4, 4, 32), processors=4).processors == 4
+    with pytest.raises(ValueError):
+        build_schedule(ConvFirst(8, 6), TensorDims(1, 4, 4, 32), processors=3)
+    with pytest.raises(ValueError):
+        build_schedule(ConvFirst(8, 6), TensorDims(1, 4, 4, 32), processors=8)  # 4 channels per part < T
+    with pytest.raises(ValueError):
+        build_schedule(ConvFirst(8, 6, 2), TensorDims(1, 4, 4, 32), out_channels=48, processors=2)
+    with pytest.raises(ValueError):
+        build_schedule(MBConv(8, 4, 0.25), TensorDims(1, 4, 4, 32), processors=5)
 
 
 def test_execute_numeric_input_checks():
