@@ -60,6 +60,16 @@ __device__ __forceinline__ uint4 bias_act8(const uint32_t* acc, const float* bia
   return q;
 }
 
+// one 16-byte shared-memory load (keeps the compiler from splitting a uint4
+// read through a generic pointer into four 4-byte LDS, each replayed 4x)
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
 __device__ __forceinline__ void unpack8(const uint4& q, float* f) {
   const __half2* h = reinterpret_cast<const __half2*>(&q);
 #pragma unroll

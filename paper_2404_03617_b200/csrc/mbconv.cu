@@ -1120,8 +1120,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bprj[c0 + i];
             if (a.residual) {
               float r[16];
-              unpack8(*p0, r);
-              unpack8(*p1, r + 8);
+              unpack8(lds128(p0), r);
+              unpack8(lds128(p1), r + 8);
 #pragma unroll
               for (int i = 0; i < 16; ++i) f[i] += r[i];
             }
