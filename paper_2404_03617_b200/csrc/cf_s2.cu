@@ -373,9 +373,8 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
           const int k0 = (yo0 + ro == 0) ? 2 : 2 * ro;  // xc rows of conv rows 2yo-1 (reflect -1 -> 1), 2yo, 2yo+1
           const __half* pl = plc + (size_t)x * 8;
           *reinterpret_cast<uint4*>(ahc + (size_t)p * 16) =
-              tri3(*reinterpret_cast<const uint4*>(pl + (size_t)k0 * W * 8),
-                   *reinterpret_cast<const uint4*>(pl + (size_t)(2 * ro + 1) * W * 8),
-                   *reinterpret_cast<const uint4*>(pl + (size_t)(2 * ro + 2) * W * 8));
+              tri3(lds128(pl + (size_t)k0 * W * 8), lds128(pl + (size_t)(2 * ro + 1) * W * 8),
+                   lds128(pl + (size_t)(2 * ro + 2) * W * 8));  // explicit 16-byte loads (no 4x split)
           x += 128;
           while (x >= W) {
             x -= W;
@@ -486,9 +485,8 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
           const int x0 = xo == 0 ? 1 : 2 * xo - 1;  // reflect column -1 -> 1
           const __half* rb = s_zs + (size_t)ro * W * KP + c8 * 8;
           *reinterpret_cast<uint4*>(s_zo + ((size_t)qi * K + c8 * 8)) =
-              tri3(*reinterpret_cast<const uint4*>(rb + (size_t)x0 * KP),
-                   *reinterpret_cast<const uint4*>(rb + (size_t)(2 * xo) * KP),
-                   *reinterpret_cast<const uint4*>(rb + (size_t)(2 * xo + 1) * KP));
+              tri3(lds128(rb + (size_t)x0 * KP), lds128(rb + (size_t)(2 * xo) * KP),
+                   lds128(rb + (size_t)(2 * xo + 1) * KP));
           c8 += sc;
           int dq = sq;
           if (c8 >= k8) {
