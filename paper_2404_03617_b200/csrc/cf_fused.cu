@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
           for (int dy = 0; dy < KS; ++dy) {
 #pragma unroll
             for (int dx = 0; dx < KS; ++dx) {
-              const uint4 qv = *reinterpret_cast<const uint4*>(hb + ((g * HH + tr + dy) * HWD + tc + dx) * 16);
+              const uint4 qv = lds128(hb + ((g * HH + tr + dy) * HWD + tc + dx) * 16);
               float hv[8];
               unpack8(qv, hv);
               const float4 w0 = *reinterpret_cast<const float4*>(s_w + (dy * KS + dx) * C + g * 8);
@@ -387,8 +387,8 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         WL_TMEM_LD16(tmem_lane_addr(tmem, q, pl.t_z + c0), v);
         tmem_ld_wait();
         float f[16], res[16];
-        unpack8(*reinterpret_cast<const uint4*>(hb + (((c0 / 8) * HH + tr + P) * HWD + tc + P) * 16), res);
-        unpack8(*reinterpret_cast<const uint4*>(hb + (((c0 / 8 + 1) * HH + tr + P) * HWD + tc + P) * 16), res + 8);
+        unpack8(lds128(hb + (((c0 / 8) * HH + tr + P) * HWD + tc + P) * 16), res);
+        unpack8(lds128(hb + (((c0 / 8 + 1) * HH + tr + P) * HWD + tc + P) * 16), res + 8);
 #pragma unroll
         for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + s_b[c0 + i] + res[i];
         if (inside) {

@@ -497,11 +497,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           if (a.xsw) {  // pixel row f of 64-channel block pg/4, 16-byte chunk c at (c ^ f%8)
             const uint8_t* row = s_x + ((size_t)(pg / 4) * a.n_et * 128 + f) * 128;
             const int c = (pg % 4) * 2;
-            lo = *reinterpret_cast<const uint4*>(row + ((c ^ (f & 7)) << 4));
-            hi = *reinterpret_cast<const uint4*>(row + (((c + 1) ^ (f & 7)) << 4));
+            lo = lds128(row + ((c ^ (f & 7)) << 4));
+            hi = lds128(row + (((c + 1) ^ (f & 7)) << 4));
           } else {
-            lo = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg) * a.x_alloc + f) * 16);
-            hi = *reinterpret_cast<const uint4*>(s_x + ((size_t)(2 * pg + 1) * a.x_alloc + f) * 16);
+            lo = lds128(s_x + ((size_t)(2 * pg) * a.x_alloc + f) * 16);
+            hi = lds128(s_x + ((size_t)(2 * pg + 1) * a.x_alloc + f) * 16);
           }
           const uint32_t r8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
           WL_TMEM_ST8(tmem_lane_addr(tmem, q, a.t_x + t * (a.C / 2) + pg * 8), r8);
@@ -591,8 +591,8 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
               for (int tap = 0; tap < 9; ++tap) {
                 const int ff = f + (tap / 3 - 1) * a.Wp + (tap % 3 - 1);
                 float hv[16];
-                unpack8(*reinterpret_cast<const uint4*>(h1c + ((size_t)(c0 / 8) * a.flat_h1 + ff) * 16), hv);
-                unpack8(*reinterpret_cast<const uint4*>(h1c + ((size_t)(c0 / 8 + 1) * a.flat_h1 + ff) * 16), hv + 8);
+                unpack8(lds128(h1c + ((size_t)(c0 / 8) * a.flat_h1 + ff) * 16), hv);
+                unpack8(lds128(h1c + ((size_t)(c0 / 8 + 1) * a.flat_h1 + ff) * 16), hv + 8);
                 const float* w = s_cw + tap * a.HR + j * HC + c0;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) fv[i] += hv[i] * w[i];
@@ -643,9 +643,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
           auto hrow = [&](int cr, float (&o)[8]) {  // horizontal [1 2 1]/4 of band conv row cr
             const uint8_t* p0 = plane + (size_t)cr * a.W * 16;
             float h0[8], h1[8], h2[8];
-            unpack8(*reinterpret_cast<const uint4*>(p0 + dxm), h0);
-            unpack8(*reinterpret_cast<const uint4*>(p0), h1);
-            unpack8(*reinterpret_cast<const uint4*>(p0 + 16), h2);
+            unpack8(lds128(p0 + dxm), h0);  // explicit 16-byte loads (no 4x split)
+            unpack8(lds128(p0), h1);
+            unpack8(lds128(p0 + 16), h2);
 #pragma unroll
             for (int k = 0; k < 8; ++k) o[k] = 0.25f * (h0[k] + h2[k]) + 0.5f * h1[k];
           };
