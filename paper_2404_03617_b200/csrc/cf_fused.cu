@@ -307,10 +307,11 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
           uint32_t v[16];
           WL_TMEM_LD16(tmem_lane_addr(tmem, q, pl.t_cacc + c0), v);
           tmem_ld_wait();
-          float f[16];
+          float f[16], bc16[16];
+          load16f(s_bconv + c0, bc16);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            f[i] = __uint_as_float(v[i]) + s_bconv[c0 + i];
+            f[i] = __uint_as_float(v[i]) + bc16[i];
             sum += f[i];
             sq += f[i] * f[i];
           }
@@ -389,8 +390,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
         float f[16], res[16];
         unpack8(lds128(hb + (((c0 / 8) * HH + tr + P) * HWD + tc + P) * 16), res);
         unpack8(lds128(hb + (((c0 / 8 + 1) * HH + tr + P) * HWD + tc + P) * 16), res + 8);
+        float b16[16];
+        load16f(s_b + c0, b16);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + s_b[c0 + i] + res[i];
+        for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + b16[i] + res[i];
         if (inside) {
           reinterpret_cast<uint4*>(zp + c0)[0] = pack8(f);
           reinterpret_cast<uint4*>(zp + c0)[1] = pack8(f + 8);

@@ -46,18 +46,34 @@ __device__ __forceinline__ __half2 act_h2(__half2 x) {
   return x;
 }
 // fp32 accumulators (+ fp32 bias) -> packed-half activation: 8 values -> uint4
+// (bias is 16-byte aligned: two vector loads instead of eight scalar ones —
+// each scalar load of a broadcast bias costs a shared-memory wavefront)
 template <int ACT>
 __device__ __forceinline__ uint4 bias_act8(const uint32_t* acc, const float* bias) {
   uint4 q;
   uint32_t* o = reinterpret_cast<uint32_t*>(&q);
+  const float4 b0 = *reinterpret_cast<const float4*>(bias), b1 = *reinterpret_cast<const float4*>(bias + 4);
+  const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    __half2 h = __floats2half2_rn(__uint_as_float(acc[2 * i]) + bias[2 * i],
-                                  __uint_as_float(acc[2 * i + 1]) + bias[2 * i + 1]);
+    __half2 h = __floats2half2_rn(__uint_as_float(acc[2 * i]) + bv[2 * i],
+                                  __uint_as_float(acc[2 * i + 1]) + bv[2 * i + 1]);
     h = act_h2<ACT>(h);
     o[i] = *reinterpret_cast<uint32_t*>(&h);
   }
   return q;
+}
+
+// 16 consecutive fp32 values (16-byte aligned) as four vector loads
+__device__ __forceinline__ void load16f(const float* p, float* out) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float4 v = reinterpret_cast<const float4*>(p)[k];
+    out[4 * k] = v.x;
+    out[4 * k + 1] = v.y;
+    out[4 * k + 2] = v.z;
+    out[4 * k + 3] = v.w;
+  }
 }
 
 // one 16-byte shared-memory load (keeps the compiler from splitting a uint4
