@@ -405,28 +405,14 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         for (int t = 0; t < a.n_eh; ++t) {
           const int p = t * 128 + q * 32 + lane;
           const uint32_t tcol = a.t_e + (es * a.n_eh + t) * r;
-          for (int c0 = hh * 32; c0 < r; c0 += 64) {
-            uint32_t v[2][16];
-            const bool two = c0 + 16 < r;
-            WL_TMEM_LD16(tmem_lane_addr(tmem, q, tcol + c0), v[0]);
-            if (two) WL_TMEM_LD16(tmem_lane_addr(tmem, q, tcol + c0 + 16), v[1]);
+          // 16-column blocks alternate between the two warps of a quadrant (both
+          // busy for any chunk width r >= 32); biases are two vector loads each
+          for (int c0 = hh * 16; c0 < r; c0 += 32) {
+            uint32_t v[16];
+            WL_TMEM_LD16(tmem_lane_addr(tmem, q, tcol + c0), v);
             tmem_ld_wait();
-#pragma unroll
-            for (int b = 0; b < 2; ++b) {
-              if (b == 1 && !two) break;
-              const int cc = c0 + 16 * b;
-              float bias[16];
-#pragma unroll
-              for (int k4 = 0; k4 < 4; ++k4) {
-                const float4 bb = *reinterpret_cast<const float4*>(avj + cc + 4 * k4);
-                bias[4 * k4] = bb.x;
-                bias[4 * k4 + 1] = bb.y;
-                bias[4 * k4 + 2] = bb.z;
-                bias[4 * k4 + 3] = bb.w;
-              }
-              *reinterpret_cast<uint4*>(aq + ((size_t)(cc / 8) * MH + p) * 16) = bias_act8<ACT>(v[b], bias);
-              *reinterpret_cast<uint4*>(aq + ((size_t)(cc / 8 + 1) * MH + p) * 16) = bias_act8<ACT>(v[b] + 8, bias + 8);
-            }
+            *reinterpret_cast<uint4*>(aq + ((size_t)(c0 / 8) * MH + p) * 16) = bias_act8<ACT>(v, avj + c0);
+            *reinterpret_cast<uint4*>(aq + ((size_t)(c0 / 8 + 1) * MH + p) * 16) = bias_act8<ACT>(v + 8, avj + c0 + 8);
           }
         }
         tc_fence_before();
@@ -463,9 +449,10 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
           for (int b = 0; b < 2; ++b) {
             if (b == 1 && !two) break;
             const int cc = c0 + 16 * b;
-            float fv[16];
+            float fv[16], b16[16];
+            load16f(bv + cc, b16);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + bv[cc + k];
+            for (int k = 0; k < 16; ++k) fv[k] = __uint_as_float(v[b][k]) + b16[k];
             *reinterpret_cast<uint4*>(s_zs + (size_t)p * KP + cc) = pack8(fv);
             *reinterpret_cast<uint4*>(s_zs + (size_t)p * KP + cc + 8) = pack8(fv + 8);
           }
