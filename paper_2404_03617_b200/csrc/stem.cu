@@ -99,9 +99,10 @@ __global__ void __launch_bounds__(256, 1) stem_kernel(const __grid_constant__ St
         WL_TMEM_LD16(tmem_lane_addr(tmem, q, (ab * a.R + t) * a.Np + c0), v);
         tmem_ld_wait();
         if (xo >= a.Wo || yo >= a.Ho) continue;
-        float f[16];
+        float f[16], b16[16];
+        load16f(bias + c0, b16);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) f[k] = act<ACT>(__uint_as_float(v[k]) + bias[c0 + k]);
+        for (int k = 0; k < 16; ++k) f[k] = act<ACT>(__uint_as_float(v[k]) + b16[k]);
         __half* zp = a.z + (((size_t)n * a.Ho + yo) * a.Wo + xo) * a.Cs + c0;
         for (int k = 0; k < 16 && c0 + k < a.Cs; k += 8) *reinterpret_cast<uint4*>(zp + k) = pack8(f + k);
       }
@@ -131,13 +132,21 @@ __global__ void __launch_bounds__(256, 1) stem_kernel(const __grid_constant__ St
           const int r = 2 * t + dy;
           if (r < ylo || r >= yhi) continue;
           const __half* rowp = reinterpret_cast<const __half*>(in + (size_t)r * row_bytes);
+          // the row's 9 halves (dx = -1..1 x 3 channels) start at half 6xo - 3: five
+          // aligned 32-bit words from half 6xo - 4 cover them (the words left of the
+          // image at xo = 0 are the zero padding) — 5 loads instead of 9
+          const int h0 = 6 * xo - 4;
+          float hv[10];
 #pragma unroll
-          for (int dx = 0; dx < 3; ++dx) {
-            const int xx = 2 * xo - 1 + dx;
-            if (xx < 0 || xx >= a.W) continue;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) f[(dy * 3 + dx) * 3 + c] = __half2float(rowp[xx * 3 + c]);
+          for (int k = 0; k < 5; ++k) {
+            uint32_t wv = 0u;
+            if (h0 + 2 * k >= 0) wv = *reinterpret_cast<const uint32_t*>(rowp + h0 + 2 * k);
+            const float2 t2 = __half22float2(*reinterpret_cast<const __half2*>(&wv));
+            hv[2 * k] = t2.x;
+            hv[2 * k + 1] = t2.y;
           }
+#pragma unroll
+          for (int k = 0; k < 9; ++k) f[dy * 9 + k] = hv[k + 1];
         }
       }
 #pragma unroll
