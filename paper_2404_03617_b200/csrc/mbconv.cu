@@ -1116,8 +1116,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             uint4* p0 = reinterpret_cast<uint4*>(rb + ((ch ^ (p & 7)) << 4));
             uint4* p1 = reinterpret_cast<uint4*>(rb + (((ch + 1) ^ (p & 7)) << 4));
             float f[16];
+            float pb16[16];
+            load16f(bprj + c0, pb16);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bprj[c0 + i];
+            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + pb16[i];
             if (a.residual) {
               float r[16];
               unpack8(lds128(p0), r);
@@ -1184,8 +1186,10 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             if (gi * 2 + b >= nblk || !inside) continue;
             const int c0 = hh * 16 + (gi * 2 + b) * 32;
             float f[16];
+            float pb16[16];
+            load16f(bprj + c0, pb16);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[b][i]) + bprj[c0 + i];
+            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[b][i]) + pb16[i];
             if (a.residual) {
               float r[16];
               unpack8(cur[2 * b], r);
@@ -1242,8 +1246,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
             if (!inside) continue;
             float f[16], r[16];
             const float* zr = s_zr + (size_t)(t * 128 + m) * RS + c0;
+            float pb16[16], zr16[16];
+            load16f(bprj + oc0 + c0, pb16);
+            load16f(zr, zr16);  // the peer's partial (rows padded to 16-byte multiples)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + zr[i] + bprj[oc0 + c0 + i];
+            for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + zr16[i] + pb16[i];
             if (a.residual) {
               const uint4* xp = reinterpret_cast<const uint4*>(a.x + gp * a.K + oc0 + c0);
               unpack8(__ldg(xp), r);
