@@ -831,6 +831,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     const __half* wsq = reinterpret_cast<const __half*>(seb + a.o_wsq);
     const float* bsq = reinterpret_cast<const float*>(seb + a.o_bsq);
     const __half* wexT = reinterpret_cast<const __half*>(seb + a.o_wex);
+    // w_ex^T rows hold their 16-byte blocks XOR-swizzled by (row >> 1): the
+    // excite's row-per-thread loads then hit 8 distinct bank groups per 8 lanes
+    auto wex_blk = [&](int h, int b8) -> uint4 {
+      return *reinterpret_cast<const uint4*>(wexT + (size_t)h * a.SQP + (b8 ^ ((h >> 1) & (a.SQP / 8 - 1))) * 8);
+    };
     const float* bex = reinterpret_cast<const float*>(seb + a.o_bex);
     float* s_vec = reinterpret_cast<float*>(smem + a.s_gate) + a.imgs * a.hid;  // [imgs][hid] pool
     float* s_red = s_vec + a.imgs * a.hid;                                       // [20 warps][imgs][SQP]
@@ -849,7 +854,7 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (JB <= 4 && tid < SEH)
 #pragma unroll
       for (int b8 = 0; b8 < 4; ++b8)
-        if (b8 < JB) wx[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)(seh0 + tid) * a.SQP + b8 * 8);
+        if (b8 < JB) wx[b8] = wex_blk(seh0 + tid, b8);
     if (!FUSED) {
       for (int i = tid; i < a.imgs * a.hid; i += nt) {
         const int im = i / a.hid;
@@ -936,11 +941,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       } else {
 #pragma unroll
         for (int b8 = 0; b8 < 8; ++b8)
-          if (b8 < JB) wq[b8] = *reinterpret_cast<const uint4*>(wexT + (size_t)hch * a.SQP + b8 * 8);
+          if (b8 < JB) wq[b8] = wex_blk(hch, b8);
       }
       for (int b8 = 0; b8 < JB; ++b8) {
         float wv[8];
-        unpack8(b8 < 8 ? wq[b8] : *reinterpret_cast<const uint4*>(wexT + (size_t)hch * a.SQP + b8 * 8), wv);
+        unpack8(b8 < 8 ? wq[b8] : wex_blk(hch, b8), wv);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           e0 += s_sq[b8 * 8 + k] * wv[k];
@@ -1802,7 +1807,9 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   for (int i = 0; i < hid; ++i)
     for (int j = 0; j < sq; ++j) {
       put_h(out + f.o_wsq, ((size_t)i * f.SQP + j) * 2, w[4][(size_t)i * sq + j]);   // w_sq (hid, sq)
-      put_h(out + f.o_wex, ((size_t)i * f.SQP + j) * 2, w[6][(size_t)j * hid + i]);  // w_ex (sq, hid)^T
+      // w_ex (sq, hid)^T, 16-byte blocks of row i XOR-swizzled by (i >> 1) (see the excite)
+      const int jp = ((j / 8) ^ ((i >> 1) & (f.SQP / 8 - 1))) * 8 + j % 8;
+      put_h(out + f.o_wex, ((size_t)i * f.SQP + jp) * 2, w[6][(size_t)j * hid + i]);
     }
   memcpy(out + f.o_bsq, w[5], sizeof(float) * sq);
   memcpy(out + f.o_bex, w[7], sizeof(float) * hid);
