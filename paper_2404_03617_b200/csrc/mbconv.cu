@@ -917,7 +917,17 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         s_sq[i] = v;
         st_peer_f32(peer_smem(s_sqx + i, peer), v);
       }
+      if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // per-CTA: partial squeeze ready
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        a.trace[2560 + 2 * blockIdx.x] = (long long)gt;
+      }
       cluster_sync_all();
+      if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // per-CTA: pair met
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        a.trace[2560 + 2 * blockIdx.x + 1] = (long long)gt;
+      }
       for (int i = tid; i < a.imgs * a.SQP; i += nt) s_sq[i] = fmaxf(s_sq[i] + s_sqx[i] + bsq[i % a.SQP], 0.f);
     } else {
       for (int i = tid; i < a.imgs * a.SQP; i += nt) {

@@ -14,7 +14,7 @@ for nm in sys.argv[1:]:
     m = FusedBlock(blk, dims, k)
     x = torch.randn(dims.n, dims.h, dims.w, dims.c, device="cuda").half()
     out = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
-    buf = torch.zeros(512 + 2048, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(512 + 2048 + 2048, dtype=torch.int64, device="cuda")
     for _ in range(3): m.launch(x, out)
     _lib.lib().wl_debug_set_trace(buf.data_ptr())
     m.launch(x, out)
@@ -27,6 +27,10 @@ for nm in sys.argv[1:]:
         starts = sorted((a - s0) / 1e3 for a, _ in spans)
         ends = sorted((b - s0) / 1e3 for _, b in spans)
         durs = sorted((b - a) / 1e3 for a, b in spans)
+        waits = [(t[2561 + 2 * b] - t[2560 + 2 * b]) / 1e3 for b in range(1024) if t[2560 + 2 * b]]
+        if waits:
+            w = sorted(waits)
+            print(nm, f"pair squeeze barrier wait min/med/max {w[0]:.2f}/{w[len(w)//2]:.2f}/{w[-1]:.2f} us over {len(w)} CTAs")
         print(nm, f"CTAs {len(spans)}: start spread {starts[0]:.1f}..{starts[-1]:.1f} us, end {ends[0]:.1f}..{ends[-1]:.1f} us, "
               f"span min/med/max {durs[0]:.1f}/{durs[len(durs)//2]:.1f}/{durs[-1]:.1f} us")
     t0 = t[0]
