@@ -4,11 +4,14 @@ efficiency = 2 MACs B / t / R_peak).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--model NAME] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU, NCCL only for the barrier and
-the max-over-ranks of the step time): every rank processes an independent
-128-image shard (weak scaling; no collective on the data path).
-``--impl reference`` times the CPU oracle port of the reference algorithm on
-the host cores (rank 0 only) on a bounded sample of the same workload.
+N > 1 runs one process per GPU (under torchrun; ``bench.py --gpus N`` without
+a launcher re-executes itself through torch.distributed.run). NCCL carries only
+the barrier and the max-over-ranks of the step time: every rank processes an
+independent 128-image shard (weak scaling; no collective on the data path).
+``--impl reference`` times the reference's CPU path on every host core (rank 0
+only; oracle/reference_net.py): the unmodified reference execute_numeric
+(baseline/_ref) for the stride-1 units, the oracle port for the units the
+reference cannot execute, one image per core per step.
 """
 
 from __future__ import annotations
@@ -46,51 +49,38 @@ def _net(name: str):
 # --------------------------------------------------------------- CPU arm
 
 
-def cpu_sample(model: str, images: int = 1, seed: int = 0):
-    """Time the CPU oracle (numpy restatement of the reference path) on
-    ``images`` images of the workload. Returns (seconds, images, threads)."""
-    import numpy as np
+def cpu_pool(model: str):
+    """The reference's CPU path on every host core (oracle/reference_net.py):
+    stride-1 units through the unmodified reference execute_numeric
+    (baseline/_ref), stem / stride-2 / head through the oracle port."""
+    from oracle.reference_net import ReferencePool
 
-    from oracle import model as om
-    from paper_2404_03617_b200.blocks import init_weights
-    from paper_2404_03617_b200.core import plan_blocks
-    from paper_2404_03617_b200.machine import build_schedule
+    return ReferencePool(model)
 
-    net = _net(model)
-    units = plan_blocks(net)
-    weights = {}
-    for i, u in enumerate(units):
-        s = build_schedule(u.block, u.dims(images), out_channels=u.out_channels)
-        weights[u.label] = init_weights(s, np.random.default_rng(seed + i))
-    x = np.random.default_rng(seed).standard_normal((images, 224, 224, 3)).astype(np.float16).astype(np.float32)
-    threads = 1
-    try:
-        from threadpoolctl import threadpool_info
 
-        threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
-    except Exception:
-        pass
-    t0 = time.perf_counter()
-    om.network_forward(units, weights, x)
-    return time.perf_counter() - t0, images, threads
+def cpu_describe(pool, steps: int, t: float) -> dict:
+    return {"value": pool.workers * steps / t, "unit": "images/s", "cores": pool.workers, "kind": pool.kind,
+            "sample": (f"{steps} x {pool.workers} images ({pool.workers} single-threaded worker processes, one "
+                       f"image each per step; nproc={os.cpu_count()}): the 24 stride-1 units of the network through "
+                       f"the unmodified reference waterline.machine.execute_numeric (LAYER_WISE, baseline/_ref), "
+                       f"stem / stride-2 units / head through the oracle port; {t:.1f} s")}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    times = []
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_sample(args.model, 1)
-    threads = 1
-    for _ in range(args.steps):
-        t, imgs, threads = cpu_sample(args.model, 1)
-        times.append(t / imgs)
-    per_img = statistics.mean(times)
+    pool = cpu_pool(args.model)
+    for _ in range(min(args.warmup, 1)):
+        pool.step()
+    times = [pool.step() for _ in range(args.steps)]
+    pool.close()
+    total = sum(times)
     from paper_2404_03617_b200 import complexity
 
     macs = complexity.network_macs(_net(args.model))
-    v = 1.0 / per_img
+    v = pool.workers * args.steps / total
+    cpu = cpu_describe(pool, args.steps, total)
     line = {
         "impl": "reference",
         "metric": f"images/sec ({args.model}@224 inference)",
@@ -99,17 +89,17 @@ def run_reference(args):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": per_img * 1e3,
+        "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "fp32 storage / fp64 accumulate (reference tensor-machine numerics)",
         "data": "synthetic (fan-in scaled random-init weights, N(0,1) images)",
-        "config": {"workload": f"{args.model}@224 forward, 1 image per step (bounded CPU sample of the b128 batch)",
-                   "model": args.model, "global_batch": 1, "parallelism": "cpu"},
+        "config": {"workload": f"{args.model}@224 forward, {pool.workers} images per step (bounded CPU sample of "
+                               f"the b128 batch, one image per host core)",
+                   "model": args.model, "global_batch": pool.workers, "parallelism": f"cpu x{pool.workers}"},
         "efficiency": {"macs_per_image": macs, "gflops": 2 * macs * v / 1e9},
-        "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": "1 image per step through the numpy oracle (oracle/model.py)"},
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -288,10 +278,10 @@ def run_gpu(args):
             pass
         cpu = None
         if not args.skip_cpu:
-            t_cpu, imgs, threads = cpu_sample(args.model, 1)
-            cpu = {"value": imgs / t_cpu, "unit": "images/s", "cores": threads, "kind": "port",
-                   "sample": f"{imgs} image through the numpy oracle of the same network (oracle/model.py), "
-                             f"{t_cpu:.1f} s"}
+            pool = cpu_pool(args.model)
+            steps = 2
+            cpu = cpu_describe(pool, steps, sum(pool.step() for _ in range(steps)))
+            pool.close()
         line = {
             "metric": f"images/sec ({args.model}@224 inference)",
             "value": value,
@@ -351,6 +341,20 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def _relaunch_distributed(n: int) -> int:
+    """``bench.py --gpus N`` without a launcher: re-exec under torchrun with
+    one process per GPU (the driver's own form of the command)."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -363,6 +367,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(_relaunch_distributed(args.gpus))
+    if world and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -23,3 +23,15 @@ def golden_names(prefix=""):
 def load_costs():
     with open(os.path.join(GOLDEN, "costs.json")) as fh:
         return json.load(fh)
+
+
+def big_golden_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "big", "*.npz")))
+
+
+def load_big_golden(name):
+    """A full-size BASELINE-config case: (meta, reference outputs of the picked
+    images). The inputs are regenerated from meta['seed'] with
+    machine.random_inputs (the reference's stream) and fp16-rounded."""
+    z = np.load(os.path.join(GOLDEN, "big", name + ".npz"))
+    return json.loads(str(z["meta"])), z["out_picked"]

@@ -1,4 +1,5 @@
 // blocks.cu — dispatch of the C ABI over block families.
+#include <mutex>
 #include "launch.h"
 
 namespace wl {
@@ -13,14 +14,21 @@ static const Family* family_of(const wl_block_desc& d) {
   return nullptr;
 }
 
+// kernel attributes (max dynamic shared memory) are per device context: run
+// the family init once per device ordinal, thread-safely
 int init_kernels() {
-  static int status = 1;
-  if (status == 1) {
-    status = WL_OK;
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static int status[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return set_error(WL_ECUDA, "no current CUDA device");
+  std::call_once(once[dev], [dev] {
+    status[dev] = WL_OK;
     for (const Family* f : {&kCfFamily, &kCf2Family, &kMbFamily, &kStemFamily, &kHeadFamily})
-      if (f->init && (status = f->init()) != WL_OK) break;
-  }
-  return status;
+      if (f->init && (status[dev] = f->init()) != WL_OK) break;
+  });
+  return status[dev];
 }
 
 int validate_desc(const wl_block_desc& d) {

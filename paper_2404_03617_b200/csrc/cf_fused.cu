@@ -292,7 +292,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
     auto conv_epi = [&](int u) {
       const int xb = u & 1;
       uint8_t* xcb = s_xc + xb * pl.xc_bytes;
-      float sum = 0.f, sq = 0.f;
+      // LayerNorm statistics on values shifted by the pixel's first channel
+      // (a sample of the same distribution): no E[x^2] - mean^2 cancellation
+      // for large-mean activations
+      float sum = 0.f, sq = 0.f, piv = 0.f;
       if constexpr (T8) {
         mbar_wait(&B.conv_full, u & 1);
         tc_fence_after();
@@ -309,11 +312,13 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
           tmem_ld_wait();
           float f[16], bc16[16];
           load16f(s_bconv + c0, bc16);
+          if (c0 == 0) piv = __uint_as_float(v[0]) + bc16[0];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             f[i] = __uint_as_float(v[i]) + bc16[i];
-            sum += f[i];
-            sq += f[i] * f[i];
+            const float dv = f[i] - piv;
+            sum += dv;
+            sq += dv * dv;
           }
           *reinterpret_cast<uint4*>(xcb + (c0 / 8) * 2048 + m * 16) = pack8(f);
           *reinterpret_cast<uint4*>(xcb + (c0 / 8 + 1) * 2048 + m * 16) = pack8(f + 8);
@@ -342,18 +347,21 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
               f[4] += hv[4] * w1.x; f[5] += hv[5] * w1.y; f[6] += hv[6] * w1.z; f[7] += hv[7] * w1.w;
             }
           }
+          if (g == 0) piv = f[0];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            sum += f[i];
-            sq += f[i] * f[i];
+            const float dv = f[i] - piv;
+            sum += dv;
+            sq += dv * dv;
           }
           *reinterpret_cast<uint4*>(xcb + g * 2048 + m * 16) = pack8(f);
         }
       }
       if (args.norm) {
         // LayerNorm over the C channels of this pixel (biased variance)
-        const float mean = sum * (1.f / C);
-        const float var = fmaxf(sq * (1.f / C) - mean * mean, 0.f);
+        const float dm = sum * (1.f / C);
+        const float mean = piv + dm;
+        const float var = fmaxf(sq * (1.f / C) - dm * dm, 0.f);
         const float rstd = rsqrtf(var + args.ln_eps);
 #pragma unroll 1
         for (int g = 0; g < G; ++g) {

@@ -542,7 +542,8 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   // row, subject to TMEM (512 columns) and shared memory
   double best = 1e30;
   Cf2Args bestA{};
-  const char* force_r = getenv("WL_CF2_R");  // planner experiments: pin the band height
+  // planner experiments: WL_CF2_R pins the band height (read once per process)
+  static const char* force_r = getenv("WL_CF2_R");
   for (int R = 1; R <= 8; ++R) {
     if (R > a.Ho) break;
     // measured: bands wider than 256 pixels lengthen each band's chain, and odd

@@ -1450,6 +1450,21 @@ struct MbPlanH {
   int64_t h2_bytes, pool_bytes, gate_bytes;
 };
 
+// planner debug knobs, read ONCE per process: the plan is recomputed by
+// validate / pack / workspace / forward and must not change between them
+static bool env_dw_cuda() {
+  static const bool v = getenv("WL_MB_DW_CUDA") != nullptr;
+  return v;
+}
+static const int* env_force() {  // WL_MB_FORCE="xt,eb,cb,hc" pins the TMEM / chunk choice
+  static int f[4] = {-1, -1, -1, -1};
+  static const bool once = [] {
+    if (const char* e = getenv("WL_MB_FORCE")) sscanf(e, "%d,%d,%d,%d", &f[0], &f[1], &f[2], &f[3]);
+    return true;
+  }();
+  (void)once;
+  return f;
+}
 // WL_MB_DEBUG=1 names the planner check that rejected a configuration
 static bool mb_plan_fail(int id, int line) {
   if (getenv("WL_MB_DEBUG")) fprintf(stderr, "mb plan: rejected at check %d (mbconv.cu:%d)\n", id, line);
@@ -1467,7 +1482,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused, int bands 
   f.sq = d.se_sq;
   // depthwise (T=1) convs run on the same tensor-core path as T=8: each 8x8
   // block of the block-diagonal B is itself diagonal (exact, zeros elsewhere)
-  f.T8 = d.group_width == 8 || (d.group_width == 1 && !getenv("WL_MB_DW_CUDA"));
+  f.T8 = d.group_width == 8 || (d.group_width == 1 && !env_dw_cuda());
   f.stride = d.stride;
   f.H = d.h;
   f.W = d.w;
@@ -1501,7 +1516,8 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused, int bands 
   f.st_stores = (f.P_out + 255) / 256;
   while (f.P_out % f.st_stores) ++f.st_stores;
   f.st_rows = f.P_out / f.st_stores;
-  if (f.groups > (int)(kCounterBytes / 4)) return mb_plan_fail(2, __LINE__);
+  // arrival counters exist only in the two-launch (unfused) form
+  if (!want_fused && f.groups > (int)(kCounterBytes / 4)) return mb_plan_fail(2, __LINE__);
   if (f.sq < 1 || f.sq > 128) return mb_plan_fail(3, __LINE__);
   // fused mode: the CTA owns every hidden channel of its images, or - when the
   // image groups would leave over half the SMs idle - a cluster pair splits them
@@ -1515,8 +1531,7 @@ bool mb_plan_try(const wl_block_desc& d, MbPlanH& P, bool want_fused, int bands 
                                (C % 64 == 0) ? C * 2 * f.n_et * 128 : 0);
   const int se_scratch = align_up((hid + 640 + f.sq) * 4, 16);
   // planner experiments: WL_MB_FORCE="xt,eb,cb,hc" pins the TMEM / chunk choice
-  int force[4] = {-1, -1, -1, -1};
-  if (const char* e = getenv("WL_MB_FORCE")) sscanf(e, "%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3]);
+  const int* force = env_force();
   for (int hc = hc_cap; hc >= 16; hc -= 16) {
     if (f.HR % hc || (force[3] > 0 && hc != force[3])) continue;
     const int tiles1 = f.T8 ? f.n_et + f.n_ct : f.n_et;

@@ -166,11 +166,13 @@ def build_schedule(
     chunk: int | None = None,
     processors: int | None = None,
 ) -> FusedSchedule:
-    """Same contract as machine.build_schedule (machine.py:736-772). On B200
-    both schemes execute the fused kernel (the layer-wise schedule is only an
-    accounting device there); ``chunk`` / ``processors`` are accepted for
-    signature compatibility — the launch plan picks hidden-chunk widths and
-    CTA partitions from the TMEM / shared-memory budget."""
+    """Same contract as machine.build_schedule (machine.py:736-772). Both
+    schemes build (their traffic is accounted by ``simulate_traffic``); only
+    BLOCK_FUSION schedules execute on the B200 — the layer-wise schedule is
+    the CPU oracle's. ``chunk`` / ``processors`` follow the reference's
+    validity rules; the fused kernel computes the same values whatever the
+    partition (its hidden-chunk widths and CTA split come from the TMEM /
+    shared-memory budget)."""
     if not isinstance(block, (FFN, ConvFirst, ConvNeXtBlock, MBConv, Stem, Head)):
         raise ValueError(f"{type(block).__name__} blocks have no tensor-machine schedule")
     k = out_channels if out_channels is not None else dims.c
@@ -184,6 +186,8 @@ def build_schedule(
         hid = getattr(block, "expansion", 1) * dims.c
         if not 1 <= chunk <= hid or hid % chunk:
             raise ValueError(f"chunk {chunk} does not divide {hid} hidden channels")
+    if not processors:  # the reference treats 0 / None as "default partition" (machine.py:655)
+        processors = None
     if processors is not None and scheme == ExecutionScheme.BLOCK_FUSION:
         # the reference's partition rules; the B200 kernel computes the same
         # values whatever the partition (its CTA split is planned on chip)
@@ -350,8 +354,9 @@ def execute_numeric(s: FusedSchedule, inputs: dict) -> np.ndarray:
     output; missing or mis-shaped inputs raise ScheduleError. Inputs are
     rounded to fp16 on the way in (the kernels' storage type), accumulation
     is fp32 in TMEM, and the result is the fp16 output widened to float32."""
-    if isinstance(s.block, FFN):
-        raise ScheduleError("FFN blocks have no standalone B200 kernel; use ConvFirst with the FFN weights")
+    if s.scheme != ExecutionScheme.BLOCK_FUSION:
+        raise ScheduleError("the B200 backend executes BLOCK_FUSION schedules; the layer-wise schedule is the "
+                            "CPU oracle's (machine.py:418-459, 593-646)")
     arrays = {}
     for t in s.tensors:
         if t.role not in ("input", "weights"):
@@ -416,3 +421,14 @@ def microbatch_plan(stage: StageSpec, dims: TensorDims, device: DeviceSpec, conv
             nmb = min(dims.n, budget // per_image)
             return MicrobatchPlan(True, int(nmb), depth, int(nmb) * per_image, depth * per_block, device.l2_bytes)
     return MicrobatchPlan(False, 0, 0, 0, per_block, device.l2_bytes)
+
+
+# the reference's accounting / FFN helpers (machine.py:228-252, 786-897)
+from .traffic import (  # noqa: E402,F401
+    TrafficReport,
+    dram_bytes_by_role,
+    ffn_fused,
+    ffn_layerwise,
+    simulate_traffic,
+    validate_schedule,
+)

@@ -46,9 +46,6 @@ class FusedNetwork:
         self.batch = batch
         self.device = torch.device(device)
         self.instances = plan_blocks(net)
-        h, w = net.input_resolution
-        c0 = self.instances[0].in_channels
-        self.x = torch.zeros((batch, h, w, c0), dtype=torch.float16, device=self.device)
         self.units: list[Unit] = []
         ws_bytes = 256
         for i, inst in enumerate(self.instances):
@@ -63,6 +60,10 @@ class FusedNetwork:
             ws_bytes = max(ws_bytes, mod.workspace.numel())
             out = torch.empty(mod.out_shape, dtype=torch.float16, device=self.device)
             self.units.append(Unit(inst.label, inst.block, mod, out))
+        # the static input carries the first unit's DEVICE width (a stem-less
+        # stack at C % 16 != 0 runs zero-padded); __call__ pads into it
+        self.x = torch.zeros(self.units[0].module.in_shape, dtype=torch.float16, device=self.device)
+        self.in_channels = self.instances[0].in_channels
         # one workspace shared by every unit (launches are stream-ordered)
         self.workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device)
         for u in self.units:
@@ -72,7 +73,14 @@ class FusedNetwork:
     # ----------------------------------------------------------- execution
     @property
     def output(self) -> torch.Tensor:
-        return self.units[-1].out
+        """The last unit's output at the reference channel count (a view)."""
+        return self.units[-1].module.binding.real_output(self.units[-1].out)
+
+    def _load_input(self, dst: torch.Tensor, src: torch.Tensor, non_blocking=True) -> None:
+        if src.shape[-1] == dst.shape[-1]:
+            dst.copy_(src, non_blocking=non_blocking)
+        else:  # reference width -> zero-padded device width (pad channels stay zero)
+            dst[..., : src.shape[-1]].copy_(src, non_blocking=non_blocking)
 
     def launch_all(self, stream=None, x: torch.Tensor | None = None) -> None:
         src = self.x if x is None else x
@@ -104,14 +112,15 @@ class FusedNetwork:
         forward of batch i runs, and each batch's logits are read back right
         behind its forward on the compute stream."""
         if not hasattr(self, "_slots"):
-            self._slots = [self.x, torch.empty_like(self.x)]
+            self._slots = [self.x, torch.zeros_like(self.x)]
             self._graphs = [self.graph or self.capture(), self._capture_on(self._slots[1])]
             self._copy = torch.cuda.Stream(device=self.device)
             self._d2h = torch.cuda.Stream(device=self.device)
             self._h2d = [torch.cuda.Event(), torch.cuda.Event()]
             self._free = [torch.cuda.Event(), torch.cuda.Event()]
             self._done = [torch.cuda.Event(), torch.cuda.Event()]
-            self._logits = [torch.empty_like(self.output), torch.empty_like(self.output)]
+            self._logits = [torch.empty(self.output.shape, dtype=self.output.dtype, device=self.device)
+                            for _ in range(2)]
         comp = torch.cuda.current_stream(self.device)
         for b in range(2):
             self._free[b].record(comp)
@@ -120,7 +129,7 @@ class FusedNetwork:
             b = i & 1
             with torch.cuda.stream(self._copy):
                 self._copy.wait_event(self._free[b])  # slot's previous forward has read it
-                self._slots[b].copy_(hb, non_blocking=True)
+                self._load_input(self._slots[b], hb)
                 self._h2d[b].record(self._copy)
             comp.wait_event(self._h2d[b])
             comp.wait_event(self._done[b])  # the slot's logits of batch i-2 have left the device
@@ -145,7 +154,7 @@ class FusedNetwork:
 
     def __call__(self, x: torch.Tensor) -> torch.Tensor:
         """Forward on an NHWC fp16 batch (copied into the static input)."""
-        self.x.copy_(x, non_blocking=True)
+        self._load_input(self.x, x)
         self.replay()
         return self.output
 

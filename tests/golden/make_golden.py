@@ -83,6 +83,45 @@ def main() -> None:
         print(name, dims, "max|out|=%.3g" % np.abs(out_lw).max(), "lw-vs-fused %.2g" % meta["fused_vs_layerwise_max_abs"])
     with open(os.path.join(HERE, "index.json"), "w") as fh:
         json.dump(index, fh, indent=1, sort_keys=True)
+    make_big(build_schedule, execute_numeric, random_inputs, ConvFirst, MBConv, TensorDims, ExecutionScheme)
+
+
+# BASELINE.json configs at full size: the whole batch's inputs come from the
+# reference's own random_inputs stream (seeded; our machine.random_inputs is
+# bit-identical, tests/test_machine_api.py), the unmodified reference
+# execute_numeric (LAYER_WISE) runs on the picked images only (images are
+# independent), and only those outputs are stored. The GPU test regenerates
+# the full batch from the seed, runs it at full batch and compares the picks.
+BIG_CASES = [
+    # config 1's closest reference form (3x3 depthwise ConvFirst, no LN) and the ConvFirstNet form
+    ("big_convfirst_t1_a4_56x56x96_b8", "ConvFirst", dict(group_width=1, expansion=4, stride=1, activation="relu"),
+     (8, 56, 56, 96), 21, [0, 7]),
+    ("big_convfirst_t8_a6_56x56x96_b8", "ConvFirst", dict(group_width=8, expansion=6, stride=1, activation="relu"),
+     (8, 56, 56, 96), 22, [0, 7]),
+    # config 2: MBConv(1, 4, .25) 28x28x80 at batch 128
+    ("big_mbconv_t1_a4_28x28x80_b128", "MBConv", dict(group_width=1, expansion=4, se_ratio=0.25, stride=1,
+                                                       activation="silu"), (128, 28, 28, 80), 23, [0, 63, 127]),
+    # the ConvFirstNet-Pico 14x14 MBConv at batch 128
+    ("big_mbconv_t8_a4_14x14x128_b128", "MBConv", dict(group_width=8, expansion=4, se_ratio=0.25, stride=1,
+                                                        activation="silu"), (128, 14, 14, 128), 24, [0, 63, 127]),
+]
+
+
+def make_big(build_schedule, execute_numeric, random_inputs, ConvFirst, MBConv, TensorDims, ExecutionScheme):
+    kinds = {"ConvFirst": ConvFirst, "MBConv": MBConv}
+    for name, kind, params, dims, seed, picks in BIG_CASES:
+        block = kinds[kind](**params)
+        lw = build_schedule(block, TensorDims(*dims), ExecutionScheme.LAYER_WISE)
+        ins = random_inputs(lw, np.random.default_rng(seed))
+        ins = {k: v.astype(np.float16).astype(np.float32) for k, v in ins.items()}
+        sub = dict(ins, x=ins["x"][picks])
+        lw_sub = build_schedule(block, TensorDims(len(picks), *dims[1:]), ExecutionScheme.LAYER_WISE)
+        out = execute_numeric(lw_sub, sub)
+        meta = {"block": kind, "params": params, "dims": list(dims), "seed": seed, "picks": picks,
+                "x_checksum": float(ins["x"].astype(np.float64).sum()),
+                "w_checksum": float(sum(v.astype(np.float64).sum() for k, v in ins.items() if k != "x"))}
+        np.savez_compressed(os.path.join(HERE, "big", f"{name}.npz"), out_picked=out, meta=json.dumps(meta))
+        print(name, dims, picks, "max|out|=%.3g" % np.abs(out).max())
 
 
 if __name__ == "__main__":

@@ -51,3 +51,21 @@ def test_gloo_sharding_and_max_over_ranks():
 def test_shard_range_edges():
     assert shard_range(128, 8, 7) == (112, 128)
     assert [shard_range(10, 3, r) for r in range(3)] == [(0, 4), (4, 7), (7, 10)]
+
+
+def test_bench_gpus_flag_relaunches_one_process_per_rank():
+    """``bench.py --gpus 2`` without a launcher re-executes itself under
+    torch.distributed.run (2 ranks); the reference arm runs on rank 0 only
+    and prints exactly one JSON line."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WL_REF_WORKERS="2")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+    assert lines[0]["cpu_baseline"]["kind"] == "reference" and lines[0]["cpu_baseline"]["cores"] == 2
