@@ -1,0 +1,732 @@
+// mb_s1.cu — stride-1 MBConv + squeeze-excite with the grouped conv on the
+// warp-level tensor path (core.py:112-122; fused schedule machine.py:649-733,
+// layer-wise numerics machine.py:593-646). One CTA per image, one launch.
+//
+// Why two tensor paths: a tcgen05.mma costs max(~44, N/2) cycles per K=16
+// step (profiles/r01_probe_mma_align.txt), so the T=8 grouped conv — N = 8
+// output channels per group — can only reach it block-diagonally at 1/11 of
+// the dense rate. The paper's own shape, mma.sync m16n8k{8,16} (K = 8 = T, no
+// waste), runs on sm_100a at 1015 MAC/cycle/SM for k16 and overlaps with
+// tcgen05 issued by another warp (profiles/r02_probe_hmma.txt). So:
+//   tcgen05 (one issuing thread)   : expand  E_j = x . W_exp[:, j]   (SS, TMEM)
+//                                    project Z  += h2_j' . W_prj[j]  (SS, TMEM)
+//   mma.sync (8 conv warps)        : h2_j = phi(conv3x3_T8(h1_j) + b_conv)
+//                                    from ldmatrix fragments of h1 in smem
+// Geometry: the image sits in a flat padded layout of row pitch 16 (W <= 14):
+// flat row m = 16 y + i holds pixel (y, i - 1); i = 0 and i > W are zero pads.
+// An m16 HMMA fragment is one padded image row, so the three input rows of a
+// 3x3 tap window slide down the image and every ldmatrix fragment is used by
+// three output rows. x arrives by one TMA box per 64 channels ({64, 16, H}
+// from x = -1: OOB columns zero-filled, 128B-swizzled = the tcgen05 A layout);
+// z leaves through the same map from x = 0 (the OOB pad columns are dropped).
+//
+// Phases per CTA (hidden chunks of 64 = 8 groups):
+//   A  producer: x, biases, W_exp ring     MMA: expand chunk j -> E[j%2]
+//      E warps (8): E + b_exp, phi -> h1[j%2] (padded image, per-group planes)
+//      conv warps (8, one group each): HMMA conv + b_conv, phi -> registers,
+//      SE pool in registers; h2_j stored (whole 128-byte lines per warp store)
+//      to the L2-resident workspace in the projection's A layout (the tensor
+//      machine's GLOBAL tier, machine.py:667-687)
+//   B  conv warps: squeeze-excite gates (pool -> W_sq, ReLU -> W_ex, sigmoid)
+//   C  producer reloads h2 + W_prj by half-chunks (4-slot ring over the dead
+//      h1 / W_exp buffers); conv warps gate them in place; MMA: Z += h2' . W_prj
+//   D  E warps: z = Z + b_prj + x (in place over the x tile) -> TMA store
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <cstring>
+#include "common.cuh"
+#include "plan.h"
+
+namespace wl {
+
+struct Mb1Args {
+  int n, H, W, C, hid, sq, nch, NT;
+  int s_x, s_h1, s_h1_bytes, s_w, s_wex, s_hdr, s_se, s_bar, smem;
+  int o_bexp, o_bconv, o_bprj, hdr_bytes;  // header (fp32) in the packed blob
+  int64_t o_se, o_frag, o_wexp, o_wprj;    // packed-blob sections
+  int o_bsq, o_wex, o_bex;                 // inside the SE section (fp16 matrices, fp32 biases)
+  int t_e, t_z, tmem_cols;
+  int slot_bytes;  // phase C ring slot: h2 half-chunk (NT x 8 KB) + W_prj half-chunk (C x 32 x 2)
+  const uint8_t* wpack;
+  uint8_t* h2;  // workspace: [n][nch][NT][8 groups][128 rows][16 B]
+  long long* trace;
+};
+
+namespace mb1 {
+constexpr int kWarps = 18;
+constexpr int kThreads = kWarps * 32;
+constexpr int kProd = 0, kMma = 1, kE0 = 2, kC0 = 10;
+constexpr int kHC = 64;  // hidden channels per chunk (8 groups of T = 8)
+struct Bars {
+  uint64_t x_full, hdr_full;
+  uint64_t w_full[2], w_empty[2];
+  uint64_t e_full[2], e_empty[2];
+  uint64_t h1_full[2], h1_empty[2];
+  uint64_t a_done;
+  uint64_t pa_full[4], pa_ready[4], pa_empty[4];
+  uint64_t z_full, se_full;
+  uint32_t tmem_base;
+};
+}  // namespace mb1
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+// D += A(16x16) B(16x8), fp16 operands, fp32 accumulators
+__device__ __forceinline__ void hmma16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void hmma8(float* d, uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+__device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const void* tmap, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_s1() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0_s1() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0_s1() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+#define MB1_TRACE(slot)                                                  \
+  do {                                                                   \
+    if (a.trace && blockIdx.x == 0) a.trace[(slot)] = clock64();         \
+  } while (0)
+
+// H: image rows (flat rows 16 H <= 128 NT); C: block channels (64 or 128)
+template <int H, int C, int ACT>
+__global__ void __launch_bounds__(mb1::kThreads, 1)
+    mb_s1_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_z,
+                 const __grid_constant__ Mb1Args a) {
+  using namespace mb1;
+  constexpr int NT = (16 * H + 127) / 128;  // M tiles of the flat image
+  constexpr int KH = C / 64;                 // 64-channel (128-byte) halves of x
+  constexpr int XH = NT * 128 * 128;         // bytes of one x half
+  constexpr int GS = ((H + 3) * 16 + 2) * 16;  // bytes of one h1 group plane (halo rows, margins, P overrun)
+  static_assert(16 * H <= 256 && (C == 64 || C == 128), "geometry");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* s_x = smem + a.s_x;
+  uint8_t* s_h1 = smem + a.s_h1;   // 2 buffers x 8 group planes; phase C ring overlays s_h1 .. s_w end
+  uint8_t* s_w = smem + a.s_w;     // W_exp ring, 2 x (64 x C fp16)
+  uint8_t* s_hdr = smem + a.s_hdr;
+  uint8_t* s_se = smem + a.s_se;   // pool f32[hid] | gates h2[hid/2] | scratch f32[256 + 32]
+  uint8_t* s_wex = smem + a.s_wex; // W_ex (sq x hid fp16), prefetched for the excite
+  Bars& B = *reinterpret_cast<Bars*>(smem + a.s_bar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int img = blockIdx.x;
+  const int nch = a.nch;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&B.x_full, 1);
+    mbar_init(&B.hdr_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.w_full[i], 1);
+      mbar_init(&B.w_empty[i], 1);
+      mbar_init(&B.e_full[i], 1);
+      mbar_init(&B.e_empty[i], 256);
+      mbar_init(&B.h1_full[i], 256);
+      mbar_init(&B.h1_empty[i], 256);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&B.pa_full[i], 1);
+      mbar_init(&B.pa_ready[i], 256);
+      mbar_init(&B.pa_empty[i], 1);
+    }
+    mbar_init(&B.a_done, 1);
+    mbar_init(&B.z_full, 1);
+    mbar_init(&B.se_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == kMma) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
+  // zero the h1 planes (halo rows / margins stay zero for phase A) and the pool
+  for (int i = threadIdx.x; i < (2 * 8 * GS) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < a.hid; i += kThreads) reinterpret_cast<float*>(s_se)[i] = 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
+  const uint32_t tmem = B.tmem_base;
+  MB1_TRACE(0);
+
+  if (warp == kProd) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      prefetch_tmap(&tmap_x);
+      mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
+      bulk_g2s(s_hdr, a.wpack, a.hdr_bytes, &B.hdr_full);
+      mbar_arrive_expect_tx(&B.x_full, KH * 64 * 2 * 16 * H);
+      for (int kh = 0; kh < KH; ++kh) tma_load_4d(s_x + kh * XH, &tmap_x, kh * 64, -1, 0, img, &B.x_full);
+      mbar_arrive_expect_tx(&B.se_full, a.sq * a.hid * 2);
+      bulk_g2s(s_wex, a.wpack + a.o_se + a.o_wex, a.sq * a.hid * 2, &B.se_full);
+      const uint32_t wbytes = kHC * C * 2;
+      for (int j = 0; j < nch; ++j) {
+        const int b = j & 1, u = j >> 1;
+        mbar_wait(&B.w_empty[b], (u & 1) ^ 1);
+        mbar_arrive_expect_tx(&B.w_full[b], wbytes);
+        bulk_g2s(s_w + b * wbytes, a.wpack + a.o_wexp + (size_t)j * wbytes, wbytes, &B.w_full[b]);
+      }
+      // phase C: h2 chunks come back once phase A stored them all and released
+      // the h1 / W_exp buffers the ring overlays
+      // ring of 4 half-chunks (32 hidden channels: NT x 8 KB of h2 + the
+      // matching 4 K-columns of W_prj), so several reloads are in flight
+      mbar_wait(&B.a_done, 0);
+      const uint32_t vbytes = C * 32 * 2;
+      const uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
+      for (int qq = 0; qq < 2 * nch; ++qq) {
+        const int s = qq & 3, u = qq >> 2, j = qq >> 1, half = qq & 1;
+        mbar_wait(&B.pa_empty[s], (u & 1) ^ 1);
+        uint8_t* slot = s_h1 + s * a.slot_bytes;
+        mbar_arrive_expect_tx(&B.pa_full[s], NT * 8192 + vbytes);
+        for (int t = 0; t < NT; ++t)
+          bulk_g2s(slot + t * 8192, h2img + ((size_t)j * NT + t) * 16384 + half * 8192, 8192, &B.pa_full[s]);
+        bulk_g2s(slot + NT * 8192, a.wpack + a.o_wprj + (size_t)j * 2 * vbytes + half * vbytes, vbytes,
+                 &B.pa_full[s]);
+      }
+    }
+  } else if (warp == kMma) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      const uint32_t idesc_e = make_idesc_f16(128, kHC);
+      const uint32_t idesc_z = make_idesc_f16(128, C);
+      const uint32_t wbytes = kHC * C * 2;
+      mbar_wait(&B.x_full, 0);
+      tc_fence_after();
+      MB1_TRACE(70);
+      for (int j = 0; j < nch; ++j) {
+        const int b = j & 1, u = j >> 1;
+        mbar_wait(&B.w_full[b], u & 1);
+        mbar_wait(&B.e_empty[b], (u & 1) ^ 1);
+        tc_fence_after();
+        MB1_TRACE(36 + j);
+        const uint32_t wb = smem_u32(s_w + b * wbytes);
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int k = 0; k < C / 16; ++k) {
+            const uint64_t ad = make_sdesc_sw128(smem_u32(s_x) + (k / 4) * XH + t * 16384 + (k % 4) * 32);
+            const uint64_t bd = make_sdesc(wb + k * 2 * 1024, 1024, 128);
+            mma_ss(tmem + a.t_e + (b * NT + t) * kHC, ad, bd, idesc_e, k > 0);
+          }
+        mma_commit(&B.e_full[b]);
+        mma_commit(&B.w_empty[b]);
+      }
+      for (int qq = 0; qq < 2 * nch; ++qq) {
+        const int s = qq & 3, u = qq >> 2;
+        mbar_wait(&B.pa_ready[s], u & 1);
+        tc_fence_after();
+        if (!(qq & 1)) MB1_TRACE(52 + (qq >> 1));
+        const uint32_t slot = smem_u32(s_h1 + s * a.slot_bytes);
+        const uint32_t vb = slot + NT * 8192;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const uint64_t ad = make_sdesc(slot + t * 8192 + k * 2 * 2048, 2048, 128);
+            const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
+            mma_ss(tmem + a.t_z + t * C, ad, bd, idesc_z, (qq > 0 || k > 0));
+          }
+        mma_commit(&B.pa_empty[s]);
+      }
+      mma_commit(&B.z_full);
+    }
+  } else if (warp < kC0) {
+    // ---------------------------------------------- E warps: expand epilogue
+    const int e = warp - kE0, q = warp & 3, hh = e >> 2;  // TMEM lane quadrant = warp % 4
+    const float* s_bexp = reinterpret_cast<const float*>(s_hdr + a.o_bexp);
+    mbar_wait(&B.hdr_full, 0);
+    for (int j = 0; j < nch; ++j) {
+      const int b = j & 1, u = j >> 1;
+      mbar_wait(&B.e_full[b], u & 1);
+      mbar_wait(&B.h1_empty[b], (u & 1) ^ 1);
+      tc_fence_after();
+      uint8_t* h1 = s_h1 + b * 8 * GS;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        uint32_t v[32];
+        const uint32_t ta = tmem_lane_addr(tmem, q, a.t_e + (b * NT + t) * kHC + hh * 32);
+        WL_TMEM_LD16(ta, v);
+        WL_TMEM_LD16(ta + 16, (v + 16));
+        tmem_ld_wait();
+        const int m = t * 128 + q * 32 + lane;
+        const int i = m & 15;
+        if (m < 16 * H) {
+          const bool real = i >= 1 && i <= a.W;
+          const float* bb = s_bexp + j * kHC + hh * 32;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint4 val = real ? bias_act8<ACT>(v + 8 * g, bb + 8 * g) : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(h1 + (hh * 4 + g) * GS + (m + 17) * 16) = val;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&B.e_empty[b]);
+      mbar_arrive(&B.h1_full[b]);
+      if (e == 0 && lane == 0) MB1_TRACE(4 + j);
+    }
+    // ------------------------------------------------ phase D: z epilogue
+    mbar_wait(&B.z_full, 0);
+    tc_fence_after();
+    if (e == 0 && lane == 0) MB1_TRACE(68);
+    const float* s_bprj = reinterpret_cast<const float*>(s_hdr + a.o_bprj);
+    if (hh < KH) {
+#pragma unroll 1
+      for (int t = 0; t < NT; ++t) {
+        const int m = t * 128 + q * 32 + lane;
+        uint8_t* xrow = s_x + hh * XH + m * 128;
+        uint32_t v[64];  // the row's 64 channels in one batch of TMEM loads
+        const uint32_t za = tmem_lane_addr(tmem, q, a.t_z + t * C + hh * 64);
+        WL_TMEM_LD16(za, v);
+        WL_TMEM_LD16(za + 16, (v + 16));
+        WL_TMEM_LD16(za + 32, (v + 32));
+        WL_TMEM_LD16(za + 48, (v + 48));
+        tmem_ld_wait();
+        if (m < 16 * H) {
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) {
+            uint8_t* p = xrow + ((c8 ^ (m & 7)) << 4);
+            float res[8];
+            unpack8(lds128(p), res);
+            const float4 b0 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8);
+            const float4 b1 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8 + 4);
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            float f[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) f[r] = __uint_as_float(v[c8 * 8 + r]) + bb[r] + res[r];
+            *reinterpret_cast<uint4*>(p) = pack8(f);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    fence_async_smem();
+    nbar(2, 256);
+    if (e == 0 && lane == 0) {
+      // a TMA store may not start at a negative coordinate (illegal instruction,
+      // tools/probe_tma_store.cu): start at x = 0 one 128-byte row into the tile
+      // (the 128B swizzle is address-based, so the shifted source stays valid)
+      for (int kh = 0; kh < KH; ++kh) tma_store_4d(&tmap_z, s_x + kh * XH + 128, kh * 64, 0, 0, img);
+      bulk_commit_s1();
+      bulk_wait_read0_s1();  // the tile must outlive the reads only; the writes complete on their own
+      MB1_TRACE(69);
+    }
+  } else {
+    // ------------------------------------------ conv warps: HMMA 3x3 T=8 conv
+    const int g = warp - kC0;  // group within the chunk
+    const int tid = threadIdx.x - kC0 * 32;
+    const int gid = lane >> 2, tq = lane & 3;
+    const int sq = a.sq, hid = a.hid;
+    const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
+    float* s_pool = reinterpret_cast<float*>(s_se);
+    const uint32_t* frag = reinterpret_cast<const uint32_t*>(a.wpack + a.o_frag);
+    const __half* wsq = reinterpret_cast<const __half*>(a.wpack + a.o_se);
+    // B fragments in pair order (t0,t1) (t3,t4) (t6,t7) (t2,t5) t8: each k16
+    // pair is two consecutive registers (mb1_pack)
+    uint32_t bw[9];
+#pragma unroll
+    for (int tp = 0; tp < 9; ++tp) bw[tp] = __ldg(frag + ((size_t)(0 * 8 + g) * 9 + tp) * 32 + lane);
+    mbar_wait(&B.hdr_full, 0);
+    const uint32_t lrow = (lane & 15), lsel = lane >> 4;  // ldmatrix: row of the fragment, which fragment
+    uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
+    const __half2 one2 = __float2half2_rn(1.f), zero2 = __float2half2_rn(0.f);
+    const __half2 m0 = (gid >= 1 && gid <= a.W) ? one2 : zero2, m1 = (gid + 8 <= a.W) ? one2 : zero2;
+    float s_acc = 0.f;  // squeeze partial of output lane (sq <= 32), summed over this warp's groups
+    for (int j = 0; j < nch; ++j) {
+      const int b = j & 1, u = j >> 1;
+      const float2 bc = *reinterpret_cast<const float2*>(s_bconv + j * kHC + g * 8 + tq * 2);
+      // W_sq rows of this warp's 8 channels, output = lane (consumed after the pool below)
+      __half wq[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) wq[c] = lane < sq ? wsq[(size_t)(j * kHC + g * 8 + c) * sq + lane] : __half(0.f);
+      mbar_wait(&B.h1_full[b], u & 1);
+      const uint32_t plane = smem_u32(s_h1 + b * 8 * GS + g * GS) + 16;  // + 1 margin row
+      // Q_r: x4 of padded row r at dx = -1 (lanes 0-15) and dx = 0 (lanes 16-31)
+      // P_r: x4 of dx = +1 at rows r (lanes 0-15) and r + 1 (lanes 16-31)
+      // so every HMMA A operand is one load's four consecutive registers
+      auto load_q = [&](int r, uint32_t* f) {
+        ldsm_x4(plane + (uint32_t)((r * 16 + (int)lsel - 1 + (int)lrow) * 16), f[0], f[1], f[2], f[3]);
+      };
+      auto load_p = [&](int r, uint32_t* f) {
+        ldsm_x4(plane + (uint32_t)((r * 16 + 16 * (int)lsel + 1 + (int)lrow) * 16), f[0], f[1], f[2], f[3]);
+      };
+      uint32_t Q0[4], Q1[4], Q2[4], Q3[4], P0[4], P1[4], P2[4], P3[4];
+      __half2 pool = zero2;
+      // h2 rows go straight to the L2-resident workspace in the projection's
+      // A layout [tile][group][row][16 B]: per warp store, 8 rows x 4 lanes x
+      // 4 B = two whole 128-byte lines
+      uint8_t* h2c = h2img + (size_t)j * NT * 16384 + g * 2048 + tq * 4;
+      auto epi = [&](int y, const float* c0, const float* c1) {
+        const __half2 h0 = __hmul2(act_h2<ACT>(__floats2half2_rn(c0[0] + c1[0], c0[1] + c1[1])), m0);
+        const __half2 h1v = __hmul2(act_h2<ACT>(__floats2half2_rn(c0[2] + c1[2], c0[3] + c1[3])), m1);
+        pool = __hadd2(pool, __hadd2(h0, h1v));
+        const int mm = y * 16 + gid;
+        *reinterpret_cast<__half2*>(h2c + (mm >> 7) * 16384 + ((mm & 127) >> 3) * 128 + (mm & 7) * 16) = h0;
+        const int m8 = mm + 8;
+        *reinterpret_cast<__half2*>(h2c + (m8 >> 7) * 16384 + ((m8 & 127) >> 3) * 128 + (m8 & 7) * 16) = h1v;
+      };
+      // output row y: Q_y.(t0,t1) + Q_{y+1}.(t3,t4) + Q_{y+2}.(t6,t7) + P_y.(t2,t5) + P_{y+2}[0:2].t8
+      load_q(0, Q0);
+      load_q(1, Q1);
+      load_p(0, P0);
+      load_p(1, P1);
+#pragma unroll
+      for (int y = 0; y + 1 < H; y += 2) {
+        load_q(y + 2, Q2);
+        load_p(y + 2, P2);
+        load_q(y + 3, Q3);
+        load_p(y + 3, P3);
+        float a0[4] = {bc.x, bc.y, bc.x, bc.y}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+        float b0[4] = {bc.x, bc.y, bc.x, bc.y}, b1[4] = {0.f, 0.f, 0.f, 0.f};
+        hmma16(a0, Q0[0], Q0[1], Q0[2], Q0[3], bw[0], bw[1]);
+        hmma16(b0, Q1[0], Q1[1], Q1[2], Q1[3], bw[0], bw[1]);
+        hmma16(a1, P0[0], P0[1], P0[2], P0[3], bw[6], bw[7]);
+        hmma16(b1, P1[0], P1[1], P1[2], P1[3], bw[6], bw[7]);
+        hmma16(a0, Q1[0], Q1[1], Q1[2], Q1[3], bw[2], bw[3]);
+        hmma16(b0, Q2[0], Q2[1], Q2[2], Q2[3], bw[2], bw[3]);
+        hmma16(a1, Q2[0], Q2[1], Q2[2], Q2[3], bw[4], bw[5]);
+        hmma16(b1, Q3[0], Q3[1], Q3[2], Q3[3], bw[4], bw[5]);
+        hmma8(a0, P2[0], P2[1], bw[8]);
+        hmma8(b0, P3[0], P3[1], bw[8]);
+        epi(y, a0, a1);
+        epi(y + 1, b0, b1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          Q0[k] = Q2[k];
+          Q1[k] = Q3[k];
+          P0[k] = P2[k];
+          P1[k] = P3[k];
+        }
+      }
+      if constexpr (H % 2) {
+        constexpr int y = H - 1;
+        load_q(y + 2, Q2);
+        load_p(y + 2, P2);
+        float a0[4] = {bc.x, bc.y, bc.x, bc.y}, a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+        hmma16(a0, Q0[0], Q0[1], Q0[2], Q0[3], bw[0], bw[1]);
+        hmma16(a1, P0[0], P0[1], P0[2], P0[3], bw[6], bw[7]);
+        hmma16(a2, Q1[0], Q1[1], Q1[2], Q1[3], bw[2], bw[3]);
+        hmma16(a0, Q2[0], Q2[1], Q2[2], Q2[3], bw[4], bw[5]);
+        hmma8(a1, P2[0], P2[1], bw[8]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a1[k] += a2[k];
+        epi(y, a0, a1);
+      }
+      mbar_arrive(&B.h1_empty[b]);  // every ldmatrix of this buffer has completed (results consumed)
+      if (j + 1 < nch) {  // next chunk's B fragments: in flight under the pool / squeeze work below
+#pragma unroll
+        for (int tp = 0; tp < 9; ++tp) bw[tp] = __ldg(frag + ((size_t)((j + 1) * 8 + g) * 9 + tp) * 32 + lane);
+      }
+      if (tid == 0) MB1_TRACE(20 + j);
+      // SE pool of the chunk (fp16 per lane over <= 2H rows, fp32 across lanes):
+      // reduce the 8 rows (gid) sharing a channel pair
+      const float2 pf = __half22float2(pool);
+      float p0 = pf.x, p1 = pf.y;
+#pragma unroll
+      for (int sh = 4; sh < 32; sh <<= 1) {
+        p0 += __shfl_xor_sync(0xffffffffu, p0, sh);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, sh);
+      }
+      // partial squeeze of this warp's 8 channels: lane = squeeze output
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float q0 = __shfl_sync(0xffffffffu, p0, c), q1 = __shfl_sync(0xffffffffu, p1, c);
+        s_acc += q0 * __half2float(wq[2 * c]) + q1 * __half2float(wq[2 * c + 1]);
+      }
+    }
+    // the producer reloads h2 through the async proxy: order every thread's
+    // generic-proxy stores before it
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    float* scr = reinterpret_cast<float*>(s_se + hid * 4 + hid * 2);
+    scr[g * 32 + lane] = s_acc;
+    nbar(1, 256);
+    if (tid == 0) mbar_arrive(&B.a_done);
+    MB1_TRACE(1);
+    // ------------------------------------------------ phase B: squeeze-excite
+    __half2* s_gate = reinterpret_cast<__half2*>(s_se + hid * 4);
+    const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_se + a.o_bsq);
+    const __half2* wex = reinterpret_cast<const __half2*>(s_wex);  // prefetched by the producer
+    const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_se + a.o_bex);
+    const float inv_p = 1.f / (float)(a.H * a.W);
+    if (tid < sq) {
+      float acc = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc += scr[r * 32 + tid];
+      scr[256 + tid] = fmaxf(acc * inv_p + bsq[tid], 0.f);
+    }
+    mbar_wait(&B.se_full, 0);
+    nbar(1, 256);
+    {
+      const float* s_s = scr + 256;
+      for (int hp = tid; hp < hid / 2; hp += 256) {
+        float e0 = bex[2 * hp], e1 = bex[2 * hp + 1];
+#pragma unroll 8
+        for (int jj = 0; jj < sq; ++jj) {
+          const float2 w = __half22float2(wex[(size_t)jj * (hid / 2) + hp]);
+          e0 += s_s[jj] * w.x;
+          e1 += s_s[jj] * w.y;
+        }
+        s_gate[hp] = __floats2half2_rn(act<kSigmoid>(e0), act<kSigmoid>(e1));
+      }
+      nbar(1, 256);
+    }
+    MB1_TRACE(2);
+    // ------------------------------------------------ phase C: gate h2 chunks
+    for (int qq = 0; qq < 2 * nch; ++qq) {
+      const int s = qq & 3, u = qq >> 2, j = qq >> 1, half = qq & 1;
+      mbar_wait(&B.pa_full[s], u & 1);
+      uint8_t* slot = s_h1 + s * a.slot_bytes;
+#pragma unroll
+      for (int k = 0; k < NT * 2; ++k) {
+        const int id = tid + k * 256;  // 16-byte row (NT x 512 of them): tile, group gg of the half, row
+        const int gg = (id >> 7) & 3;
+        uint8_t* p = slot + id * 16;
+        uint4 hv = lds128(p);
+        const uint4 gv = *reinterpret_cast<const uint4*>(s_gate + j * (kHC / 2) + (half * 4 + gg) * 4);
+        __half2* h = reinterpret_cast<__half2*>(&hv);
+        const __half2* gt = reinterpret_cast<const __half2*>(&gv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __hmul2(h[i], gt[i]);
+        *reinterpret_cast<uint4*>(p) = hv;
+      }
+      fence_async_smem();
+      mbar_arrive(&B.pa_ready[s]);
+    }
+    MB1_TRACE(3);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma) {
+    __syncwarp();
+    tmem_dealloc_n(tmem, a.tmem_cols);
+  }
+}
+
+
+// =================================================================== host
+}  // namespace wl
+
+#include <cstdlib>
+#include "launch.h"
+
+namespace wl {
+long long* g_mb1_trace = nullptr;
+void mb1_set_trace(void* p) { g_mb1_trace = reinterpret_cast<long long*>(p); }
+
+namespace {
+constexpr int kSmemMax1 = 232448;
+constexpr int kWsHeader1 = 4096;  // the arrival-counter header every family leaves alone
+
+bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
+  memset(&a, 0, sizeof(a));
+  a.n = d.n;
+  a.H = d.h;
+  a.W = d.w;
+  a.C = d.c;
+  a.hid = d.expansion * d.c;
+  a.sq = d.se_sq;
+  a.nch = a.hid / mb1::kHC;
+  a.NT = (16 * a.H + 127) / 128;
+  const int C = a.C, hid = a.hid, NT = a.NT;
+  const int GS = ((a.H + 3) * 16 + 2) * 16;
+  // shared memory: x (swizzled halves) | h1 x2 | W_exp ring x2 (the phase C ring overlays h1 + ring) | hdr | SE | bars
+  int o = 0;
+  a.s_x = o;
+  o += (C / 64) * NT * 128 * 128;
+  a.s_h1 = o;
+  a.s_h1_bytes = 2 * 8 * GS;
+  o = align_up(o + a.s_h1_bytes, 128);
+  a.s_w = o;
+  o += 2 * mb1::kHC * C * 2;
+  a.slot_bytes = NT * 8192 + C * 32 * 2;
+  if (4 * a.slot_bytes > o - a.s_h1) return false;
+  a.o_bexp = 0;
+  a.o_bconv = hid * 4;
+  a.o_bprj = 2 * hid * 4;
+  a.hdr_bytes = align_up(2 * hid * 4 + C * 4, 16);
+  a.s_hdr = align_up(o, 128);
+  o = a.s_hdr + a.hdr_bytes;
+  a.s_se = align_up(o, 128);
+  o = a.s_se + hid * 4 + hid * 2 + (256 + 32) * 4;
+  a.s_wex = align_up(o, 128);
+  o = a.s_wex + a.sq * hid * 2;
+  a.s_bar = align_up(o, 128);
+  a.smem = a.s_bar + 256;
+  // packed blob
+  int64_t p = a.hdr_bytes;
+  a.o_se = p;
+  int se = hid * a.sq * 2;
+  a.o_bsq = align_up(se, 16);
+  se = a.o_bsq + a.sq * 4;
+  a.o_wex = align_up(se, 16);
+  se = a.o_wex + a.sq * hid * 2;
+  a.o_bex = align_up(se, 16);
+  se = a.o_bex + hid * 4;
+  p += align_up(se, 128);
+  a.o_frag = p;
+  p += (int64_t)a.nch * 8 * 9 * 32 * 4;
+  a.o_wexp = p;
+  p += (int64_t)a.nch * mb1::kHC * C * 2;
+  a.o_wprj = p;
+  a.t_e = 0;
+  a.t_z = 2 * NT * mb1::kHC;
+  const int cols = a.t_z + NT * C;
+  a.tmem_cols = 32;
+  while (a.tmem_cols < cols) a.tmem_cols *= 2;
+  return a.smem <= kSmemMax1 && cols <= 512;
+}
+int64_t mb1_blob_bytes(const Mb1Args& a) { return a.o_wprj + (int64_t)a.nch * a.C * mb1::kHC * 2; }
+
+static bool env_legacy() {
+  static const bool v = getenv("WL_MB_LEGACY") != nullptr;  // A/B: force the block-diagonal tcgen05 conv kernel
+  return v;
+}
+
+using Mb1K = void (*)(const CUtensorMap, const CUtensorMap, const Mb1Args);
+template <int C, int ACT>
+Mb1K mb1_pick_h(int h) {
+  switch (h) {
+    case 7: return mb_s1_kernel<7, C, ACT>;
+    case 8: return mb_s1_kernel<8, C, ACT>;
+    case 14: return mb_s1_kernel<14, C, ACT>;
+    case 16: return mb_s1_kernel<16, C, ACT>;
+  }
+  return nullptr;
+}
+Mb1K mb1_kernel(const wl_block_desc& d) {
+  if (d.c == 128) return d.act == kSilu ? mb1_pick_h<128, kSilu>(d.h) : mb1_pick_h<128, kRelu>(d.h);
+  if (d.c == 64) return d.act == kSilu ? mb1_pick_h<64, kSilu>(d.h) : mb1_pick_h<64, kRelu>(d.h);
+  return nullptr;
+}
+}  // namespace
+
+bool mb1_eligible(const wl_block_desc& d) {
+  if (env_legacy() || d.kind != WL_KIND_MBCONV || d.stride != 1 || d.group_width != 8 || d.k != d.c) return false;
+  if ((d.c != 64 && d.c != 128) || d.w > 14 || (d.act != kSilu && d.act != kRelu)) return false;
+  const int hid = d.expansion * d.c;
+  if (hid % mb1::kHC || d.se_sq < 1 || d.se_sq > 32 || hid / 2 > 256 * 4) return false;
+  Mb1Args a;
+  return mb1_plan(d, a) && mb1_kernel(d) != nullptr;
+}
+
+int64_t mb1_packed_bytes(const wl_block_desc& d) {
+  Mb1Args a;
+  mb1_plan(d, a);
+  return mb1_blob_bytes(a);
+}
+
+int64_t mb1_workspace(const wl_block_desc& d) {
+  Mb1Args a;
+  mb1_plan(d, a);
+  return kWsHeader1 + (int64_t)d.n * a.nch * a.NT * 16384;
+}
+
+int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  Mb1Args a;
+  mb1_plan(d, a);
+  memset(out, 0, (size_t)mb1_blob_bytes(a));
+  const int C = a.C, hid = a.hid, sq = a.sq, HC = mb1::kHC;
+  const float *wexp = w[0], *bexp = w[1], *wconv = w[2], *bconv = w[3], *wsq = w[4], *bsq = w[5], *wex = w[6],
+              *bex = w[7], *wprj = w[8], *bprj = w[9];
+  float* hb = reinterpret_cast<float*>(out);
+  for (int i = 0; i < hid; ++i) {
+    hb[i] = bexp[i];
+    hb[hid + i] = bconv[i];
+  }
+  for (int i = 0; i < C; ++i) hb[2 * hid + i] = bprj[i];
+  uint8_t* se = out + a.o_se;
+  for (int i = 0; i < hid * sq; ++i) put_h(se, (size_t)i * 2, wsq[i]);
+  for (int i = 0; i < sq; ++i) reinterpret_cast<float*>(se + a.o_bsq)[i] = bsq[i];
+  for (int i = 0; i < sq * hid; ++i) put_h(se + a.o_wex, (size_t)i * 2, wex[i]);
+  for (int i = 0; i < hid; ++i) reinterpret_cast<float*>(se + a.o_bex)[i] = bex[i];
+  // mma.sync B fragments: [chunk][group][slot][lane] = (w[co][tap][ci], w[co][tap][ci + 1]),
+  // co = 8 G + lane / 4, ci = 2 (lane % 4)   (w_conv is (hid, 3, 3, T=8)); slots
+  // hold the taps in k16-pair order (0,1) (3,4) (6,7) (2,5) 8
+  static const int kTapOfSlot[9] = {0, 1, 3, 4, 6, 7, 2, 5, 8};
+  uint8_t* fr = out + a.o_frag;
+  for (int G = 0; G < hid / 8; ++G)
+    for (int slot = 0; slot < 9; ++slot)
+      for (int l = 0; l < 32; ++l) {
+        const int tap = kTapOfSlot[slot];
+        const int co = 8 * G + l / 4, ci = 2 * (l % 4);
+        const size_t off = (((size_t)G * 9 + slot) * 32 + l) * 4;
+        put_h(fr, off, wconv[((size_t)co * 9 + tap) * 8 + ci]);
+        put_h(fr, off + 2, wconv[((size_t)co * 9 + tap) * 8 + ci + 1]);
+      }
+  // W_exp chunk j: B operand (N = 64 hidden x K = C), 8x8 core matrices, LBO 1024
+  for (int j = 0; j < a.nch; ++j) {
+    uint8_t* ch = out + a.o_wexp + (size_t)j * HC * C * 2;
+    for (int nn = 0; nn < HC; ++nn)
+      for (int k = 0; k < C; ++k) put_h(ch, core_off_h(nn, k, 1024), wexp[(size_t)k * hid + j * HC + nn]);
+  }
+  // W_prj chunk j: B operand (N = C x K = 64 hidden), LBO = (C / 8) 128
+  for (int j = 0; j < a.nch; ++j) {
+    uint8_t* ch = out + a.o_wprj + (size_t)j * C * HC * 2;
+    for (int nn = 0; nn < C; ++nn)
+      for (int k = 0; k < HC; ++k) put_h(ch, core_off_h(nn, k, (C / 8) * 128), wprj[(size_t)(j * HC + k) * C + nn]);
+  }
+  return WL_OK;
+}
+
+int mb1_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st) {
+  Mb1Args a;
+  mb1_plan(d, a);
+  a.wpack = reinterpret_cast<const uint8_t*>(packed);
+  a.h2 = reinterpret_cast<uint8_t*>(ws) + kWsHeader1;
+  a.trace = g_mb1_trace;
+  CUtensorMap tx, tz;
+  const uint64_t dims[4] = {(uint64_t)d.c, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n};
+  const uint64_t strides[3] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2};
+  const uint32_t box[4] = {64, 16, (uint32_t)d.h, 1};
+  if (int e = encode_tmap(&tx, x, 4, dims, strides, box, true)) return e;
+  if (int e = encode_tmap(&tz, z, 4, dims, strides, box, true)) return e;
+  return launch_pdl(mb1_kernel(d), d.n, mb1::kThreads, a.smem, st, "mb_s1 launch", tx, tz, a);
+}
+
+int mb1_init() {
+  for (int c : {64, 128})
+    for (int act : {kSilu, kRelu})
+      for (int h : {7, 8, 14, 16}) {
+        wl_block_desc d;
+        memset(&d, 0, sizeof(d));
+        d.c = c;
+        d.act = act;
+        d.h = h;
+        if (int e = check_cuda(cudaFuncSetAttribute(mb1_kernel(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    kSmemMax1),
+                               "cudaFuncSetAttribute(mb_s1)"))
+          return e;
+      }
+  return WL_OK;
+}
+
+}  // namespace wl

@@ -1437,6 +1437,15 @@ __global__ void __launch_bounds__(256, 1)
 #include "launch.h"
 
 namespace wl {
+// stride-1 T=8 MBConv with the grouped conv on mma.sync (mb_s1.cu)
+bool mb1_eligible(const wl_block_desc& d);
+int64_t mb1_packed_bytes(const wl_block_desc& d);
+int64_t mb1_workspace(const wl_block_desc& d);
+int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out);
+int mb1_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st);
+int mb1_init();
+void mb1_set_trace(void* p);
+
 namespace {
 
 constexpr int kSmemMaxMb = 232448;
@@ -1784,6 +1793,7 @@ int mb_validate(const wl_block_desc& d) {
   if (d.group_width != 8 && d.group_width != 1)
     return set_error(WL_EUNSUPPORTED, "MBConv kernel supports group width 8 or 1, got %d", d.group_width);
   if (!front_kernel(d.act)) return set_error(WL_EUNSUPPORTED, "MBConv supports relu/silu/gelu");
+  if (mb1_eligible(d)) return WL_OK;
   MbPlanH P;
   if (!mb_plan(d, P)) return set_error(WL_EUNSUPPORTED, "no MBConv launch plan for C=%d hid=%d %dx%d", d.c, hid, d.h, d.w);
   return WL_OK;
@@ -1809,6 +1819,7 @@ int64_t mb_weight_numel(const wl_block_desc& d, int i) {
 }
 
 int64_t mb_packed_bytes(const wl_block_desc& d) {
+  if (mb1_eligible(d)) return mb1_packed_bytes(d);
   MbPlanH P;
   mb_plan(d, P);
   return P.front_bytes + P.back_bytes;
@@ -1816,12 +1827,14 @@ int64_t mb_packed_bytes(const wl_block_desc& d) {
 
 // workspace: [counters 4 KiB][h2][pool][gates]; zero it once before first use
 int64_t mb_workspace(const wl_block_desc& d) {
+  if (mb1_eligible(d)) return mb1_workspace(d);
   MbPlanH P;
   mb_plan(d, P);
   return kCounterBytes + ((P.h2_bytes + 255) / 256) * 256 + P.pool_bytes + P.gate_bytes;
 }
 
 int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  if (mb1_eligible(d)) return mb1_pack(d, w, out);
   MbPlanH P;
   mb_plan(d, P);
   const MbFrontArgs& f = P.f;
@@ -1890,6 +1903,7 @@ int mb_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
 }
 
 int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st) {
+  if (mb1_eligible(d)) return mb1_forward(d, x, packed, z, ws, st);
   MbPlanH P;
   mb_plan(d, P);
   MbFrontArgs f = P.f;
@@ -1960,6 +1974,7 @@ int mb_forward(const wl_block_desc& d, const void* x, const void* packed, void* 
 }
 
 int mb_init() {
+  if (int e = mb1_init()) return e;
   for (int a : {kRelu, kSilu, kGelu})
     for (int k = 0; k < 8; ++k)
       if (int e = check_cuda(cudaFuncSetAttribute(front_kernel(a, k & 4, k & 2, k & 1),
@@ -1973,12 +1988,16 @@ int mb_init() {
 }  // namespace
 
 int mb_kernel_launches(const wl_block_desc& d) {
+  if (mb1_eligible(d)) return 1;
   MbPlanH P;
   if (!mb_plan(d, P)) return set_error(WL_EUNSUPPORTED, "no MBConv launch plan");
   return P.f.fused ? 1 : 2;
 }
 
-void mb_set_trace(void* p) { g_mb_trace = reinterpret_cast<long long*>(p); }
+void mb_set_trace(void* p) {
+  g_mb_trace = reinterpret_cast<long long*>(p);
+  mb1_set_trace(p);
+}
 
 const Family kMbFamily = {mb_validate, mb_weight_count, mb_weight_numel, mb_packed_bytes,
                           mb_pack,     mb_workspace,    mb_forward,      mb_init};
