@@ -1,0 +1,32 @@
+"""One small launch per kernel family, for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck). Usage: python tools/sanitize_cases.py [case ...]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2404_03617_b200.blocks import FusedBlock  # noqa: E402
+from paper_2404_03617_b200.core import ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims  # noqa: E402
+
+CASES = {
+    "cf_fused": (ConvFirst(8, 6), TensorDims(1, 20, 12, 32), None),
+    "cf_convnext": (ConvNeXtBlock(7, 4, "gelu"), TensorDims(1, 16, 16, 96), None),
+    "cf_s2": (ConvFirst(8, 6, 2), TensorDims(1, 56, 56, 32), 48),
+    "mb_s1_14": (MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 128), None),
+    "mb_s1_7": (MBConv(8, 4, 0.25), TensorDims(2, 7, 7, 128), None),
+    "mb_front_pair": (MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 256), None),
+    "mb_front_s2": (MBConv(8, 4, 0.25, 2), TensorDims(1, 28, 28, 48), 128),
+    "mb_front_t1": (MBConv(1, 4, 0.25), TensorDims(1, 28, 28, 80), None),
+    "stem": (Stem(16), TensorDims(1, 64, 48, 3), None),
+    "head": (Head(1280, 1000), TensorDims(2, 7, 7, 128), None),
+}
+names = sys.argv[1:] or list(CASES)
+for nm in names:
+    blk, dims, k = CASES[nm]
+    m = FusedBlock(blk, dims, k)
+    x = torch.randn(*m.in_shape, device="cuda").half()
+    out = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
+    m.launch(x, out)
+    torch.cuda.synchronize()
+    print(nm, "ok", flush=True)
