@@ -44,8 +44,13 @@ extern "C" {
 /* block kinds (core.py:92-155) */
 #define WL_KIND_CONVFIRST 1 /* ConvFirst / ConvNeXt-style conv-first block */
 #define WL_KIND_MBCONV 2    /* MBConv + squeeze-excite                      */
+#define WL_KIND_FFN 3       /* FFN z = phi(xU + a)V + b over pixels (core.py:125-132) */
 #define WL_KIND_STEM 4      /* dense 3x3 stride-2 stem                      */
 #define WL_KIND_HEAD 5      /* 1x1 conv + pool + linear classifier          */
+/* ConvNeXt-T units (BASELINE config 4; no reference constructor) */
+#define WL_KIND_PATCH_STEM 6 /* p x p stride-p conv (ksize = p) + LayerNorm   */
+#define WL_KIND_DOWNSAMPLE 7 /* LayerNorm + 2x2 stride-2 conv c -> k          */
+#define WL_KIND_LN_HEAD 8    /* global average pool + LayerNorm + linear      */
 
 /* activations (machine.py:178-188, plus GELU) */
 #define WL_ACT_IDENTITY 0
@@ -121,6 +126,15 @@ WL_API int wl_stem_fwd(const wl_block_desc* d, const void* x, const void* packed
                 void* stream);
 WL_API int wl_head_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
                 void* stream);
+/* FFN block: replaces execute_numeric on an FFN schedule (machine.py:339-365) */
+WL_API int wl_ffn_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
+               void* stream);
+WL_API int wl_patch_stem_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
+                      void* stream);
+WL_API int wl_downsample_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
+                      void* stream);
+WL_API int wl_ln_head_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
+                   void* stream);
 
 /* Host-buffer convenience with execute_numeric's exact contract
  * (machine.py:1053): float32 HOST input x (NHWC) and float32 HOST weights in

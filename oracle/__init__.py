@@ -28,6 +28,9 @@ from .blocks import (  # noqa: F401
     convfirst_block,
     convfirst_s2_block,
     convnext_block,
+    downsample_block,
+    ln_head_block,
+    patch_stem_block,
     ffn_block,
     grouped_conv2d,
     head_block,

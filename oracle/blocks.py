@@ -223,3 +223,35 @@ def head_block(x, w1, b1, w2, b2, activation="relu") -> np.ndarray:
     h = _f32(phi(activation, _f32(_mm(x, w1, b1))))
     pool = _f32(h.astype(F64).mean(axis=(1, 2)))
     return _f32(_mm(pool, w2, b2))
+
+
+# ------------------------------------------------- ConvNeXt-T units (UNPINNED)
+
+
+def patch_stem_block(x, w, b, gamma, beta, eps: float = 1e-6) -> np.ndarray:
+    """UNPINNED (ConvNeXt-T, no reference constructor). p x p
+    stride-p conv (w: (k, p, p, c)) + bias, then channel LayerNorm."""
+    x = np.asarray(x, dtype=F64)
+    n, hh, ww, c = x.shape
+    k, p = w.shape[0], w.shape[1]
+    pt = x.reshape(n, hh // p, p, ww // p, p, c).transpose(0, 1, 3, 2, 4, 5).reshape(n, hh // p, ww // p, p * p * c)
+    y = _f32(pt @ np.asarray(w, dtype=F64).reshape(k, -1).T + np.asarray(b, dtype=F64))
+    return _f32(layer_norm(y, gamma, beta, eps))
+
+
+def downsample_block(x, gamma, beta, w, b, eps: float = 1e-6) -> np.ndarray:
+    """UNPINNED (ConvNeXt-T). Channel LayerNorm, then 2x2 stride-2 conv
+    (w: (k, 2, 2, c)) + bias."""
+    xn = _f32(layer_norm(x, gamma, beta, eps)).astype(F64)
+    n, hh, ww, c = xn.shape
+    k = w.shape[0]
+    pt = xn.reshape(n, hh // 2, 2, ww // 2, 2, c).transpose(0, 1, 3, 2, 4, 5).reshape(n, hh // 2, ww // 2, 4 * c)
+    return _f32(pt @ np.asarray(w, dtype=F64).reshape(k, -1).T + np.asarray(b, dtype=F64))
+
+
+def ln_head_block(x, gamma, beta, w, b, eps: float = 1e-6) -> np.ndarray:
+    """UNPINNED (ConvNeXt-T). Global average pool, channel LayerNorm, linear
+    classifier (w: (c, classes))."""
+    pool = _f32(np.asarray(x, dtype=F64).mean(axis=(1, 2)))
+    f = _f32(layer_norm(pool, gamma, beta, eps))
+    return _f32(_mm(f, w, b))

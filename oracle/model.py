@@ -31,6 +31,14 @@ def unit_forward(block, weights: dict, x: np.ndarray) -> np.ndarray:
             x, w["w_conv"], w["b_conv"], w["u"], w["a"], w["v"], w["b"], activation=block.activation,
             ln_gamma=w["ln_gamma"], ln_beta=w["ln_beta"], ln_eps=block.layer_norm_eps,
         )
+    if kind == "patch_stem":
+        return B.patch_stem_block(x, w["w_stem"], w["b_stem"], w["ln_gamma"], w["ln_beta"], block.layer_norm_eps)
+    if kind == "downsample":
+        return B.downsample_block(x, w["ln_gamma"], w["ln_beta"], w["w_down"], w["b_down"], block.layer_norm_eps)
+    if kind == "ln_head":
+        return B.ln_head_block(x, w["ln_gamma"], w["ln_beta"], w["w_cls"], w["b_cls"], block.layer_norm_eps)
+    if kind == "ffn":
+        return B.ffn_block(x, w["u"], w["a"], w["v"], w["b"], block.activation)
     if kind == "mbconv":
         return B.mbconv_block(
             x, w["w_exp"], w["b_exp"], w["w_conv"], w["b_conv"], w["w_sq"], w["b_sq"], w["w_ex"], w["b_ex"],

@@ -17,7 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("WLFUSE_LIB_AB") or os.path.join(HERE, "libwlfuse.so")  # A/B timing override (tools/ab_build.sh)
 
 WL_OK, WL_EINVAL, WL_EUNSUPPORTED, WL_ECUDA = 0, -1, -2, -3
-KIND_CONVFIRST, KIND_MBCONV, KIND_STEM, KIND_HEAD = 1, 2, 4, 5
+KIND_CONVFIRST, KIND_MBCONV, KIND_FFN, KIND_STEM, KIND_HEAD = 1, 2, 3, 4, 5
+KIND_PATCH_STEM, KIND_DOWNSAMPLE, KIND_LN_HEAD = 6, 7, 8
 ACTS = {"identity": 0, "relu": 1, "silu": 2, "sigmoid": 3, "gelu": 4}
 NORM_NONE, NORM_LAYERNORM = 0, 1
 
@@ -38,6 +39,10 @@ EXPORTS = (
     "wl_mbconv_fwd",
     "wl_stem_fwd",
     "wl_head_fwd",
+    "wl_ffn_fwd",
+    "wl_patch_stem_fwd",
+    "wl_downsample_fwd",
+    "wl_ln_head_fwd",
     "wl_execute_numeric",
     "wl_output_dims",
     "wl_debug_set_trace",
@@ -105,6 +110,10 @@ def lib() -> ctypes.CDLL:
         "wl_mbconv_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
         "wl_stem_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
         "wl_head_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_ffn_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_patch_stem_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_downsample_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
+        "wl_ln_head_fwd": (ctypes.c_int, [D, vp, vp, vp, vp, vp]),
         "wl_execute_numeric": (
             ctypes.c_int,
             [D, P(ctypes.c_float), P(P(ctypes.c_float)), ctypes.c_int, P(ctypes.c_float)],

@@ -175,6 +175,19 @@ int wl_head_fwd(const wl_block_desc* d, const void* x, const void* p, void* z, v
   return fwd_kind(WL_KIND_HEAD, d, x, p, z, ws, s);
 }
 
+int wl_ffn_fwd(const wl_block_desc* d, const void* x, const void* p, void* z, void* ws, void* s) {
+  return fwd_kind(WL_KIND_FFN, d, x, p, z, ws, s);
+}
+int wl_patch_stem_fwd(const wl_block_desc* d, const void* x, const void* p, void* z, void* ws, void* s) {
+  return fwd_kind(WL_KIND_PATCH_STEM, d, x, p, z, ws, s);
+}
+int wl_downsample_fwd(const wl_block_desc* d, const void* x, const void* p, void* z, void* ws, void* s) {
+  return fwd_kind(WL_KIND_DOWNSAMPLE, d, x, p, z, ws, s);
+}
+int wl_ln_head_fwd(const wl_block_desc* d, const void* x, const void* p, void* z, void* ws, void* s) {
+  return fwd_kind(WL_KIND_LN_HEAD, d, x, p, z, ws, s);
+}
+
 int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float* const* weights, int count,
                        float* z_host) {
   if (int e = wl_validate(d)) return e;

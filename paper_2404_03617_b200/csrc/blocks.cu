@@ -10,6 +10,10 @@ static const Family* family_of(const wl_block_desc& d) {
     case WL_KIND_MBCONV: return &kMbFamily;
     case WL_KIND_STEM: return &kStemFamily;
     case WL_KIND_HEAD: return &kHeadFamily;
+    case WL_KIND_FFN: return &kFfnFamily;
+    case WL_KIND_PATCH_STEM: return &kPatchStemFamily;
+    case WL_KIND_DOWNSAMPLE: return &kDownsampleFamily;
+    case WL_KIND_LN_HEAD: return &kLnHeadFamily;
   }
   return nullptr;
 }
@@ -25,7 +29,7 @@ int init_kernels() {
     return set_error(WL_ECUDA, "no current CUDA device");
   std::call_once(once[dev], [dev] {
     status[dev] = WL_OK;
-    for (const Family* f : {&kCfFamily, &kCf2Family, &kMbFamily, &kStemFamily, &kHeadFamily})
+    for (const Family* f : {&kCfFamily, &kCf2Family, &kMbFamily, &kStemFamily, &kHeadFamily, &kFfnFamily})
       if (f->init && (status[dev] = f->init()) != WL_OK) break;
   });
   return status[dev];
@@ -42,7 +46,11 @@ int64_t packed_bytes(const wl_block_desc& d) { return family_of(d)->packed_bytes
 int pack_weights(const wl_block_desc& d, const float* const* w, uint8_t* out) { return family_of(d)->pack(d, w, out); }
 int64_t workspace_bytes(const wl_block_desc& d) { return family_of(d)->workspace_bytes(d); }
 int kernel_launches(const wl_block_desc& d) {
-  if (d.kind == WL_KIND_HEAD) return 2;
+  if (d.kind == WL_KIND_HEAD || d.kind == WL_KIND_PATCH_STEM || d.kind == WL_KIND_DOWNSAMPLE ||
+      d.kind == WL_KIND_LN_HEAD)
+    return 2;
+  if (d.kind == WL_KIND_FFN) return 2 * ffn_row_batches(d);
+  if (cnx_wide(d)) return 1 + 2 * ffn_row_batches(d);
   if (d.kind == WL_KIND_MBCONV) return mb_kernel_launches(d);
   return 1;
 }
@@ -52,13 +60,14 @@ int forward(const wl_block_desc& d, const void* x, const void* p, void* z, void*
 
 void output_dims(const wl_block_desc& d, int32_t* n, int32_t* h, int32_t* w, int32_t* c) {
   *n = d.n;
-  if (d.kind == WL_KIND_HEAD) {
+  if (d.kind == WL_KIND_HEAD || d.kind == WL_KIND_LN_HEAD) {
     *h = 1;
     *w = 1;
     *c = d.classes;
     return;
   }
-  const int s = d.kind == WL_KIND_STEM ? 2 : d.stride;
+  int s = d.kind == WL_KIND_STEM ? 2 : d.kind == WL_KIND_PATCH_STEM ? d.ksize : d.kind == WL_KIND_DOWNSAMPLE ? 2 : d.stride;
+  if (d.kind == WL_KIND_FFN || s < 1) s = 1;  // FFN rows keep their geometry
   *h = d.h / s;
   *w = d.w / s;
   *c = d.k;

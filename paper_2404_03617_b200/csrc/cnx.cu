@@ -1,0 +1,637 @@
+// cnx.cu — the units that ConvNeXt-T (BASELINE config 4) needs beyond the
+// fused conv-first kernel, and the FFN block of the reference
+// (core.py:125-132; machine.py:228-252, 339-365):
+//
+//   WL_KIND_FFN         z = phi(x U + a) V + b over the rows of x
+//   ConvNeXt block, C > 128 (WL_KIND_CONVFIRST, LayerNorm, depthwise k x k):
+//                       x^ = LN(dwconv(x) + b_dw)        dwln_kernel (CUDA cores)
+//                       z  = x + GELU(x^ U + a) V + b    two tcgen05 GEMMs, hidden
+//                                                         in L2-sized row batches
+//   WL_KIND_PATCH_STEM  z = LN(conv_pxp/stride p(x) + b) patchify + GEMM (LN epilogue)
+//   WL_KIND_DOWNSAMPLE  z = conv_2x2/s2(LN(x)) + b      ln_s2d_kernel + GEMM
+//   WL_KIND_LN_HEAD     z = LN(mean_hw(x)) W + b        pool_ln_kernel + GEMM
+//
+// The wide block is the reference's "scaling variant" problem
+// (machine.py:528-569): at C = 384..768 one CTA can hold neither the whole
+// hidden nor the whole output row (TMEM is 512 fp32 columns), so the hidden
+// goes through the GLOBAL tier as the reference's partitioned schedule does,
+// sized so that a row batch of it stays L2-resident (126 MB L2).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <cstring>
+#include "common.cuh"
+#include "gemm.h"
+#include "launch.h"
+#include "plan.h"
+
+namespace wl {
+
+constexpr int kWsHdr = 4096;                     // the arrival-counter header every family leaves alone
+constexpr int64_t kHiddenBatchBytes = 40 << 20;  // hidden row batch kept L2-resident
+
+__device__ __forceinline__ void ld8f(const float* p, float* o) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+
+// ================================================================= kernels
+// patchify: x (n, H, W, cin) -> A (n * H/p * W/p, p * p * cin), column
+// (dy * p + dx) * cin + ci (the weight layout (k, p, p, cin))
+__global__ void patchify_kernel(const __half* __restrict__ x, __half* __restrict__ A, int n, int H, int W, int cin,
+                                int p) {
+  const int Ho = H / p, Wo = W / p, kk = p * p * cin;
+  const int64_t total = (int64_t)n * Ho * Wo * kk;
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % kk);
+    const int64_t m = i / kk;
+    const int ox = (int)(m % Wo), oy = (int)((m / Wo) % Ho), img = (int)(m / ((int64_t)Wo * Ho));
+    const int ci = k % cin, dx = (k / cin) % p, dy = k / (cin * p);
+    A[i] = x[(((int64_t)img * H + oy * p + dy) * W + ox * p + dx) * cin + ci];
+  }
+  pdl_trigger();
+}
+
+// depthwise KS x KS conv + bias + channel LayerNorm. One CTA per (image,
+// output row); thread = (8-channel chunk, PX consecutive pixels); inputs kept
+// as packed halves, fp32 accumulation, two-pass LayerNorm statistics through
+// shared-memory sums.
+constexpr int kDwPx = 2;
+template <int KS>
+__global__ void __launch_bounds__(512) dwln_kernel(const __half* __restrict__ x, const float* __restrict__ wdw,
+                                                   const float* __restrict__ bdw, const float* __restrict__ g,
+                                                   const float* __restrict__ be, __half* __restrict__ y, int H, int W,
+                                                   int C, float eps) {
+  constexpr int R = KS / 2, PX = kDwPx, NI = PX + 2 * R;
+  __shared__ float s_sum[256], s_sq[256];
+  const int C8 = C / 8, WQ = (W + PX - 1) / PX;
+  const int img = blockIdx.x / H, oy = blockIdx.x % H;
+  const int tid = threadIdx.x;
+  const bool on = tid < C8 * WQ;
+  const int c8 = tid % C8, x0 = (tid / C8) * PX;
+  for (int i = tid; i < W; i += blockDim.x) {
+    s_sum[i] = 0.f;
+    s_sq[i] = 0.f;
+  }
+  pdl_wait();
+  __syncthreads();
+  float acc[PX][8];
+  if (on) {
+    float b[8];
+    ld8f(bdw + c8 * 8, b);
+#pragma unroll
+    for (int p = 0; p < PX; ++p)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[p][i] = b[i];
+#pragma unroll 1
+    for (int dy = -R; dy <= R; ++dy) {
+      const int iy = oy + dy;
+      if (iy < 0 || iy >= H) continue;
+      const __half* row = x + (((size_t)img * H + iy) * W) * C + c8 * 8;
+      uint4 in[NI];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int ix = x0 - R + j;
+        in[j] = (ix >= 0 && ix < W) ? __ldg(reinterpret_cast<const uint4*>(row + (size_t)ix * C)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int dx = 0; dx < KS; ++dx) {
+        float w[8];
+        ld8f(wdw + (size_t)((dy + R) * KS + dx) * C + c8 * 8, w);
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          const __half2* h = reinterpret_cast<const __half2*>(&in[p + dx]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(h[i]);
+            acc[p][2 * i] = fmaf(f.x, w[2 * i], acc[p][2 * i]);
+            acc[p][2 * i + 1] = fmaf(f.y, w[2 * i + 1], acc[p][2 * i + 1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PX; ++p) {
+      if (x0 + p >= W) break;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += acc[p][i];
+      atomicAdd(&s_sum[x0 + p], s);
+    }
+  }
+  __syncthreads();
+  float mean[PX];
+  if (on) {
+#pragma unroll
+    for (int p = 0; p < PX; ++p) {
+      mean[p] = x0 + p < W ? s_sum[x0 + p] / (float)C : 0.f;
+      if (x0 + p >= W) break;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += (acc[p][i] - mean[p]) * (acc[p][i] - mean[p]);
+      atomicAdd(&s_sq[x0 + p], s);
+    }
+  }
+  __syncthreads();
+  if (on) {
+    float gg[8], bb[8];
+    ld8f(g + c8 * 8, gg);
+    ld8f(be + c8 * 8, bb);
+#pragma unroll
+    for (int p = 0; p < PX; ++p) {
+      if (x0 + p >= W) break;
+      const float rstd = rsqrtf(s_sq[x0 + p] / (float)C + eps);
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (acc[p][i] - mean[p]) * rstd * gg[i] + bb[i];
+      *reinterpret_cast<uint4*>(y + (((size_t)img * H + oy) * W + x0 + p) * C + c8 * 8) = pack8(o);
+    }
+  }
+  pdl_trigger();
+}
+
+// LayerNorm per input pixel written in 2x2 space-to-depth order: warp per
+// pixel, A[(img, y/2, x/2)][((y%2) 2 + x%2) C + c]
+__global__ void __launch_bounds__(256) ln_s2d_kernel(const __half* __restrict__ x, const float* __restrict__ g,
+                                                     const float* __restrict__ be, __half* __restrict__ A, int n,
+                                                     int H, int W, int C, float eps) {
+  constexpr int kMaxChunks = 4;  // C <= 1024
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  const int npix = n * H * W, C8 = C / 8;
+  if (warp < npix) {
+    const __half* px = x + (size_t)warp * C;
+    float v[kMaxChunks][8];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxChunks; ++j) {
+      const int c8 = lane + 32 * j;
+      if (c8 < C8) {
+        unpack8(__ldg(reinterpret_cast<const uint4*>(px + c8 * 8)), v[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += v[j][i];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s / (float)C;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxChunks; ++j)
+      if (lane + 32 * j < C8) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q += (v[j][i] - mean) * (v[j][i] - mean);
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float rstd = rsqrtf(q / (float)C + eps);
+    const int xx = warp % W, yy = (warp / W) % H, img = warp / (W * H);
+    __half* dst = A + ((((size_t)img * (H / 2) + yy / 2) * (W / 2) + xx / 2) * 4 + (yy % 2) * 2 + xx % 2) * C;
+#pragma unroll
+    for (int j = 0; j < kMaxChunks; ++j) {
+      const int c8 = lane + 32 * j;
+      if (c8 < C8) {
+        float gg[8], bb[8], o[8];
+        ld8f(g + c8 * 8, gg);
+        ld8f(be + c8 * 8, bb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = (v[j][i] - mean) * rstd * gg[i] + bb[i];
+        *reinterpret_cast<uint4*>(dst + c8 * 8) = pack8(o);
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+// global average pool + LayerNorm: one CTA per image, thread = channel pair
+__global__ void __launch_bounds__(512) pool_ln_kernel(const __half* __restrict__ x, const float* __restrict__ g,
+                                                      const float* __restrict__ be, __half* __restrict__ f, int HW,
+                                                      int C, float eps) {
+  __shared__ float red[2][32];
+  const int img = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool on = 2 * tid < C;
+  pdl_wait();
+  float m0 = 0.f, m1 = 0.f;
+  if (on) {
+    const __half2* px = reinterpret_cast<const __half2*>(x + (size_t)img * HW * C) + tid;
+    for (int p = 0; p < HW; ++p) {
+      const float2 v = __half22float2(px[(size_t)p * (C / 2)]);
+      m0 += v.x;
+      m1 += v.y;
+    }
+    m0 /= (float)HW;
+    m1 /= (float)HW;
+  }
+  auto block_sum = [&](float v, int slot) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[slot][warp] = v;
+    __syncthreads();
+    float t = 0.f;
+    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) t += red[slot][i];
+    return t;
+  };
+  const float mean = block_sum(on ? m0 + m1 : 0.f, 0) / (float)C;
+  const float d0 = m0 - mean, d1 = m1 - mean;
+  const float var = block_sum(on ? d0 * d0 + d1 * d1 : 0.f, 1) / (float)C;
+  const float rstd = rsqrtf(var + eps);
+  if (on)
+    reinterpret_cast<__half2*>(f + (size_t)img * C)[tid] =
+        __floats2half2_rn(d0 * rstd * g[2 * tid] + be[2 * tid], d1 * rstd * g[2 * tid + 1] + be[2 * tid + 1]);
+  pdl_trigger();
+}
+
+// ============================================================ host helpers
+namespace {
+
+template <typename Kern, typename... Args>
+int launch_simple(Kern k, int grid, int block, cudaStream_t st, const char* what, Args... args) {
+  return launch_pdl(k, grid, block, 0, st, what, args...);
+}
+
+int64_t a128(int64_t v) { return (v + 127) / 128 * 128; }
+
+void put_f32(uint8_t* base, int64_t off, const float* src, int64_t count) {
+  memcpy(base + off, src, (size_t)count * 4);
+}
+// B operand (N rows of K fp16, K contiguous) from a reference (K, N) matrix
+void put_t16(uint8_t* base, int64_t off, const float* src, int K, int N) {
+  for (int nn = 0; nn < N; ++nn)
+    for (int k = 0; k < K; ++k) put_h(base, off + ((int64_t)nn * K + k) * 2, src[(int64_t)k * N + nn]);
+}
+
+// row batch of the two-GEMM FFN so that the hidden stays L2-resident
+int64_t hidden_rows(int64_t M, int hid) {
+  int64_t r = kHiddenBatchBytes / ((int64_t)hid * 2);
+  r = r / 128 * 128;
+  if (r < 128) r = 128;
+  return r < M ? r : M;
+}
+
+// z = phi(x U + a) V + b (+ res): two GEMMs per row batch, hidden in ws
+int ffn_rows(const __half* x, int64_t M, int C, int hid, int K, const __half* ut, const float* a, const __half* vt,
+             const float* b, int act, const __half* res, __half* z, __half* hbuf, cudaStream_t st) {
+  const int64_t rb = hidden_rows(M, hid);
+  for (int64_t r0 = 0; r0 < M; r0 += rb) {
+    const int rows = (int)(M - r0 < rb ? M - r0 : rb);
+    GemmEpi e1;
+    e1.bias = a;
+    e1.act = act;
+    if (int e = gemm_run(x + r0 * C, rows, C, C, ut, hid, C, hbuf, hid, e1, st)) return e;
+    GemmEpi e2;
+    e2.bias = b;
+    if (res) {
+      e2.res = res + r0 * K;
+      e2.ldr = K;
+    }
+    if (int e = gemm_run(hbuf, rows, hid, hid, vt, K, hid, z + r0 * K, K, e2, st)) return e;
+  }
+  return WL_OK;
+}
+
+int common_dims(const wl_block_desc& d) {
+  if (d.n < 1 || d.h < 1 || d.w < 1 || d.c < 1) return set_error(WL_EINVAL, "dims must be positive");
+  if (d.c % 8) return set_error(WL_EUNSUPPORTED, "channel count %d must be a multiple of 8", d.c);
+  return WL_OK;
+}
+
+// ------------------------------------------------------------------ FFN
+// weights (reference order, machine.py:345-351): u (C, hid), a (hid), v (hid, C), b (C)
+struct FfnLayout {
+  int64_t o_a, o_b, o_u, o_v, total;
+};
+FfnLayout ffn_layout(const wl_block_desc& d) {
+  const int64_t C = d.c, hid = (int64_t)d.expansion * d.c;
+  FfnLayout L;
+  L.o_a = 0;
+  L.o_b = a128(hid * 4);
+  L.o_u = L.o_b + a128(C * 4 + 64);
+  L.o_v = L.o_u + a128(hid * C * 2);
+  L.total = L.o_v + a128(hid * C * 2);
+  return L;
+}
+int ffn_validate(const wl_block_desc& d) {
+  if (int e = common_dims(d)) return e;
+  if (d.expansion < 1) return set_error(WL_EINVAL, "expansion must be at least 1");
+  if (d.k != d.c) return set_error(WL_EINVAL, "FFN blocks keep their channel count");
+  if (d.act < 0 || d.act > 4) return set_error(WL_EINVAL, "unknown activation");
+  return WL_OK;
+}
+int ffn_wc(const wl_block_desc&) { return 4; }
+int64_t ffn_wn(const wl_block_desc& d, int i) {
+  const int64_t C = d.c, hid = (int64_t)d.expansion * d.c;
+  switch (i) {
+    case 0: return C * hid;
+    case 1: return hid;
+    case 2: return hid * C;
+    case 3: return C;
+  }
+  return set_error(WL_EINVAL, "weight index out of range");
+}
+int64_t ffn_pb(const wl_block_desc& d) { return ffn_layout(d).total; }
+int ffn_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  const FfnLayout L = ffn_layout(d);
+  const int C = d.c, hid = d.expansion * d.c;
+  memset(out, 0, (size_t)L.total);
+  put_f32(out, L.o_a, w[1], hid);
+  put_f32(out, L.o_b, w[3], C);
+  put_t16(out, L.o_u, w[0], C, hid);  // U^T: (hid, C)
+  put_t16(out, L.o_v, w[2], hid, C);  // V^T: (C, hid)
+  return WL_OK;
+}
+int64_t ffn_ws(const wl_block_desc& d) {
+  const int64_t M = (int64_t)d.n * d.h * d.w, hid = (int64_t)d.expansion * d.c;
+  return kWsHdr + a128(hidden_rows(M, (int)hid) * hid * 2);
+}
+int ffn_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  const FfnLayout L = ffn_layout(d);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
+  const int64_t M = (int64_t)d.n * d.h * d.w;
+  return ffn_rows(reinterpret_cast<const __half*>(x), M, d.c, d.expansion * d.c, d.c,
+                  reinterpret_cast<const __half*>(pk + L.o_u), reinterpret_cast<const float*>(pk + L.o_a),
+                  reinterpret_cast<const __half*>(pk + L.o_v), reinterpret_cast<const float*>(pk + L.o_b), d.act,
+                  nullptr, reinterpret_cast<__half*>(z), reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr), st);
+}
+
+// ------------------------------------------------- wide ConvNeXt block
+// weights (cf_weight_numel order): w_conv (C, k, k, 1), b_conv (C), ln_gamma, ln_beta,
+// u (C, hid), a (hid), v (hid, C), b (C)
+struct WideLayout {
+  int64_t o_wdw, o_bdw, o_g, o_be, o_a, o_b, o_u, o_v, total;
+};
+WideLayout wide_layout(const wl_block_desc& d) {
+  const int64_t C = d.c, hid = (int64_t)d.expansion * d.c, taps = (int64_t)d.ksize * d.ksize;
+  WideLayout L;
+  L.o_wdw = 0;  // [tap][C] fp32
+  L.o_bdw = a128(taps * C * 4 + 64);
+  L.o_g = L.o_bdw + a128(C * 4 + 64);
+  L.o_be = L.o_g + a128(C * 4 + 64);
+  L.o_a = L.o_be + a128(C * 4 + 64);
+  L.o_b = L.o_a + a128(hid * 4 + 64);
+  L.o_u = L.o_b + a128(C * 4 + 64);
+  L.o_v = L.o_u + a128(hid * C * 2);
+  L.total = L.o_v + a128(hid * C * 2);
+  return L;
+}
+}  // namespace
+
+int ffn_row_batches(const wl_block_desc& d) {
+  const int64_t M = (int64_t)d.n * d.h * d.w, rb = hidden_rows(M, d.expansion * d.c);
+  return (int)((M + rb - 1) / rb);
+}
+
+bool cnx_wide(const wl_block_desc& d) {
+  return d.kind == WL_KIND_CONVFIRST && d.norm == WL_NORM_LAYERNORM && d.group_width == 1 && d.stride == 1 &&
+         d.c > 128;
+}
+int cnx_wide_validate(const wl_block_desc& d) {
+  if (int e = common_dims(d)) return e;
+  if (d.ksize != 7 && d.ksize != 3) return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: 3x3 or 7x7 only");
+  if (d.c > 1024) return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: C <= 1024");
+  if ((d.c / 8) * ((d.w + kDwPx - 1) / kDwPx) > 512 || d.w > 256)
+    return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: (C/8) * ceil(W/2) must not exceed 512");
+  return WL_OK;
+}
+int64_t cnx_wide_pb(const wl_block_desc& d) { return wide_layout(d).total; }
+int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  const WideLayout L = wide_layout(d);
+  const int C = d.c, hid = d.expansion * d.c, taps = d.ksize * d.ksize;
+  memset(out, 0, (size_t)L.total);
+  float* wdw = reinterpret_cast<float*>(out + L.o_wdw);
+  for (int c = 0; c < C; ++c)
+    for (int t = 0; t < taps; ++t) wdw[(size_t)t * C + c] = w[0][(size_t)c * taps + t];
+  put_f32(out, L.o_bdw, w[1], C);
+  put_f32(out, L.o_g, w[2], C);
+  put_f32(out, L.o_be, w[3], C);
+  put_f32(out, L.o_a, w[5], hid);
+  put_f32(out, L.o_b, w[7], C);
+  put_t16(out, L.o_u, w[4], C, hid);
+  put_t16(out, L.o_v, w[6], hid, C);
+  return WL_OK;
+}
+int64_t cnx_wide_ws(const wl_block_desc& d) {
+  const int64_t M = (int64_t)d.n * d.h * d.w, hid = (int64_t)d.expansion * d.c;
+  return kWsHdr + a128(M * d.c * 2) + a128(hidden_rows(M, (int)hid) * hid * 2);
+}
+int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  const WideLayout L = wide_layout(d);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
+  const int64_t M = (int64_t)d.n * d.h * d.w;
+  __half* xh = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
+  __half* hb = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr + a128(M * d.c * 2));
+  const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
+  const int threads = align_up((d.c / 8) * ((d.w + kDwPx - 1) / kDwPx), 32);
+  auto k = d.ksize == 7 ? dwln_kernel<7> : dwln_kernel<3>;
+  if (int e = launch_simple(k, d.n * d.h, threads, st, "dwln launch", reinterpret_cast<const __half*>(x),
+                            reinterpret_cast<const float*>(pk + L.o_wdw), reinterpret_cast<const float*>(pk + L.o_bdw),
+                            reinterpret_cast<const float*>(pk + L.o_g), reinterpret_cast<const float*>(pk + L.o_be), xh,
+                            d.h, d.w, d.c, eps))
+    return e;
+  return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
+                  reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
+                  reinterpret_cast<const float*>(pk + L.o_b), d.act, reinterpret_cast<const __half*>(x),
+                  reinterpret_cast<__half*>(z), hb, st);
+}
+
+namespace {
+// ------------------------------------------------------- patchify stem
+// desc: c = input channels, k = output channels, ksize = patch = stride
+// weights: w (k, p, p, c), b (k), ln_gamma (k), ln_beta (k)
+struct PsLayout {
+  int64_t o_b, o_g, o_be, o_w, total;
+  int kk;
+};
+PsLayout ps_layout(const wl_block_desc& d) {
+  PsLayout L;
+  L.kk = d.ksize * d.ksize * d.c;
+  L.o_b = 0;
+  L.o_g = a128(d.k * 4 + 64);
+  L.o_be = L.o_g + a128(d.k * 4 + 64);
+  L.o_w = L.o_be + a128(d.k * 4 + 64);
+  L.total = L.o_w + a128((int64_t)d.k * L.kk * 2);
+  return L;
+}
+int ps_validate(const wl_block_desc& d) {
+  if (d.n < 1 || d.h < 1 || d.w < 1 || d.c < 1 || d.k < 1) return set_error(WL_EINVAL, "dims must be positive");
+  if (d.ksize < 1 || d.h % d.ksize || d.w % d.ksize)
+    return set_error(WL_EINVAL, "patch %d must divide the input %dx%d", d.ksize, d.h, d.w);
+  if ((d.ksize * d.ksize * d.c) % 8 || d.k % 8 || d.k > 256)
+    return set_error(WL_EUNSUPPORTED, "patchify stem: p*p*c and k multiples of 8, k <= 256");
+  return WL_OK;
+}
+int ps_wc(const wl_block_desc& d) { return d.norm == WL_NORM_LAYERNORM ? 4 : 2; }
+int64_t ps_wn(const wl_block_desc& d, int i) {
+  switch (i) {
+    case 0: return (int64_t)d.k * d.ksize * d.ksize * d.c;
+    case 1:
+    case 2:
+    case 3: return d.k;
+  }
+  return set_error(WL_EINVAL, "weight index out of range");
+}
+int64_t ps_pb(const wl_block_desc& d) { return ps_layout(d).total; }
+int ps_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  const PsLayout L = ps_layout(d);
+  memset(out, 0, (size_t)L.total);
+  put_f32(out, L.o_b, w[1], d.k);
+  if (d.norm == WL_NORM_LAYERNORM) {
+    put_f32(out, L.o_g, w[2], d.k);
+    put_f32(out, L.o_be, w[3], d.k);
+  }
+  for (int64_t i = 0; i < (int64_t)d.k * L.kk; ++i) put_h(out, L.o_w + i * 2, w[0][i]);  // (k, p, p, c) = B rows
+  return WL_OK;
+}
+int64_t ps_ws(const wl_block_desc& d) {
+  const int64_t M = (int64_t)d.n * (d.h / d.ksize) * (d.w / d.ksize);
+  return kWsHdr + a128(M * ps_layout(d).kk * 2);
+}
+int ps_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  const PsLayout L = ps_layout(d);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
+  const int64_t M = (int64_t)d.n * (d.h / d.ksize) * (d.w / d.ksize);
+  __half* A = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
+  const int64_t total = M * L.kk;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 16);
+  if (int e = launch_simple(patchify_kernel, grid, 256, st, "patchify launch", reinterpret_cast<const __half*>(x), A,
+                            d.n, d.h, d.w, d.c, d.ksize))
+    return e;
+  GemmEpi ep;
+  ep.bias = reinterpret_cast<const float*>(pk + L.o_b);
+  ep.act = d.act;
+  if (d.norm == WL_NORM_LAYERNORM) {
+    ep.ln_g = reinterpret_cast<const float*>(pk + L.o_g);
+    ep.ln_b = reinterpret_cast<const float*>(pk + L.o_be);
+    ep.ln_eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
+  }
+  return gemm_run(A, (int)M, L.kk, L.kk, pk + L.o_w, d.k, L.kk, z, d.k, ep, st);
+}
+
+// ----------------------------------------------------------- downsample
+// desc: c -> k, stride 2 (2x2 patches); weights ln_gamma (c), ln_beta (c), w (k, 2, 2, c), b (k)
+struct DsLayout {
+  int64_t o_g, o_be, o_b, o_w, total;
+};
+DsLayout ds_layout(const wl_block_desc& d) {
+  DsLayout L;
+  L.o_g = 0;
+  L.o_be = a128(d.c * 4 + 64);
+  L.o_b = L.o_be + a128(d.c * 4 + 64);
+  L.o_w = L.o_b + a128(d.k * 4 + 64);
+  L.total = L.o_w + a128((int64_t)d.k * 4 * d.c * 2);
+  return L;
+}
+int ds_validate(const wl_block_desc& d) {
+  if (int e = common_dims(d)) return e;
+  if (d.k < 8 || d.k % 8) return set_error(WL_EUNSUPPORTED, "downsample: k must be a multiple of 8");
+  if (d.h % 2 || d.w % 2) return set_error(WL_EINVAL, "downsample needs an even resolution (%dx%d)", d.h, d.w);
+  if (d.c > 1024) return set_error(WL_EUNSUPPORTED, "downsample: C <= 1024");
+  return WL_OK;
+}
+int ds_wc(const wl_block_desc&) { return 4; }
+int64_t ds_wn(const wl_block_desc& d, int i) {
+  switch (i) {
+    case 0:
+    case 1: return d.c;
+    case 2: return (int64_t)d.k * 4 * d.c;
+    case 3: return d.k;
+  }
+  return set_error(WL_EINVAL, "weight index out of range");
+}
+int64_t ds_pb(const wl_block_desc& d) { return ds_layout(d).total; }
+int ds_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  const DsLayout L = ds_layout(d);
+  memset(out, 0, (size_t)L.total);
+  put_f32(out, L.o_g, w[0], d.c);
+  put_f32(out, L.o_be, w[1], d.c);
+  put_f32(out, L.o_b, w[3], d.k);
+  for (int64_t i = 0; i < (int64_t)d.k * 4 * d.c; ++i) put_h(out, L.o_w + i * 2, w[2][i]);
+  return WL_OK;
+}
+int64_t ds_ws(const wl_block_desc& d) { return kWsHdr + a128((int64_t)d.n * d.h * d.w * d.c * 2); }
+int ds_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  const DsLayout L = ds_layout(d);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
+  __half* A = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
+  const int64_t npix = (int64_t)d.n * d.h * d.w;
+  const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
+  if (int e = launch_simple(ln_s2d_kernel, (int)((npix + 7) / 8), 256, st, "ln_s2d launch",
+                            reinterpret_cast<const __half*>(x), reinterpret_cast<const float*>(pk + L.o_g),
+                            reinterpret_cast<const float*>(pk + L.o_be), A, d.n, d.h, d.w, d.c, eps))
+    return e;
+  GemmEpi ep;
+  ep.bias = reinterpret_cast<const float*>(pk + L.o_b);
+  return gemm_run(A, (int)(npix / 4), 4 * d.c, 4 * d.c, pk + L.o_w, d.k, 4 * d.c, z, d.k, ep, st);
+}
+
+// -------------------------------------------------------------- LN head
+// desc: c, classes; weights ln_gamma (c), ln_beta (c), w_cls (c, classes), b_cls (classes)
+struct LhLayout {
+  int64_t o_g, o_be, o_b, o_w, total;
+};
+LhLayout lh_layout(const wl_block_desc& d) {
+  LhLayout L;
+  L.o_g = 0;
+  L.o_be = a128(d.c * 4 + 64);
+  L.o_b = L.o_be + a128(d.c * 4 + 64);
+  L.o_w = L.o_b + a128(d.classes * 4 + 64);
+  L.total = L.o_w + a128((int64_t)d.classes * d.c * 2);
+  return L;
+}
+int lh_validate(const wl_block_desc& d) {
+  if (int e = common_dims(d)) return e;
+  if (d.classes < 8 || d.classes % 8) return set_error(WL_EUNSUPPORTED, "LN head: classes must be a multiple of 8");
+  if (d.c > 1024) return set_error(WL_EUNSUPPORTED, "LN head: C <= 1024");
+  return WL_OK;
+}
+int lh_wc(const wl_block_desc&) { return 4; }
+int64_t lh_wn(const wl_block_desc& d, int i) {
+  switch (i) {
+    case 0:
+    case 1: return d.c;
+    case 2: return (int64_t)d.c * d.classes;
+    case 3: return d.classes;
+  }
+  return set_error(WL_EINVAL, "weight index out of range");
+}
+int64_t lh_pb(const wl_block_desc& d) { return lh_layout(d).total; }
+int lh_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  const LhLayout L = lh_layout(d);
+  memset(out, 0, (size_t)L.total);
+  put_f32(out, L.o_g, w[0], d.c);
+  put_f32(out, L.o_be, w[1], d.c);
+  put_f32(out, L.o_b, w[3], d.classes);
+  put_t16(out, L.o_w, w[2], d.c, d.classes);
+  return WL_OK;
+}
+int64_t lh_ws(const wl_block_desc& d) { return kWsHdr + a128((int64_t)d.n * d.c * 2); }
+int lh_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  const LhLayout L = lh_layout(d);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
+  __half* f = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
+  const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
+  const int threads = align_up(d.c / 2, 32);
+  if (int e = launch_simple(pool_ln_kernel, d.n, threads, st, "pool_ln launch", reinterpret_cast<const __half*>(x),
+                            reinterpret_cast<const float*>(pk + L.o_g), reinterpret_cast<const float*>(pk + L.o_be), f,
+                            d.h * d.w, d.c, eps))
+    return e;
+  GemmEpi ep;
+  ep.bias = reinterpret_cast<const float*>(pk + L.o_b);
+  return gemm_run(f, d.n, d.c, d.c, pk + L.o_w, d.classes, d.c, z, d.classes, ep, st);
+}
+
+int cnx_init() {
+  if (int e = gemm_init()) return e;
+  return WL_OK;
+}
+int no_init() { return WL_OK; }
+
+}  // namespace
+
+const Family kFfnFamily = {ffn_validate, ffn_wc, ffn_wn, ffn_pb, ffn_pack, ffn_ws, ffn_fwd, cnx_init};
+const Family kPatchStemFamily = {ps_validate, ps_wc, ps_wn, ps_pb, ps_pack, ps_ws, ps_fwd, no_init};
+const Family kDownsampleFamily = {ds_validate, ds_wc, ds_wn, ds_pb, ds_pack, ds_ws, ds_fwd, no_init};
+const Family kLnHeadFamily = {lh_validate, lh_wc, lh_wn, lh_pb, lh_pack, lh_ws, lh_fwd, no_init};
+
+}  // namespace wl

@@ -74,6 +74,18 @@ extern const Family kCf2Family;
 extern const Family kMbFamily;
 extern const Family kStemFamily;
 extern const Family kHeadFamily;
+extern const Family kFfnFamily;
+extern const Family kPatchStemFamily;
+extern const Family kDownsampleFamily;
+extern const Family kLnHeadFamily;
+// wide ConvNeXt block (C > 128): dwln + two GEMMs (cnx.cu), reached through the conv-first family
+bool cnx_wide(const wl_block_desc& d);
+int cnx_wide_validate(const wl_block_desc& d);
+int64_t cnx_wide_pb(const wl_block_desc& d);
+int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out);
+int64_t cnx_wide_ws(const wl_block_desc& d);
+int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st);
+int ffn_row_batches(const wl_block_desc& d);
 void mb_set_trace(void* p);
 void cf2_set_trace(void* p);
 void cf_set_trace(void* p);

@@ -313,6 +313,11 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // cluster pairs exchange partial pools / squeezes / Z over DSMEM: a CTA may
+  // only write its peer's shared memory once the peer is known to have
+  // started (compute-sanitizer racecheck flagged the unsynchronised first
+  // store, profiles/r02_sanitizer.txt)
+  if (FUSED && (a.ranges == 2 || a.bands == 2)) cluster_sync_all();
   if (FUSED) pdl_trigger();  // single-wave persistent grid: let the next kernel stage its prologue
   pdl_wait();
   const uint32_t tmem = B.tmem_base;

@@ -19,10 +19,13 @@ from .core import (
     ConvFirst,
     ConvNeXtBlock,
     DeviceSpec,
+    Downsample,
     ExecutionScheme,
     FFN,
     Head,
+    LNHead,
     MBConv,
+    PatchifyStem,
     StageSpec,
     Stem,
     TensorDims,
@@ -136,6 +139,35 @@ def tensor_table(block, dims: TensorDims, k: int) -> tuple[TensorEntry, ...]:
             TensorEntry("b_prj", (k,), "weights"),
             out,
         )
+    if isinstance(block, PatchifyStem):  # extension (ConvNeXt-T): p x p stride-p conv + LayerNorm
+        cs, pt = block.out_channels, block.patch
+        return (
+            x,
+            TensorEntry("w_stem", (cs, pt, pt, c), "weights"),
+            TensorEntry("b_stem", (cs,), "weights"),
+            TensorEntry("ln_gamma", (cs,), "weights"),
+            TensorEntry("ln_beta", (cs,), "weights"),
+            TensorEntry("z", (n, h // pt, w // pt, cs), "output"),
+        )
+    if isinstance(block, Downsample):  # extension (ConvNeXt-T): LayerNorm + 2x2 stride-2 conv
+        return (
+            x,
+            TensorEntry("ln_gamma", (c,), "weights"),
+            TensorEntry("ln_beta", (c,), "weights"),
+            TensorEntry("w_down", (k, 2, 2, c), "weights"),
+            TensorEntry("b_down", (k,), "weights"),
+            TensorEntry("z", (n, h // 2, w // 2, k), "output"),
+        )
+    if isinstance(block, LNHead):  # extension (ConvNeXt-T): pool + LayerNorm + classifier
+        m = block.num_classes
+        return (
+            x,
+            TensorEntry("ln_gamma", (c,), "weights"),
+            TensorEntry("ln_beta", (c,), "weights"),
+            TensorEntry("w_cls", (c, m), "weights"),
+            TensorEntry("b_cls", (m,), "weights"),
+            TensorEntry("z", (n, m), "output"),
+        )
     if isinstance(block, Stem):  # extension: dense 3x3 stride 2 (core.py:135-141)
         cs = block.out_channels
         return (
@@ -173,12 +205,12 @@ def build_schedule(
     validity rules; the fused kernel computes the same values whatever the
     partition (its hidden-chunk widths and CTA split come from the TMEM /
     shared-memory budget)."""
-    if not isinstance(block, (FFN, ConvFirst, ConvNeXtBlock, MBConv, Stem, Head)):
+    if not isinstance(block, (FFN, ConvFirst, ConvNeXtBlock, MBConv, Stem, Head, PatchifyStem, Downsample, LNHead)):
         raise ValueError(f"{type(block).__name__} blocks have no tensor-machine schedule")
     k = out_channels if out_channels is not None else dims.c
-    if isinstance(block, Stem):
+    if isinstance(block, (Stem, PatchifyStem, Downsample)):
         k = block.out_channels
-    elif isinstance(block, Head):
+    elif isinstance(block, (Head, LNHead)):
         k = block.num_classes
     elif getattr(block, "stride", 1) == 1 and k != dims.c:
         raise ValueError("stride-1 blocks keep their channel count")
@@ -243,6 +275,22 @@ def block_descriptor(block, dims: TensorDims, k: int):
         d.expansion, d.group_width, d.ksize, d.stride = block.expansion, block.group_width, 3, block.stride
         d.se_sq = int(block.se_ratio * dims.c)
         d.act = _act(block.activation)
+    elif isinstance(block, FFN):
+        d.kind = _lib.KIND_FFN
+        d.expansion = block.expansion
+        d.act = _act(block.activation)
+    elif isinstance(block, PatchifyStem):
+        d.kind = _lib.KIND_PATCH_STEM
+        d.k, d.ksize, d.stride = block.out_channels, block.patch, block.patch
+        d.norm, d.ln_eps = _lib.NORM_LAYERNORM, block.layer_norm_eps
+    elif isinstance(block, Downsample):
+        d.kind = _lib.KIND_DOWNSAMPLE
+        d.k, d.ksize, d.stride = block.out_channels, 2, 2
+        d.norm, d.ln_eps = _lib.NORM_LAYERNORM, block.layer_norm_eps
+    elif isinstance(block, LNHead):
+        d.kind = _lib.KIND_LN_HEAD
+        d.classes, d.k = block.num_classes, block.num_classes
+        d.norm, d.ln_eps = _lib.NORM_LAYERNORM, block.layer_norm_eps
     elif isinstance(block, Stem):
         d.kind = _lib.KIND_STEM
         d.k, d.stride, d.ksize = block.out_channels, 2, 3
@@ -324,6 +372,11 @@ class DeviceBinding:
 
 def device_binding(s: FusedSchedule) -> DeviceBinding:
     block, dims = s.block, s.dims
+    if isinstance(block, (FFN, PatchifyStem, Downsample, LNHead)):
+        # row-wise units (FFN rows, LayerNorm units): run at the reference widths (C % 8 == 0)
+        if dims.c % 8 and not isinstance(block, PatchifyStem):
+            raise ScheduleError(f"{type(block).__name__} needs C % 8 == 0 on the device (C = {dims.c})")
+        return DeviceBinding(s, block, dims, s.out_channels, block_descriptor(block, dims, s.out_channels))
     cin = dims.c if isinstance(block, Stem) else device_channels(dims.c)
     k = s.out_channels if isinstance(block, Head) else device_channels(s.out_channels)
     if isinstance(block, ConvNeXtBlock) and cin != dims.c:

@@ -45,7 +45,9 @@ class FusedNetwork:
         self.net = net
         self.batch = batch
         self.device = torch.device(device)
-        self.instances = plan_blocks(net)
+        # a ConvFirstNet NetworkSpec plans through core.plan_blocks; a
+        # ConvNeXtSpec (convnext.py) carries its own unit plan
+        self.instances = net.plan() if hasattr(net, "plan") else plan_blocks(net)
         self.units: list[Unit] = []
         ws_bytes = 256
         for i, inst in enumerate(self.instances):

@@ -104,3 +104,35 @@ def test_kernel_launches_per_block():
         assert L.wl_kernel_launches(ctypes.byref(d)) == 1
     d = _desc(Head(1280, 1000), TensorDims(128, 7, 7, 128))
     assert L.wl_kernel_launches(ctypes.byref(d)) == 2
+
+
+@pytest.mark.parametrize(
+    "block,dims,out",
+    [
+        ("ffn", TensorDims(2, 14, 14, 384), (2, 14, 14, 384)),
+        ("patch", TensorDims(2, 224, 224, 3), (2, 56, 56, 96)),
+        ("down", TensorDims(2, 56, 56, 96), (2, 28, 28, 192)),
+        ("lnhead", TensorDims(3, 7, 7, 768), (3, 1, 1, 1000)),
+        ("wide", TensorDims(2, 14, 14, 384), (2, 14, 14, 384)),
+    ],
+)
+def test_convnext_units_descriptors_without_gpu(block, dims, out):
+    """The ConvNeXt-T / FFN kinds validate, size their packed blobs and
+    workspaces and report output geometry through the ABI on a CPU-only host."""
+    from paper_2404_03617_b200.core import FFN, ConvNeXtBlock, Downsample, LNHead, PatchifyStem
+
+    blk = {"ffn": FFN(4, "gelu"), "patch": PatchifyStem(96), "down": Downsample(192), "lnhead": LNHead(1000),
+           "wide": ConvNeXtBlock(7, 4, "gelu")}[block]
+    s = build_schedule(blk, dims)
+    d = block_descriptor(blk, dims, s.out_channels)
+    L = _lib.lib()
+    assert L.wl_validate(ctypes.byref(d)) == 0
+    n, h, w, c = (ctypes.c_int32() for _ in range(4))
+    assert L.wl_output_dims(ctypes.byref(d), *(ctypes.byref(v) for v in (n, h, w, c))) == 0
+    assert (n.value, h.value, w.value, c.value) == out
+    assert L.wl_packed_bytes(ctypes.byref(d)) > 0 and L.wl_workspace_bytes(ctypes.byref(d)) > 4096
+    assert L.wl_weight_count(ctypes.byref(d)) == len(weight_names(s))
+    for i, name in enumerate(weight_names(s)):
+        assert L.wl_weight_numel(ctypes.byref(d), i) == int(np.prod(s.tensor(name).dims))
+    packed = _lib.pack_weights(d, [np.ones(s.tensor(nm).dims, np.float32) for nm in weight_names(s)])
+    assert packed.nbytes == L.wl_packed_bytes(ctypes.byref(d))

@@ -14,7 +14,7 @@ from oracle import model as om  # noqa: E402
 from oracle.fixtures import golden_names, load_golden  # noqa: E402
 from paper_2404_03617_b200 import zoo  # noqa: E402
 from paper_2404_03617_b200.blocks import FusedBlock, init_weights  # noqa: E402
-from paper_2404_03617_b200.core import ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims  # noqa: E402
+from paper_2404_03617_b200.core import FFN, ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims  # noqa: E402
 from paper_2404_03617_b200.machine import ScheduleError, build_schedule, execute_numeric, random_inputs  # noqa: E402
 from paper_2404_03617_b200.scheduler import FusedNetwork  # noqa: E402
 
@@ -41,9 +41,7 @@ def oracle_unit(block, w, x):
 @pytest.mark.parametrize("name", golden_names())
 def test_golden_vectors(name):
     meta, ins, out_lw, _ = load_golden(name)
-    kinds = {"ConvFirst": ConvFirst, "MBConv": MBConv}
-    if meta["block"] not in kinds:
-        pytest.skip("FFN has no standalone kernel")
+    kinds = {"ConvFirst": ConvFirst, "MBConv": MBConv, "FFN": FFN}
     s = build_schedule(kinds[meta["block"]](**meta["params"]), TensorDims(*meta["dims"]),
                        processors=meta.get("processors"))
     close(execute_numeric(s, ins), out_lw)

@@ -68,4 +68,8 @@ def test_bench_gpus_flag_relaunches_one_process_per_rank():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
-    assert lines[0]["cpu_baseline"]["kind"] == "reference" and lines[0]["cpu_baseline"]["cores"] == 2
+    from oracle.reference_net import load_reference
+
+    # "reference" when baseline/_ref holds the installed reference, else the oracle port
+    want = "reference" if load_reference() is not None else "port"
+    assert lines[0]["cpu_baseline"]["kind"] == want and lines[0]["cpu_baseline"]["cores"] == 2

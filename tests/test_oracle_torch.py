@@ -162,3 +162,52 @@ def test_head_vs_torch(rng):
     e = F.relu(F.conv2d(nchw(x), t64(w1).T[:, :, None, None], t64(b1)))
     ref = F.linear(F.adaptive_avg_pool2d(e, 1).flatten(1), t64(w2).T, t64(b2))
     close(got, ref.numpy())
+
+
+# ------------------------------------------------- ConvNeXt-T units (UNPINNED)
+
+
+def test_patch_stem_vs_torch(rng):
+    x = rng.standard_normal((2, 16, 12, 3))
+    w = rng.standard_normal((32, 4, 4, 3))
+    b, g, be = rng.standard_normal(32), 1 + 0.1 * rng.standard_normal(32), 0.1 * rng.standard_normal(32)
+    got = oracle.patch_stem_block(x, w, b, g, be)
+    y = F.conv2d(nchw(x), conv_weight(w), t64(b), stride=4).permute(0, 2, 3, 1)
+    ref = F.layer_norm(y, (32,), t64(g), t64(be), eps=1e-6).numpy()
+    close(got, ref)
+
+
+def test_downsample_vs_torch(rng):
+    x = rng.standard_normal((2, 8, 6, 24))
+    w = rng.standard_normal((48, 2, 2, 24))
+    b, g, be = rng.standard_normal(48), 1 + 0.1 * rng.standard_normal(24), 0.1 * rng.standard_normal(24)
+    got = oracle.downsample_block(x, g, be, w, b)
+    xn = F.layer_norm(t64(x), (24,), t64(g), t64(be), eps=1e-6).permute(0, 3, 1, 2)
+    ref = nhwc(F.conv2d(xn, conv_weight(w), t64(b), stride=2))
+    close(got, ref)
+
+
+def test_ln_head_vs_torch(rng):
+    x = rng.standard_normal((3, 7, 7, 64))
+    w, b = rng.standard_normal((64, 40)), rng.standard_normal(40)
+    g, be = 1 + 0.1 * rng.standard_normal(64), 0.1 * rng.standard_normal(64)
+    got = oracle.ln_head_block(x, g, be, w, b)
+    f = F.layer_norm(t64(x).mean(dim=(1, 2)), (64,), t64(g), t64(be), eps=1e-6)
+    ref = F.linear(f, t64(w).T, t64(b)).numpy()
+    close(got, ref)
+
+
+def test_convnext_block_vs_torch_module(rng):
+    """The ConvNeXt block as the original code writes it (dwconv groups=C ->
+    permute -> LayerNorm -> Linear -> GELU(erf) -> Linear -> + x)."""
+    c = 48
+    x = rng.standard_normal((2, 9, 10, c))
+    wdw, bdw = rng.standard_normal((c, 7, 7, 1)) / 7, rng.standard_normal(c)
+    g, be = 1 + 0.1 * rng.standard_normal(c), 0.1 * rng.standard_normal(c)
+    u, a = rng.standard_normal((c, 4 * c)) / np.sqrt(c), rng.standard_normal(4 * c)
+    v, b = rng.standard_normal((4 * c, c)) / np.sqrt(4 * c), rng.standard_normal(c)
+    got = oracle.convnext_block(x, wdw, bdw, u, a, v, b, activation="gelu", ln_gamma=g, ln_beta=be)
+    y = F.conv2d(nchw(x), conv_weight(wdw), t64(bdw), padding=3, groups=c).permute(0, 2, 3, 1)
+    y = F.layer_norm(y, (c,), t64(g), t64(be), eps=1e-6)
+    y = F.linear(F.gelu(F.linear(y, t64(u).T, t64(a))), t64(v).T, t64(b))
+    close(got, (y + t64(x)).numpy(), tol=1e-5)
