@@ -136,6 +136,16 @@ WL_API int wl_downsample_fwd(const wl_block_desc* d, const void* x, const void* 
 WL_API int wl_ln_head_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
                    void* stream);
 
+/* The pointwise contraction of the layer-wise units (1x1 conv / linear),
+ * exposed for the layer-wise FFN schedule and for direct testing:
+ * D[M][N] = act(A[M][K] . B[N][K]^T + bias[N]) (+ res[M][N]); fp16 storage,
+ * fp32 accumulation in TMEM. A, B, D, res: DEVICE pointers with leading
+ * dimensions lda/ldb/ldd/ldr (elements, multiples of 8); bias: DEVICE fp32
+ * or null; res: null for none. Replaces the float64 `x @ w` of the
+ * reference executor (machine.py:1017) on the device. */
+WL_API int wl_gemm(const void* a, int m, int k, int lda, const void* b, int n, int ldb, void* d, int ldd,
+                   const float* bias, int act, const void* res, int ldr, void* stream);
+
 /* Host-buffer convenience with execute_numeric's exact contract
  * (machine.py:1053): float32 HOST input x (NHWC) and float32 HOST weights in
  * reference order, float32 HOST output. Allocates, copies, runs, copies

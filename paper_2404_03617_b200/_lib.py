@@ -44,6 +44,7 @@ EXPORTS = (
     "wl_downsample_fwd",
     "wl_ln_head_fwd",
     "wl_execute_numeric",
+    "wl_gemm",
     "wl_output_dims",
     "wl_debug_set_trace",
 )
@@ -119,6 +120,8 @@ def lib() -> ctypes.CDLL:
             [D, P(ctypes.c_float), P(P(ctypes.c_float)), ctypes.c_int, P(ctypes.c_float)],
         ),
         "wl_output_dims": (ctypes.c_int, [D] + [P(ctypes.c_int32)] * 4),
+        "wl_gemm": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
+                                   ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, vp]),
         "wl_debug_set_trace": (None, [vp]),
     }
     for name, (res, args) in sig.items():
@@ -198,4 +201,22 @@ def execute_numeric_host(desc: BlockDesc, x: np.ndarray, weights) -> np.ndarray:
         ),
         "wl_execute_numeric",
     )
+    return out
+
+
+def gemm(a, b, bias=None, act: str = "identity", res=None, out=None, stream=None):
+    """D = act(a @ b.T + bias) (+ res) on the device through ``wl_gemm``:
+    a (M, K), b (N, K), res / out (M, N) fp16 CUDA tensors (row-major,
+    contiguous), bias fp32 (N,) or None."""
+    import torch
+
+    m, k = a.shape
+    n = b.shape[0]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float16, device=a.device)
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    check(lib().wl_gemm(a.data_ptr(), m, k, a.stride(0), b.data_ptr(), n, b.stride(0), out.data_ptr(), out.stride(0),
+                        bias.data_ptr() if bias is not None else None, ACTS[act],
+                        res.data_ptr() if res is not None else None, res.stride(0) if res is not None else 0, st),
+          "wl_gemm")
     return out

@@ -14,6 +14,7 @@
 
 #include "../../include/wlfuse.h"
 #include "launch.h"
+#include "gemm.h"
 
 namespace wl {
 
@@ -186,6 +187,21 @@ int wl_downsample_fwd(const wl_block_desc* d, const void* x, const void* p, void
 }
 int wl_ln_head_fwd(const wl_block_desc* d, const void* x, const void* p, void* z, void* ws, void* s) {
   return fwd_kind(WL_KIND_LN_HEAD, d, x, p, z, ws, s);
+}
+
+int wl_gemm(const void* a, int m, int k, int lda, const void* b, int n, int ldb, void* d, int ldd, const float* bias,
+            int act, const void* res, int ldr, void* stream) {
+  if (!a || !b || !d) return set_error(WL_EINVAL, "null tensor pointer");
+  if (act < 0 || act > 4) return set_error(WL_EINVAL, "unknown activation %d", act);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int e = init_kernels()) return e;
+  GemmEpi e;
+  e.bias = bias;
+  e.act = act;
+  e.res = reinterpret_cast<const __half*>(res);
+  e.ldr = ldr;
+  return gemm_run(a, m, k, lda, b, n, ldb, d, ldd, e, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float* const* weights, int count,

@@ -38,79 +38,130 @@ __device__ __forceinline__ void ld8f(const float* p, float* o) {
 
 // ================================================================= kernels
 // patchify: x (n, H, W, cin) -> A (n * H/p * W/p, p * p * cin), column
-// (dy * p + dx) * cin + ci (the weight layout (k, p, p, cin))
+// (dy * p + dx) * cin + ci (the weight layout (k, p, p, cin)). Generic path:
+// one element per thread; p * cin % 4 == 0 (the 4x4 x 3 stem): thread per
+// (patch, dy) moving p * cin halves as 8-byte words.
 __global__ void patchify_kernel(const __half* __restrict__ x, __half* __restrict__ A, int n, int H, int W, int cin,
                                 int p) {
-  const int Ho = H / p, Wo = W / p, kk = p * p * cin;
-  const int64_t total = (int64_t)n * Ho * Wo * kk;
+  const int Ho = H / p, Wo = W / p, kk = p * p * cin, seg = p * cin;
   pdl_wait();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(i % kk);
-    const int64_t m = i / kk;
-    const int ox = (int)(m % Wo), oy = (int)((m / Wo) % Ho), img = (int)(m / ((int64_t)Wo * Ho));
-    const int ci = k % cin, dx = (k / cin) % p, dy = k / (cin * p);
-    A[i] = x[(((int64_t)img * H + oy * p + dy) * W + ox * p + dx) * cin + ci];
+  if (seg % 4 == 0) {
+    const int64_t total = (int64_t)n * Ho * Wo * p;
+    const int words = seg / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int dy = (int)(i % p);
+      const int64_t m = i / p;
+      const int ox = (int)(m % Wo);
+      const int64_t rest = m / Wo;
+      const int oy = (int)(rest % Ho), img = (int)(rest / Ho);
+      const uint2* src = reinterpret_cast<const uint2*>(x + (((int64_t)img * H + oy * p + dy) * W + ox * p) * cin);
+      uint2* dst = reinterpret_cast<uint2*>(A + m * kk + dy * seg);
+      for (int w = 0; w < words; ++w) dst[w] = __ldg(src + w);
+    }
+  } else {
+    const int64_t total = (int64_t)n * Ho * Wo * kk;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int k = (int)(i % kk);
+      const int64_t m = i / kk;
+      const int ox = (int)(m % Wo), oy = (int)((m / Wo) % Ho), img = (int)(m / ((int64_t)Wo * Ho));
+      const int ci = k % cin, dx = (k / cin) % p, dy = k / (cin * p);
+      A[i] = x[(((int64_t)img * H + oy * p + dy) * W + ox * p + dx) * cin + ci];
+    }
   }
   pdl_trigger();
 }
 
 // depthwise KS x KS conv + bias + channel LayerNorm. One CTA per (image,
-// output row); thread = (8-channel chunk, PX consecutive pixels); inputs kept
-// as packed halves, fp32 accumulation, two-pass LayerNorm statistics through
-// shared-memory sums.
-constexpr int kDwPx = 2;
+// band of kDwRows output rows): the band's input rows (+ halo) are staged in
+// shared memory with coalesced 16-byte loads (an image row is W * C
+// contiguous halves); thread item = (output row, kDwPx pixels, 8 channels).
+// Per input row the KS taps accumulate in packed half (HFMA2), rows add in
+// fp32; the pre-norm result is kept in shared memory (fp16) while the
+// per-pixel mean and centred second moment are reduced (two passes).
+// The band height RB (4, 2 or 1 rows) is the largest whose tile fits shared
+// memory (ConvNeXt-T at 224: 4 rows for C = 192 / 384, 2 for C = 768).
+constexpr int kDwPx = 4;
+constexpr int kDwThreads = 512;
 template <int KS>
-__global__ void __launch_bounds__(512) dwln_kernel(const __half* __restrict__ x, const float* __restrict__ wdw,
-                                                   const float* __restrict__ bdw, const float* __restrict__ g,
-                                                   const float* __restrict__ be, __half* __restrict__ y, int H, int W,
-                                                   int C, float eps) {
+__global__ void __launch_bounds__(kDwThreads, 1) dwln_kernel(const __half* __restrict__ x, const __half* __restrict__ wdw,
+                                                      const float* __restrict__ bdw, const float* __restrict__ g,
+                                                      const float* __restrict__ be, __half* __restrict__ y, int H, int W,
+                                                      int C, float eps, int RB) {
   constexpr int R = KS / 2, PX = kDwPx, NI = PX + 2 * R;
-  __shared__ float s_sum[256], s_sq[256];
-  const int C8 = C / 8, WQ = (W + PX - 1) / PX;
-  const int img = blockIdx.x / H, oy = blockIdx.x % H;
-  const int tid = threadIdx.x;
-  const bool on = tid < C8 * WQ;
-  const int c8 = tid % C8, x0 = (tid / C8) * PX;
-  for (int i = tid; i < W; i += blockDim.x) {
-    s_sum[i] = 0.f;
-    s_sq[i] = 0.f;
-  }
+  const int IR = RB + 2 * R;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int C8 = C / 8, WG = (W + PX - 1) / PX, rowh = W * C;
+  __half* s_in = reinterpret_cast<__half*>(dsm);               // [IR][W + 2R][C]
+  const int prowh = (W + 2 * R) * C;                            // padded input row (halves)
+  __half* s_y = s_in + (size_t)IR * prowh;                      // [RB][W][C] pre-norm
+  float* s_sum = reinterpret_cast<float*>(s_y + (size_t)RB * rowh);  // [RB * W] mean, then rstd
+  float* s_sq = s_sum + RB * W;
+  float* s_part = s_sq + RB * W;  // [RB * W][C8] per-chunk partials (fixed-order reduction)
+  const int bands = (H + RB - 1) / RB;
+  const int img = blockIdx.x / bands, y0 = (blockIdx.x % bands) * RB;
+  const int tid = threadIdx.x, nt = blockDim.x;
   pdl_wait();
+  {
+    // rows of the band plus halo, each padded by R zero columns on both
+    // sides (no bounds checks in the stencil)
+    const int per_row = rowh / 8, prow = (W + 2 * R) * C8;
+    for (int i = tid; i < IR * prow; i += nt) {
+      const int rr = i / prow, off = i - rr * prow;
+      const int iy = y0 - R + rr, px = off / C8 - R;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (iy >= 0 && iy < H && px >= 0 && px < W)
+        v = __ldg(reinterpret_cast<const uint4*>(x + ((size_t)img * H + iy) * rowh) + off - R * C8);
+      reinterpret_cast<uint4*>(s_in)[i] = v;
+    }
+    (void)per_row;
+  }
   __syncthreads();
-  float acc[PX][8];
-  if (on) {
-    float b[8];
-    ld8f(bdw + c8 * 8, b);
+  const int items = RB * WG * C8;
+  for (int it = tid; it < items; it += nt) {
+    const int c8 = it % C8, rest = it / C8, pg = rest % WG, ry = rest / WG;
+    const int x0 = pg * PX;
+    if (y0 + ry >= H) continue;
+    float acc[PX][8];
+    {
+      float b[8];
+      ld8f(bdw + c8 * 8, b);
 #pragma unroll
-    for (int p = 0; p < PX; ++p)
+      for (int p = 0; p < PX; ++p)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[p][i] = b[i];
-#pragma unroll 1
-    for (int dy = -R; dy <= R; ++dy) {
-      const int iy = oy + dy;
-      if (iy < 0 || iy >= H) continue;
-      const __half* row = x + (((size_t)img * H + iy) * W) * C + c8 * 8;
+        for (int i = 0; i < 8; ++i) acc[p][i] = b[i];
+    }
+#pragma unroll
+    for (int dy = 0; dy < KS; ++dy) {
+      const __half* row = s_in + (size_t)(ry + dy) * prowh + (size_t)x0 * C + c8 * 8;
       uint4 in[NI];
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int ix = x0 - R + j;
-        in[j] = (ix >= 0 && ix < W) ? __ldg(reinterpret_cast<const uint4*>(row + (size_t)ix * C)) : make_uint4(0, 0, 0, 0);
-      }
+      for (int j = 0; j < NI; ++j) in[j] = (x0 + j < W + 2 * R) ? lds128(row + (size_t)j * C) : make_uint4(0, 0, 0, 0);
+      __half2 h[PX][4];
+#pragma unroll
+      for (int p = 0; p < PX; ++p)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[p][i] = __float2half2_rn(0.f);
 #pragma unroll
       for (int dx = 0; dx < KS; ++dx) {
-        float w[8];
-        ld8f(wdw + (size_t)((dy + R) * KS + dx) * C + c8 * 8, w);
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wdw + (size_t)(dy * KS + dx) * C + c8 * 8));
+        const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
 #pragma unroll
         for (int p = 0; p < PX; ++p) {
-          const __half2* h = reinterpret_cast<const __half2*>(&in[p + dx]);
+          const __half2* i2 = reinterpret_cast<const __half2*>(&in[p + dx]);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float2 f = __half22float2(h[i]);
-            acc[p][2 * i] = fmaf(f.x, w[2 * i], acc[p][2 * i]);
-            acc[p][2 * i + 1] = fmaf(f.y, w[2 * i + 1], acc[p][2 * i + 1]);
-          }
+          for (int i = 0; i < 4; ++i) h[p][i] = __hfma2(i2[i], w2[i], h[p][i]);
         }
       }
+#pragma unroll
+      for (int p = 0; p < PX; ++p)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __half22float2(h[p][i]);
+          acc[p][2 * i] += f.x;
+          acc[p][2 * i + 1] += f.y;
+        }
     }
 #pragma unroll
     for (int p = 0; p < PX; ++p) {
@@ -118,89 +169,114 @@ __global__ void __launch_bounds__(512) dwln_kernel(const __half* __restrict__ x,
       float s = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) s += acc[p][i];
-      atomicAdd(&s_sum[x0 + p], s);
+      s_part[(ry * W + x0 + p) * C8 + c8] = s;
+      *reinterpret_cast<uint4*>(s_y + ((size_t)ry * W + x0 + p) * C + c8 * 8) = pack8(acc[p]);
     }
   }
   __syncthreads();
-  float mean[PX];
+  const int pitems = RB * W * C8;
+  for (int pix = tid; pix < RB * W; pix += nt) {
+    float t = 0.f;
+    for (int j = 0; j < C8; ++j) t += s_part[pix * C8 + j];
+    s_sum[pix] = t / (float)C;
+  }
+  __syncthreads();
+  for (int it = tid; it < pitems; it += nt) {
+    const int c8 = it % C8, pix = it / C8;
+    const float mean = s_sum[pix];
+    float v[8];
+    unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += (v[i] - mean) * (v[i] - mean);
+    s_part[it] = s;
+  }
+  __syncthreads();
+  for (int pix = tid; pix < RB * W; pix += nt) {
+    float t = 0.f;
+    for (int j = 0; j < C8; ++j) t += s_part[pix * C8 + j];
+    s_sq[pix] = rsqrtf(t / (float)C + eps);
+  }
+  __syncthreads();
+  for (int it = tid; it < pitems; it += nt) {
+    const int c8 = it % C8, pix = it / C8;
+    if (y0 + pix / W >= H) continue;
+    const float mean = s_sum[pix], rstd = s_sq[pix];
+    float v[8], gg[8], bb[8];
+    unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
+    ld8f(g + c8 * 8, gg);
+    ld8f(be + c8 * 8, bb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (v[i] - mean) * rstd * gg[i] + bb[i];
+    *reinterpret_cast<uint4*>(y + ((size_t)img * H + y0) * rowh + (size_t)pix * C + c8 * 8) = pack8(v);
+  }
+  pdl_trigger();
+}
+int dwln_smem_rb(int KS, int W, int C, int RB) {
+  return (KS - 1 + RB) * (W + KS - 1) * C * 2 + RB * W * C * 2 + 2 * RB * W * 4 + RB * W * (C / 8) * 4;
+}
+int dwln_rows(int KS, int W, int C) {
+  for (int rb : {4, 2, 1})
+    if (dwln_smem_rb(KS, W, C, rb) <= 232448) return rb;
+  return 0;
+}
+int dwln_smem(int KS, int W, int C) { return dwln_smem_rb(KS, W, C, dwln_rows(KS, W, C)); }
+
+// LayerNorm per pixel; S2D: the output row is written in 2x2 space-to-depth
+// order A[(img, y/2, x/2)][((y%2) 2 + x%2) C + c]. CTA = P pixels x C/8
+// threads; one 16-byte chunk per thread, two-pass statistics over shared sums.
+__global__ void __launch_bounds__(256) ln_s2d_kernel(const __half* __restrict__ x, const float* __restrict__ g,
+                                                     const float* __restrict__ be, __half* __restrict__ A, int n,
+                                                     int H, int W, int C, float eps) {
+  // fixed-order (deterministic) reductions: per-thread partials, then the
+  // pixel's first thread sums its C/8 partials in channel order
+  __shared__ float s_part[256], s_mean[256], s_rstd[256];
+  const int C8 = C / 8, P = 256 / C8, tid = threadIdx.x;
+  const int pl = tid / C8, c8 = tid - pl * C8;
+  const int64_t pix = (int64_t)blockIdx.x * P + pl;
+  const int64_t npix = (int64_t)n * H * W;
+  const bool on = pl < P && pix < npix;
+  pdl_wait();
+  float v[8];
+  float s = 0.f;
+  if (on) {
+    unpack8(__ldg(reinterpret_cast<const uint4*>(x + pix * C) + c8), v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[i];
+  }
+  s_part[tid] = s;
+  __syncthreads();
+  if (on && c8 == 0) {
+    float t = 0.f;
+    for (int j = 0; j < C8; ++j) t += s_part[tid + j];
+    s_mean[pl] = t / (float)C;
+  }
+  __syncthreads();
+  const float mean = on ? s_mean[pl] : 0.f;
+  s = 0.f;
   if (on) {
 #pragma unroll
-    for (int p = 0; p < PX; ++p) {
-      mean[p] = x0 + p < W ? s_sum[x0 + p] / (float)C : 0.f;
-      if (x0 + p >= W) break;
-      float s = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s += (acc[p][i] - mean[p]) * (acc[p][i] - mean[p]);
-      atomicAdd(&s_sq[x0 + p], s);
-    }
+    for (int i = 0; i < 8; ++i) s += (v[i] - mean) * (v[i] - mean);
+  }
+  s_part[tid] = s;
+  __syncthreads();
+  if (on && c8 == 0) {
+    float t = 0.f;
+    for (int j = 0; j < C8; ++j) t += s_part[tid + j];
+    s_rstd[pl] = rsqrtf(t / (float)C + eps);
   }
   __syncthreads();
   if (on) {
+    const float rstd = s_rstd[pl];
     float gg[8], bb[8];
     ld8f(g + c8 * 8, gg);
     ld8f(be + c8 * 8, bb);
 #pragma unroll
-    for (int p = 0; p < PX; ++p) {
-      if (x0 + p >= W) break;
-      const float rstd = rsqrtf(s_sq[x0 + p] / (float)C + eps);
-      float o[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = (acc[p][i] - mean[p]) * rstd * gg[i] + bb[i];
-      *reinterpret_cast<uint4*>(y + (((size_t)img * H + oy) * W + x0 + p) * C + c8 * 8) = pack8(o);
-    }
-  }
-  pdl_trigger();
-}
-
-// LayerNorm per input pixel written in 2x2 space-to-depth order: warp per
-// pixel, A[(img, y/2, x/2)][((y%2) 2 + x%2) C + c]
-__global__ void __launch_bounds__(256) ln_s2d_kernel(const __half* __restrict__ x, const float* __restrict__ g,
-                                                     const float* __restrict__ be, __half* __restrict__ A, int n,
-                                                     int H, int W, int C, float eps) {
-  constexpr int kMaxChunks = 4;  // C <= 1024
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  pdl_wait();
-  const int npix = n * H * W, C8 = C / 8;
-  if (warp < npix) {
-    const __half* px = x + (size_t)warp * C;
-    float v[kMaxChunks][8];
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < kMaxChunks; ++j) {
-      const int c8 = lane + 32 * j;
-      if (c8 < C8) {
-        unpack8(__ldg(reinterpret_cast<const uint4*>(px + c8 * 8)), v[j]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s += v[j][i];
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float mean = s / (float)C;
-    float q = 0.f;
-#pragma unroll
-    for (int j = 0; j < kMaxChunks; ++j)
-      if (lane + 32 * j < C8) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) q += (v[j][i] - mean) * (v[j][i] - mean);
-      }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-    const float rstd = rsqrtf(q / (float)C + eps);
-    const int xx = warp % W, yy = (warp / W) % H, img = warp / (W * H);
-    __half* dst = A + ((((size_t)img * (H / 2) + yy / 2) * (W / 2) + xx / 2) * 4 + (yy % 2) * 2 + xx % 2) * C;
-#pragma unroll
-    for (int j = 0; j < kMaxChunks; ++j) {
-      const int c8 = lane + 32 * j;
-      if (c8 < C8) {
-        float gg[8], bb[8], o[8];
-        ld8f(g + c8 * 8, gg);
-        ld8f(be + c8 * 8, bb);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = (v[j][i] - mean) * rstd * gg[i] + bb[i];
-        *reinterpret_cast<uint4*>(dst + c8 * 8) = pack8(o);
-      }
-    }
+    for (int i = 0; i < 8; ++i) v[i] = (v[i] - mean) * rstd * gg[i] + bb[i];
+    const int xx = (int)(pix % W), yy = (int)((pix / W) % H);
+    const int64_t img = pix / ((int64_t)W * H);
+    __half* dst = A + (((img * (H / 2) + yy / 2) * (W / 2) + xx / 2) * 4 + (yy % 2) * 2 + xx % 2) * C;
+    reinterpret_cast<uint4*>(dst)[c8] = pack8(v);
   }
   pdl_trigger();
 }
@@ -364,8 +440,8 @@ struct WideLayout {
 WideLayout wide_layout(const wl_block_desc& d) {
   const int64_t C = d.c, hid = (int64_t)d.expansion * d.c, taps = (int64_t)d.ksize * d.ksize;
   WideLayout L;
-  L.o_wdw = 0;  // [tap][C] fp32
-  L.o_bdw = a128(taps * C * 4 + 64);
+  L.o_wdw = 0;  // [tap][C] fp16
+  L.o_bdw = a128(taps * C * 2);
   L.o_g = L.o_bdw + a128(C * 4 + 64);
   L.o_be = L.o_g + a128(C * 4 + 64);
   L.o_a = L.o_be + a128(C * 4 + 64);
@@ -390,8 +466,9 @@ int cnx_wide_validate(const wl_block_desc& d) {
   if (int e = common_dims(d)) return e;
   if (d.ksize != 7 && d.ksize != 3) return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: 3x3 or 7x7 only");
   if (d.c > 1024) return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: C <= 1024");
-  if ((d.c / 8) * ((d.w + kDwPx - 1) / kDwPx) > 512 || d.w > 256)
-    return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: (C/8) * ceil(W/2) must not exceed 512");
+  if (dwln_rows(d.ksize, d.w, d.c) == 0 || d.w > 128)
+    return set_error(WL_EUNSUPPORTED, "wide ConvNeXt block: a %d-row band of %dx%d does not fit shared memory",
+                     d.ksize, d.w, d.c);
   return WL_OK;
 }
 int64_t cnx_wide_pb(const wl_block_desc& d) { return wide_layout(d).total; }
@@ -399,9 +476,8 @@ int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   const WideLayout L = wide_layout(d);
   const int C = d.c, hid = d.expansion * d.c, taps = d.ksize * d.ksize;
   memset(out, 0, (size_t)L.total);
-  float* wdw = reinterpret_cast<float*>(out + L.o_wdw);
   for (int c = 0; c < C; ++c)
-    for (int t = 0; t < taps; ++t) wdw[(size_t)t * C + c] = w[0][(size_t)c * taps + t];
+    for (int t = 0; t < taps; ++t) put_h(out, L.o_wdw + ((int64_t)t * C + c) * 2, w[0][(size_t)c * taps + t]);
   put_f32(out, L.o_bdw, w[1], C);
   put_f32(out, L.o_g, w[2], C);
   put_f32(out, L.o_be, w[3], C);
@@ -422,12 +498,13 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
   __half* xh = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
   __half* hb = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr + a128(M * d.c * 2));
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
-  const int threads = align_up((d.c / 8) * ((d.w + kDwPx - 1) / kDwPx), 32);
   auto k = d.ksize == 7 ? dwln_kernel<7> : dwln_kernel<3>;
-  if (int e = launch_simple(k, d.n * d.h, threads, st, "dwln launch", reinterpret_cast<const __half*>(x),
-                            reinterpret_cast<const float*>(pk + L.o_wdw), reinterpret_cast<const float*>(pk + L.o_bdw),
+  const int rb = dwln_rows(d.ksize, d.w, d.c), bands = (d.h + rb - 1) / rb;
+  if (int e = launch_pdl(k, d.n * bands, kDwThreads, dwln_smem(d.ksize, d.w, d.c), st, "dwln launch",
+                            reinterpret_cast<const __half*>(x),
+                            reinterpret_cast<const __half*>(pk + L.o_wdw), reinterpret_cast<const float*>(pk + L.o_bdw),
                             reinterpret_cast<const float*>(pk + L.o_g), reinterpret_cast<const float*>(pk + L.o_be), xh,
-                            d.h, d.w, d.c, eps))
+                            d.h, d.w, d.c, eps, rb))
     return e;
   return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
                   reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
@@ -492,8 +569,8 @@ int ps_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
   const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
   const int64_t M = (int64_t)d.n * (d.h / d.ksize) * (d.w / d.ksize);
   __half* A = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
-  const int64_t total = M * L.kk;
-  const int grid = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 16);
+  const int64_t total = (d.ksize * d.c) % 4 == 0 ? M * d.ksize : M * L.kk;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 32);
   if (int e = launch_simple(patchify_kernel, grid, 256, st, "patchify launch", reinterpret_cast<const __half*>(x), A,
                             d.n, d.h, d.w, d.c, d.ksize))
     return e;
@@ -526,7 +603,7 @@ int ds_validate(const wl_block_desc& d) {
   if (int e = common_dims(d)) return e;
   if (d.k < 8 || d.k % 8) return set_error(WL_EUNSUPPORTED, "downsample: k must be a multiple of 8");
   if (d.h % 2 || d.w % 2) return set_error(WL_EINVAL, "downsample needs an even resolution (%dx%d)", d.h, d.w);
-  if (d.c > 1024) return set_error(WL_EUNSUPPORTED, "downsample: C <= 1024");
+  if (d.c > 2048) return set_error(WL_EUNSUPPORTED, "downsample: C <= 2048");
   return WL_OK;
 }
 int ds_wc(const wl_block_desc&) { return 4; }
@@ -556,7 +633,8 @@ int ds_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
   __half* A = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
   const int64_t npix = (int64_t)d.n * d.h * d.w;
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
-  if (int e = launch_simple(ln_s2d_kernel, (int)((npix + 7) / 8), 256, st, "ln_s2d launch",
+  const int P = 256 / (d.c / 8);
+  if (int e = launch_simple(ln_s2d_kernel, (int)((npix + P - 1) / P), 256, st, "ln_s2d launch",
                             reinterpret_cast<const __half*>(x), reinterpret_cast<const float*>(pk + L.o_g),
                             reinterpret_cast<const float*>(pk + L.o_be), A, d.n, d.h, d.w, d.c, eps))
     return e;
@@ -623,6 +701,10 @@ int lh_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
 
 int cnx_init() {
   if (int e = gemm_init()) return e;
+  for (auto k : {dwln_kernel<7>, dwln_kernel<3>})
+    if (int e = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+                           "cudaFuncSetAttribute(dwln)"))
+      return e;
   return WL_OK;
 }
 int no_init() { return WL_OK; }

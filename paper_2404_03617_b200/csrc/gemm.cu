@@ -9,8 +9,11 @@
 // swizzled K-major layout (one box each per K step), a ring of up to 8 stages;
 // one thread issues 4 x tcgen05.mma (K = 16) per stage into one of two TMEM
 // accumulators, so the epilogue of tile i overlaps the main loop of tile i+1.
-// Warps: 0 TMA producer, 1 MMA issuer, 2-5 epilogue (TMEM lane quadrant =
-// warp % 4; thread = output row). Grid = min(tiles, SMs), tiles strided.
+// Warps: 0 TMA producer, 1 MMA issuer, 2-9 epilogue (TMEM lane quadrant =
+// warp % 4, two warps per quadrant splitting the columns; thread = output
+// row). The epilogue stages the fp16 tile in shared memory in the 128-byte
+// swizzled layout (a residual tile arrives there by TMA first) and leaves by
+// TMA stores, so HBM sees whole lines. Grid = min(tiles, SMs), tiles strided.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
@@ -23,25 +26,26 @@
 namespace wl {
 
 namespace gm {
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int kEpiThreads = 256;
 constexpr int kBK = 64;
 constexpr int kMaxStages = 8;
 constexpr int kSmemMax = 232448;
 struct Args {
-  int M, N, BN, tiles_m, tiles, kblocks, stages, stage_bytes;
-  int ldd, ldr, act;
+  int M, N, BN, tiles_m, tiles, kblocks, stages, stage_bytes, s_stage, slabs;
+  int act, has_res;
   float ln_eps;
   const float* bias;
   const float* ln_g;
   const float* ln_b;
-  const __half* res;
-  __half* D;
   uint32_t tmem_cols;
 };
 struct Bars {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t acc_full[2], acc_empty[2];
+  uint64_t res_full;
   uint32_t tmem_base;
+  float ln_red[2][2][128];  // row LayerNorm: [sum | centred sum][column half][row]
 };
 }  // namespace gm
 
@@ -52,6 +56,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0,
       "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_g() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0_g() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0_g() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void gm_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
 __device__ __forceinline__ float act_rt(float v, int a) {
   switch (a) {
@@ -62,9 +75,18 @@ __device__ __forceinline__ float act_rt(float v, int a) {
   }
   return v;
 }
+__device__ __forceinline__ __half2 act_rt_h2(__half2 v, int a) {
+  switch (a) {
+    case kRelu: return act_h2<kRelu>(v);
+    case kSilu: return act_h2<kSilu>(v);
+    case kSigmoid: return act_h2<kSigmoid>(v);
+    case kGelu: return act_h2<kGelu>(v);
+  }
+  return v;
+}
 
-// bias + activation of 16 accumulators at output column n (n + 16 may pass N)
-__device__ __forceinline__ void gemm_pre(const gm::Args& a, const uint32_t* v, int n, float* f) {
+// accumulators + bias of 16 columns starting at output column n (n + 16 may pass N)
+__device__ __forceinline__ void gemm_bias(const gm::Args& a, const uint32_t* v, int n, float* f) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
   if (a.bias) {
@@ -79,18 +101,16 @@ __device__ __forceinline__ void gemm_pre(const gm::Args& a, const uint32_t* v, i
         if (n + i < a.N) f[i] += a.bias[n + i];
     }
   }
-  if (a.act != kIdentity) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) f[i] = act_rt(f[i], a.act);
-  }
 }
 
 __global__ void __launch_bounds__(gm::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                const __grid_constant__ CUtensorMap td, const __grid_constant__ CUtensorMap tr,
                 const __grid_constant__ gm::Args a) {
   using namespace gm;
   extern __shared__ __align__(1024) uint8_t smem[];
-  Bars& B = *reinterpret_cast<Bars*>(smem + a.stages * a.stage_bytes);
+  uint8_t* s_st = smem + a.s_stage;  // output staging: slabs of [128 rows][64 cols] fp16, 128B-swizzled
+  Bars& B = *reinterpret_cast<Bars*>(smem + a.s_stage + a.slabs * 16384);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -99,8 +119,9 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.acc_full[i], 1);
-      mbar_init(&B.acc_empty[i], 4);
+      mbar_init(&B.acc_empty[i], 8);
     }
+    mbar_init(&B.res_full, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -163,78 +184,133 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;
+    // warp w: TMEM lane quadrant w % 4 (rows 32 q .. 32 q + 31), column half
+    // (w - 2) / 4 of the tile's 16-column units
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const bool leader = threadIdx.x == 64;
+    const int units = a.BN / 16;
+    const int u_lo = half ? (units + 1) / 2 : 0, u_hi = half ? units : (units + 1) / 2;
+    const int r = q * 32 + lane;  // row in the tile
     int it = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
       const int ab = it & 1, u = it >> 1;
       const int tn = tile / a.tiles_m, tm = tile % a.tiles_m;
+      const int n0 = tn * a.BN;
+      if (leader) {
+        bulk_wait_read0_g();  // the previous tile's stores have left the staging buffer
+        if (a.has_res) {
+          mbar_arrive_expect_tx(&B.res_full, a.slabs * 16384);
+          for (int sl = 0; sl < a.slabs; ++sl) tma_load_2d(s_st + sl * 16384, &tr, n0 + sl * 64, tm * 128, &B.res_full);
+        }
+      }
+      gm_bar(kEpiThreads);
       mbar_wait(&B.acc_full[ab], u & 1);
       tc_fence_after();
-      const int row = tm * 128 + q * 32 + lane;
       const uint32_t tb0 = tmem_lane_addr(tmem, q, ab * (a.tmem_cols / 2));
-      const int n0 = tn * a.BN;
-      float mean = 0.f, rstd = 1.f;
+      // stage one 16-column unit (fp16, 128B-swizzled; + residual from the staging tile)
+      auto stage_unit = [&](int uu, uint4* o) {
+        const int c16 = uu * 16, sl = c16 >> 6, c8 = (c16 & 63) >> 3;
+        uint8_t* rowp = s_st + sl * 16384 + r * 128;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint8_t* p = rowp + (((c8 + hh) ^ (r & 7)) << 4);
+          if (a.has_res) {
+            float rr[8], g[8];
+            unpack8(lds128(p), rr);
+            unpack8(o[hh], g);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) g[i] += rr[i];
+            o[hh] = pack8(g);
+          }
+          *reinterpret_cast<uint4*>(p) = o[hh];
+        }
+      };
+      if (a.has_res) mbar_wait(&B.res_full, it & 1);
       if (a.ln_g) {
-        // row LayerNorm over the whole output row (tiles_n == 1): two-pass
-        // statistics from TMEM (mean, then centred second moment)
-        float s1 = 0.f;
-        for (int c0 = 0; c0 < a.BN; c0 += 16) {
-          uint32_t v[16];
-          WL_TMEM_LD16(tb0 + c0, v);
-          tmem_ld_wait();
-          float f[16];
-          gemm_pre(a, v, n0 + c0, f);
+        // row LayerNorm over the whole output row (tiles_n == 1, N <= 128):
+        // each warp keeps its half of the row in registers; the two halves'
+        // partial sums meet in shared memory (fixed order: deterministic);
+        // two-pass statistics (mean, then the centred second moment), fp32
+        uint32_t v[64];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n0 + c0 + i < a.N) s1 += f[i];
-        }
-        mean = s1 / (float)a.N;
-        float s2 = 0.f;
-        for (int c0 = 0; c0 < a.BN; c0 += 16) {
-          uint32_t v[16];
-          WL_TMEM_LD16(tb0 + c0, v);
-          tmem_ld_wait();
-          float f[16];
-          gemm_pre(a, v, n0 + c0, f);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n0 + c0 + i < a.N) s2 += (f[i] - mean) * (f[i] - mean);
-        }
-        rstd = rsqrtf(s2 / (float)a.N + a.ln_eps);
-      }
-      for (int c0 = 0; c0 < a.BN; c0 += 16) {
-        uint32_t v[16];
-        WL_TMEM_LD16(tb0 + c0, v);
+        for (int j = 0; j < 4; ++j)
+          if (u_lo + j < u_hi) WL_TMEM_LD16(tb0 + (u_lo + j) * 16, (v + 16 * j));
         tmem_ld_wait();
-        const int n = n0 + c0;
-        if (row < a.M && n < a.N) {
-          float f[16];
-          gemm_pre(a, v, n, f);
-          if (a.ln_g) {
+        float s1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (u_lo + j < u_hi) {
+            float f[16];
+            gemm_bias(a, v + 16 * j, n0 + (u_lo + j) * 16, f);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const int c = n + i < a.N ? n + i : a.N - 1;
-              f[i] = (f[i] - mean) * rstd * a.ln_g[c] + a.ln_b[c];
+              v[16 * j + i] = __float_as_uint(f[i]);
+              if (n0 + (u_lo + j) * 16 + i < a.N) s1 += f[i];
             }
           }
+        B.ln_red[0][half][r] = s1;
+        gm_bar(kEpiThreads);
+        const float mean = (B.ln_red[0][0][r] + B.ln_red[0][1][r]) / (float)a.N;
+        float s2 = 0.f;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (n + 8 * h >= a.N) break;
-            float* g = f + 8 * h;
-            if (a.res) {
-              float r[8];
-              unpack8(__ldg(reinterpret_cast<const uint4*>(a.res + (size_t)row * a.ldr + n + 8 * h)), r);
+        for (int j = 0; j < 4; ++j)
+          if (u_lo + j < u_hi)
 #pragma unroll
-              for (int i = 0; i < 8; ++i) g[i] += r[i];
+            for (int i = 0; i < 16; ++i) {
+              const float d = __uint_as_float(v[16 * j + i]) - mean;
+              if (n0 + (u_lo + j) * 16 + i < a.N) s2 += d * d;
             }
-            *reinterpret_cast<uint4*>(a.D + (size_t)row * a.ldd + n + 8 * h) = pack8(g);
+        B.ln_red[1][half][r] = s2;
+        gm_bar(kEpiThreads);
+        const float rstd = rsqrtf((B.ln_red[1][0][r] + B.ln_red[1][1][r]) / (float)a.N + a.ln_eps);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (u_lo + j < u_hi) {
+            float f[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = n0 + (u_lo + j) * 16 + i, c = n < a.N ? n : a.N - 1;
+              f[i] = (__uint_as_float(v[16 * j + i]) - mean) * rstd * __ldg(a.ln_g + c) + __ldg(a.ln_b + c);
+            }
+            uint4 o[2] = {pack8(f), pack8(f + 8)};
+            stage_unit(u_lo + j, o);
           }
+      } else {
+        // 64 columns (four x16 TMEM loads) per wait
+        for (int u0 = u_lo; u0 < u_hi; u0 += 4) {
+          uint32_t v[64];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (u0 + j < u_hi) WL_TMEM_LD16(tb0 + (u0 + j) * 16, (v + 16 * j));
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (u0 + j < u_hi) {
+              float f[16];
+              gemm_bias(a, v + 16 * j, n0 + (u0 + j) * 16, f);
+              uint4 o[2];
+              uint32_t* ow = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+                if (a.act) h = act_rt_h2(h, a.act);
+                ow[i] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              stage_unit(u0 + j, o);
+            }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&B.acc_empty[ab]);
+      fence_async_smem();
+      gm_bar(kEpiThreads);
+      if (leader) {
+        for (int sl = 0; sl < a.slabs; ++sl) tma_store_2d(&td, s_st + sl * 16384, n0 + sl * 64, tm * 128);
+        bulk_commit_g();
+      }
     }
+    if (leader) bulk_wait0_g();
   }
   tc_fence_before();
   __syncthreads();
@@ -268,40 +344,38 @@ int gemm_run(const void* A, int M, int K, int lda, const void* Bw, int N, int ld
   a.M = M;
   a.N = N;
   a.BN = pick_bn(N);
-  if (e.ln_g && a.BN < N) return set_error(WL_EUNSUPPORTED, "gemm: row LayerNorm needs N <= 256 (N = %d)", N);
+  if (e.ln_g && (a.BN < N || N > 128 || e.act))
+    return set_error(WL_EUNSUPPORTED, "gemm: the row-LayerNorm epilogue needs N <= 128 and no activation (N = %d)", N);
   a.tiles_m = (M + 127) / 128;
   a.tiles = a.tiles_m * ((N + a.BN - 1) / a.BN);
   a.kblocks = (K + gm::kBK - 1) / gm::kBK;
   a.stage_bytes = 16384 + a.BN * 128;
-  a.stages = (gm::kSmemMax - (int)sizeof(gm::Bars) - 64) / a.stage_bytes;
+  a.slabs = (a.BN + 63) / 64;
+  a.stages = (gm::kSmemMax - a.slabs * 16384 - (int)sizeof(gm::Bars) - 64) / a.stage_bytes;
   if (a.stages > gm::kMaxStages) a.stages = gm::kMaxStages;
-  a.ldd = ldd;
-  a.ldr = e.ldr;
+  a.s_stage = a.stages * a.stage_bytes;
   a.act = e.act;
+  a.has_res = e.res != nullptr;
   a.ln_eps = e.ln_eps;
   a.bias = e.bias;
   a.ln_g = e.ln_g;
   a.ln_b = e.ln_b;
-  a.res = e.res;
-  a.D = reinterpret_cast<__half*>(D);
   a.tmem_cols = 32;
   while (a.tmem_cols < (uint32_t)(2 * a.BN)) a.tmem_cols *= 2;
-  CUtensorMap tA, tB;
-  {
-    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
-    const uint64_t strides[1] = {(uint64_t)lda * 2};
-    const uint32_t box[2] = {64, 128};
-    if (int r = encode_tmap(&tA, A, 2, dims, strides, box, true)) return r;
-  }
-  {
-    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
-    const uint64_t strides[1] = {(uint64_t)ldb * 2};
-    const uint32_t box[2] = {64, (uint32_t)a.BN};
-    if (int r = encode_tmap(&tB, Bw, 2, dims, strides, box, true)) return r;
-  }
-  const int smem = a.stages * a.stage_bytes + (int)sizeof(gm::Bars);
+  CUtensorMap tA, tB, tD, tR;
+  auto map2 = [](CUtensorMap* m, const void* base, int inner, int outer, int ld, int box_outer) {
+    const uint64_t dims[2] = {(uint64_t)inner, (uint64_t)outer};
+    const uint64_t strides[1] = {(uint64_t)ld * 2};
+    const uint32_t box[2] = {64, (uint32_t)box_outer};
+    return encode_tmap(m, base, 2, dims, strides, box, true);
+  };
+  if (int r = map2(&tA, A, K, M, lda, 128)) return r;
+  if (int r = map2(&tB, Bw, K, N, ldb, a.BN)) return r;
+  if (int r = map2(&tD, D, N, M, ldd, 128)) return r;
+  if (int r = map2(&tR, e.res ? (const void*)e.res : D, N, M, e.res ? e.ldr : ldd, 128)) return r;
+  const int smem = a.s_stage + a.slabs * 16384 + (int)sizeof(gm::Bars);
   const int grid = a.tiles < kNumSMs ? a.tiles : kNumSMs;
-  return launch_pdl(gemm_kernel, grid, gm::kThreads, smem, st, "gemm launch", tA, tB, a);
+  return launch_pdl(gemm_kernel, grid, gm::kThreads, smem, st, "gemm launch", tA, tB, tD, tR, a);
 }
 
 int gemm_init() {
