@@ -94,6 +94,7 @@ void wl_debug_set_trace(void* dev_ptr) {
   wl::mb_set_trace(dev_ptr);
   wl::cf2_set_trace(dev_ptr);
   wl::cf_set_trace(dev_ptr);
+  wl::ffn_set_trace(dev_ptr);
 }
 
 const char* wl_last_error(void) { return g_last_error.c_str(); }

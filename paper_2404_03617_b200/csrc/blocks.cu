@@ -49,8 +49,8 @@ int kernel_launches(const wl_block_desc& d) {
   if (d.kind == WL_KIND_HEAD || d.kind == WL_KIND_PATCH_STEM || d.kind == WL_KIND_DOWNSAMPLE ||
       d.kind == WL_KIND_LN_HEAD)
     return 2;
-  if (d.kind == WL_KIND_FFN) return 2 * ffn_row_batches(d);
-  if (cnx_wide(d)) return 1 + 2 * ffn_row_batches(d);
+  if (d.kind == WL_KIND_FFN) return ffn_launches(d);
+  if (cnx_wide(d)) return 1 + ffn_launches(d);
   if (d.kind == WL_KIND_MBCONV) return mb_kernel_launches(d);
   return 1;
 }

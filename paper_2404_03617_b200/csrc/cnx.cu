@@ -346,9 +346,13 @@ int64_t hidden_rows(int64_t M, int hid) {
   return r < M ? r : M;
 }
 
-// z = phi(x U + a) V + b (+ res): two GEMMs per row batch, hidden in ws
+// z = phi(x U + a) V + b (+ res): the fused kernel (hidden on chip, ffn.cu)
+// when its TMEM plan fits (C <= 384), else two GEMMs per row batch with the
+// hidden in the L2-resident workspace
 int ffn_rows(const __half* x, int64_t M, int C, int hid, int K, const __half* ut, const float* a, const __half* vt,
-             const float* b, int act, const __half* res, __half* z, __half* hbuf, cudaStream_t st) {
+             const float* b, int act, const __half* res, __half* z, __half* hbuf, const uint8_t* wimg,
+             cudaStream_t st) {
+  if (K == C && wimg && ffn_fused_ok(M, C, hid)) return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st);
   const int64_t rb = hidden_rows(M, hid);
   for (int64_t r0 = 0; r0 < M; r0 += rb) {
     const int rows = (int)(M - r0 < rb ? M - r0 : rb);
@@ -376,7 +380,7 @@ int common_dims(const wl_block_desc& d) {
 // ------------------------------------------------------------------ FFN
 // weights (reference order, machine.py:345-351): u (C, hid), a (hid), v (hid, C), b (C)
 struct FfnLayout {
-  int64_t o_a, o_b, o_u, o_v, total;
+  int64_t o_a, o_b, o_u, o_v, o_img, total;
 };
 FfnLayout ffn_layout(const wl_block_desc& d) {
   const int64_t C = d.c, hid = (int64_t)d.expansion * d.c;
@@ -385,7 +389,8 @@ FfnLayout ffn_layout(const wl_block_desc& d) {
   L.o_b = a128(hid * 4);
   L.o_u = L.o_b + a128(C * 4 + 64);
   L.o_v = L.o_u + a128(hid * C * 2);
-  L.total = L.o_v + a128(hid * C * 2);
+  L.o_img = L.o_v + a128(hid * C * 2);  // fused-kernel weight images (0 bytes when it has no plan)
+  L.total = L.o_img + a128(ffn_images_bytes((int)C, (int)hid));
   return L;
 }
 int ffn_validate(const wl_block_desc& d) {
@@ -415,6 +420,7 @@ int ffn_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   put_f32(out, L.o_b, w[3], C);
   put_t16(out, L.o_u, w[0], C, hid);  // U^T: (hid, C)
   put_t16(out, L.o_v, w[2], hid, C);  // V^T: (C, hid)
+  ffn_pack_images(C, hid, w[0], w[2], out + L.o_img);
   return WL_OK;
 }
 int64_t ffn_ws(const wl_block_desc& d) {
@@ -428,14 +434,15 @@ int ffn_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void*
   return ffn_rows(reinterpret_cast<const __half*>(x), M, d.c, d.expansion * d.c, d.c,
                   reinterpret_cast<const __half*>(pk + L.o_u), reinterpret_cast<const float*>(pk + L.o_a),
                   reinterpret_cast<const __half*>(pk + L.o_v), reinterpret_cast<const float*>(pk + L.o_b), d.act,
-                  nullptr, reinterpret_cast<__half*>(z), reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr), st);
+                  nullptr, reinterpret_cast<__half*>(z), reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr),
+                  L.o_img < L.total ? pk + L.o_img : nullptr, st);
 }
 
 // ------------------------------------------------- wide ConvNeXt block
 // weights (cf_weight_numel order): w_conv (C, k, k, 1), b_conv (C), ln_gamma, ln_beta,
 // u (C, hid), a (hid), v (hid, C), b (C)
 struct WideLayout {
-  int64_t o_wdw, o_bdw, o_g, o_be, o_a, o_b, o_u, o_v, total;
+  int64_t o_wdw, o_bdw, o_g, o_be, o_a, o_b, o_u, o_v, o_img, total;
 };
 WideLayout wide_layout(const wl_block_desc& d) {
   const int64_t C = d.c, hid = (int64_t)d.expansion * d.c, taps = (int64_t)d.ksize * d.ksize;
@@ -448,7 +455,8 @@ WideLayout wide_layout(const wl_block_desc& d) {
   L.o_b = L.o_a + a128(hid * 4 + 64);
   L.o_u = L.o_b + a128(C * 4 + 64);
   L.o_v = L.o_u + a128(hid * C * 2);
-  L.total = L.o_v + a128(hid * C * 2);
+  L.o_img = L.o_v + a128(hid * C * 2);
+  L.total = L.o_img + a128(ffn_images_bytes((int)C, (int)hid));
   return L;
 }
 }  // namespace
@@ -457,10 +465,14 @@ int ffn_row_batches(const wl_block_desc& d) {
   const int64_t M = (int64_t)d.n * d.h * d.w, rb = hidden_rows(M, d.expansion * d.c);
   return (int)((M + rb - 1) / rb);
 }
+int ffn_launches(const wl_block_desc& d) {
+  const int64_t M = (int64_t)d.n * d.h * d.w;
+  return ffn_fused_ok(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
+}
 
 bool cnx_wide(const wl_block_desc& d) {
   return d.kind == WL_KIND_CONVFIRST && d.norm == WL_NORM_LAYERNORM && d.group_width == 1 && d.stride == 1 &&
-         d.c > 128;
+         (d.c > 128 || (d.c >= 96 && d.ksize == 7));
 }
 int cnx_wide_validate(const wl_block_desc& d) {
   if (int e = common_dims(d)) return e;
@@ -485,6 +497,7 @@ int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   put_f32(out, L.o_b, w[7], C);
   put_t16(out, L.o_u, w[4], C, hid);
   put_t16(out, L.o_v, w[6], hid, C);
+  ffn_pack_images(C, hid, w[4], w[6], out + L.o_img);
   return WL_OK;
 }
 int64_t cnx_wide_ws(const wl_block_desc& d) {
@@ -509,7 +522,7 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
   return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
                   reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
                   reinterpret_cast<const float*>(pk + L.o_b), d.act, reinterpret_cast<const __half*>(x),
-                  reinterpret_cast<__half*>(z), hb, st);
+                  reinterpret_cast<__half*>(z), hb, L.o_img < L.total ? pk + L.o_img : nullptr, st);
 }
 
 namespace {
@@ -701,6 +714,7 @@ int lh_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
 
 int cnx_init() {
   if (int e = gemm_init()) return e;
+  if (int e = ffn_fused_init()) return e;
   for (auto k : {dwln_kernel<7>, dwln_kernel<3>})
     if (int e = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
                            "cudaFuncSetAttribute(dwln)"))

@@ -86,8 +86,17 @@ int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out);
 int64_t cnx_wide_ws(const wl_block_desc& d);
 int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st);
 int ffn_row_batches(const wl_block_desc& d);
+int ffn_launches(const wl_block_desc& d);
+// fused FFN (ffn.cu): hidden kept on chip
+bool ffn_fused_ok(int64_t M, int C, int hid);
+int ffn_fused_run(const void* x, int64_t M, int C, int hid, const void* wimg, const float* abias, const float* bbias,
+                  int act, const void* res, void* z, cudaStream_t st);
+int64_t ffn_images_bytes(int C, int hid);
+void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* out);
+int ffn_fused_init();
 void mb_set_trace(void* p);
 void cf2_set_trace(void* p);
 void cf_set_trace(void* p);
+void ffn_set_trace(void* p);
 
 }  // namespace wl

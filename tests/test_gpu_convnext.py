@@ -34,6 +34,10 @@ CASES = [
     ("ffn_c48_relu", FFN(4, "relu"), TensorDims(1, 7, 9, 48), None),
     ("ffn_c192_silu", FFN(4, "silu"), TensorDims(2, 5, 33, 192), None),
     ("ffn_c768", FFN(4, "gelu"), TensorDims(1, 1, 200, 768), None),
+    # the fused kernel (hidden on chip, ffn.cu): HC = 128 (C <= 256) / 64 (C = 384), multi-tile grids
+    ("ffn_fused_c384", FFN(4, "gelu"), TensorDims(2, 14, 14, 384), None),
+    ("ffn_fused_c256_identity", FFN(2, "identity"), TensorDims(1, 3, 700, 256), None),
+    ("ffn_fused_c128_many_tiles", FFN(4, "relu"), TensorDims(4, 56, 100, 128), None),
     # ConvNeXt-T units at their network shapes (small batch)
     ("patch_stem_224", PatchifyStem(96), TensorDims(2, 224, 224, 3), None),
     ("patch_stem_rect", PatchifyStem(64, 4), TensorDims(1, 40, 24, 3), None),
