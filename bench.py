@@ -282,6 +282,7 @@ def run_gpu(args):
             steps = 2
             cpu = cpu_describe(pool, steps, sum(pool.step() for _ in range(steps)))
             pool.close()
+        others = None if args.skip_configs else other_configs(peak_burst, flush)
         line = {
             "metric": f"images/sec ({args.model}@224 inference)",
             "value": value,
@@ -334,11 +335,74 @@ def run_gpu(args):
             "clocks": clocks,
             "gpu_launches": model.launch_count() * args.steps,
             "units": {u.label: round(t * 1e6, 1) for u, t in zip(model.units, unit_s)},
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _device_time(launch, flush, steps=10, warmup=3):
+    """Mean device time (s) of ``launch`` captured in a CUDA graph, L2
+    flushed before every timed replay (outside the event pair)."""
+    import torch
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        launch()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        launch()
+    for _ in range(warmup):
+        g.replay()
+    ts = []
+    for _ in range(steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    return statistics.mean(ts)
+
+
+def other_configs(peak_burst, flush):
+    """The other BASELINE.json configs, measured on this GPU beside the
+    headline: C1 (ConvNeXt-style block 56x56x96 b8), C2 (MBConv T=1
+    28x28x80 b128), C4 (ConvNeXt-T 224 b128 end to end). Device-resident
+    inputs, CUDA graphs, L2 flushed per replay; efficiency = algorithmic
+    FLOPs / time / measured bf16 burst."""
+    import torch
+
+    from paper_2404_03617_b200 import complexity
+    from paper_2404_03617_b200.blocks import FusedBlock
+    from paper_2404_03617_b200.convnext import convnext_tiny, network_macs
+    from paper_2404_03617_b200.core import ConvNeXtBlock, MBConv, TensorDims
+    from paper_2404_03617_b200.scheduler import FusedNetwork
+
+    out = {}
+    for key, blk, dims in (("C1_convnext_block_56x56x96_b8", ConvNeXtBlock(7, 4, "gelu"), TensorDims(8, 56, 56, 96)),
+                           ("C2_mbconv_t1_28x28x80_b128", MBConv(1, 4, 0.25), TensorDims(128, 28, 28, 80))):
+        m = FusedBlock(blk, dims, seed=3)
+        x = torch.randn(*m.in_shape, device="cuda").half()
+        z = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
+        t = _device_time(lambda: m.launch(x, z), flush)
+        ops = complexity.block_ops(blk, dims, dims.c)
+        out[key] = {"us": t * 1e6, "tflops": ops / t / 1e12, "frac_of_burst": ops / t / peak_burst,
+                    "images_per_s": dims.n / t}
+    spec = convnext_tiny(224)
+    net = FusedNetwork(spec, batch=128, seed=5)
+    net.x.normal_()
+    t = _device_time(lambda: net.launch_all(), flush)
+    ops = 2 * network_macs(spec) * 128
+    out["C4_convnext_tiny_224_b128"] = {"ms": t * 1e3, "images_per_s": 128 / t, "tflops": ops / t / 1e12,
+                                        "frac_of_burst": ops / t / peak_burst, "gpu_launches": net.launch_count()}
+    return out
 
 
 def _relaunch_distributed(n: int) -> int:
@@ -364,6 +428,7 @@ def main():
     ap.add_argument("--model", default="convfirstnet-pico")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-configs", action="store_true", help="skip the C1/C2/C4 side measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
