@@ -136,6 +136,19 @@ WL_API int wl_downsample_fwd(const wl_block_desc* d, const void* x, const void* 
 WL_API int wl_ln_head_fwd(const wl_block_desc* d, const void* x, const void* packed, void* z, void* workspace,
                    void* stream);
 
+/* A stage: nblocks consecutive blocks with the SAME descriptor (stride 1,
+ * channels kept) in one launch; block i+1 consumes block i's output without
+ * it leaving the SM (the per-stage persistent kernel of machine.py:1091-1120,
+ * PAPER.md:1328-1347). packed: HOST array of nblocks DEVICE pointers to each
+ * block's packed weights; x / z: the stage's input / output; workspace as
+ * for one block. Currently the stride-1 T=8 MBConv (W <= 14, <= 20 blocks);
+ * WL_EUNSUPPORTED otherwise (launch the blocks one by one). */
+WL_API int wl_stage_forward(const wl_block_desc* d, int nblocks, const void* x, const void* const* packed, void* z,
+                            void* workspace, void* stream);
+/* most blocks one wl_stage_forward may run for this descriptor (0: no stage
+ * kernel for it) */
+WL_API int wl_stage_max_blocks(const wl_block_desc* d);
+
 /* The pointwise contraction of the layer-wise units (1x1 conv / linear),
  * exposed for the layer-wise FFN schedule and for direct testing:
  * D[M][N] = act(A[M][K] . B[N][K]^T + bias[N]) (+ res[M][N]); fp16 storage,

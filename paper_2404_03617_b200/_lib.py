@@ -45,6 +45,8 @@ EXPORTS = (
     "wl_ln_head_fwd",
     "wl_execute_numeric",
     "wl_gemm",
+    "wl_stage_forward",
+    "wl_stage_max_blocks",
     "wl_output_dims",
     "wl_debug_set_trace",
 )
@@ -120,6 +122,8 @@ def lib() -> ctypes.CDLL:
             [D, P(ctypes.c_float), P(P(ctypes.c_float)), ctypes.c_int, P(ctypes.c_float)],
         ),
         "wl_output_dims": (ctypes.c_int, [D] + [P(ctypes.c_int32)] * 4),
+        "wl_stage_forward": (ctypes.c_int, [D, ctypes.c_int, vp, P(vp), vp, vp, vp]),
+        "wl_stage_max_blocks": (ctypes.c_int, [D]),
         "wl_gemm": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
                                    ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, vp]),
         "wl_debug_set_trace": (None, [vp]),

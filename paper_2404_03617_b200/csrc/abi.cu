@@ -190,6 +190,19 @@ int wl_ln_head_fwd(const wl_block_desc* d, const void* x, const void* p, void* z
   return fwd_kind(WL_KIND_LN_HEAD, d, x, p, z, ws, s);
 }
 
+int wl_stage_forward(const wl_block_desc* d, int nblocks, const void* x, const void* const* packed, void* z, void* ws,
+                     void* stream) {
+  if (int e = wl_validate(d)) return e;
+  if (!x || !packed || !z || !ws) return set_error(WL_EINVAL, "null tensor pointer");
+  if (d->kind != WL_KIND_MBCONV) return set_error(WL_EUNSUPPORTED, "stage launches cover MBConv blocks");
+  return mb1_stage_forward(*d, nblocks, x, packed, z, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int wl_stage_max_blocks(const wl_block_desc* d) {
+  if (!d || validate_desc(*d) != WL_OK || d->kind != WL_KIND_MBCONV) return 0;
+  return mb1_stage_max(*d);
+}
+
 int wl_gemm(const void* a, int m, int k, int lda, const void* b, int n, int ldb, void* d, int ldd, const float* bias,
             int act, const void* res, int ldr, void* stream) {
   if (!a || !b || !d) return set_error(WL_EINVAL, "null tensor pointer");

@@ -94,6 +94,10 @@ int ffn_fused_run(const void* x, int64_t M, int C, int hid, const void* wimg, co
 int64_t ffn_images_bytes(int C, int hid);
 void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* out);
 int ffn_fused_init();
+// stride-1 MBConv stage launch (mb_s1.cu)
+int mb1_stage_max(const wl_block_desc& d);
+int mb1_stage_forward(const wl_block_desc& d, int nblk, const void* x, const void* const* packed, void* z, void* ws,
+                      cudaStream_t st);
 void mb_set_trace(void* p);
 void cf2_set_trace(void* p);
 void cf_set_trace(void* p);

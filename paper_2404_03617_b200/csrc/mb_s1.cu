@@ -31,6 +31,12 @@
 //   C  producer reloads h2 + W_prj by half-chunks (4-slot ring over the dead
 //      h1 / W_exp buffers); conv warps gate them in place; MMA: Z += h2' . W_prj
 //   D  E warps: z = Z + b_prj + x (in place over the x tile) -> TMA store
+// Stage mode (nblk > 1, the paper's per-stage persistence, machine.py:1091-1120 /
+// PAPER.md:1328-1347): the CTA runs nblk consecutive stride-1 blocks of its
+// image; block b's z stays in the x tile in shared memory as block b+1's input
+// (only the stage's first input and last output cross HBM), the next block's
+// header and W_ex land after phase D, and every barrier keeps counting phases
+// across blocks.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
@@ -40,6 +46,7 @@
 
 namespace wl {
 
+constexpr int kMb1MaxStage = 20;
 struct Mb1Args {
   int n, H, W, C, hid, sq, nch, NT;
   int s_x, s_h1, s_h1_bytes, s_w, s_wex, s_hdr, s_se, s_bar, smem;
@@ -49,6 +56,8 @@ struct Mb1Args {
   int t_e, t_z, tmem_cols;
   int slot_bytes;  // phase C ring slot: h2 half-chunk (NT x 8 KB) + W_prj half-chunk (C x 32 x 2)
   const uint8_t* wpack;
+  int nblk;                           // consecutive blocks run by this launch (a stage)
+  const uint8_t* wpacks[kMb1MaxStage];  // their packed blobs (nblk > 1)
   uint8_t* h2;  // workspace: [n][nch][NT][8 groups][128 rows][16 B]
   long long* trace;
 };
@@ -66,6 +75,7 @@ struct Bars {
   uint64_t a_done;
   uint64_t pa_full[4], pa_ready[4], pa_empty[4];
   uint64_t z_full, se_full;
+  uint64_t d_done;  // stage: block b's output tile is in place (x of block b + 1), hdr / W_ex free
   uint32_t tmem_base;
 };
 }  // namespace mb1
@@ -143,6 +153,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int img = blockIdx.x;
   const int nch = a.nch;
+  const int nblk = a.nblk;
+  auto wp_of = [&](int blk) -> const uint8_t* { return nblk > 1 ? a.wpacks[blk] : a.wpack; };
 
   if (threadIdx.x == 0) {
     mbar_init(&B.x_full, 1);
@@ -163,6 +175,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     mbar_init(&B.a_done, 1);
     mbar_init(&B.z_full, 1);
     mbar_init(&B.se_full, 1);
+    mbar_init(&B.d_done, 256);
     fence_mbar_init();
   }
   if (warp == kMma) tmem_alloc_n(&B.tmem_base, a.tmem_cols);
@@ -182,35 +195,43 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------------------ producer
       prefetch_tmap(&tmap_x);
-      mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
-      bulk_g2s(s_hdr, a.wpack, a.hdr_bytes, &B.hdr_full);
-      mbar_arrive_expect_tx(&B.x_full, KH * 64 * 2 * 16 * H);
-      for (int kh = 0; kh < KH; ++kh) tma_load_4d(s_x + kh * XH, &tmap_x, kh * 64, -1, 0, img, &B.x_full);
-      mbar_arrive_expect_tx(&B.se_full, a.sq * a.hid * 2);
-      bulk_g2s(s_wex, a.wpack + a.o_se + a.o_wex, a.sq * a.hid * 2, &B.se_full);
-      const uint32_t wbytes = kHC * C * 2;
-      for (int j = 0; j < nch; ++j) {
-        const int b = j & 1, u = j >> 1;
-        mbar_wait(&B.w_empty[b], (u & 1) ^ 1);
-        mbar_arrive_expect_tx(&B.w_full[b], wbytes);
-        bulk_g2s(s_w + b * wbytes, a.wpack + a.o_wexp + (size_t)j * wbytes, wbytes, &B.w_full[b]);
-      }
-      // phase C: h2 chunks come back once phase A stored them all and released
-      // the h1 / W_exp buffers the ring overlays
-      // ring of 4 half-chunks (32 hidden channels: NT x 8 KB of h2 + the
-      // matching 4 K-columns of W_prj), so several reloads are in flight
-      mbar_wait(&B.a_done, 0);
-      const uint32_t vbytes = C * 32 * 2;
+      const uint32_t wbytes = kHC * C * 2, vbytes = C * 32 * 2;
       const uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
-      for (int qq = 0; qq < 2 * nch; ++qq) {
-        const int s = qq & 3, u = qq >> 2, j = qq >> 1, half = qq & 1;
-        mbar_wait(&B.pa_empty[s], (u & 1) ^ 1);
-        uint8_t* slot = s_h1 + s * a.slot_bytes;
-        mbar_arrive_expect_tx(&B.pa_full[s], NT * 8192 + vbytes);
-        for (int t = 0; t < NT; ++t)
-          bulk_g2s(slot + t * 8192, h2img + ((size_t)j * NT + t) * 16384 + half * 8192, 8192, &B.pa_full[s]);
-        bulk_g2s(slot + NT * 8192, a.wpack + a.o_wprj + (size_t)j * 2 * vbytes + half * vbytes, vbytes,
-                 &B.pa_full[s]);
+      for (int blk = 0; blk < nblk; ++blk) {
+        const uint8_t* wp = wp_of(blk);
+        if (blk > 0) mbar_wait(&B.d_done, (blk - 1) & 1);  // previous block's phase D done: hdr, W_ex, x free
+        mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
+        bulk_g2s(s_hdr, wp, a.hdr_bytes, &B.hdr_full);
+        if (blk == 0) {
+          mbar_arrive_expect_tx(&B.x_full, KH * 64 * 2 * 16 * H);
+          for (int kh = 0; kh < KH; ++kh) tma_load_4d(s_x + kh * XH, &tmap_x, kh * 64, -1, 0, img, &B.x_full);
+        } else {
+          mbar_arrive(&B.x_full);  // the previous block's z, in place (its writers fenced before d_done)
+        }
+        mbar_arrive_expect_tx(&B.se_full, a.sq * a.hid * 2);
+        bulk_g2s(s_wex, wp + a.o_se + a.o_wex, a.sq * a.hid * 2, &B.se_full);
+        for (int j = 0; j < nch; ++j) {
+          const int g = blk * nch + j, b = g & 1, u = g >> 1;
+          mbar_wait(&B.w_empty[b], (u & 1) ^ 1);
+          mbar_arrive_expect_tx(&B.w_full[b], wbytes);
+          bulk_g2s(s_w + b * wbytes, wp + a.o_wexp + (size_t)j * wbytes, wbytes, &B.w_full[b]);
+        }
+        // phase C: h2 chunks come back once phase A stored them all and released
+        // the h1 / W_exp buffers the ring overlays
+        // ring of 4 half-chunks (32 hidden channels: NT x 8 KB of h2 + the
+        // matching 4 K-columns of W_prj), so several reloads are in flight
+        mbar_wait(&B.a_done, blk & 1);
+        for (int qq = 0; qq < 2 * nch; ++qq) {
+          const int gq = blk * 2 * nch + qq;
+          const int s = gq & 3, u = gq >> 2, j = qq >> 1, half = qq & 1;
+          mbar_wait(&B.pa_empty[s], (u & 1) ^ 1);
+          uint8_t* slot = s_h1 + s * a.slot_bytes;
+          mbar_arrive_expect_tx(&B.pa_full[s], NT * 8192 + vbytes);
+          for (int t = 0; t < NT; ++t)
+            bulk_g2s(slot + t * 8192, h2img + ((size_t)j * NT + t) * 16384 + half * 8192, 8192, &B.pa_full[s]);
+          bulk_g2s(slot + NT * 8192, wp + a.o_wprj + (size_t)j * 2 * vbytes + half * vbytes, vbytes,
+                   &B.pa_full[s]);
+        }
       }
     }
   } else if (warp == kMma) {
@@ -219,126 +240,143 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       const uint32_t idesc_e = make_idesc_f16(128, kHC);
       const uint32_t idesc_z = make_idesc_f16(128, C);
       const uint32_t wbytes = kHC * C * 2;
-      mbar_wait(&B.x_full, 0);
-      tc_fence_after();
-      MB1_TRACE(70);
-      for (int j = 0; j < nch; ++j) {
-        const int b = j & 1, u = j >> 1;
-        mbar_wait(&B.w_full[b], u & 1);
-        mbar_wait(&B.e_empty[b], (u & 1) ^ 1);
+      for (int blk = 0; blk < nblk; ++blk) {
+        mbar_wait(&B.x_full, blk & 1);
         tc_fence_after();
-        MB1_TRACE(36 + j);
-        const uint32_t wb = smem_u32(s_w + b * wbytes);
+        MB1_TRACE(70);
+        for (int j = 0; j < nch; ++j) {
+          const int g = blk * nch + j, b = g & 1, u = g >> 1;
+          mbar_wait(&B.w_full[b], u & 1);
+          mbar_wait(&B.e_empty[b], (u & 1) ^ 1);
+          tc_fence_after();
+          MB1_TRACE(36 + j);
+          const uint32_t wb = smem_u32(s_w + b * wbytes);
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
+          for (int t = 0; t < NT; ++t)
 #pragma unroll
-          for (int k = 0; k < C / 16; ++k) {
-            const uint64_t ad = make_sdesc_sw128(smem_u32(s_x) + (k / 4) * XH + t * 16384 + (k % 4) * 32);
-            const uint64_t bd = make_sdesc(wb + k * 2 * 1024, 1024, 128);
-            mma_ss(tmem + a.t_e + (b * NT + t) * kHC, ad, bd, idesc_e, k > 0);
-          }
-        mma_commit(&B.e_full[b]);
-        mma_commit(&B.w_empty[b]);
+            for (int k = 0; k < C / 16; ++k) {
+              const uint64_t ad = make_sdesc_sw128(smem_u32(s_x) + (k / 4) * XH + t * 16384 + (k % 4) * 32);
+              const uint64_t bd = make_sdesc(wb + k * 2 * 1024, 1024, 128);
+              mma_ss(tmem + a.t_e + (b * NT + t) * kHC, ad, bd, idesc_e, k > 0);
+            }
+          mma_commit(&B.e_full[b]);
+          mma_commit(&B.w_empty[b]);
+        }
+        // Z of the previous block must have been drained (phase D) before the
+        // first projection of this one overwrites it: d_done(blk - 1) precedes
+        // x_full(blk), waited above
+        for (int qq = 0; qq < 2 * nch; ++qq) {
+          const int gq = blk * 2 * nch + qq;
+          const int s = gq & 3, u = gq >> 2;
+          mbar_wait(&B.pa_ready[s], u & 1);
+          tc_fence_after();
+          if (!(qq & 1)) MB1_TRACE(52 + (qq >> 1));
+          const uint32_t slot = smem_u32(s_h1 + s * a.slot_bytes);
+          const uint32_t vb = slot + NT * 8192;
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint64_t ad = make_sdesc(slot + t * 8192 + k * 2 * 2048, 2048, 128);
+              const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
+              mma_ss(tmem + a.t_z + t * C, ad, bd, idesc_z, (qq > 0 || k > 0));
+            }
+          mma_commit(&B.pa_empty[s]);
+        }
+        mma_commit(&B.z_full);
       }
-      for (int qq = 0; qq < 2 * nch; ++qq) {
-        const int s = qq & 3, u = qq >> 2;
-        mbar_wait(&B.pa_ready[s], u & 1);
-        tc_fence_after();
-        if (!(qq & 1)) MB1_TRACE(52 + (qq >> 1));
-        const uint32_t slot = smem_u32(s_h1 + s * a.slot_bytes);
-        const uint32_t vb = slot + NT * 8192;
-#pragma unroll
-        for (int t = 0; t < NT; ++t)
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const uint64_t ad = make_sdesc(slot + t * 8192 + k * 2 * 2048, 2048, 128);
-            const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
-            mma_ss(tmem + a.t_z + t * C, ad, bd, idesc_z, (qq > 0 || k > 0));
-          }
-        mma_commit(&B.pa_empty[s]);
-      }
-      mma_commit(&B.z_full);
     }
   } else if (warp < kC0) {
     // ---------------------------------------------- E warps: expand epilogue
     const int e = warp - kE0, q = warp & 3, hh = e >> 2;  // TMEM lane quadrant = warp % 4
     const float* s_bexp = reinterpret_cast<const float*>(s_hdr + a.o_bexp);
-    mbar_wait(&B.hdr_full, 0);
-    for (int j = 0; j < nch; ++j) {
-      const int b = j & 1, u = j >> 1;
-      mbar_wait(&B.e_full[b], u & 1);
-      mbar_wait(&B.h1_empty[b], (u & 1) ^ 1);
-      tc_fence_after();
-      uint8_t* h1 = s_h1 + b * 8 * GS;
+    const float* s_bprj = reinterpret_cast<const float*>(s_hdr + a.o_bprj);
+    for (int blk = 0; blk < nblk; ++blk) {
+      mbar_wait(&B.hdr_full, blk & 1);
+      for (int j = 0; j < nch; ++j) {
+        const int g2 = blk * nch + j, b = g2 & 1, u = g2 >> 1;
+        mbar_wait(&B.e_full[b], u & 1);
+        mbar_wait(&B.h1_empty[b], (u & 1) ^ 1);
+        tc_fence_after();
+        uint8_t* h1 = s_h1 + b * 8 * GS;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        uint32_t v[32];
-        const uint32_t ta = tmem_lane_addr(tmem, q, a.t_e + (b * NT + t) * kHC + hh * 32);
-        WL_TMEM_LD16(ta, v);
-        WL_TMEM_LD16(ta + 16, (v + 16));
-        tmem_ld_wait();
-        const int m = t * 128 + q * 32 + lane;
-        const int i = m & 15;
-        if (m < 16 * H) {
-          const bool real = i >= 1 && i <= a.W;
-          const float* bb = s_bexp + j * kHC + hh * 32;
+        for (int t = 0; t < NT; ++t) {
+          uint32_t v[32];
+          const uint32_t ta = tmem_lane_addr(tmem, q, a.t_e + (b * NT + t) * kHC + hh * 32);
+          WL_TMEM_LD16(ta, v);
+          WL_TMEM_LD16(ta + 16, (v + 16));
+          tmem_ld_wait();
+          const int m = t * 128 + q * 32 + lane;
+          const int i = m & 15;
+          if (m < 16 * H) {
+            const bool real = i >= 1 && i <= a.W;
+            const float* bb = s_bexp + j * kHC + hh * 32;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint4 val = real ? bias_act8<ACT>(v + 8 * g, bb + 8 * g) : make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(h1 + (hh * 4 + g) * GS + (m + 17) * 16) = val;
+            for (int g = 0; g < 4; ++g) {
+              const uint4 val = real ? bias_act8<ACT>(v + 8 * g, bb + 8 * g) : make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4*>(h1 + (hh * 4 + g) * GS + (m + 17) * 16) = val;
+            }
           }
         }
+        tc_fence_before();
+        mbar_arrive(&B.e_empty[b]);
+        mbar_arrive(&B.h1_full[b]);
+        if (e == 0 && lane == 0) MB1_TRACE(4 + j);
+      }
+      // ---------------------------------------------- phase D: z epilogue
+      mbar_wait(&B.z_full, blk & 1);
+      tc_fence_after();
+      if (e == 0 && lane == 0) MB1_TRACE(68);
+      if (hh < KH) {
+#pragma unroll 1
+        for (int t = 0; t < NT; ++t) {
+          const int m = t * 128 + q * 32 + lane;
+          uint8_t* xrow = s_x + hh * XH + m * 128;
+          uint32_t v[64];  // the row's 64 channels in one batch of TMEM loads
+          const uint32_t za = tmem_lane_addr(tmem, q, a.t_z + t * C + hh * 64);
+          WL_TMEM_LD16(za, v);
+          WL_TMEM_LD16(za + 16, (v + 16));
+          WL_TMEM_LD16(za + 32, (v + 32));
+          WL_TMEM_LD16(za + 48, (v + 48));
+          tmem_ld_wait();
+          if (m < 16 * H) {
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+              uint8_t* p = xrow + ((c8 ^ (m & 7)) << 4);
+              float res[8];
+              unpack8(lds128(p), res);
+              const float4 b0 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8);
+              const float4 b1 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8 + 4);
+              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+              float f[8];
+#pragma unroll
+              for (int r = 0; r < 8; ++r) f[r] = __uint_as_float(v[c8 * 8 + r]) + bb[r] + res[r];
+              *reinterpret_cast<uint4*>(p) = pack8(f);
+            }
+          }
+        }
+      }
+      if (blk + 1 < nblk) {
+        // the phase C ring overlaid the h1 planes: restore their zero halo
+        // rows / margins for the next block's conv
+        for (int i = threadIdx.x - kE0 * 32; i < (2 * 8 * GS) / 16; i += 256)
+          reinterpret_cast<uint4*>(s_h1)[i] = make_uint4(0, 0, 0, 0);
       }
       tc_fence_before();
-      mbar_arrive(&B.e_empty[b]);
-      mbar_arrive(&B.h1_full[b]);
-      if (e == 0 && lane == 0) MB1_TRACE(4 + j);
-    }
-    // ------------------------------------------------ phase D: z epilogue
-    mbar_wait(&B.z_full, 0);
-    tc_fence_after();
-    if (e == 0 && lane == 0) MB1_TRACE(68);
-    const float* s_bprj = reinterpret_cast<const float*>(s_hdr + a.o_bprj);
-    if (hh < KH) {
-#pragma unroll 1
-      for (int t = 0; t < NT; ++t) {
-        const int m = t * 128 + q * 32 + lane;
-        uint8_t* xrow = s_x + hh * XH + m * 128;
-        uint32_t v[64];  // the row's 64 channels in one batch of TMEM loads
-        const uint32_t za = tmem_lane_addr(tmem, q, a.t_z + t * C + hh * 64);
-        WL_TMEM_LD16(za, v);
-        WL_TMEM_LD16(za + 16, (v + 16));
-        WL_TMEM_LD16(za + 32, (v + 32));
-        WL_TMEM_LD16(za + 48, (v + 48));
-        tmem_ld_wait();
-        if (m < 16 * H) {
-#pragma unroll
-          for (int c8 = 0; c8 < 8; ++c8) {
-            uint8_t* p = xrow + ((c8 ^ (m & 7)) << 4);
-            float res[8];
-            unpack8(lds128(p), res);
-            const float4 b0 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8);
-            const float4 b1 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8 + 4);
-            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-            float f[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) f[r] = __uint_as_float(v[c8 * 8 + r]) + bb[r] + res[r];
-            *reinterpret_cast<uint4*>(p) = pack8(f);
-          }
+      fence_async_smem();
+      mbar_arrive(&B.d_done);  // z (the next block's x) written and fenced; hdr / W_ex / ring free
+      if (blk + 1 == nblk) {
+        nbar(2, 256);
+        if (e == 0 && lane == 0) {
+          // a TMA store may not start at a negative coordinate (illegal instruction,
+          // tools/probe_tma_store.cu): start at x = 0 one 128-byte row into the tile
+          // (the 128B swizzle is address-based, so the shifted source stays valid)
+          for (int kh = 0; kh < KH; ++kh) tma_store_4d(&tmap_z, s_x + kh * XH + 128, kh * 64, 0, 0, img);
+          bulk_commit_s1();
+          bulk_wait_read0_s1();  // the tile must outlive the reads only; the writes complete on their own
+          MB1_TRACE(69);
         }
       }
-    }
-    tc_fence_before();
-    fence_async_smem();
-    nbar(2, 256);
-    if (e == 0 && lane == 0) {
-      // a TMA store may not start at a negative coordinate (illegal instruction,
-      // tools/probe_tma_store.cu): start at x = 0 one 128-byte row into the tile
-      // (the 128B swizzle is address-based, so the shifted source stays valid)
-      for (int kh = 0; kh < KH; ++kh) tma_store_4d(&tmap_z, s_x + kh * XH + 128, kh * 64, 0, 0, img);
-      bulk_commit_s1();
-      bulk_wait_read0_s1();  // the tile must outlive the reads only; the writes complete on their own
-      MB1_TRACE(69);
     }
   } else {
     // ------------------------------------------ conv warps: HMMA 3x3 T=8 conv
@@ -347,22 +385,23 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     const int gid = lane >> 2, tq = lane & 3;
     const int sq = a.sq, hid = a.hid;
     const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
-    float* s_pool = reinterpret_cast<float*>(s_se);
-    const uint32_t* frag = reinterpret_cast<const uint32_t*>(a.wpack + a.o_frag);
-    const __half* wsq = reinterpret_cast<const __half*>(a.wpack + a.o_se);
+    const uint32_t lrow = (lane & 15), lsel = lane >> 4;  // ldmatrix: row of the fragment, which fragment
+    uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
+    const __half2 one2 = __float2half2_rn(1.f), zero2 = __float2half2_rn(0.f);
+    const __half2 m0 = (gid >= 1 && gid <= a.W) ? one2 : zero2, m1 = (gid + 8 <= a.W) ? one2 : zero2;
+    for (int blk = 0; blk < nblk; ++blk) {
+    const uint8_t* wp = wp_of(blk);
+    const uint32_t* frag = reinterpret_cast<const uint32_t*>(wp + a.o_frag);
+    const __half* wsq = reinterpret_cast<const __half*>(wp + a.o_se);
     // B fragments in pair order (t0,t1) (t3,t4) (t6,t7) (t2,t5) t8: each k16
     // pair is two consecutive registers (mb1_pack)
     uint32_t bw[9];
 #pragma unroll
     for (int tp = 0; tp < 9; ++tp) bw[tp] = __ldg(frag + ((size_t)(0 * 8 + g) * 9 + tp) * 32 + lane);
-    mbar_wait(&B.hdr_full, 0);
-    const uint32_t lrow = (lane & 15), lsel = lane >> 4;  // ldmatrix: row of the fragment, which fragment
-    uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
-    const __half2 one2 = __float2half2_rn(1.f), zero2 = __float2half2_rn(0.f);
-    const __half2 m0 = (gid >= 1 && gid <= a.W) ? one2 : zero2, m1 = (gid + 8 <= a.W) ? one2 : zero2;
+    mbar_wait(&B.hdr_full, blk & 1);
     float s_acc = 0.f;  // squeeze partial of output lane (sq <= 32), summed over this warp's groups
     for (int j = 0; j < nch; ++j) {
-      const int b = j & 1, u = j >> 1;
+      const int g2 = blk * nch + j, b = g2 & 1, u = g2 >> 1;
       const float2 bc = *reinterpret_cast<const float2*>(s_bconv + j * kHC + g * 8 + tq * 2);
       // W_sq rows of this warp's 8 channels, output = lane (consumed after the pool below)
       __half wq[8];
@@ -473,9 +512,9 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     MB1_TRACE(1);
     // ------------------------------------------------ phase B: squeeze-excite
     __half2* s_gate = reinterpret_cast<__half2*>(s_se + hid * 4);
-    const float* bsq = reinterpret_cast<const float*>(a.wpack + a.o_se + a.o_bsq);
+    const float* bsq = reinterpret_cast<const float*>(wp + a.o_se + a.o_bsq);
     const __half2* wex = reinterpret_cast<const __half2*>(s_wex);  // prefetched by the producer
-    const float* bex = reinterpret_cast<const float*>(a.wpack + a.o_se + a.o_bex);
+    const float* bex = reinterpret_cast<const float*>(wp + a.o_se + a.o_bex);
     const float inv_p = 1.f / (float)(a.H * a.W);
     if (tid < sq) {
       float acc = 0.f;
@@ -483,7 +522,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       for (int r = 0; r < 8; ++r) acc += scr[r * 32 + tid];
       scr[256 + tid] = fmaxf(acc * inv_p + bsq[tid], 0.f);
     }
-    mbar_wait(&B.se_full, 0);
+    mbar_wait(&B.se_full, blk & 1);
     nbar(1, 256);
     {
       const float* s_s = scr + 256;
@@ -502,7 +541,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     MB1_TRACE(2);
     // ------------------------------------------------ phase C: gate h2 chunks
     for (int qq = 0; qq < 2 * nch; ++qq) {
-      const int s = qq & 3, u = qq >> 2, j = qq >> 1, half = qq & 1;
+      const int gq = blk * 2 * nch + qq;
+      const int s = gq & 3, u = gq >> 2, j = qq >> 1, half = qq & 1;
       mbar_wait(&B.pa_full[s], u & 1);
       uint8_t* slot = s_h1 + s * a.slot_bytes;
 #pragma unroll
@@ -522,6 +562,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       mbar_arrive(&B.pa_ready[s]);
     }
     MB1_TRACE(3);
+    }  // blocks
   }
   tc_fence_before();
   __syncthreads();
@@ -697,12 +738,7 @@ int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   return WL_OK;
 }
 
-int mb1_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st) {
-  Mb1Args a;
-  mb1_plan(d, a);
-  a.wpack = reinterpret_cast<const uint8_t*>(packed);
-  a.h2 = reinterpret_cast<uint8_t*>(ws) + kWsHeader1;
-  a.trace = g_mb1_trace;
+static int mb1_launch(const wl_block_desc& d, Mb1Args& a, const void* x, void* z, cudaStream_t st) {
   CUtensorMap tx, tz;
   const uint64_t dims[4] = {(uint64_t)d.c, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n};
   const uint64_t strides[3] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2};
@@ -710,6 +746,38 @@ int mb1_forward(const wl_block_desc& d, const void* x, const void* packed, void*
   if (int e = encode_tmap(&tx, x, 4, dims, strides, box, true)) return e;
   if (int e = encode_tmap(&tz, z, 4, dims, strides, box, true)) return e;
   return launch_pdl(mb1_kernel(d), d.n, mb1::kThreads, a.smem, st, "mb_s1 launch", tx, tz, a);
+}
+
+int mb1_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st) {
+  Mb1Args a;
+  mb1_plan(d, a);
+  a.wpack = reinterpret_cast<const uint8_t*>(packed);
+  a.nblk = 1;
+  a.h2 = reinterpret_cast<uint8_t*>(ws) + kWsHeader1;
+  a.trace = g_mb1_trace;
+  return mb1_launch(d, a, x, z, st);
+}
+
+int mb1_stage_max(const wl_block_desc& d) { return mb1_eligible(d) ? kMb1MaxStage : 0; }
+
+// nblk consecutive identical stride-1 MBConv blocks in one launch: the image
+// stays in shared memory between blocks (the per-stage persistent kernel)
+int mb1_stage_forward(const wl_block_desc& d, int nblk, const void* x, const void* const* packed, void* z, void* ws,
+                      cudaStream_t st) {
+  if (!mb1_eligible(d)) return set_error(WL_EUNSUPPORTED, "stage launch: block is not a stride-1 T=8 MBConv (W <= 14)");
+  if (nblk < 1 || nblk > kMb1MaxStage)
+    return set_error(WL_EUNSUPPORTED, "stage launch: 1..%d blocks (got %d)", kMb1MaxStage, nblk);
+  Mb1Args a;
+  mb1_plan(d, a);
+  a.nblk = nblk;
+  for (int i = 0; i < nblk; ++i) {
+    if (!packed[i]) return set_error(WL_EINVAL, "stage launch: packed blob %d is null", i);
+    a.wpacks[i] = reinterpret_cast<const uint8_t*>(packed[i]);
+  }
+  a.wpack = a.wpacks[0];
+  a.h2 = reinterpret_cast<uint8_t*>(ws) + kWsHeader1;
+  a.trace = g_mb1_trace;
+  return mb1_launch(d, a, x, z, st);
 }
 
 int mb1_init() {

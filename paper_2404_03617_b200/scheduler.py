@@ -41,7 +41,7 @@ class FusedNetwork:
     """
 
     def __init__(self, net: NetworkSpec, batch: int, device: str | torch.device = "cuda", seed: int = 0,
-                 weights: dict | None = None):
+                 weights: dict | None = None, stages: bool = True):
         self.net = net
         self.batch = batch
         self.device = torch.device(device)
@@ -71,6 +71,27 @@ class FusedNetwork:
         for u in self.units:
             u.module.workspace = self.workspace
         self.graph: torch.cuda.CUDAGraph | None = None
+        self.steps = self._plan_steps(stages)
+
+    def _plan_steps(self, stages: bool) -> list[tuple[int, int]]:
+        """Launch plan: [(first unit, unit count)]. With ``stages``, runs of
+        consecutive units that share one descriptor and have a stage kernel
+        (``wl_stage_max_blocks``) become ONE launch: each block's output stays
+        on chip as the next block's input (the per-stage persistent kernel,
+        machine.py:1091-1120; only the stage's last output is written). The
+        intermediate units' ``out`` tensors are then not produced."""
+        L = _lib.lib()
+        steps, i = [], 0
+        while i < len(self.units):
+            d = self.units[i].module.desc
+            cap = L.wl_stage_max_blocks(ctypes.byref(d)) if stages else 0
+            j = i + 1
+            while cap and j < len(self.units) and j - i < cap and \
+                    self.units[j].module.desc.as_tuple() == d.as_tuple():
+                j += 1
+            steps.append((i, j - i))
+            i = j
+        return steps
 
     # ----------------------------------------------------------- execution
     @property
@@ -86,9 +107,21 @@ class FusedNetwork:
 
     def launch_all(self, stream=None, x: torch.Tensor | None = None) -> None:
         src = self.x if x is None else x
-        for u in self.units:
-            u.module.launch(src, u.out, self.workspace, stream)
+        for first, count in self.steps:
+            if count == 1:
+                u = self.units[first]
+                u.module.launch(src, u.out, self.workspace, stream)
+            else:
+                u = self.units[first + count - 1]
+                self._launch_stage(first, count, src, u.out, stream)
             src = u.out
+
+    def _launch_stage(self, first: int, count: int, x: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+        mods = [self.units[k].module for k in range(first, first + count)]
+        ptrs = (ctypes.c_void_p * count)(*[m.packed.data_ptr() for m in mods])
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        _lib.check(_lib.lib().wl_stage_forward(ctypes.byref(mods[0].desc), count, x.data_ptr(), ptrs, out.data_ptr(),
+                                               self.workspace.data_ptr(), st), "wl_stage_forward")
 
     def _capture_on(self, x: torch.Tensor) -> torch.cuda.CUDAGraph:
         s = torch.cuda.Stream(device=self.device)
@@ -166,10 +199,14 @@ class FusedNetwork:
 
     def launch_count(self) -> int:
         """Kernels this forward launches, as the library plans them
-        (``wl_kernel_launches``: 1 per fused block, 2 for the head)."""
+        (``wl_kernel_launches``: 1 per fused block, 2 for the head; one per
+        stage launch)."""
         n = 0
-        for u in self.units:
-            k = _lib.lib().wl_kernel_launches(ctypes.byref(u.module.desc))
+        for first, count in self.steps:
+            if count > 1:
+                n += 1
+                continue
+            k = _lib.lib().wl_kernel_launches(ctypes.byref(self.units[first].module.desc))
             _lib.check(k if k < 0 else 0, "wl_kernel_launches")
             n += k
         return n
@@ -184,17 +221,23 @@ class FusedNetwork:
         torch.cuda.synchronize(self.device)
         times = []
         src = self.x
-        for u in self.units:
+        for first, count in self.steps:
+            u = self.units[first + count - 1]
+            if count == 1:
+                go = lambda s=src, u=u: u.module.launch(s, u.out, self.workspace)  # noqa: E731
+            else:
+                go = lambda s=src, f=first, c=count, u=u: self._launch_stage(f, c, s, u.out)  # noqa: E731
             for _ in range(3):
-                u.module.launch(src, u.out, self.workspace)
+                go()
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record()
             for _ in range(iters):
-                u.module.launch(src, u.out, self.workspace)
+                go()
             ev1.record()
             ev1.synchronize()
-            times.append(ev0.elapsed_time(ev1) / iters / 1e3)
+            # a stage launch's time is shared equally by its units
+            times += [ev0.elapsed_time(ev1) / iters / 1e3 / count] * count
             src = u.out
         return times
 

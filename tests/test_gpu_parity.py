@@ -130,7 +130,7 @@ def test_deterministic_and_graph_equals_eager():
                                        ("convfirstnet-tiny", 256), ("convfirstnet-small", 256)])
 def test_network_per_unit_and_logits(model, res):
     net = zoo.at_resolution(zoo.from_name(model), res)
-    m = FusedNetwork(net, batch=2, seed=11)
+    m = FusedNetwork(net, batch=2, seed=11, stages=False)  # every unit's output materialised
     rng = np.random.default_rng(1)
     x = r16(rng, (2, res, res, 3))
     out = m(torch.from_numpy(x).half().cuda())
@@ -155,7 +155,7 @@ def test_full_size_b128_sampled_images(model, res):
     same batch): images 0, 63 and 127 of the b128 forward match the oracle
     unit by unit (the oracle runs on the three images)."""
     net = zoo.at_resolution(zoo.from_name(model), res)
-    m = FusedNetwork(net, batch=128, seed=5)
+    m = FusedNetwork(net, batch=128, seed=5, stages=False)
     m.x.normal_()
     m.replay()
     torch.cuda.synchronize()
@@ -193,3 +193,47 @@ def test_pipelined_host_batches_match_single_calls():
     torch.cuda.synchronize()
     for r, o in zip(ref, outs):
         assert torch.equal(r.cpu(), o)
+
+
+@pytest.mark.parametrize("batch", [4, 128])
+def test_stage_launches_match_per_block_launches(batch):
+    """Per-stage persistent launches (wl_stage_forward: consecutive stride-1
+    MBConv blocks with the image kept in shared memory) give exactly the
+    logits of one launch per block, with fewer launches."""
+    net = zoo.at_resolution(zoo.from_name("convfirstnet-pico"), 224)
+    staged = FusedNetwork(net, batch=batch, seed=17)
+    single = FusedNetwork(net, batch=batch, seed=17, stages=False)
+    assert any(c > 1 for _, c in staged.steps) and staged.launch_count() < single.launch_count()
+    staged.x.normal_()
+    single.x.copy_(staged.x)
+    staged.replay()
+    single.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(staged.output, single.output)
+
+
+def test_stage_forward_abi_three_blocks():
+    """wl_stage_forward over three different-weight 14x14 MBConv blocks equals
+    the oracle applied block by block."""
+    import ctypes
+
+    from paper_2404_03617_b200 import _lib
+
+    dims = TensorDims(3, 14, 14, 128)
+    mods, ws = [], []
+    rng = np.random.default_rng(8)
+    for i in range(3):
+        s, w, _ = _block_case(MBConv(8, 4, 0.25), dims, seed=30 + i)
+        mods.append(FusedBlock(s.block, s.dims, weights=w))
+        ws.append(w)
+    x = r16(rng, (3, 14, 14, 128))
+    xd = torch.from_numpy(x).half().cuda()
+    out = torch.empty_like(xd)
+    ptrs = (ctypes.c_void_p * 3)(*[m.packed.data_ptr() for m in mods])
+    _lib.check(_lib.lib().wl_stage_forward(ctypes.byref(mods[0].desc), 3, xd.data_ptr(), ptrs, out.data_ptr(),
+                                           mods[0].workspace.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    ref = x
+    for w in ws:
+        ref = om.unit_forward(MBConv(8, 4, 0.25), w, ref).astype(np.float16).astype(np.float32)
+    close(out.float().cpu().numpy(), ref)
