@@ -40,3 +40,17 @@ def test_bad_csv_reports_row(tmp_path):
     p.write_text("model,macs_g,batch,latency_ms,accuracy_pct\nx,notanumber,1,1,\n")
     with pytest.raises(ValueError, match="row 2"):
         gap.load_samples_csv(p)
+
+
+def test_b200_device_files_and_gap_plot():
+    from paper_2404_03617_b200 import gap as g
+
+    ds, me = g.load_device("b200-datasheet"), g.load_device("b200-measured")
+    assert abs(ds.op_byte - 281.25) < 1e-9 and me.peak_throughput < ds.peak_throughput
+    with pytest.raises(KeyError):
+        g.load_device("h100")
+    pts = g.gap_series([g.MeasuredSample("pico", 0.659e9, 128, 1.1e-3, 79.9),
+                        g.MeasuredSample("nx", 4.46e9, 128, 6.3e-3, None)], me)
+    svg = g.gap_plot(pts, me, "gap <b200>")
+    assert svg.startswith("<svg") and svg.rstrip().endswith("</svg>") and "&lt;b200&gt;" in svg
+    assert svg.count("<circle") == 4
