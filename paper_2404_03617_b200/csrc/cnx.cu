@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include "common.cuh"
 #include "gemm.h"
@@ -73,147 +74,172 @@ __global__ void patchify_kernel(const __half* __restrict__ x, __half* __restrict
   pdl_trigger();
 }
 
-// depthwise KS x KS conv + bias + channel LayerNorm. One CTA per (image,
-// band of kDwRows output rows): the band's input rows (+ halo) are staged in
-// shared memory with coalesced 16-byte loads (an image row is W * C
-// contiguous halves); thread item = (output row, kDwPx pixels, 8 channels).
-// Per input row the KS taps accumulate in packed half (HFMA2), rows add in
-// fp32; the pre-norm result is kept in shared memory (fp16) while the
-// per-pixel mean and centred second moment are reduced (two passes).
-// The band height RB (4, 2 or 1 rows) is the largest whose tile fits shared
-// memory (ConvNeXt-T at 224: 4 rows for C = 192 / 384, 2 for C = 768).
+// depthwise KS x KS conv + bias + channel LayerNorm. Persistent CTAs walk
+// work items (image, vertical segment of SR rows) and slide a ring of padded
+// input rows down the segment: each step computes RB output rows from the
+// window [y0 - R, y0 + RB + R) while cp.async brings in the next RB rows, so
+// every input row is read from L2/HBM about once and the loads overlap the
+// stencil. Thread item = (output row, kDwPx pixels, 8 channels); the KS x KS
+// taps accumulate in packed half (HFMA2) and are widened once; the pre-norm
+// result is kept in shared memory (fp16) for the two-pass, fixed-order
+// per-pixel LayerNorm statistics.
 constexpr int kDwPx = 4;
-constexpr int kDwThreads = 512;
+constexpr int kDwThreads = 384;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 template <int KS>
-__global__ void __launch_bounds__(kDwThreads, 1) dwln_kernel(const __half* __restrict__ x, const __half* __restrict__ wdw,
-                                                      const float* __restrict__ bdw, const float* __restrict__ g,
-                                                      const float* __restrict__ be, __half* __restrict__ y, int H, int W,
-                                                      int C, float eps, int RB) {
+__global__ void __launch_bounds__(kDwThreads, 1)
+    dwln_kernel(const __half* __restrict__ x, const __half* __restrict__ wdw, const float* __restrict__ bdw,
+                const float* __restrict__ g, const float* __restrict__ be, __half* __restrict__ y, int N, int H, int W,
+                int C, float eps, int RB, int nseg) {
   constexpr int R = KS / 2, PX = kDwPx, NI = PX + 2 * R;
-  const int IR = RB + 2 * R;
   extern __shared__ __align__(16) uint8_t dsm[];
   const int C8 = C / 8, WG = (W + PX - 1) / PX, rowh = W * C;
-  __half* s_in = reinterpret_cast<__half*>(dsm);               // [IR][W + 2R][C]
-  const int prowh = (W + 2 * R) * C;                            // padded input row (halves)
-  __half* s_y = s_in + (size_t)IR * prowh;                      // [RB][W][C] pre-norm
-  float* s_sum = reinterpret_cast<float*>(s_y + (size_t)RB * rowh);  // [RB * W] mean, then rstd
-  float* s_sq = s_sum + RB * W;
-  float* s_part = s_sq + RB * W;  // [RB * W][C8] per-chunk partials (fixed-order reduction)
-  const int bands = (H + RB - 1) / RB;
-  const int img = blockIdx.x / bands, y0 = (blockIdx.x % bands) * RB;
+  const int NR = 2 * RB + 2 * R;                 // ring rows
+  const int WP = WG * PX + 2 * R;                // padded row width (zero columns both sides + tail)
+  const int prowh = WP * C;                      // padded row (halves)
+  __half* s_in = reinterpret_cast<__half*>(dsm);  // [NR][W + 2R][C]
+  __half* s_y = s_in + (size_t)NR * prowh;        // [RB][W][C] pre-norm
+  float* s_sum = reinterpret_cast<float*>(s_y + (size_t)RB * rowh);  // [RB * W] mean
+  float* s_sq = s_sum + RB * W;                                       // [RB * W] rstd
+  float* s_part = s_sq + RB * W;                                      // [RB * W][C8]
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int SR = (H + nseg - 1) / nseg;
+  // the pad columns of every ring row stay zero
+  for (int i = tid; i < NR * WP * C8; i += nt) reinterpret_cast<uint4*>(s_in)[i] = make_uint4(0, 0, 0, 0);
   pdl_wait();
-  {
-    // rows of the band plus halo, each padded by R zero columns on both
-    // sides (no bounds checks in the stencil)
-    const int per_row = rowh / 8, prow = (W + 2 * R) * C8;
-    for (int i = tid; i < IR * prow; i += nt) {
-      const int rr = i / prow, off = i - rr * prow;
-      const int iy = y0 - R + rr, px = off / C8 - R;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (iy >= 0 && iy < H && px >= 0 && px < W)
-        v = __ldg(reinterpret_cast<const uint4*>(x + ((size_t)img * H + iy) * rowh) + off - R * C8);
-      reinterpret_cast<uint4*>(s_in)[i] = v;
-    }
-    (void)per_row;
-  }
   __syncthreads();
-  const int items = RB * WG * C8;
-  for (int it = tid; it < items; it += nt) {
-    const int c8 = it % C8, rest = it / C8, pg = rest % WG, ry = rest / WG;
-    const int x0 = pg * PX;
-    if (y0 + ry >= H) continue;
-    float acc[PX][8];
-    {
-      float b[8];
-      ld8f(bdw + c8 * 8, b);
+  const int per_row = rowh / 8;
+  for (int item = blockIdx.x; item < N * nseg; item += gridDim.x) {
+    const int img = item / nseg, ys = (item % nseg) * SR, ye = min(H, ys + SR);
+    if (ys >= ye) continue;
+    const int base = ys - R;  // ring slot of input row iy: (iy - base) % NR
+    auto load_rows = [&](int lo, int hi) {
+      lo = max(lo, ys - R);
+      hi = min(hi, ye + R);
+      for (int i = tid; i < (hi - lo) * per_row; i += nt) {
+        const int iy = lo + i / per_row, off = i % per_row;
+        __half* dst = s_in + (size_t)((iy - base) % NR) * prowh + R * C + off * 8;
+        if (iy >= 0 && iy < H)
+          cp_async16(dst, x + ((size_t)img * H + iy) * rowh + off * 8);
+        else
+          *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    load_rows(ys - R, ys + RB + R);  // the first window
+    for (int y0 = ys; y0 < ye; y0 += RB) {
+      load_rows(y0 + RB + R, y0 + 2 * RB + R);  // the next step's new rows (overlap this step)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+      const int rows = min(RB, ye - y0);
+      const int items = rows * WG * C8;
+      for (int it = tid; it < items; it += nt) {
+        const int c8 = it % C8, rest = it / C8, pg = rest % WG, ry = rest / WG;
+        const int x0 = pg * PX;
+        __half2 h[PX][4];
 #pragma unroll
-      for (int p = 0; p < PX; ++p)
+        for (int p = 0; p < PX; ++p)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[p][i] = b[i];
-    }
+          for (int i = 0; i < 4; ++i) h[p][i] = __float2half2_rn(0.f);
+        float acc[PX][8];
 #pragma unroll
-    for (int dy = 0; dy < KS; ++dy) {
-      const __half* row = s_in + (size_t)(ry + dy) * prowh + (size_t)x0 * C + c8 * 8;
-      uint4 in[NI];
+        for (int p = 0; p < PX; ++p)
 #pragma unroll
-      for (int j = 0; j < NI; ++j) in[j] = (x0 + j < W + 2 * R) ? lds128(row + (size_t)j * C) : make_uint4(0, 0, 0, 0);
-      __half2 h[PX][4];
+          for (int i = 0; i < 8; ++i) acc[p][i] = 0.f;
+        int slot = (y0 + ry - R - base) % NR;  // ring slot of the window's first row
 #pragma unroll
-      for (int p = 0; p < PX; ++p)
+        for (int dy = 0; dy < KS; ++dy) {
+          const __half* row = s_in + (size_t)slot * prowh + (size_t)x0 * C + c8 * 8;
+          slot = slot + 1 == NR ? 0 : slot + 1;
+          uint4 in[NI];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) h[p][i] = __float2half2_rn(0.f);
+          for (int j = 0; j < NI; ++j) in[j] = lds128(row + (size_t)j * C);
 #pragma unroll
-      for (int dx = 0; dx < KS; ++dx) {
-        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wdw + (size_t)(dy * KS + dx) * C + c8 * 8));
-        const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
+          for (int dx = 0; dx < KS; ++dx) {
+            const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wdw + (size_t)(dy * KS + dx) * C + c8 * 8));
+            const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
+#pragma unroll
+            for (int p = 0; p < PX; ++p) {
+              const __half2* i2 = reinterpret_cast<const __half2*>(&in[p + dx]);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) h[p][i] = __hfma2(i2[i], w2[i], h[p][i]);
+            }
+          }
+          if (dy == R || dy == KS - 1) {  // widen to fp32 twice per window (at most 4 rows of taps in half)
+#pragma unroll
+            for (int p = 0; p < PX; ++p)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 f = __half22float2(h[p][i]);
+                acc[p][2 * i] += f.x;
+                acc[p][2 * i + 1] += f.y;
+                h[p][i] = __float2half2_rn(0.f);
+              }
+          }
+        }
+        float b[8];
+        ld8f(bdw + c8 * 8, b);
 #pragma unroll
         for (int p = 0; p < PX; ++p) {
-          const __half2* i2 = reinterpret_cast<const __half2*>(&in[p + dx]);
+          if (x0 + p >= W) break;
+          float s = 0.f;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) h[p][i] = __hfma2(i2[i], w2[i], h[p][i]);
+          for (int i = 0; i < 8; ++i) {
+            acc[p][i] += b[i];
+            s += acc[p][i];
+          }
+          s_part[(ry * W + x0 + p) * C8 + c8] = s;
+          *reinterpret_cast<uint4*>(s_y + ((size_t)ry * W + x0 + p) * C + c8 * 8) = pack8(acc[p]);
         }
       }
+      __syncthreads();
+      const int npix = rows * W, pitems = npix * C8;
+      for (int pix = tid; pix < npix; pix += nt) {
+        float t = 0.f;
+        for (int j = 0; j < C8; ++j) t += s_part[pix * C8 + j];
+        s_sum[pix] = t / (float)C;
+      }
+      __syncthreads();
+      for (int it = tid; it < pitems; it += nt) {
+        const int c8 = it % C8, pix = it / C8;
+        const float mean = s_sum[pix];
+        float v[8];
+        unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
+        float s = 0.f;
 #pragma unroll
-      for (int p = 0; p < PX; ++p)
+        for (int i = 0; i < 8; ++i) s += (v[i] - mean) * (v[i] - mean);
+        s_part[it] = s;
+      }
+      __syncthreads();
+      for (int pix = tid; pix < npix; pix += nt) {
+        float t = 0.f;
+        for (int j = 0; j < C8; ++j) t += s_part[pix * C8 + j];
+        s_sq[pix] = rsqrtf(t / (float)C + eps);
+      }
+      __syncthreads();
+      for (int it = tid; it < pitems; it += nt) {
+        const int c8 = it % C8, pix = it / C8;
+        const float mean = s_sum[pix], rstd = s_sq[pix];
+        float v[8], gg[8], bb[8];
+        unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
+        ld8f(g + c8 * 8, gg);
+        ld8f(be + c8 * 8, bb);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = __half22float2(h[p][i]);
-          acc[p][2 * i] += f.x;
-          acc[p][2 * i + 1] += f.y;
-        }
+        for (int i = 0; i < 8; ++i) v[i] = (v[i] - mean) * rstd * gg[i] + bb[i];
+        *reinterpret_cast<uint4*>(y + ((size_t)img * H + y0) * rowh + (size_t)pix * C + c8 * 8) = pack8(v);
+      }
+      __syncthreads();  // the ring rows of this window may be overwritten by the next prefetch
     }
-#pragma unroll
-    for (int p = 0; p < PX; ++p) {
-      if (x0 + p >= W) break;
-      float s = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s += acc[p][i];
-      s_part[(ry * W + x0 + p) * C8 + c8] = s;
-      *reinterpret_cast<uint4*>(s_y + ((size_t)ry * W + x0 + p) * C + c8 * 8) = pack8(acc[p]);
-    }
-  }
-  __syncthreads();
-  const int pitems = RB * W * C8;
-  for (int pix = tid; pix < RB * W; pix += nt) {
-    float t = 0.f;
-    for (int j = 0; j < C8; ++j) t += s_part[pix * C8 + j];
-    s_sum[pix] = t / (float)C;
-  }
-  __syncthreads();
-  for (int it = tid; it < pitems; it += nt) {
-    const int c8 = it % C8, pix = it / C8;
-    const float mean = s_sum[pix];
-    float v[8];
-    unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) s += (v[i] - mean) * (v[i] - mean);
-    s_part[it] = s;
-  }
-  __syncthreads();
-  for (int pix = tid; pix < RB * W; pix += nt) {
-    float t = 0.f;
-    for (int j = 0; j < C8; ++j) t += s_part[pix * C8 + j];
-    s_sq[pix] = rsqrtf(t / (float)C + eps);
-  }
-  __syncthreads();
-  for (int it = tid; it < pitems; it += nt) {
-    const int c8 = it % C8, pix = it / C8;
-    if (y0 + pix / W >= H) continue;
-    const float mean = s_sum[pix], rstd = s_sq[pix];
-    float v[8], gg[8], bb[8];
-    unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
-    ld8f(g + c8 * 8, gg);
-    ld8f(be + c8 * 8, bb);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = (v[i] - mean) * rstd * gg[i] + bb[i];
-    *reinterpret_cast<uint4*>(y + ((size_t)img * H + y0) * rowh + (size_t)pix * C + c8 * 8) = pack8(v);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
   }
   pdl_trigger();
 }
 int dwln_smem_rb(int KS, int W, int C, int RB) {
-  return (KS - 1 + RB) * (W + KS - 1) * C * 2 + RB * W * C * 2 + 2 * RB * W * 4 + RB * W * (C / 8) * 4;
+  const int WP = (W + kDwPx - 1) / kDwPx * kDwPx + KS - 1;
+  return (2 * RB + KS - 1) * WP * C * 2 + RB * W * C * 2 + 2 * RB * W * 4 + RB * W * (C / 8) * 4;
 }
 int dwln_rows(int KS, int W, int C) {
   for (int rb : {4, 2, 1})
@@ -221,6 +247,12 @@ int dwln_rows(int KS, int W, int C) {
   return 0;
 }
 int dwln_smem(int KS, int W, int C) { return dwln_smem_rb(KS, W, C, dwln_rows(KS, W, C)); }
+int dwln_segments(int N, int H, int RB) {
+  int nseg = (3 * kNumSMs + N - 1) / N;
+  const int cap = H / (2 * RB);
+  if (nseg > cap) nseg = cap;
+  return nseg < 1 ? 1 : nseg;
+}
 
 // LayerNorm per pixel; S2D: the output row is written in 2x2 space-to-depth
 // order A[(img, y/2, x/2)][((y%2) 2 + x%2) C + c]. CTA = P pixels x C/8
@@ -352,7 +384,10 @@ int64_t hidden_rows(int64_t M, int hid) {
 int ffn_rows(const __half* x, int64_t M, int C, int hid, int K, const __half* ut, const float* a, const __half* vt,
              const float* b, int act, const __half* res, __half* z, __half* hbuf, const uint8_t* wimg,
              cudaStream_t st) {
-  if (K == C && wimg && ffn_fused_ok(M, C, hid)) return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st);
+  // the fused kernel wins up to C = 256 (HC = 128); at C = 384 its HC = 64 chain is
+  // slower than the two GEMMs (measured 250 vs 121 us for ConvNeXt-T's 14x14 stage)
+  if (K == C && C <= 256 && wimg && ffn_fused_ok(M, C, hid))
+    return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st);
   const int64_t rb = hidden_rows(M, hid);
   for (int64_t r0 = 0; r0 < M; r0 += rb) {
     const int rows = (int)(M - r0 < rb ? M - r0 : rb);
@@ -467,7 +502,7 @@ int ffn_row_batches(const wl_block_desc& d) {
 }
 int ffn_launches(const wl_block_desc& d) {
   const int64_t M = (int64_t)d.n * d.h * d.w;
-  return ffn_fused_ok(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
+  return d.c <= 256 && ffn_fused_ok(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
 }
 
 bool cnx_wide(const wl_block_desc& d) {
@@ -512,12 +547,13 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
   __half* hb = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr + a128(M * d.c * 2));
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
   auto k = d.ksize == 7 ? dwln_kernel<7> : dwln_kernel<3>;
-  const int rb = dwln_rows(d.ksize, d.w, d.c), bands = (d.h + rb - 1) / rb;
-  if (int e = launch_pdl(k, d.n * bands, kDwThreads, dwln_smem(d.ksize, d.w, d.c), st, "dwln launch",
+  const int rb = dwln_rows(d.ksize, d.w, d.c), nseg = dwln_segments(d.n, d.h, rb);
+  const int grid = std::min(d.n * nseg, kNumSMs);
+  if (int e = launch_pdl(k, grid, kDwThreads, dwln_smem(d.ksize, d.w, d.c), st, "dwln launch",
                             reinterpret_cast<const __half*>(x),
                             reinterpret_cast<const __half*>(pk + L.o_wdw), reinterpret_cast<const float*>(pk + L.o_bdw),
                             reinterpret_cast<const float*>(pk + L.o_g), reinterpret_cast<const float*>(pk + L.o_be), xh,
-                            d.h, d.w, d.c, eps, rb))
+                            d.n, d.h, d.w, d.c, eps, rb, nseg))
     return e;
   return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
                   reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
