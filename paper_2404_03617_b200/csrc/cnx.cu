@@ -29,7 +29,7 @@
 namespace wl {
 
 constexpr int kWsHdr = 4096;                     // the arrival-counter header every family leaves alone
-constexpr int64_t kHiddenBatchBytes = 40 << 20;  // hidden row batch kept L2-resident
+constexpr int64_t kHiddenBatchBytes = 80 << 20;  // hidden row batch kept L2-resident (126 MB L2)
 
 __device__ __forceinline__ void ld8f(const float* p, float* o) {
   const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);

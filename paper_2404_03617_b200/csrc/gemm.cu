@@ -46,6 +46,7 @@ struct Bars {
   uint64_t res_full;
   uint32_t tmem_base;
   float ln_red[2][2][128];  // row LayerNorm: [sum | centred sum][column half][row]
+  alignas(16) float bias[256];  // the tile's bias slice (0 past N or without bias)
 };
 }  // namespace gm
 
@@ -85,22 +86,12 @@ __device__ __forceinline__ __half2 act_rt_h2(__half2 v, int a) {
   return v;
 }
 
-// accumulators + bias of 16 columns starting at output column n (n + 16 may pass N)
-__device__ __forceinline__ void gemm_bias(const gm::Args& a, const uint32_t* v, int n, float* f) {
+// accumulators + bias of 16 columns at column c of the tile (bias staged in shared memory)
+__device__ __forceinline__ void gemm_bias(const float* s_bias, const uint32_t* v, int c, float* f) {
+  float b[16];
+  load16f(s_bias + c, b);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
-  if (a.bias) {
-    if (n + 16 <= a.N) {
-      float b[16];
-      load16f(a.bias + n, b);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) f[i] += b[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (n + i < a.N) f[i] += a.bias[n + i];
-    }
-  }
+  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + b[i];
 }
 
 __global__ void __launch_bounds__(gm::kThreads, 1)
@@ -203,6 +194,8 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           for (int sl = 0; sl < a.slabs; ++sl) tma_load_2d(s_st + sl * 16384, &tr, n0 + sl * 64, tm * 128, &B.res_full);
         }
       }
+      for (int c = threadIdx.x - 64; c < a.BN; c += kEpiThreads)
+        B.bias[c] = (a.bias && n0 + c < a.N) ? a.bias[n0 + c] : 0.f;
       gm_bar(kEpiThreads);
       mbar_wait(&B.acc_full[ab], u & 1);
       tc_fence_after();
@@ -241,7 +234,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
         for (int j = 0; j < 4; ++j)
           if (u_lo + j < u_hi) {
             float f[16];
-            gemm_bias(a, v + 16 * j, n0 + (u_lo + j) * 16, f);
+            gemm_bias(B.bias, v + 16 * j, (u_lo + j) * 16, f);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               v[16 * j + i] = __float_as_uint(f[i]);
@@ -287,7 +280,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           for (int j = 0; j < 4; ++j)
             if (u0 + j < u_hi) {
               float f[16];
-              gemm_bias(a, v + 16 * j, n0 + (u0 + j) * 16, f);
+              gemm_bias(B.bias, v + 16 * j, (u0 + j) * 16, f);
               uint4 o[2];
               uint32_t* ow = reinterpret_cast<uint32_t*>(o);
 #pragma unroll
