@@ -26,8 +26,9 @@
 namespace wl {
 
 namespace gm {
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
-constexpr int kEpiThreads = 256;
+constexpr int kGroups = 4;                  // epilogue warp groups per TMEM lane quadrant
+constexpr int kEpiThreads = kGroups * 128;
+constexpr int kThreads = 64 + kEpiThreads;  // warp 0 TMA, warp 1 MMA, then the epilogue warps
 constexpr int kBK = 64;
 constexpr int kMaxStages = 8;
 constexpr int kSmemMax = 232448;
@@ -45,7 +46,7 @@ struct Bars {
   uint64_t acc_full[2], acc_empty[2];
   uint64_t res_full;
   uint32_t tmem_base;
-  float ln_red[2][2][128];  // row LayerNorm: [sum | centred sum][column half][row]
+  float ln_red[2][kGroups][128];  // row LayerNorm: [sum | centred sum][column group][row]
   alignas(16) float bias[256];  // the tile's bias slice (0 past N or without bias)
 };
 }  // namespace gm
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.acc_full[i], 1);
-      mbar_init(&B.acc_empty[i], 8);
+      mbar_init(&B.acc_empty[i], kEpiThreads / 32);
     }
     mbar_init(&B.res_full, 1);
     fence_mbar_init();
@@ -177,10 +178,10 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     // ------------------------------------------------------------ epilogue
     // warp w: TMEM lane quadrant w % 4 (rows 32 q .. 32 q + 31), column half
     // (w - 2) / 4 of the tile's 16-column units
-    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int q = warp & 3, half = (warp - 2) >> 2;  // half: the warp's column group
     const bool leader = threadIdx.x == 64;
     const int units = a.BN / 16;
-    const int u_lo = half ? (units + 1) / 2 : 0, u_hi = half ? units : (units + 1) / 2;
+    const int u_lo = half * units / kGroups, u_hi = (half + 1) * units / kGroups;
     const int r = q * 32 + lane;  // row in the tile
     int it = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
@@ -221,17 +222,17 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       if (a.has_res) mbar_wait(&B.res_full, it & 1);
       if (a.ln_g) {
         // row LayerNorm over the whole output row (tiles_n == 1, N <= 128):
-        // each warp keeps its half of the row in registers; the two halves'
-        // partial sums meet in shared memory (fixed order: deterministic);
+        // each warp keeps its part of the row (<= 2 units) in registers; the
+        // groups' partial sums meet in shared memory (fixed order: deterministic);
         // two-pass statistics (mean, then the centred second moment), fp32
-        uint32_t v[64];
+        uint32_t v[32];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 2; ++j)
           if (u_lo + j < u_hi) WL_TMEM_LD16(tb0 + (u_lo + j) * 16, (v + 16 * j));
         tmem_ld_wait();
         float s1 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 2; ++j)
           if (u_lo + j < u_hi) {
             float f[16];
             gemm_bias(B.bias, v + 16 * j, (u_lo + j) * 16, f);
@@ -243,10 +244,13 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           }
         B.ln_red[0][half][r] = s1;
         gm_bar(kEpiThreads);
-        const float mean = (B.ln_red[0][0][r] + B.ln_red[0][1][r]) / (float)a.N;
+        float mean = 0.f;
+#pragma unroll
+        for (int gq = 0; gq < kGroups; ++gq) mean += B.ln_red[0][gq][r];
+        mean /= (float)a.N;
         float s2 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 2; ++j)
           if (u_lo + j < u_hi)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -255,9 +259,12 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
             }
         B.ln_red[1][half][r] = s2;
         gm_bar(kEpiThreads);
-        const float rstd = rsqrtf((B.ln_red[1][0][r] + B.ln_red[1][1][r]) / (float)a.N + a.ln_eps);
+        float var = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int gq = 0; gq < kGroups; ++gq) var += B.ln_red[1][gq][r];
+        const float rstd = rsqrtf(var / (float)a.N + a.ln_eps);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
           if (u_lo + j < u_hi) {
             float f[16];
 #pragma unroll
@@ -269,15 +276,15 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
             stage_unit(u_lo + j, o);
           }
       } else {
-        // 64 columns (four x16 TMEM loads) per wait
-        for (int u0 = u_lo; u0 < u_hi; u0 += 4) {
-          uint32_t v[64];
+        // 32 columns (two x16 TMEM loads) per wait
+        for (int u0 = u_lo; u0 < u_hi; u0 += 2) {
+          uint32_t v[32];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 2; ++j)
             if (u0 + j < u_hi) WL_TMEM_LD16(tb0 + (u0 + j) * 16, (v + 16 * j));
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 2; ++j)
             if (u0 + j < u_hi) {
               float f[16];
               gemm_bias(B.bias, v + 16 * j, (u0 + j) * 16, f);
