@@ -384,9 +384,10 @@ int64_t hidden_rows(int64_t M, int hid) {
 int ffn_rows(const __half* x, int64_t M, int C, int hid, int K, const __half* ut, const float* a, const __half* vt,
              const float* b, int act, const __half* res, __half* z, __half* hbuf, const uint8_t* wimg,
              cudaStream_t st) {
-  // the fused kernel wins up to C = 256 (HC = 128); at C = 384 its HC = 64 chain is
-  // slower than the two GEMMs (measured 250 vs 121 us for ConvNeXt-T's 14x14 stage)
-  if (K == C && C <= 256 && wimg && ffn_fused_ok(M, C, hid))
+  // the fused kernel wins while its weights stay resident (C <= 128); from C = 192
+  // the two GEMMs with an L2-resident hidden are faster (ConvNeXt-T b128: 14x14 stage
+  // 250 vs 121 us, 28x28 stage 300 vs 272 us per block, profiles/r02_convnext_*)
+  if (K == C && C <= 128 && wimg && ffn_fused_ok(M, C, hid))
     return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st);
   const int64_t rb = hidden_rows(M, hid);
   for (int64_t r0 = 0; r0 < M; r0 += rb) {
@@ -502,7 +503,7 @@ int ffn_row_batches(const wl_block_desc& d) {
 }
 int ffn_launches(const wl_block_desc& d) {
   const int64_t M = (int64_t)d.n * d.h * d.w;
-  return d.c <= 256 && ffn_fused_ok(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
+  return d.c <= 128 && ffn_fused_ok(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
 }
 
 bool cnx_wide(const wl_block_desc& d) {

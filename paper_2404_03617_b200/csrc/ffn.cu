@@ -30,6 +30,7 @@ namespace wl {
 namespace ff {
 constexpr int kEpiWarps = 8;  // kGroups warp groups per TMEM lane quadrant
 constexpr int kGroups = kEpiWarps / 4;
+constexpr int kHU = 128 / kGroups / 16;  // 16-column units of E per warp (HC <= 128)
 constexpr int kXWarp = 2 + kEpiWarps;
 constexpr int kVWarp = kXWarp + 1;
 constexpr int kThreads = (kVWarp + 1) * 32;  // warp 0 U-slab loads, 1 MMA, epilogue, x / residual TMA, V-slab loads
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
             const uint32_t st = sr + s * a.us_bytes;
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
+              if (sl * 64 + k4 * 16 >= C) break;  // zero-padded channels of a partial slab
               const uint64_t ad = make_sdesc_sw128(sx + sl * 16384 + k4 * 32);
               const uint64_t bd = make_sdesc_sw128(st + k4 * 32);
               mma_ss(d, ad, bd, idesc_e, (sl | k4) != 0);
@@ -294,13 +296,13 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
         tc_fence_after();
         if (threadIdx.x == 64) FF_TRACE(16 + g * 4 + 2);
         const uint32_t eb = tmem_lane_addr(tmem, q, a.t_e + b * HC + grp * hw);
-        uint32_t v[64];
+        uint32_t v[16 * kHU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kHU; ++u)
           if (u * 16 < hw) WL_TMEM_LD16(eb + u * 16, (v + 16 * u));
         tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kHU; ++u)
           if (u * 16 < hw) {
             float bb[16];
             load16f(aj + u * 16, bb);
