@@ -149,6 +149,19 @@ WL_API int wl_stage_forward(const wl_block_desc* d, int nblocks, const void* x, 
  * kernel for it) */
 WL_API int wl_stage_max_blocks(const wl_block_desc* d);
 
+/* Two consecutive units fused into one launch, the intermediate activation
+ * kept on chip: currently the dense 3x3 stride-2 stem (3 -> 16, ReLU) with the
+ * first stride-1 ConvFirst block (T = 8, C = 16, expansion 3) — ConvFirstNet-
+ * Pico's stem + s1b0. d0 / d1 are the
+ * two units' descriptors; weights in each unit's reference order; packed:
+ * wl_pair_packed_bytes bytes. */
+WL_API int wl_pair_supported(const wl_block_desc* d0, const wl_block_desc* d1);
+WL_API int64_t wl_pair_packed_bytes(const wl_block_desc* d0, const wl_block_desc* d1);
+WL_API int wl_pair_pack(const wl_block_desc* d0, const wl_block_desc* d1, const float* const* w0, int n0,
+                        const float* const* w1, int n1, void* packed_host);
+WL_API int wl_pair_forward(const wl_block_desc* d0, const wl_block_desc* d1, const void* x, const void* packed,
+                           void* z, void* stream);
+
 /* The pointwise contraction of the layer-wise units (1x1 conv / linear),
  * exposed for the layer-wise FFN schedule and for direct testing:
  * D[M][N] = act(A[M][K] . B[N][K]^T + bias[N]) (+ res[M][N]); fp16 storage,

@@ -47,6 +47,10 @@ EXPORTS = (
     "wl_gemm",
     "wl_stage_forward",
     "wl_stage_max_blocks",
+    "wl_pair_supported",
+    "wl_pair_packed_bytes",
+    "wl_pair_pack",
+    "wl_pair_forward",
     "wl_output_dims",
     "wl_debug_set_trace",
 )
@@ -124,6 +128,10 @@ def lib() -> ctypes.CDLL:
         "wl_output_dims": (ctypes.c_int, [D] + [P(ctypes.c_int32)] * 4),
         "wl_stage_forward": (ctypes.c_int, [D, ctypes.c_int, vp, P(vp), vp, vp, vp]),
         "wl_stage_max_blocks": (ctypes.c_int, [D]),
+        "wl_pair_supported": (ctypes.c_int, [D, D]),
+        "wl_pair_packed_bytes": (ctypes.c_int64, [D, D]),
+        "wl_pair_pack": (ctypes.c_int, [D, D, P(P(ctypes.c_float)), ctypes.c_int, P(P(ctypes.c_float)), ctypes.c_int, vp]),
+        "wl_pair_forward": (ctypes.c_int, [D, D, vp, vp, vp, vp]),
         "wl_gemm": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
                                    ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, vp]),
         "wl_debug_set_trace": (None, [vp]),

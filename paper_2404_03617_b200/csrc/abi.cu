@@ -198,6 +198,28 @@ int wl_stage_forward(const wl_block_desc* d, int nblocks, const void* x, const v
   return mb1_stage_forward(*d, nblocks, x, packed, z, ws, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int wl_pair_supported(const wl_block_desc* d0, const wl_block_desc* d1) {
+  if (!d0 || !d1 || validate_desc(*d0) != WL_OK || validate_desc(*d1) != WL_OK) return 0;
+  return stem_cf_supported(*d0, *d1) ? 1 : 0;
+}
+int64_t wl_pair_packed_bytes(const wl_block_desc* d0, const wl_block_desc* d1) {
+  if (!wl_pair_supported(d0, d1)) return set_error(WL_EUNSUPPORTED, "no fused kernel for this unit pair");
+  return stem_cf_packed_bytes();
+}
+int wl_pair_pack(const wl_block_desc* d0, const wl_block_desc* d1, const float* const* w0, int n0,
+                 const float* const* w1, int n1, void* packed_host) {
+  if (!wl_pair_supported(d0, d1)) return set_error(WL_EUNSUPPORTED, "no fused kernel for this unit pair");
+  if (n0 != weight_count(*d0) || n1 != weight_count(*d1))
+    return set_error(WL_EINVAL, "expected %d + %d weight tensors", weight_count(*d0), weight_count(*d1));
+  return stem_cf_pack(w0, w1, reinterpret_cast<uint8_t*>(packed_host));
+}
+int wl_pair_forward(const wl_block_desc* d0, const wl_block_desc* d1, const void* x, const void* packed, void* z,
+                    void* stream) {
+  if (!x || !packed || !z) return set_error(WL_EINVAL, "null tensor pointer");
+  if (!wl_pair_supported(d0, d1)) return set_error(WL_EUNSUPPORTED, "no fused kernel for this unit pair");
+  return stem_cf_forward(*d0, *d1, x, packed, z, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int wl_stage_max_blocks(const wl_block_desc* d) {
   if (!d || validate_desc(*d) != WL_OK || d->kind != WL_KIND_MBCONV) return 0;
   return mb1_stage_max(*d);

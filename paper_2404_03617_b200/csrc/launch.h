@@ -96,6 +96,12 @@ void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* ou
 int ffn_fused_init();
 // stride-1 MBConv stage launch (mb_s1.cu)
 int mb1_stage_max(const wl_block_desc& d);
+// stem + first ConvFirst block (stem_cf.cu)
+bool stem_cf_supported(const wl_block_desc& d0, const wl_block_desc& d1);
+int64_t stem_cf_packed_bytes();
+int stem_cf_pack(const float* const* w0, const float* const* w1, uint8_t* out);
+int stem_cf_forward(const wl_block_desc& d0, const wl_block_desc& d1, const void* x, const void* packed, void* z,
+                    cudaStream_t st);
 int mb1_stage_forward(const wl_block_desc& d, int nblk, const void* x, const void* const* packed, void* z, void* ws,
                       cudaStream_t st);
 void mb_set_trace(void* p);

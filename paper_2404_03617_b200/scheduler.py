@@ -73,25 +73,66 @@ class FusedNetwork:
         self.graph: torch.cuda.CUDAGraph | None = None
         self.steps = self._plan_steps(stages)
 
-    def _plan_steps(self, stages: bool) -> list[tuple[int, int]]:
-        """Launch plan: [(first unit, unit count)]. With ``stages``, runs of
-        consecutive units that share one descriptor and have a stage kernel
-        (``wl_stage_max_blocks``) become ONE launch: each block's output stays
-        on chip as the next block's input (the per-stage persistent kernel,
-        machine.py:1091-1120; only the stage's last output is written). The
-        intermediate units' ``out`` tensors are then not produced."""
+    def _plan_steps(self, stages: bool) -> list[tuple[int, int, str]]:
+        """Launch plan: [(first unit, unit count, kind)]. With ``stages``:
+        * "pair": a unit pair with one fused kernel (``wl_pair_supported``:
+          the stem + first ConvFirst block of ConvFirstNet-Pico), the stem
+          output kept on chip;
+        * "stage": a run of consecutive units sharing one descriptor with a
+          stage kernel (``wl_stage_max_blocks``) — ONE launch, each block's
+          output stays on chip as the next block's input (the per-stage
+          persistent kernel, machine.py:1091-1120);
+        * "unit": one launch per unit.
+        Only a step's last output is written; the intermediate units' ``out``
+        tensors are then not produced."""
         L = _lib.lib()
         steps, i = [], 0
+        self._pair_packed = {}
         while i < len(self.units):
             d = self.units[i].module.desc
+            if stages and i + 1 < len(self.units) and \
+                    L.wl_pair_supported(ctypes.byref(d), ctypes.byref(self.units[i + 1].module.desc)):
+                self._pair_packed[i] = self._pack_pair(i)
+                steps.append((i, 2, "pair"))
+                i += 2
+                continue
             cap = L.wl_stage_max_blocks(ctypes.byref(d)) if stages else 0
             j = i + 1
             while cap and j < len(self.units) and j - i < cap and \
                     self.units[j].module.desc.as_tuple() == d.as_tuple():
                 j += 1
-            steps.append((i, j - i))
+            steps.append((i, j - i, "stage" if j - i > 1 else "unit"))
             i = j
         return steps
+
+    def _pack_pair(self, i: int) -> torch.Tensor:
+        m0, m1 = self.units[i].module, self.units[i + 1].module
+        w0 = m0.binding.device_weights(m0.weights)
+        w1 = m1.binding.device_weights(m1.weights)
+        L = _lib.lib()
+        nb = _lib.check(L.wl_pair_packed_bytes(ctypes.byref(m0.desc), ctypes.byref(m1.desc)), "wl_pair_packed_bytes")
+        out = np.zeros(nb, dtype=np.uint8)
+        c0 = [np.ascontiguousarray(w, dtype=np.float32) for w in w0]
+        c1 = [np.ascontiguousarray(w, dtype=np.float32) for w in w1]
+        fp0, fp1 = _lib.float_ptr_array(c0), _lib.float_ptr_array(c1)
+        _lib.check(L.wl_pair_pack(ctypes.byref(m0.desc), ctypes.byref(m1.desc), fp0[1], len(c0),
+                                  fp1[1], len(c1), out.ctypes.data_as(ctypes.c_void_p)),
+                   "wl_pair_pack")
+        return torch.from_numpy(out).to(self.device)
+
+    def _launch_step(self, first: int, count: int, kind: str, x: torch.Tensor, stream=None) -> torch.Tensor:
+        u = self.units[first + count - 1]
+        if kind == "unit":
+            u.module.launch(x, u.out, self.workspace, stream)
+        elif kind == "stage":
+            self._launch_stage(first, count, x, u.out, stream)
+        else:
+            st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+            m0, m1 = self.units[first].module, self.units[first + 1].module
+            _lib.check(_lib.lib().wl_pair_forward(ctypes.byref(m0.desc), ctypes.byref(m1.desc), x.data_ptr(),
+                                                  self._pair_packed[first].data_ptr(), u.out.data_ptr(), st),
+                       "wl_pair_forward")
+        return u.out
 
     # ----------------------------------------------------------- execution
     @property
@@ -107,14 +148,8 @@ class FusedNetwork:
 
     def launch_all(self, stream=None, x: torch.Tensor | None = None) -> None:
         src = self.x if x is None else x
-        for first, count in self.steps:
-            if count == 1:
-                u = self.units[first]
-                u.module.launch(src, u.out, self.workspace, stream)
-            else:
-                u = self.units[first + count - 1]
-                self._launch_stage(first, count, src, u.out, stream)
-            src = u.out
+        for first, count, kind in self.steps:
+            src = self._launch_step(first, count, kind, src, stream)
 
     def _launch_stage(self, first: int, count: int, x: torch.Tensor, out: torch.Tensor, stream=None) -> None:
         mods = [self.units[k].module for k in range(first, first + count)]
@@ -202,8 +237,8 @@ class FusedNetwork:
         (``wl_kernel_launches``: 1 per fused block, 2 for the head; one per
         stage launch)."""
         n = 0
-        for first, count in self.steps:
-            if count > 1:
+        for first, count, kind in self.steps:
+            if kind != "unit":
                 n += 1
                 continue
             k = _lib.lib().wl_kernel_launches(ctypes.byref(self.units[first].module.desc))
@@ -221,12 +256,9 @@ class FusedNetwork:
         torch.cuda.synchronize(self.device)
         times = []
         src = self.x
-        for first, count in self.steps:
+        for first, count, kind in self.steps:
             u = self.units[first + count - 1]
-            if count == 1:
-                go = lambda s=src, u=u: u.module.launch(s, u.out, self.workspace)  # noqa: E731
-            else:
-                go = lambda s=src, f=first, c=count, u=u: self._launch_stage(f, c, s, u.out)  # noqa: E731
+            go = lambda s=src, f=first, c=count, k=kind: self._launch_step(f, c, k, s)  # noqa: E731
             for _ in range(3):
                 go()
             ev0 = torch.cuda.Event(enable_timing=True)
@@ -236,7 +268,7 @@ class FusedNetwork:
                 go()
             ev1.record()
             ev1.synchronize()
-            # a stage launch's time is shared equally by its units
+            # a stage / pair launch's time is shared equally by its units
             times += [ev0.elapsed_time(ev1) / iters / 1e3 / count] * count
             src = u.out
         return times

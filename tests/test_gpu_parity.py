@@ -203,13 +203,50 @@ def test_stage_launches_match_per_block_launches(batch):
     net = zoo.at_resolution(zoo.from_name("convfirstnet-pico"), 224)
     staged = FusedNetwork(net, batch=batch, seed=17)
     single = FusedNetwork(net, batch=batch, seed=17, stages=False)
-    assert any(c > 1 for _, c in staged.steps) and staged.launch_count() < single.launch_count()
+    assert any(k == "stage" for _, _, k in staged.steps) and any(k == "pair" for _, _, k in staged.steps)
+    assert staged.launch_count() < single.launch_count()
     staged.x.normal_()
     single.x.copy_(staged.x)
     staged.replay()
     single.replay()
     torch.cuda.synchronize()
-    assert torch.equal(staged.output, single.output)
+    # the stem + s1b0 pair kernel (mma.sync, fp32 accumulation in another
+    # order) is not bitwise identical to the two tcgen05 launches
+    close(staged.output.float().cpu().numpy(), single.output.float().cpu().numpy(), max_rel=2e-2, l2_rel=1e-2)
+
+
+def test_stem_block_pair_vs_oracle():
+    """The fused stem + first ConvFirst block (wl_pair_forward, stem_cf.cu)
+    against the oracle's stem then block, at Pico's 224 input and at a ragged
+    resolution (partial 8 x 16 tiles)."""
+    import ctypes
+
+    from paper_2404_03617_b200 import _lib
+
+    for hw in ((224, 224), (40, 72)):
+        net_in = TensorDims(2, hw[0], hw[1], 3)
+        s0, w0, x = _block_case(Stem(16), net_in, seed=5)
+        s1, w1, _ = _block_case(ConvFirst(8, 3), TensorDims(2, hw[0] // 2, hw[1] // 2, 16), seed=6)
+        m0 = FusedBlock(s0.block, s0.dims, weights=w0)
+        m1 = FusedBlock(s1.block, s1.dims, weights=w1)
+        L = _lib.lib()
+        assert L.wl_pair_supported(ctypes.byref(m0.desc), ctypes.byref(m1.desc)) == 1
+        nb = L.wl_pair_packed_bytes(ctypes.byref(m0.desc), ctypes.byref(m1.desc))
+        packed = np.zeros(nb, np.uint8)
+        c0 = [np.ascontiguousarray(v, np.float32) for v in m0.binding.device_weights(w0)]
+        c1 = [np.ascontiguousarray(v, np.float32) for v in m1.binding.device_weights(w1)]
+        fp0, fp1 = _lib.float_ptr_array(c0), _lib.float_ptr_array(c1)
+        _lib.check(L.wl_pair_pack(ctypes.byref(m0.desc), ctypes.byref(m1.desc), fp0[1], len(c0),
+                                  fp1[1], len(c1), packed.ctypes.data_as(ctypes.c_void_p)))
+        pd = torch.from_numpy(packed).cuda()
+        xd = torch.from_numpy(x).half().cuda()
+        out = torch.empty(m1.out_shape, dtype=torch.float16, device="cuda")
+        _lib.check(L.wl_pair_forward(ctypes.byref(m0.desc), ctypes.byref(m1.desc), xd.data_ptr(), pd.data_ptr(),
+                                     out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        h = om.unit_forward(Stem(16), w0, x).astype(np.float16).astype(np.float32)
+        ref = om.unit_forward(ConvFirst(8, 3), w1, h)
+        close(out.float().cpu().numpy(), ref)
 
 
 def test_stage_forward_abi_three_blocks():
