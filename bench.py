@@ -396,12 +396,15 @@ def other_configs(peak_burst, flush):
         out[key] = {"us": t * 1e6, "tflops": ops / t / 1e12, "frac_of_burst": ops / t / peak_burst,
                     "images_per_s": dims.n / t}
     spec = convnext_tiny(224)
-    net = FusedNetwork(spec, batch=128, seed=5)
-    net.x.normal_()
-    t = _device_time(lambda: net.launch_all(), flush)
     ops = 2 * network_macs(spec) * 128
-    out["C4_convnext_tiny_224_b128"] = {"ms": t * 1e3, "images_per_s": 128 / t, "tflops": ops / t / 1e12,
-                                        "frac_of_burst": ops / t / peak_burst, "gpu_launches": net.launch_count()}
+    for key, dt in (("C4_convnext_tiny_224_b128", torch.float16), ("C4_convnext_tiny_224_b128_bf16", torch.bfloat16)):
+        net = FusedNetwork(spec, batch=128, seed=5, dtype=dt)
+        net.x.normal_()
+        t = _device_time(lambda: net.launch_all(), flush)
+        out[key] = {"ms": t * 1e3, "images_per_s": 128 / t, "tflops": ops / t / 1e12,
+                    "frac_of_burst": ops / t / peak_burst, "gpu_launches": net.launch_count()}
+        del net
+        torch.cuda.empty_cache()
     return out
 
 

@@ -59,6 +59,12 @@ extern "C" {
 #define WL_ACT_SIGMOID 3
 #define WL_ACT_GELU 4
 
+/* storage types (fp32 accumulation either way). bf16 covers the FFN block,
+ * the ConvNeXt-T units (patchify stem, ConvNeXt blocks with C >= 96,
+ * downsample, LN head) and wl_gemm; the other families are fp16 only. */
+#define WL_DTYPE_F16 0
+#define WL_DTYPE_BF16 1
+
 /* normalisation after the conv of a conv-first block */
 #define WL_NORM_NONE 0
 #define WL_NORM_LAYERNORM 1
@@ -77,7 +83,8 @@ typedef struct wl_block_desc {
   float ln_eps;          /* LayerNorm epsilon                             */
   int32_t embed;         /* head: embedding width                         */
   int32_t classes;       /* head: classifier width                        */
-  int32_t reserved[4];
+  int32_t dtype;         /* WL_DTYPE_*: activation / weight storage type  */
+  int32_t reserved[3];
 } wl_block_desc;
 
 /* library / device ------------------------------------------------------ */
@@ -170,7 +177,7 @@ WL_API int wl_pair_forward(const wl_block_desc* d0, const wl_block_desc* d1, con
  * or null; res: null for none. Replaces the float64 `x @ w` of the
  * reference executor (machine.py:1017) on the device. */
 WL_API int wl_gemm(const void* a, int m, int k, int lda, const void* b, int n, int ldb, void* d, int ldd,
-                   const float* bias, int act, const void* res, int ldr, void* stream);
+                   const float* bias, int act, const void* res, int ldr, int dtype, void* stream);
 
 /* Host-buffer convenience with execute_numeric's exact contract
  * (machine.py:1053): float32 HOST input x (NHWC) and float32 HOST weights in

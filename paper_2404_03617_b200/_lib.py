@@ -21,6 +21,7 @@ KIND_CONVFIRST, KIND_MBCONV, KIND_FFN, KIND_STEM, KIND_HEAD = 1, 2, 3, 4, 5
 KIND_PATCH_STEM, KIND_DOWNSAMPLE, KIND_LN_HEAD = 6, 7, 8
 ACTS = {"identity": 0, "relu": 1, "silu": 2, "sigmoid": 3, "gelu": 4}
 NORM_NONE, NORM_LAYERNORM = 0, 1
+DTYPE_F16, DTYPE_BF16 = 0, 1
 
 # every symbol include/wlfuse.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -74,7 +75,8 @@ class BlockDesc(ctypes.Structure):
         ("ln_eps", ctypes.c_float),
         ("embed", ctypes.c_int32),
         ("classes", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 4),
+        ("dtype", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
     def as_tuple(self):
@@ -133,7 +135,7 @@ def lib() -> ctypes.CDLL:
         "wl_pair_pack": (ctypes.c_int, [D, D, P(P(ctypes.c_float)), ctypes.c_int, P(P(ctypes.c_float)), ctypes.c_int, vp]),
         "wl_pair_forward": (ctypes.c_int, [D, D, vp, vp, vp, vp]),
         "wl_gemm": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
-                                   ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, vp]),
+                                   ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp]),
         "wl_debug_set_trace": (None, [vp]),
     }
     for name, (res, args) in sig.items():
@@ -218,17 +220,20 @@ def execute_numeric_host(desc: BlockDesc, x: np.ndarray, weights) -> np.ndarray:
 
 def gemm(a, b, bias=None, act: str = "identity", res=None, out=None, stream=None):
     """D = act(a @ b.T + bias) (+ res) on the device through ``wl_gemm``:
-    a (M, K), b (N, K), res / out (M, N) fp16 CUDA tensors (row-major,
-    contiguous), bias fp32 (N,) or None."""
+    a (M, K), b (N, K), res / out (M, N) fp16 or bf16 CUDA tensors (one
+    dtype, row-major, contiguous), bias fp32 (N,) or None."""
     import torch
 
     m, k = a.shape
     n = b.shape[0]
+    if a.dtype not in (torch.float16, torch.bfloat16) or b.dtype != a.dtype:
+        raise ValueError("wl_gemm takes fp16 or bf16 operands of one dtype")
+    dt = DTYPE_BF16 if a.dtype == torch.bfloat16 else DTYPE_F16
     if out is None:
-        out = torch.empty((m, n), dtype=torch.float16, device=a.device)
+        out = torch.empty((m, n), dtype=a.dtype, device=a.device)
     st = (stream or torch.cuda.current_stream()).cuda_stream
     check(lib().wl_gemm(a.data_ptr(), m, k, a.stride(0), b.data_ptr(), n, b.stride(0), out.data_ptr(), out.stride(0),
                         bias.data_ptr() if bias is not None else None, ACTS[act],
-                        res.data_ptr() if res is not None else None, res.stride(0) if res is not None else 0, st),
+                        res.data_ptr() if res is not None else None, res.stride(0) if res is not None else 0, dt, st),
           "wl_gemm")
     return out

@@ -53,13 +53,18 @@ class FusedBlock(torch.nn.Module):
     model-level scheduler). ``weights`` uses the reference tensor names."""
 
     def __init__(self, block, dims: TensorDims, out_channels: int | None = None, weights: dict | None = None,
-                 seed: int = 0, device: str | torch.device = "cuda"):
+                 seed: int = 0, device: str | torch.device = "cuda", dtype: torch.dtype = torch.float16):
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("FusedBlock needs a CUDA device (there is no CPU fallback)")
+        if dtype not in (torch.float16, torch.bfloat16):
+            raise ValueError("FusedBlock stores activations and weights in fp16 or bf16")
+        self.dtype = dtype
         self.schedule = build_schedule(block, dims, out_channels=out_channels)
         self.binding = device_binding(self.schedule)  # zero-padded channels where C % 16 != 0
         self.desc = self.binding.desc
+        self.desc.dtype = _lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F16
+        _lib.check(_lib.lib().wl_validate(ctypes.byref(self.desc)), f"{self.schedule.label} ({dtype})")
         L = _lib.lib()
         dev = torch.device(device)
         _lib.check(L.wl_init(dev.index if dev.index is not None else torch.cuda.current_device()), "wl_init")
@@ -87,14 +92,14 @@ class FusedBlock(torch.nn.Module):
         )
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        if x.dtype != torch.float16 or not x.is_cuda or not x.is_contiguous():
-            raise ValueError("FusedBlock expects a contiguous NHWC fp16 CUDA tensor")
+        if x.dtype != self.dtype or not x.is_cuda or not x.is_contiguous():
+            raise ValueError(f"FusedBlock expects a contiguous NHWC {self.dtype} CUDA tensor")
         want = (self.schedule.dims.n, self.schedule.dims.h, self.schedule.dims.w, self.schedule.dims.c)
         if tuple(x.shape) != want:
             raise ValueError(f"input shape {tuple(x.shape)} does not match the bound dims {want}")
         if self.in_shape != want:
             x = torch.nn.functional.pad(x, (0, self.in_shape[3] - want[3]))
-        out = torch.empty(self.out_shape, dtype=torch.float16, device=x.device)
+        out = torch.empty(self.out_shape, dtype=self.dtype, device=x.device)
         self.launch(x, out)
         return self.binding.real_output(out).contiguous() if self.binding.padded else out
 

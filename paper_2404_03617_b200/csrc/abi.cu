@@ -2,6 +2,7 @@
 // launch planning, weight packing from the reference's float32 tensors,
 // tensor-map encoding and kernel launches.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -76,8 +77,18 @@ static inline uint16_t f2h(float v) {
   memcpy(&u, &h, 2);
   return u;
 }
+static inline uint16_t f2bf(float v) {
+  __nv_bfloat16 h = __float2bfloat16_rn(v);
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
+}
 void put_h(uint8_t* base, size_t off, float v) {
   uint16_t u = f2h(v);
+  memcpy(base + off, &u, 2);
+}
+void put_v(uint8_t* base, size_t off, float v, int dtype) {
+  uint16_t u = dtype == WL_DTYPE_BF16 ? f2bf(v) : f2h(v);
   memcpy(base + off, &u, 2);
 }
 
@@ -226,7 +237,8 @@ int wl_stage_max_blocks(const wl_block_desc* d) {
 }
 
 int wl_gemm(const void* a, int m, int k, int lda, const void* b, int n, int ldb, void* d, int ldd, const float* bias,
-            int act, const void* res, int ldr, void* stream) {
+            int act, const void* res, int ldr, int dtype, void* stream) {
+  if (dtype != WL_DTYPE_F16 && dtype != WL_DTYPE_BF16) return set_error(WL_EINVAL, "unknown dtype %d", dtype);
   if (!a || !b || !d) return set_error(WL_EINVAL, "null tensor pointer");
   if (act < 0 || act > 4) return set_error(WL_EINVAL, "unknown activation %d", act);
   int dev = 0;
@@ -237,7 +249,7 @@ int wl_gemm(const void* a, int m, int k, int lda, const void* b, int n, int ldb,
   e.act = act;
   e.res = reinterpret_cast<const __half*>(res);
   e.ldr = ldr;
-  return gemm_run(a, m, k, lda, b, n, ldb, d, ldd, e, reinterpret_cast<cudaStream_t>(stream));
+  return gemm_run(a, m, k, lda, b, n, ldb, d, ldd, e, reinterpret_cast<cudaStream_t>(stream), dtype);
 }
 
 int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float* const* weights, int count,
@@ -254,7 +266,8 @@ int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float*
   output_dims(*d, &on, &oh, &ow, &oc);
   const size_t nx = (size_t)d->n * d->h * d->w * d->c, nz = (size_t)on * oh * ow * oc;
   std::vector<uint16_t> xh(nx), zh(nz);
-  for (size_t i = 0; i < nx; ++i) xh[i] = f2h(x_host[i]);
+  const bool bf = d->dtype == WL_DTYPE_BF16;
+  for (size_t i = 0; i < nx; ++i) xh[i] = bf ? f2bf(x_host[i]) : f2h(x_host[i]);
   void *dx = nullptr, *dz = nullptr, *dp = nullptr, *dws = nullptr;
   const int64_t wsb = workspace_bytes(*d);
   int rc = WL_OK;
@@ -279,9 +292,15 @@ int wl_execute_numeric(const wl_block_desc* d, const float* x_host, const float*
   cudaFree(dws);
   if (rc) return rc;
   for (size_t i = 0; i < nz; ++i) {
-    __half h;
-    memcpy(&h, &zh[i], 2);
-    z_host[i] = __half2float(h);
+    if (bf) {
+      __nv_bfloat16 h;
+      memcpy(&h, &zh[i], 2);
+      z_host[i] = __bfloat162float(h);
+    } else {
+      __half h;
+      memcpy(&h, &zh[i], 2);
+      z_host[i] = __half2float(h);
+    }
   }
   return WL_OK;
 }

@@ -38,6 +38,12 @@ int init_kernels() {
 int validate_desc(const wl_block_desc& d) {
   const Family* f = family_of(d);
   if (!f) return set_error(WL_EINVAL, "unknown block kind %d", d.kind);
+  if (d.dtype != WL_DTYPE_F16 && d.dtype != WL_DTYPE_BF16) return set_error(WL_EINVAL, "unknown dtype %d", d.dtype);
+  if (d.dtype == WL_DTYPE_BF16) {
+    const bool ok = d.kind == WL_KIND_FFN || d.kind == WL_KIND_PATCH_STEM || d.kind == WL_KIND_DOWNSAMPLE ||
+                    d.kind == WL_KIND_LN_HEAD || cnx_wide(d);
+    if (!ok) return set_error(WL_EUNSUPPORTED, "bf16 storage is built for the FFN and ConvNeXt-T units only");
+  }
   return f->validate(d);
 }
 int weight_count(const wl_block_desc& d) { return family_of(d)->weight_count(d); }

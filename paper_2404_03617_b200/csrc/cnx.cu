@@ -88,19 +88,20 @@ constexpr int kDwThreads = 384;
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-template <int KS>
+template <int KS, typename T>
 __global__ void __launch_bounds__(kDwThreads, 1)
-    dwln_kernel(const __half* __restrict__ x, const __half* __restrict__ wdw, const float* __restrict__ bdw,
-                const float* __restrict__ g, const float* __restrict__ be, __half* __restrict__ y, int N, int H, int W,
+    dwln_kernel(const T* __restrict__ x, const T* __restrict__ wdw, const float* __restrict__ bdw,
+                const float* __restrict__ g, const float* __restrict__ be, T* __restrict__ y, int N, int H, int W,
                 int C, float eps, int RB, int nseg) {
+  constexpr bool kF16 = Dt<T>::kIdescAB == 0;  // fp16: taps in packed half; bf16: fp32 FMAs
   constexpr int R = KS / 2, PX = kDwPx, NI = PX + 2 * R;
   extern __shared__ __align__(16) uint8_t dsm[];
   const int C8 = C / 8, WG = (W + PX - 1) / PX, rowh = W * C;
   const int NR = 2 * RB + 2 * R;                 // ring rows
   const int WP = WG * PX + 2 * R;                // padded row width (zero columns both sides + tail)
   const int prowh = WP * C;                      // padded row (halves)
-  __half* s_in = reinterpret_cast<__half*>(dsm);  // [NR][W + 2R][C]
-  __half* s_y = s_in + (size_t)NR * prowh;        // [RB][W][C] pre-norm
+  T* s_in = reinterpret_cast<T*>(dsm);  // [NR][W + 2R][C]
+  T* s_y = s_in + (size_t)NR * prowh;   // [RB][W][C] pre-norm
   float* s_sum = reinterpret_cast<float*>(s_y + (size_t)RB * rowh);  // [RB * W] mean
   float* s_sq = s_sum + RB * W;                                       // [RB * W] rstd
   float* s_part = s_sq + RB * W;                                      // [RB * W][C8]
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
       hi = min(hi, ye + R);
       for (int i = tid; i < (hi - lo) * per_row; i += nt) {
         const int iy = lo + i / per_row, off = i % per_row;
-        __half* dst = s_in + (size_t)((iy - base) % NR) * prowh + R * C + off * 8;
+        T* dst = s_in + (size_t)((iy - base) % NR) * prowh + R * C + off * 8;
         if (iy >= 0 && iy < H)
           cp_async16(dst, x + ((size_t)img * H + iy) * rowh + off * 8);
         else
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
         int slot = (y0 + ry - R - base) % NR;  // ring slot of the window's first row
 #pragma unroll
         for (int dy = 0; dy < KS; ++dy) {
-          const __half* row = s_in + (size_t)slot * prowh + (size_t)x0 * C + c8 * 8;
+          const T* row = s_in + (size_t)slot * prowh + (size_t)x0 * C + c8 * 8;
           slot = slot + 1 == NR ? 0 : slot + 1;
           uint4 in[NI];
 #pragma unroll
@@ -159,15 +160,27 @@ __global__ void __launch_bounds__(kDwThreads, 1)
 #pragma unroll
           for (int dx = 0; dx < KS; ++dx) {
             const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wdw + (size_t)(dy * KS + dx) * C + c8 * 8));
-            const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
+            if constexpr (kF16) {
+              const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
 #pragma unroll
-            for (int p = 0; p < PX; ++p) {
-              const __half2* i2 = reinterpret_cast<const __half2*>(&in[p + dx]);
+              for (int p = 0; p < PX; ++p) {
+                const __half2* i2 = reinterpret_cast<const __half2*>(&in[p + dx]);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) h[p][i] = __hfma2(i2[i], w2[i], h[p][i]);
+                for (int i = 0; i < 4; ++i) h[p][i] = __hfma2(i2[i], w2[i], h[p][i]);
+              }
+            } else {
+              float wf[8];
+              unpack8t<T>(wv, wf);
+#pragma unroll
+              for (int p = 0; p < PX; ++p) {
+                float xf[8];
+                unpack8t<T>(in[p + dx], xf);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[p][i] = fmaf(xf[i], wf[i], acc[p][i]);
+              }
             }
           }
-          if (dy == R || dy == KS - 1) {  // widen to fp32 twice per window (at most 4 rows of taps in half)
+          if (kF16 && (dy == R || dy == KS - 1)) {  // widen to fp32 twice per window (<= 4 rows of taps in half)
 #pragma unroll
             for (int p = 0; p < PX; ++p)
 #pragma unroll
@@ -191,7 +204,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
             s += acc[p][i];
           }
           s_part[(ry * W + x0 + p) * C8 + c8] = s;
-          *reinterpret_cast<uint4*>(s_y + ((size_t)ry * W + x0 + p) * C + c8 * 8) = pack8(acc[p]);
+          *reinterpret_cast<uint4*>(s_y + ((size_t)ry * W + x0 + p) * C + c8 * 8) = pack8t<T>(acc[p]);
         }
       }
       __syncthreads();
@@ -206,7 +219,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
         const int c8 = it % C8, pix = it / C8;
         const float mean = s_sum[pix];
         float v[8];
-        unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
+        unpack8t<T>(lds128(s_y + (size_t)pix * C + c8 * 8), v);
         float s = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) s += (v[i] - mean) * (v[i] - mean);
@@ -223,12 +236,12 @@ __global__ void __launch_bounds__(kDwThreads, 1)
         const int c8 = it % C8, pix = it / C8;
         const float mean = s_sum[pix], rstd = s_sq[pix];
         float v[8], gg[8], bb[8];
-        unpack8(lds128(s_y + (size_t)pix * C + c8 * 8), v);
+        unpack8t<T>(lds128(s_y + (size_t)pix * C + c8 * 8), v);
         ld8f(g + c8 * 8, gg);
         ld8f(be + c8 * 8, bb);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = (v[i] - mean) * rstd * gg[i] + bb[i];
-        *reinterpret_cast<uint4*>(y + ((size_t)img * H + y0) * rowh + (size_t)pix * C + c8 * 8) = pack8(v);
+        *reinterpret_cast<uint4*>(y + ((size_t)img * H + y0) * rowh + (size_t)pix * C + c8 * 8) = pack8t<T>(v);
       }
       __syncthreads();  // the ring rows of this window may be overwritten by the next prefetch
     }
@@ -257,8 +270,9 @@ int dwln_segments(int N, int H, int RB) {
 // LayerNorm per pixel; S2D: the output row is written in 2x2 space-to-depth
 // order A[(img, y/2, x/2)][((y%2) 2 + x%2) C + c]. CTA = P pixels x C/8
 // threads; one 16-byte chunk per thread, two-pass statistics over shared sums.
-__global__ void __launch_bounds__(256) ln_s2d_kernel(const __half* __restrict__ x, const float* __restrict__ g,
-                                                     const float* __restrict__ be, __half* __restrict__ A, int n,
+template <typename T>
+__global__ void __launch_bounds__(256) ln_s2d_kernel(const T* __restrict__ x, const float* __restrict__ g,
+                                                     const float* __restrict__ be, T* __restrict__ A, int n,
                                                      int H, int W, int C, float eps) {
   // fixed-order (deterministic) reductions: per-thread partials, then the
   // pixel's first thread sums its C/8 partials in channel order
@@ -272,7 +286,7 @@ __global__ void __launch_bounds__(256) ln_s2d_kernel(const __half* __restrict__ 
   float v[8];
   float s = 0.f;
   if (on) {
-    unpack8(__ldg(reinterpret_cast<const uint4*>(x + pix * C) + c8), v);
+    unpack8t<T>(__ldg(reinterpret_cast<const uint4*>(x + pix * C) + c8), v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += v[i];
   }
@@ -307,15 +321,16 @@ __global__ void __launch_bounds__(256) ln_s2d_kernel(const __half* __restrict__ 
     for (int i = 0; i < 8; ++i) v[i] = (v[i] - mean) * rstd * gg[i] + bb[i];
     const int xx = (int)(pix % W), yy = (int)((pix / W) % H);
     const int64_t img = pix / ((int64_t)W * H);
-    __half* dst = A + (((img * (H / 2) + yy / 2) * (W / 2) + xx / 2) * 4 + (yy % 2) * 2 + xx % 2) * C;
-    reinterpret_cast<uint4*>(dst)[c8] = pack8(v);
+    T* dst = A + (((img * (H / 2) + yy / 2) * (W / 2) + xx / 2) * 4 + (yy % 2) * 2 + xx % 2) * C;
+    reinterpret_cast<uint4*>(dst)[c8] = pack8t<T>(v);
   }
   pdl_trigger();
 }
 
 // global average pool + LayerNorm: one CTA per image, thread = channel pair
-__global__ void __launch_bounds__(512) pool_ln_kernel(const __half* __restrict__ x, const float* __restrict__ g,
-                                                      const float* __restrict__ be, __half* __restrict__ f, int HW,
+template <typename T>
+__global__ void __launch_bounds__(512) pool_ln_kernel(const T* __restrict__ x, const float* __restrict__ g,
+                                                      const float* __restrict__ be, T* __restrict__ f, int HW,
                                                       int C, float eps) {
   __shared__ float red[2][32];
   const int img = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -323,9 +338,9 @@ __global__ void __launch_bounds__(512) pool_ln_kernel(const __half* __restrict__
   pdl_wait();
   float m0 = 0.f, m1 = 0.f;
   if (on) {
-    const __half2* px = reinterpret_cast<const __half2*>(x + (size_t)img * HW * C) + tid;
+    const uint32_t* px = reinterpret_cast<const uint32_t*>(x + (size_t)img * HW * C) + tid;
     for (int p = 0; p < HW; ++p) {
-      const float2 v = __half22float2(px[(size_t)p * (C / 2)]);
+      const float2 v = Dt<T>::unpack2(px[(size_t)p * (C / 2)]);
       m0 += v.x;
       m1 += v.y;
     }
@@ -346,8 +361,8 @@ __global__ void __launch_bounds__(512) pool_ln_kernel(const __half* __restrict__
   const float var = block_sum(on ? d0 * d0 + d1 * d1 : 0.f, 1) / (float)C;
   const float rstd = rsqrtf(var + eps);
   if (on)
-    reinterpret_cast<__half2*>(f + (size_t)img * C)[tid] =
-        __floats2half2_rn(d0 * rstd * g[2 * tid] + be[2 * tid], d1 * rstd * g[2 * tid + 1] + be[2 * tid + 1]);
+    reinterpret_cast<uint32_t*>(f + (size_t)img * C)[tid] =
+        Dt<T>::pack2(d0 * rstd * g[2 * tid] + be[2 * tid], d1 * rstd * g[2 * tid + 1] + be[2 * tid + 1]);
   pdl_trigger();
 }
 
@@ -365,9 +380,9 @@ void put_f32(uint8_t* base, int64_t off, const float* src, int64_t count) {
   memcpy(base + off, src, (size_t)count * 4);
 }
 // B operand (N rows of K fp16, K contiguous) from a reference (K, N) matrix
-void put_t16(uint8_t* base, int64_t off, const float* src, int K, int N) {
+void put_t16(uint8_t* base, int64_t off, const float* src, int K, int N, int dtype) {
   for (int nn = 0; nn < N; ++nn)
-    for (int k = 0; k < K; ++k) put_h(base, off + ((int64_t)nn * K + k) * 2, src[(int64_t)k * N + nn]);
+    for (int k = 0; k < K; ++k) put_v(base, off + ((int64_t)nn * K + k) * 2, src[(int64_t)k * N + nn], dtype);
 }
 
 // row batch of the two-GEMM FFN so that the hidden stays L2-resident
@@ -383,26 +398,26 @@ int64_t hidden_rows(int64_t M, int hid) {
 // hidden in the L2-resident workspace
 int ffn_rows(const __half* x, int64_t M, int C, int hid, int K, const __half* ut, const float* a, const __half* vt,
              const float* b, int act, const __half* res, __half* z, __half* hbuf, const uint8_t* wimg,
-             cudaStream_t st) {
+             cudaStream_t st, int dtype) {
   // the fused kernel wins while its weights stay resident (C <= 128); from C = 192
   // the two GEMMs with an L2-resident hidden are faster (ConvNeXt-T b128: 14x14 stage
   // 250 vs 121 us, 28x28 stage 300 vs 272 us per block, profiles/r02_convnext_*)
   if (K == C && C <= 128 && wimg && ffn_fused_ok(M, C, hid))
-    return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st);
+    return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st, dtype);
   const int64_t rb = hidden_rows(M, hid);
   for (int64_t r0 = 0; r0 < M; r0 += rb) {
     const int rows = (int)(M - r0 < rb ? M - r0 : rb);
     GemmEpi e1;
     e1.bias = a;
     e1.act = act;
-    if (int e = gemm_run(x + r0 * C, rows, C, C, ut, hid, C, hbuf, hid, e1, st)) return e;
+    if (int e = gemm_run(x + r0 * C, rows, C, C, ut, hid, C, hbuf, hid, e1, st, dtype)) return e;
     GemmEpi e2;
     e2.bias = b;
     if (res) {
       e2.res = res + r0 * K;
       e2.ldr = K;
     }
-    if (int e = gemm_run(hbuf, rows, hid, hid, vt, K, hid, z + r0 * K, K, e2, st)) return e;
+    if (int e = gemm_run(hbuf, rows, hid, hid, vt, K, hid, z + r0 * K, K, e2, st, dtype)) return e;
   }
   return WL_OK;
 }
@@ -454,9 +469,9 @@ int ffn_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   memset(out, 0, (size_t)L.total);
   put_f32(out, L.o_a, w[1], hid);
   put_f32(out, L.o_b, w[3], C);
-  put_t16(out, L.o_u, w[0], C, hid);  // U^T: (hid, C)
-  put_t16(out, L.o_v, w[2], hid, C);  // V^T: (C, hid)
-  ffn_pack_images(C, hid, w[0], w[2], out + L.o_img);
+  put_t16(out, L.o_u, w[0], C, hid, d.dtype);  // U^T: (hid, C)
+  put_t16(out, L.o_v, w[2], hid, C, d.dtype);  // V^T: (C, hid)
+  ffn_pack_images(C, hid, w[0], w[2], out + L.o_img, d.dtype);
   return WL_OK;
 }
 int64_t ffn_ws(const wl_block_desc& d) {
@@ -471,7 +486,7 @@ int ffn_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void*
                   reinterpret_cast<const __half*>(pk + L.o_u), reinterpret_cast<const float*>(pk + L.o_a),
                   reinterpret_cast<const __half*>(pk + L.o_v), reinterpret_cast<const float*>(pk + L.o_b), d.act,
                   nullptr, reinterpret_cast<__half*>(z), reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr),
-                  L.o_img < L.total ? pk + L.o_img : nullptr, st);
+                  L.o_img < L.total ? pk + L.o_img : nullptr, st, d.dtype);
 }
 
 // ------------------------------------------------- wide ConvNeXt block
@@ -525,15 +540,15 @@ int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   const int C = d.c, hid = d.expansion * d.c, taps = d.ksize * d.ksize;
   memset(out, 0, (size_t)L.total);
   for (int c = 0; c < C; ++c)
-    for (int t = 0; t < taps; ++t) put_h(out, L.o_wdw + ((int64_t)t * C + c) * 2, w[0][(size_t)c * taps + t]);
+    for (int t = 0; t < taps; ++t) put_v(out, L.o_wdw + ((int64_t)t * C + c) * 2, w[0][(size_t)c * taps + t], d.dtype);
   put_f32(out, L.o_bdw, w[1], C);
   put_f32(out, L.o_g, w[2], C);
   put_f32(out, L.o_be, w[3], C);
   put_f32(out, L.o_a, w[5], hid);
   put_f32(out, L.o_b, w[7], C);
-  put_t16(out, L.o_u, w[4], C, hid);
-  put_t16(out, L.o_v, w[6], hid, C);
-  ffn_pack_images(C, hid, w[4], w[6], out + L.o_img);
+  put_t16(out, L.o_u, w[4], C, hid, d.dtype);
+  put_t16(out, L.o_v, w[6], hid, C, d.dtype);
+  ffn_pack_images(C, hid, w[4], w[6], out + L.o_img, d.dtype);
   return WL_OK;
 }
 int64_t cnx_wide_ws(const wl_block_desc& d) {
@@ -547,19 +562,26 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
   __half* xh = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
   __half* hb = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr + a128(M * d.c * 2));
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
-  auto k = d.ksize == 7 ? dwln_kernel<7> : dwln_kernel<3>;
   const int rb = dwln_rows(d.ksize, d.w, d.c), nseg = dwln_segments(d.n, d.h, rb);
   const int grid = std::min(d.n * nseg, kNumSMs);
-  if (int e = launch_pdl(k, grid, kDwThreads, dwln_smem(d.ksize, d.w, d.c), st, "dwln launch",
-                            reinterpret_cast<const __half*>(x),
-                            reinterpret_cast<const __half*>(pk + L.o_wdw), reinterpret_cast<const float*>(pk + L.o_bdw),
-                            reinterpret_cast<const float*>(pk + L.o_g), reinterpret_cast<const float*>(pk + L.o_be), xh,
-                            d.n, d.h, d.w, d.c, eps, rb, nseg))
-    return e;
+  auto run_dw = [&](auto kern, auto tag) {
+    using T = decltype(tag);
+    return launch_pdl(kern, grid, kDwThreads, dwln_smem(d.ksize, d.w, d.c), st, "dwln launch",
+                      reinterpret_cast<const T*>(x), reinterpret_cast<const T*>(pk + L.o_wdw),
+                      reinterpret_cast<const float*>(pk + L.o_bdw), reinterpret_cast<const float*>(pk + L.o_g),
+                      reinterpret_cast<const float*>(pk + L.o_be), reinterpret_cast<T*>(xh), d.n, d.h, d.w, d.c, eps,
+                      rb, nseg);
+  };
+  int e;
+  if (d.dtype == WL_DTYPE_BF16)
+    e = d.ksize == 7 ? run_dw(dwln_kernel<7, __nv_bfloat16>, __nv_bfloat16{}) : run_dw(dwln_kernel<3, __nv_bfloat16>, __nv_bfloat16{});
+  else
+    e = d.ksize == 7 ? run_dw(dwln_kernel<7, __half>, __half{}) : run_dw(dwln_kernel<3, __half>, __half{});
+  if (e) return e;
   return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
                   reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
                   reinterpret_cast<const float*>(pk + L.o_b), d.act, reinterpret_cast<const __half*>(x),
-                  reinterpret_cast<__half*>(z), hb, L.o_img < L.total ? pk + L.o_img : nullptr, st);
+                  reinterpret_cast<__half*>(z), hb, L.o_img < L.total ? pk + L.o_img : nullptr, st, d.dtype);
 }
 
 namespace {
@@ -607,7 +629,7 @@ int ps_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
     put_f32(out, L.o_g, w[2], d.k);
     put_f32(out, L.o_be, w[3], d.k);
   }
-  for (int64_t i = 0; i < (int64_t)d.k * L.kk; ++i) put_h(out, L.o_w + i * 2, w[0][i]);  // (k, p, p, c) = B rows
+  for (int64_t i = 0; i < (int64_t)d.k * L.kk; ++i) put_v(out, L.o_w + i * 2, w[0][i], d.dtype);  // (k, p, p, c) = B rows
   return WL_OK;
 }
 int64_t ps_ws(const wl_block_desc& d) {
@@ -632,7 +654,7 @@ int ps_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
     ep.ln_b = reinterpret_cast<const float*>(pk + L.o_be);
     ep.ln_eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
   }
-  return gemm_run(A, (int)M, L.kk, L.kk, pk + L.o_w, d.k, L.kk, z, d.k, ep, st);
+  return gemm_run(A, (int)M, L.kk, L.kk, pk + L.o_w, d.k, L.kk, z, d.k, ep, st, d.dtype);
 }
 
 // ----------------------------------------------------------- downsample
@@ -673,7 +695,7 @@ int ds_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   put_f32(out, L.o_g, w[0], d.c);
   put_f32(out, L.o_be, w[1], d.c);
   put_f32(out, L.o_b, w[3], d.k);
-  for (int64_t i = 0; i < (int64_t)d.k * 4 * d.c; ++i) put_h(out, L.o_w + i * 2, w[2][i]);
+  for (int64_t i = 0; i < (int64_t)d.k * 4 * d.c; ++i) put_v(out, L.o_w + i * 2, w[2][i], d.dtype);
   return WL_OK;
 }
 int64_t ds_ws(const wl_block_desc& d) { return kWsHdr + a128((int64_t)d.n * d.h * d.w * d.c * 2); }
@@ -684,13 +706,19 @@ int ds_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
   const int64_t npix = (int64_t)d.n * d.h * d.w;
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
   const int P = 256 / (d.c / 8);
-  if (int e = launch_simple(ln_s2d_kernel, (int)((npix + P - 1) / P), 256, st, "ln_s2d launch",
-                            reinterpret_cast<const __half*>(x), reinterpret_cast<const float*>(pk + L.o_g),
-                            reinterpret_cast<const float*>(pk + L.o_be), A, d.n, d.h, d.w, d.c, eps))
-    return e;
+  const int grid = (int)((npix + P - 1) / P);
+  const float* g = reinterpret_cast<const float*>(pk + L.o_g);
+  const float* be = reinterpret_cast<const float*>(pk + L.o_be);
+  const int e = d.dtype == WL_DTYPE_BF16
+                    ? launch_simple(ln_s2d_kernel<__nv_bfloat16>, grid, 256, st, "ln_s2d launch",
+                                    reinterpret_cast<const __nv_bfloat16*>(x), g, be,
+                                    reinterpret_cast<__nv_bfloat16*>(A), d.n, d.h, d.w, d.c, eps)
+                    : launch_simple(ln_s2d_kernel<__half>, grid, 256, st, "ln_s2d launch",
+                                    reinterpret_cast<const __half*>(x), g, be, A, d.n, d.h, d.w, d.c, eps);
+  if (e) return e;
   GemmEpi ep;
   ep.bias = reinterpret_cast<const float*>(pk + L.o_b);
-  return gemm_run(A, (int)(npix / 4), 4 * d.c, 4 * d.c, pk + L.o_w, d.k, 4 * d.c, z, d.k, ep, st);
+  return gemm_run(A, (int)(npix / 4), 4 * d.c, 4 * d.c, pk + L.o_w, d.k, 4 * d.c, z, d.k, ep, st, d.dtype);
 }
 
 // -------------------------------------------------------------- LN head
@@ -730,7 +758,7 @@ int lh_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   put_f32(out, L.o_g, w[0], d.c);
   put_f32(out, L.o_be, w[1], d.c);
   put_f32(out, L.o_b, w[3], d.classes);
-  put_t16(out, L.o_w, w[2], d.c, d.classes);
+  put_t16(out, L.o_w, w[2], d.c, d.classes, d.dtype);
   return WL_OK;
 }
 int64_t lh_ws(const wl_block_desc& d) { return kWsHdr + a128((int64_t)d.n * d.c * 2); }
@@ -740,21 +768,30 @@ int lh_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
   __half* f = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
   const int threads = align_up(d.c / 2, 32);
-  if (int e = launch_simple(pool_ln_kernel, d.n, threads, st, "pool_ln launch", reinterpret_cast<const __half*>(x),
-                            reinterpret_cast<const float*>(pk + L.o_g), reinterpret_cast<const float*>(pk + L.o_be), f,
-                            d.h * d.w, d.c, eps))
-    return e;
+  const float* g = reinterpret_cast<const float*>(pk + L.o_g);
+  const float* be = reinterpret_cast<const float*>(pk + L.o_be);
+  const int e = d.dtype == WL_DTYPE_BF16
+                    ? launch_simple(pool_ln_kernel<__nv_bfloat16>, d.n, threads, st, "pool_ln launch",
+                                    reinterpret_cast<const __nv_bfloat16*>(x), g, be,
+                                    reinterpret_cast<__nv_bfloat16*>(f), d.h * d.w, d.c, eps)
+                    : launch_simple(pool_ln_kernel<__half>, d.n, threads, st, "pool_ln launch",
+                                    reinterpret_cast<const __half*>(x), g, be, f, d.h * d.w, d.c, eps);
+  if (e) return e;
   GemmEpi ep;
   ep.bias = reinterpret_cast<const float*>(pk + L.o_b);
-  return gemm_run(f, d.n, d.c, d.c, pk + L.o_w, d.classes, d.c, z, d.classes, ep, st);
+  return gemm_run(f, d.n, d.c, d.c, pk + L.o_w, d.classes, d.c, z, d.classes, ep, st, d.dtype);
 }
 
 int cnx_init() {
   if (int e = gemm_init()) return e;
   if (int e = ffn_fused_init()) return e;
-  for (auto k : {dwln_kernel<7>, dwln_kernel<3>})
+  for (auto k : {dwln_kernel<7, __half>, dwln_kernel<3, __half>})
     if (int e = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
                            "cudaFuncSetAttribute(dwln)"))
+      return e;
+  for (auto k : {dwln_kernel<7, __nv_bfloat16>, dwln_kernel<3, __nv_bfloat16>})
+    if (int e = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+                           "cudaFuncSetAttribute(dwln bf16)"))
       return e;
   return WL_OK;
 }

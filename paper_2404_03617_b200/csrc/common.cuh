@@ -1,5 +1,6 @@
 // common.cuh — element-wise helpers shared by the fused kernels.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
 #include "sm100.cuh"
@@ -102,6 +103,55 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
   q.z = pack_h2(f[4], f[5]);
   q.w = pack_h2(f[6], f[7]);
   return q;
+}
+
+// ---- storage-type helpers (fp16 / bf16 activations and weights, fp32 math)
+template <typename T>
+struct Dt;
+template <>
+struct Dt<__half> {
+  static constexpr uint32_t kIdescAB = 0;  // kind::f16 A / B format: f16
+  static __device__ __forceinline__ uint32_t pack2(float a, float b) { return pack_h2(a, b); }
+  static __device__ __forceinline__ float2 unpack2(uint32_t v) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&v));
+  }
+};
+template <>
+struct Dt<__nv_bfloat16> {
+  static constexpr uint32_t kIdescAB = (1u << 7) | (1u << 10);  // A / B format: bf16
+  static __device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack2(uint32_t v) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v));
+  }
+};
+template <typename T>
+__device__ __forceinline__ uint4 pack8t(const float* f) {
+  return make_uint4(Dt<T>::pack2(f[0], f[1]), Dt<T>::pack2(f[2], f[3]), Dt<T>::pack2(f[4], f[5]),
+                    Dt<T>::pack2(f[6], f[7]));
+}
+template <typename T>
+__device__ __forceinline__ void unpack8t(const uint4& q, float* f) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = Dt<T>::unpack2(w[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+// bias-added pair -> activation -> packed storage: packed half math for fp16
+// (MUFU tanh form), fp32 math for bf16
+template <typename T, int ACT>
+__device__ __forceinline__ uint32_t act_pack2(float a, float b) {
+  if constexpr (sizeof(T) == 2 && Dt<T>::kIdescAB == 0) {
+    const __half2 h = act_h2<ACT>(__floats2half2_rn(a, b));
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    return Dt<T>::pack2(act<ACT>(a), act<ACT>(b));
+  }
 }
 
 __device__ __forceinline__ uint32_t tmem_lane_addr(uint32_t base, int quad, int col) {

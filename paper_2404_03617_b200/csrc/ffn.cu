@@ -89,7 +89,7 @@ __device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32
 }
 __device__ __forceinline__ void ff_bar(int n) { asm volatile("bar.sync 2, %0;" ::"r"(n) : "memory"); }
 
-template <int ACT>
+template <int ACT, typename T>
 __global__ void __launch_bounds__(ff::kThreads, 1)
     ffn_fused_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tu,
                      const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tr,
@@ -213,9 +213,9 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------------------------------------------------- MMA issuer
-      const uint32_t idesc_e = make_idesc_f16(128, HC);
+      const uint32_t idesc_e = make_idesc_f16(128, HC) | Dt<T>::kIdescAB;
       const int zn = C > 256 ? C / 2 : C;
-      const uint32_t idesc_z = make_idesc_f16(128, zn);
+      const uint32_t idesc_z = make_idesc_f16(128, zn) | Dt<T>::kIdescAB;
       const uint32_t sa = smem_u32(s_a), sr = smem_u32(s_ring), svr = smem_u32(s_vring);
       int useq = 0, vseq = 0;
       for (int t = 0; t < my_tiles; ++t) {
@@ -308,12 +308,9 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
             load16f(aj + u * 16, bb);
             uint32_t o[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __half2 h = __floats2half2_rn(__uint_as_float(v[16 * u + 2 * i]) + bb[2 * i],
-                                            __uint_as_float(v[16 * u + 2 * i + 1]) + bb[2 * i + 1]);
-              h = act_h2<ACT>(h);
-              o[i] = *reinterpret_cast<uint32_t*>(&h);
-            }
+            for (int i = 0; i < 8; ++i)
+              o[i] = act_pack2<T, ACT>(__uint_as_float(v[16 * u + 2 * i]) + bb[2 * i],
+                                       __uint_as_float(v[16 * u + 2 * i + 1]) + bb[2 * i + 1]);
             WL_TMEM_ST8(eb + u * 8, o);
           }
         tmem_st_wait();
@@ -354,21 +351,21 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
                 if (grow < a.M) {
                   if (a.has_res) {
                     float rr[8];
-                    unpack8(__ldg(reinterpret_cast<const uint4*>(a.res + grow * C + c16 + 8 * hh)), rr);
+                    unpack8t<T>(__ldg(reinterpret_cast<const uint4*>(a.res + grow * C + c16 + 8 * hh)), rr);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) f[i] += rr[i];
                   }
-                  *reinterpret_cast<uint4*>(a.z + grow * C + c16 + 8 * hh) = pack8(f);
+                  *reinterpret_cast<uint4*>(a.z + grow * C + c16 + 8 * hh) = pack8t<T>(f);
                 }
               } else {
                 uint8_t* p = rowp + (((c8 + hh) ^ (r & 7)) << 4);
                 if (a.has_res) {
                   float rr[8];
-                  unpack8(lds128(p), rr);
+                  unpack8t<T>(lds128(p), rr);
 #pragma unroll
                   for (int i = 0; i < 8; ++i) f[i] += rr[i];
                 }
-                *reinterpret_cast<uint4*>(p) = pack8(f);
+                *reinterpret_cast<uint4*>(p) = pack8t<T>(f);
               }
             }
           }
@@ -454,14 +451,18 @@ bool ffn_fused_plan(int M, int C, int hid, ff::Args& a) {
 }
 using FfnK = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                       const ff::Args);
-FfnK ffn_kernel_for(int act) {
+template <typename T>
+FfnK ffn_kernel_t(int act) {
   switch (act) {
-    case kRelu: return ffn_fused_kernel<kRelu>;
-    case kSilu: return ffn_fused_kernel<kSilu>;
-    case kSigmoid: return ffn_fused_kernel<kSigmoid>;
-    case kGelu: return ffn_fused_kernel<kGelu>;
+    case kRelu: return ffn_fused_kernel<kRelu, T>;
+    case kSilu: return ffn_fused_kernel<kSilu, T>;
+    case kSigmoid: return ffn_fused_kernel<kSigmoid, T>;
+    case kGelu: return ffn_fused_kernel<kGelu, T>;
   }
-  return ffn_fused_kernel<kIdentity>;
+  return ffn_fused_kernel<kIdentity, T>;
+}
+FfnK ffn_kernel_for(int act, int dtype) {
+  return dtype == WL_DTYPE_BF16 ? ffn_kernel_t<__nv_bfloat16>(act) : ffn_kernel_t<__half>(act);
 }
 }  // namespace
 
@@ -472,7 +473,7 @@ bool ffn_fused_ok(int64_t M, int C, int hid) {
 
 // x, res, z: [M][C] fp16; ut: [hid][C] fp16; vt: [C][hid] fp16; a: [hid], b: [C] fp32
 int ffn_fused_run(const void* x, int64_t M, int C, int hid, const void* wimg, const float* abias, const float* bbias,
-                  int act, const void* res, void* z, cudaStream_t st) {
+                  int act, const void* res, void* z, cudaStream_t st, int dtype) {
   ff::Args a;
   if (!ffn_fused_plan((int)M, C, hid, a)) return set_error(WL_EUNSUPPORTED, "fused FFN: no plan for C=%d hid=%d", C, hid);
   a.act = act;
@@ -497,7 +498,7 @@ int ffn_fused_run(const void* x, int64_t M, int C, int hid, const void* wimg, co
   if (int e = map2(&tz, z, C, M, C, 128)) return e;
   const int smem = a.s_vring + a.NV * a.vs_bytes + ((int)sizeof(ff::Bars) + 15) / 16 * 16 + (hid + C) * 4;
   const int grid = a.tiles < kNumSMs ? a.tiles : kNumSMs;
-  return launch_pdl(ffn_kernel_for(act), grid, ff::kThreads, smem, st, "ffn_fused launch", tx, tu, tv, tr, tz, a);
+  return launch_pdl(ffn_kernel_for(act, dtype), grid, ff::kThreads, smem, st, "ffn_fused launch", tx, tu, tv, tr, tz, a);
 }
 
 int64_t ffn_images_bytes(int C, int hid) {
@@ -509,7 +510,7 @@ int64_t ffn_images_bytes(int C, int hid) {
 // u: reference (C, hid); v: reference (hid, C). Chunk j image: U_j as
 // ceil(C/64) K-slabs of [HC rows][128 B], V_j as HC/64 K-slabs of [C rows][128 B],
 // 16-byte chunk c of row n at n * 128 + ((c ^ n % 8) << 4) (the 128-byte swizzle)
-void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* out) {
+void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* out, int dtype) {
   ff::Args a;
   if (!ffn_fused_plan(128, C, hid, a)) return;
   const int HC = a.HC;
@@ -521,23 +522,25 @@ void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* ou
         for (int kk = 0; kk < 64; ++kk) {
           const int k = sl * 64 + kk;
           const float val = k < C ? u[(size_t)k * hid + j * HC + n] : 0.f;
-          put_h(ui, (size_t)sl * HC * 128 + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2, val);
+          put_v(ui, (size_t)sl * HC * 128 + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2, val, dtype);
         }
     for (int sl = 0; sl < HC / 64; ++sl)
       for (int n = 0; n < C; ++n)
         for (int kk = 0; kk < 64; ++kk) {
           const int k = j * HC + sl * 64 + kk;
-          put_h(vi, (size_t)sl * C * 128 + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2, v[(size_t)k * C + n]);
+          put_v(vi, (size_t)sl * C * 128 + n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2, v[(size_t)k * C + n],
+                dtype);
         }
   }
 }
 
 int ffn_fused_init() {
-  for (int act : {kIdentity, kRelu, kSilu, kSigmoid, kGelu})
-    if (int e = check_cuda(cudaFuncSetAttribute(ffn_kernel_for(act), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                ff::kSmemMax),
-                           "cudaFuncSetAttribute(ffn_fused)"))
-      return e;
+  for (int dt : {WL_DTYPE_F16, WL_DTYPE_BF16})
+    for (int act : {kIdentity, kRelu, kSilu, kSigmoid, kGelu})
+      if (int e = check_cuda(cudaFuncSetAttribute(ffn_kernel_for(act, dt),
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, ff::kSmemMax),
+                             "cudaFuncSetAttribute(ffn_fused)"))
+        return e;
   return WL_OK;
 }
 

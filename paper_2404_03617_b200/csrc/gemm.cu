@@ -95,6 +95,7 @@ __device__ __forceinline__ void gemm_bias(const float* s_bias, const uint32_t* v
   for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + b[i];
 }
 
+template <typename T>
 __global__ void __launch_bounds__(gm::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                 const __grid_constant__ CUtensorMap td, const __grid_constant__ CUtensorMap tr,
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------------------------------------------------- MMA issuer
-      const uint32_t idesc = make_idesc_f16(128, a.BN);
+      const uint32_t idesc = make_idesc_f16(128, a.BN) | Dt<T>::kIdescAB;
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -210,11 +211,11 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           uint8_t* p = rowp + (((c8 + hh) ^ (r & 7)) << 4);
           if (a.has_res) {
             float rr[8], g[8];
-            unpack8(lds128(p), rr);
-            unpack8(o[hh], g);
+            unpack8t<T>(lds128(p), rr);
+            unpack8t<T>(o[hh], g);
 #pragma unroll
             for (int i = 0; i < 8; ++i) g[i] += rr[i];
-            o[hh] = pack8(g);
+            o[hh] = pack8t<T>(g);
           }
           *reinterpret_cast<uint4*>(p) = o[hh];
         }
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
               const int n = n0 + (u_lo + j) * 16 + i, c = n < a.N ? n : a.N - 1;
               f[i] = (__uint_as_float(v[16 * j + i]) - mean) * rstd * __ldg(a.ln_g + c) + __ldg(a.ln_b + c);
             }
-            uint4 o[2] = {pack8(f), pack8(f + 8)};
+            uint4 o[2] = {pack8t<T>(f), pack8t<T>(f + 8)};
             stage_unit(u_lo + j, o);
           }
       } else {
@@ -292,9 +293,13 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
               uint32_t* ow = reinterpret_cast<uint32_t*>(o);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
-                if (a.act) h = act_rt_h2(h, a.act);
-                ow[i] = *reinterpret_cast<uint32_t*>(&h);
+                if constexpr (Dt<T>::kIdescAB == 0) {
+                  __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+                  if (a.act) h = act_rt_h2(h, a.act);
+                  ow[i] = *reinterpret_cast<uint32_t*>(&h);
+                } else {
+                  ow[i] = Dt<T>::pack2(act_rt(f[2 * i], a.act), act_rt(f[2 * i + 1], a.act));
+                }
               }
               stage_unit(u0 + j, o);
             }
@@ -335,7 +340,7 @@ static int pick_bn(int N) {
 }
 
 int gemm_run(const void* A, int M, int K, int lda, const void* Bw, int N, int ldb, void* D, int ldd,
-             const GemmEpi& e, cudaStream_t st) {
+             const GemmEpi& e, cudaStream_t st, int dtype) {
   if (M < 1 || N < 1 || K < 1 || K % 8 || lda % 8 || ldb % 8 || ldd % 8 || N % 8 || (e.res && e.ldr % 8))
     return set_error(WL_EINVAL, "gemm: M=%d N=%d K=%d lda=%d ldb=%d ldd=%d: sizes/strides must be multiples of 8", M,
                      N, K, lda, ldb, ldd);
@@ -375,12 +380,19 @@ int gemm_run(const void* A, int M, int K, int lda, const void* Bw, int N, int ld
   if (int r = map2(&tR, e.res ? (const void*)e.res : D, N, M, e.res ? e.ldr : ldd, 128)) return r;
   const int smem = a.s_stage + a.slabs * 16384 + (int)sizeof(gm::Bars);
   const int grid = a.tiles < kNumSMs ? a.tiles : kNumSMs;
-  return launch_pdl(gemm_kernel, grid, gm::kThreads, smem, st, "gemm launch", tA, tB, tD, tR, a);
+  if (dtype == WL_DTYPE_BF16)
+    return launch_pdl(gemm_kernel<__nv_bfloat16>, grid, gm::kThreads, smem, st, "gemm launch", tA, tB, tD, tR, a);
+  return launch_pdl(gemm_kernel<__half>, grid, gm::kThreads, smem, st, "gemm launch", tA, tB, tD, tR, a);
 }
 
 int gemm_init() {
-  return check_cuda(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gm::kSmemMax),
-                    "cudaFuncSetAttribute(gemm)");
+  if (int e = check_cuda(cudaFuncSetAttribute(gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              gm::kSmemMax),
+                         "cudaFuncSetAttribute(gemm)"))
+    return e;
+  return check_cuda(cudaFuncSetAttribute(gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         gm::kSmemMax),
+                    "cudaFuncSetAttribute(gemm bf16)");
 }
 
 }  // namespace wl

@@ -6,6 +6,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include "../../include/wlfuse.h"
 
 namespace wl {
 
@@ -25,7 +26,7 @@ struct GemmEpi {
 // weight stored output-major), D: [M][ldd] fp16. K, lda, ldb, ldd, ldr
 // multiples of 8; M, N >= 1. Stream-ordered, graph-capturable.
 int gemm_run(const void* A, int M, int K, int lda, const void* B, int N, int ldb, void* D, int ldd,
-             const GemmEpi& e, cudaStream_t st);
+             const GemmEpi& e, cudaStream_t st, int dtype = 0);  // dtype: WL_DTYPE_*
 int gemm_init();
 
 }  // namespace wl

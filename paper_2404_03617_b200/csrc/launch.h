@@ -13,6 +13,7 @@ int check_cuda(cudaError_t e, const char* what);
 int encode_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                 const uint32_t* box, bool swizzle128 = false);
 void put_h(uint8_t* base, size_t off, float v);
+void put_v(uint8_t* base, size_t off, float v, int dtype);  // fp16 or bf16 by WL_DTYPE_*
 static inline size_t core_off_h(int row, int k, int lbo) {
   return (size_t)(k / 8) * lbo + (size_t)(row / 8) * 128 + (size_t)(row % 8) * 16 + (size_t)(k % 8) * 2;
 }
@@ -90,9 +91,9 @@ int ffn_launches(const wl_block_desc& d);
 // fused FFN (ffn.cu): hidden kept on chip
 bool ffn_fused_ok(int64_t M, int C, int hid);
 int ffn_fused_run(const void* x, int64_t M, int C, int hid, const void* wimg, const float* abias, const float* bbias,
-                  int act, const void* res, void* z, cudaStream_t st);
+                  int act, const void* res, void* z, cudaStream_t st, int dtype);
 int64_t ffn_images_bytes(int C, int hid);
-void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* out);
+void ffn_pack_images(int C, int hid, const float* u, const float* v, uint8_t* out, int dtype);
 int ffn_fused_init();
 // stride-1 MBConv stage launch (mb_s1.cu)
 int mb1_stage_max(const wl_block_desc& d);

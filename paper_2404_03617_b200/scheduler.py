@@ -41,7 +41,7 @@ class FusedNetwork:
     """
 
     def __init__(self, net: NetworkSpec, batch: int, device: str | torch.device = "cuda", seed: int = 0,
-                 weights: dict | None = None, stages: bool = True):
+                 weights: dict | None = None, stages: bool = True, dtype: torch.dtype = torch.float16):
         self.net = net
         self.batch = batch
         self.device = torch.device(device)
@@ -58,13 +58,14 @@ class FusedNetwork:
                 wts = weights[inst.label]
             else:
                 wts = init_weights(sched, np.random.default_rng(seed + i))
-            mod = FusedBlock(inst.block, dims, inst.out_channels, weights=wts, device=self.device)
+            mod = FusedBlock(inst.block, dims, inst.out_channels, weights=wts, device=self.device, dtype=dtype)
             ws_bytes = max(ws_bytes, mod.workspace.numel())
-            out = torch.empty(mod.out_shape, dtype=torch.float16, device=self.device)
+            out = torch.empty(mod.out_shape, dtype=dtype, device=self.device)
             self.units.append(Unit(inst.label, inst.block, mod, out))
         # the static input carries the first unit's DEVICE width (a stem-less
         # stack at C % 16 != 0 runs zero-padded); __call__ pads into it
-        self.x = torch.zeros(self.units[0].module.in_shape, dtype=torch.float16, device=self.device)
+        self.dtype = dtype
+        self.x = torch.zeros(self.units[0].module.in_shape, dtype=dtype, device=self.device)
         self.in_channels = self.instances[0].in_channels
         # one workspace shared by every unit (launches are stream-ordered)
         self.workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device)

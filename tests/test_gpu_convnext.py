@@ -115,3 +115,56 @@ def test_ffn_module_device_path():
     dev(xd, out)
     torch.cuda.synchronize()
     close(out.float().cpu().numpy(), om.unit_forward(s.block, w, x))
+
+
+# ---------------------------------------------------------------- bf16
+BF_MAX, BF_L2 = 4e-2, 8e-3  # bf16 storage (8-bit mantissa), fp32 accumulation
+
+
+def _bf16(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()
+
+
+@pytest.mark.parametrize("name,block,dims", [
+    ("ffn_c96", FFN(4, "gelu"), TensorDims(1, 10, 100, 96)),
+    ("ffn_c384", FFN(4, "gelu"), TensorDims(2, 14, 14, 384)),
+    ("patch_stem", PatchifyStem(96), TensorDims(2, 64, 64, 3)),
+    ("downsample", Downsample(192), TensorDims(2, 28, 28, 96)),
+    ("ln_head", LNHead(1000), TensorDims(3, 7, 7, 768)),
+    ("convnext_96", ConvNeXtBlock(7, 4, "gelu"), TensorDims(2, 28, 28, 96)),
+    ("convnext_384", ConvNeXtBlock(7, 4, "gelu"), TensorDims(2, 14, 14, 384)),
+    ("convnext_768", ConvNeXtBlock(7, 4, "gelu"), TensorDims(2, 7, 7, 768)),
+])
+def test_bf16_units_vs_oracle(name, block, dims):
+    s, w, x = _case(block, dims)
+    w = {k: _bf16(v) for k, v in w.items()}
+    x = _bf16(x)
+    m = FusedBlock(s.block, s.dims, weights=w, dtype=torch.bfloat16)
+    xd = torch.from_numpy(x).cuda().bfloat16().reshape(m.in_shape if block.kind != "ffn" else x.shape)
+    out = torch.empty(m.out_shape, dtype=torch.bfloat16, device="cuda")
+    m.launch(xd, out)
+    torch.cuda.synchronize()
+    close(out.float().cpu().numpy(), om.unit_forward(block, w, x), max_rel=BF_MAX, l2_rel=BF_L2)
+
+
+def test_convnext_tiny_bf16_logits():
+    """ConvNeXt-T end to end in bf16 storage."""
+    m = FusedNetwork(convnext_tiny(224), batch=2, seed=21, dtype=torch.bfloat16)
+    rng = np.random.default_rng(2)
+    x = _bf16(rng.standard_normal((2, 224, 224, 3)))
+    out = m(torch.from_numpy(x).cuda().bfloat16())
+    torch.cuda.synchronize()
+    src = x
+    for u, inst in zip(m.units, m.instances):
+        got = u.out.float().cpu().numpy()
+        ref = om.unit_forward(inst.block, {k: _bf16(v) for k, v in u.module.weights.items()}, src)
+        close(got.reshape(ref.shape), ref, max_rel=BF_MAX, l2_rel=BF_L2)
+        src = got.reshape(ref.shape)
+    assert out.dtype == torch.bfloat16 and torch.isfinite(out.float()).all()
+
+
+def test_fp16_only_families_refuse_bf16():
+    from paper_2404_03617_b200.core import MBConv
+
+    with pytest.raises(Exception):
+        FusedBlock(MBConv(8, 4, 0.25), TensorDims(1, 14, 14, 128), dtype=torch.bfloat16)

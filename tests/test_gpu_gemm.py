@@ -54,3 +54,17 @@ def test_gemm_rejects_bad_strides():
     b = torch.zeros(16, 20, device="cuda").half()
     with pytest.raises(ValueError):
         _lib.gemm(a, b)
+
+
+def test_gemm_bf16_vs_torch():
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(700, 384, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(1536, 384, device="cuda", generator=g) / 384 ** 0.5).bfloat16()
+    bias = torch.randn(1536, device="cuda", generator=g)
+    r = torch.randn(700, 1536, device="cuda", generator=g).bfloat16()
+    out = _lib.gemm(a, b, bias, "gelu", r)
+    torch.cuda.synchronize()
+    ref = _ref(a, b, bias, "gelu", r)
+    assert out.dtype == torch.bfloat16
+    err = (out.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= 4e-2, err
