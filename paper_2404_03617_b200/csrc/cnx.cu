@@ -522,8 +522,12 @@ int ffn_launches(const wl_block_desc& d) {
 }
 
 bool cnx_wide(const wl_block_desc& d) {
+  // C > 128: only this path. C = 96..128 with a 7x7 stencil: this path for large
+  // batches (ConvNeXt-T b128 56x56 stage: 453 vs 544 us per block), the single
+  // fused conv-first kernel for small ones (BASELINE config 1, b8: 50 vs 63 us)
+  const bool big = (int64_t)d.n * d.h * d.w >= 65536;
   return d.kind == WL_KIND_CONVFIRST && d.norm == WL_NORM_LAYERNORM && d.group_width == 1 && d.stride == 1 &&
-         (d.c > 128 || (d.c >= 96 && d.ksize == 7));
+         (d.c > 128 || (d.c >= 96 && d.ksize == 7 && (big || d.dtype == WL_DTYPE_BF16)));
 }
 int cnx_wide_validate(const wl_block_desc& d) {
   if (int e = common_dims(d)) return e;
