@@ -88,11 +88,14 @@ constexpr int kDwThreads = 384;
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-template <int KS, typename T>
+// CT: the channel count as a compile-time constant (0: runtime C) so every
+// shared-memory and weight offset of the stencil folds into an immediate
+template <int KS, typename T, int CT>
 __global__ void __launch_bounds__(kDwThreads, 1)
     dwln_kernel(const T* __restrict__ x, const T* __restrict__ wdw, const float* __restrict__ bdw,
                 const float* __restrict__ g, const float* __restrict__ be, T* __restrict__ y, int N, int H, int W,
-                int C, float eps, int RB, int nseg) {
+                int C_rt, float eps, int RB, int nseg) {
+  const int C = CT ? CT : C_rt;
   constexpr bool kF16 = Dt<T>::kIdescAB == 0;  // fp16: taps in packed half; bf16: fp32 FMAs
   constexpr int R = KS / 2, PX = kDwPx, NI = PX + 2 * R;
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -576,11 +579,18 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
                       reinterpret_cast<const float*>(pk + L.o_be), reinterpret_cast<T*>(xh), d.n, d.h, d.w, d.c, eps,
                       rb, nseg);
   };
-  int e;
-  if (d.dtype == WL_DTYPE_BF16)
-    e = d.ksize == 7 ? run_dw(dwln_kernel<7, __nv_bfloat16>, __nv_bfloat16{}) : run_dw(dwln_kernel<3, __nv_bfloat16>, __nv_bfloat16{});
-  else
-    e = d.ksize == 7 ? run_dw(dwln_kernel<7, __half>, __half{}) : run_dw(dwln_kernel<3, __half>, __half{});
+  auto pick = [&](auto tag) {
+    using T = decltype(tag);
+    if (d.ksize == 3) return run_dw(dwln_kernel<3, T, 0>, tag);
+    switch (d.c) {
+      case 96: return run_dw(dwln_kernel<7, T, 96>, tag);
+      case 192: return run_dw(dwln_kernel<7, T, 192>, tag);
+      case 384: return run_dw(dwln_kernel<7, T, 384>, tag);
+      case 768: return run_dw(dwln_kernel<7, T, 768>, tag);
+    }
+    return run_dw(dwln_kernel<7, T, 0>, tag);
+  };
+  const int e = d.dtype == WL_DTYPE_BF16 ? pick(__nv_bfloat16{}) : pick(__half{});
   if (e) return e;
   return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
                   reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
@@ -789,14 +799,16 @@ int lh_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* 
 int cnx_init() {
   if (int e = gemm_init()) return e;
   if (int e = ffn_fused_init()) return e;
-  for (auto k : {dwln_kernel<7, __half>, dwln_kernel<3, __half>})
-    if (int e = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
-                           "cudaFuncSetAttribute(dwln)"))
-      return e;
-  for (auto k : {dwln_kernel<7, __nv_bfloat16>, dwln_kernel<3, __nv_bfloat16>})
-    if (int e = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
-                           "cudaFuncSetAttribute(dwln bf16)"))
-      return e;
+  auto set = [](auto k) {
+    return check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+                      "cudaFuncSetAttribute(dwln)");
+  };
+  for (int e : {set(dwln_kernel<3, __half, 0>), set(dwln_kernel<7, __half, 0>), set(dwln_kernel<7, __half, 96>),
+                set(dwln_kernel<7, __half, 192>), set(dwln_kernel<7, __half, 384>), set(dwln_kernel<7, __half, 768>),
+                set(dwln_kernel<3, __nv_bfloat16, 0>), set(dwln_kernel<7, __nv_bfloat16, 0>),
+                set(dwln_kernel<7, __nv_bfloat16, 96>), set(dwln_kernel<7, __nv_bfloat16, 192>),
+                set(dwln_kernel<7, __nv_bfloat16, 384>), set(dwln_kernel<7, __nv_bfloat16, 768>)})
+    if (e) return e;
   return WL_OK;
 }
 int no_init() { return WL_OK; }
