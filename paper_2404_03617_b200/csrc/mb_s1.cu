@@ -404,9 +404,9 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       const int g2 = blk * nch + j, b = g2 & 1, u = g2 >> 1;
       const float2 bc = *reinterpret_cast<const float2*>(s_bconv + j * kHC + g * 8 + tq * 2);
       // W_sq rows of this warp's 8 channels, output = lane (consumed after the pool below)
-      __half wq[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) wq[c] = lane < sq ? wsq[(size_t)(j * kHC + g * 8 + c) * sq + lane] : __half(0.f);
+      // (W_sq stored transposed: the lane's 8 channels are one 16-byte load)
+      const uint4 wq4 = __ldg(reinterpret_cast<const uint4*>(wsq + (size_t)lane * hid + j * kHC + g * 8));
+      const __half* wq = reinterpret_cast<const __half*>(&wq4);
       mbar_wait(&B.h1_full[b], u & 1);
       const uint32_t plane = smem_u32(s_h1 + b * 8 * GS + g * GS) + 16;  // + 1 margin row
       // Q_r: x4 of padded row r at dx = -1 (lanes 0-15) and dx = 0 (lanes 16-31)
@@ -625,7 +625,7 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   // packed blob
   int64_t p = a.hdr_bytes;
   a.o_se = p;
-  int se = hid * a.sq * 2;
+  int se = hid * 32 * 2;  // W_sq transposed: [32 squeeze outputs (zero past sq)][hid]
   a.o_bsq = align_up(se, 16);
   se = a.o_bsq + a.sq * 4;
   a.o_wex = align_up(se, 16);
@@ -705,7 +705,8 @@ int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   }
   for (int i = 0; i < C; ++i) hb[2 * hid + i] = bprj[i];
   uint8_t* se = out + a.o_se;
-  for (int i = 0; i < hid * sq; ++i) put_h(se, (size_t)i * 2, wsq[i]);
+  for (int o = 0; o < sq; ++o)  // transposed [o][hid]; rows sq..31 stay zero
+    for (int i = 0; i < hid; ++i) put_h(se, ((size_t)o * hid + i) * 2, wsq[(size_t)i * sq + o]);
   for (int i = 0; i < sq; ++i) reinterpret_cast<float*>(se + a.o_bsq)[i] = bsq[i];
   for (int i = 0; i < sq * hid; ++i) put_h(se + a.o_wex, (size_t)i * 2, wex[i]);
   for (int i = 0; i < hid; ++i) reinterpret_cast<float*>(se + a.o_bex)[i] = bex[i];
