@@ -283,6 +283,7 @@ def run_gpu(args):
             cpu = cpu_describe(pool, steps, sum(pool.step() for _ in range(steps)))
             pool.close()
         others = None if args.skip_configs else other_configs(peak_burst, flush)
+        fvl = None if args.skip_configs else fused_vs_layer_wise(flush)
         line = {
             "metric": f"images/sec ({args.model}@224 inference)",
             "value": value,
@@ -336,6 +337,7 @@ def run_gpu(args):
             "gpu_launches": model.launch_count() * args.steps,
             "units": {u.label: round(t * 1e6, 1) for u, t in zip(model.units, unit_s)},
             "other_configs": others,
+            "fused_vs_layer_wise": fvl,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -404,6 +406,46 @@ def other_configs(peak_burst, flush):
         out[key] = {"ms": t * 1e3, "images_per_s": 128 / t, "tflops": ops / t / 1e12,
                     "frac_of_burst": ops / t / peak_burst, "gpu_launches": net.launch_count()}
         del net
+        torch.cuda.empty_cache()
+    return out
+
+
+def fused_vs_layer_wise(flush):
+    """The paper's comparison measured on this GPU: each
+    block once as the fused kernel and once as the reference's LAYER_WISE
+    schedule on the device (layerwise.cu: one launch per layer, every
+    intermediate through HBM), same weights and inputs, CUDA graphs, L2
+    flushed per replay. ``model_bytes`` is the reference's DRAM accounting
+    of each schedule (complexity.block_costs, fp16)."""
+    import torch
+
+    from paper_2404_03617_b200 import complexity
+    from paper_2404_03617_b200.blocks import FusedBlock
+    from paper_2404_03617_b200.core import ConvFirst, ExecutionScheme, MBConv, TensorDims
+    from paper_2404_03617_b200.machine import DeviceSpec
+
+    acct = DeviceSpec("accounting", 1.0, 1.0, bytes_per_element=2)
+    out = {}
+    for key, blk, dims in (("convfirst_pico_112x112x16_b128", ConvFirst(8, 3), TensorDims(128, 112, 112, 16)),
+                           ("convfirst_c1_56x56x96_b8", ConvFirst(8, 6), TensorDims(8, 56, 56, 96)),
+                           ("mbconv_pico_14x14x128_b128", MBConv(8, 4, 0.25), TensorDims(128, 14, 14, 128)),
+                           ("mbconv_c2_t1_28x28x80_b128", MBConv(1, 4, 0.25), TensorDims(128, 28, 28, 80))):
+        row = {}
+        fused = FusedBlock(blk, dims, seed=3)
+        x = torch.randn(*fused.in_shape, device="cuda").half()
+        for name, m in (("fused", fused),
+                        ("layer_wise", FusedBlock(blk, dims, weights=fused.weights,
+                                                  scheme=ExecutionScheme.LAYER_WISE))):
+            z = torch.empty(m.out_shape, dtype=torch.float16, device="cuda")
+            t = _device_time(lambda: m.launch(x, z), flush)
+            scheme = ExecutionScheme.BLOCK_FUSION if name == "fused" else ExecutionScheme.LAYER_WISE
+            costs = complexity.block_costs(blk, dims, scheme, acct)
+            mb = sum(c.bytes for c in costs) if isinstance(costs, list) else costs.bytes
+            row[name] = {"us": t * 1e6, "launches": m.launch_count(), "model_bytes": mb,
+                         "model_gbps": mb / t / 1e9}
+            del m
+        row["speedup"] = row["layer_wise"]["us"] / row["fused"]["us"]
+        out[key] = row
         torch.cuda.empty_cache()
     return out
 

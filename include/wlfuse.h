@@ -65,6 +65,13 @@ extern "C" {
 #define WL_DTYPE_F16 0
 #define WL_DTYPE_BF16 1
 
+/* execution scheme (core.py:15-17 ExecutionScheme): the fused block kernels,
+ * or the reference's LAYER_WISE schedule — one launch per layer, every
+ * intermediate through HBM (ConvFirst / MBConv stride 1, FFN; fp16) — the
+ * baseline block fusion is measured against */
+#define WL_SCHEME_FUSED 0
+#define WL_SCHEME_LAYER_WISE 1
+
 /* normalisation after the conv of a conv-first block */
 #define WL_NORM_NONE 0
 #define WL_NORM_LAYERNORM 1
@@ -84,7 +91,8 @@ typedef struct wl_block_desc {
   int32_t embed;         /* head: embedding width                         */
   int32_t classes;       /* head: classifier width                        */
   int32_t dtype;         /* WL_DTYPE_*: activation / weight storage type  */
-  int32_t reserved[3];
+  int32_t scheme;        /* WL_SCHEME_*: fused block or the layer-wise baseline */
+  int32_t reserved[2];
 } wl_block_desc;
 
 /* library / device ------------------------------------------------------ */

@@ -22,6 +22,7 @@ KIND_PATCH_STEM, KIND_DOWNSAMPLE, KIND_LN_HEAD = 6, 7, 8
 ACTS = {"identity": 0, "relu": 1, "silu": 2, "sigmoid": 3, "gelu": 4}
 NORM_NONE, NORM_LAYERNORM = 0, 1
 DTYPE_F16, DTYPE_BF16 = 0, 1
+SCHEME_FUSED, SCHEME_LAYER_WISE = 0, 1
 
 # every symbol include/wlfuse.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -76,7 +77,8 @@ class BlockDesc(ctypes.Structure):
         ("embed", ctypes.c_int32),
         ("classes", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 3),
+        ("scheme", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
     def as_tuple(self):

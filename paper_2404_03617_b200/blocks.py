@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import ConvFirst, ConvNeXtBlock, Head, MBConv, Stem, TensorDims
+from .core import ConvFirst, ConvNeXtBlock, ExecutionScheme, Head, MBConv, Stem, TensorDims
 from .machine import FusedSchedule, build_schedule, device_binding, random_inputs
 
 
@@ -50,20 +50,26 @@ def init_weights(s: FusedSchedule, rng: np.random.Generator, residual_gain: floa
 
 class FusedBlock(torch.nn.Module):
     """One fused block bound to a batch geometry (the layer of the
-    model-level scheduler). ``weights`` uses the reference tensor names."""
+    model-level scheduler). ``weights`` uses the reference tensor names.
+    ``scheme=LAYER_WISE`` binds the same block to the reference's layer-wise
+    schedule (one launch per layer, intermediates through HBM) — the
+    baseline the fused kernels are compared with."""
 
     def __init__(self, block, dims: TensorDims, out_channels: int | None = None, weights: dict | None = None,
-                 seed: int = 0, device: str | torch.device = "cuda", dtype: torch.dtype = torch.float16):
+                 seed: int = 0, device: str | torch.device = "cuda", dtype: torch.dtype = torch.float16,
+                 scheme: ExecutionScheme = ExecutionScheme.BLOCK_FUSION):
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("FusedBlock needs a CUDA device (there is no CPU fallback)")
         if dtype not in (torch.float16, torch.bfloat16):
             raise ValueError("FusedBlock stores activations and weights in fp16 or bf16")
         self.dtype = dtype
-        self.schedule = build_schedule(block, dims, out_channels=out_channels)
+        self.schedule = build_schedule(block, dims, scheme=scheme, out_channels=out_channels)
         self.binding = device_binding(self.schedule)  # zero-padded channels where C % 16 != 0
         self.desc = self.binding.desc
         self.desc.dtype = _lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F16
+        if scheme == ExecutionScheme.LAYER_WISE:
+            self.desc.scheme = _lib.SCHEME_LAYER_WISE
         _lib.check(_lib.lib().wl_validate(ctypes.byref(self.desc)), f"{self.schedule.label} ({dtype})")
         L = _lib.lib()
         dev = torch.device(device)
@@ -90,6 +96,10 @@ class FusedBlock(torch.nn.Module):
             ),
             f"{self.schedule.label}",
         )
+
+    def launch_count(self) -> int:
+        """Kernel launches one ``launch`` issues (wl_kernel_launches)."""
+        return _lib.check(_lib.lib().wl_kernel_launches(ctypes.byref(self.desc)), "wl_kernel_launches")
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if x.dtype != self.dtype or not x.is_cuda or not x.is_contiguous():

@@ -5,6 +5,7 @@
 namespace wl {
 
 static const Family* family_of(const wl_block_desc& d) {
+  if (d.scheme == WL_SCHEME_LAYER_WISE) return &kLayerwiseFamily;
   switch (d.kind) {
     case WL_KIND_CONVFIRST: return &kCfFamily;
     case WL_KIND_MBCONV: return &kMbFamily;
@@ -29,7 +30,8 @@ int init_kernels() {
     return set_error(WL_ECUDA, "no current CUDA device");
   std::call_once(once[dev], [dev] {
     status[dev] = WL_OK;
-    for (const Family* f : {&kCfFamily, &kCf2Family, &kMbFamily, &kStemFamily, &kHeadFamily, &kFfnFamily})
+    for (const Family* f :
+         {&kCfFamily, &kCf2Family, &kMbFamily, &kStemFamily, &kHeadFamily, &kFfnFamily, &kLayerwiseFamily})
       if (f->init && (status[dev] = f->init()) != WL_OK) break;
   });
   return status[dev];
@@ -39,6 +41,9 @@ int validate_desc(const wl_block_desc& d) {
   const Family* f = family_of(d);
   if (!f) return set_error(WL_EINVAL, "unknown block kind %d", d.kind);
   if (d.dtype != WL_DTYPE_F16 && d.dtype != WL_DTYPE_BF16) return set_error(WL_EINVAL, "unknown dtype %d", d.dtype);
+  if (d.scheme != WL_SCHEME_FUSED && d.scheme != WL_SCHEME_LAYER_WISE)
+    return set_error(WL_EINVAL, "unknown scheme %d", d.scheme);
+  if (d.scheme == WL_SCHEME_LAYER_WISE) return f->validate(d);
   if (d.dtype == WL_DTYPE_BF16) {
     const bool ok = d.kind == WL_KIND_FFN || d.kind == WL_KIND_PATCH_STEM || d.kind == WL_KIND_DOWNSAMPLE ||
                     d.kind == WL_KIND_LN_HEAD || cnx_wide(d);
@@ -52,6 +57,7 @@ int64_t packed_bytes(const wl_block_desc& d) { return family_of(d)->packed_bytes
 int pack_weights(const wl_block_desc& d, const float* const* w, uint8_t* out) { return family_of(d)->pack(d, w, out); }
 int64_t workspace_bytes(const wl_block_desc& d) { return family_of(d)->workspace_bytes(d); }
 int kernel_launches(const wl_block_desc& d) {
+  if (d.scheme == WL_SCHEME_LAYER_WISE) return lw_launches(d);
   if (d.kind == WL_KIND_HEAD || d.kind == WL_KIND_PATCH_STEM || d.kind == WL_KIND_DOWNSAMPLE ||
       d.kind == WL_KIND_LN_HEAD)
     return 2;

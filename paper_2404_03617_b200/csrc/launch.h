@@ -79,6 +79,8 @@ extern const Family kFfnFamily;
 extern const Family kPatchStemFamily;
 extern const Family kDownsampleFamily;
 extern const Family kLnHeadFamily;
+extern const Family kLayerwiseFamily;  // the reference's LAYER_WISE schedules (layerwise.cu)
+int lw_launches(const wl_block_desc& d);
 // wide ConvNeXt block (C > 128): dwln + two GEMMs (cnx.cu), reached through the conv-first family
 bool cnx_wide(const wl_block_desc& d);
 int cnx_wide_validate(const wl_block_desc& d);

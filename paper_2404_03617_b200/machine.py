@@ -199,9 +199,10 @@ def build_schedule(
     processors: int | None = None,
 ) -> FusedSchedule:
     """Same contract as machine.build_schedule (machine.py:736-772). Both
-    schemes build (their traffic is accounted by ``simulate_traffic``); only
-    BLOCK_FUSION schedules execute on the B200 — the layer-wise schedule is
-    the CPU oracle's. ``chunk`` / ``processors`` follow the reference's
+    schemes build (their traffic is accounted by ``simulate_traffic``) and
+    execute on the B200: BLOCK_FUSION on the fused block kernels, LAYER_WISE
+    (ConvFirst / MBConv stride 1, FFN) as one launch per layer with every
+    intermediate through HBM (layerwise.cu). ``chunk`` / ``processors`` follow the reference's
     validity rules; the fused kernel computes the same values whatever the
     partition (its hidden-chunk widths and CTA split come from the TMEM /
     shared-memory budget)."""
@@ -406,10 +407,12 @@ def execute_numeric(s: FusedSchedule, inputs: dict) -> np.ndarray:
     (machine.py:1053-1061): float32 inputs keyed by tensor name, float32
     output; missing or mis-shaped inputs raise ScheduleError. Inputs are
     rounded to fp16 on the way in (the kernels' storage type), accumulation
-    is fp32 in TMEM, and the result is the fp16 output widened to float32."""
-    if s.scheme != ExecutionScheme.BLOCK_FUSION:
-        raise ScheduleError("the B200 backend executes BLOCK_FUSION schedules; the layer-wise schedule is the "
-                            "CPU oracle's (machine.py:418-459, 593-646)")
+    is fp32 in TMEM, and the result is the fp16 output widened to float32.
+    LAYER_WISE schedules run the reference's layer-by-layer order
+    (machine.py:418-459, 593-646, 339-365) as separate device launches."""
+    layer_wise = s.scheme == ExecutionScheme.LAYER_WISE
+    if layer_wise and not isinstance(s.block, (ConvFirst, MBConv, FFN)):
+        raise ScheduleError(f"the reference has no layer-wise schedule for {type(s.block).__name__} units")
     arrays = {}
     for t in s.tensors:
         if t.role not in ("input", "weights"):
@@ -423,6 +426,8 @@ def execute_numeric(s: FusedSchedule, inputs: dict) -> np.ndarray:
     from . import _lib
 
     b = device_binding(s)
+    if layer_wise:
+        b.desc.scheme = _lib.SCHEME_LAYER_WISE
     out = _lib.execute_numeric_host(b.desc, b.device_input(arrays["x"]), b.device_weights(arrays))
     return np.ascontiguousarray(b.real_output(out.reshape(b.out_dims)))
 

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from paper_2404_03617_b200 import _lib
-from paper_2404_03617_b200.core import ConvFirst, MBConv, Stem, Head, TensorDims
+from paper_2404_03617_b200.core import ConvFirst, ExecutionScheme, Head, MBConv, Stem, TensorDims
 from paper_2404_03617_b200.machine import ScheduleError, block_descriptor, build_schedule, random_inputs, weight_names
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "wlfuse.h")
@@ -136,3 +136,43 @@ def test_convnext_units_descriptors_without_gpu(block, dims, out):
         assert L.wl_weight_numel(ctypes.byref(d), i) == int(np.prod(s.tensor(name).dims))
     packed = _lib.pack_weights(d, [np.ones(s.tensor(nm).dims, np.float32) for nm in weight_names(s)])
     assert packed.nbytes == L.wl_packed_bytes(ctypes.byref(d))
+
+
+@pytest.mark.parametrize(
+    "block,dims,launches",
+    [
+        (ConvFirst(8, 6), TensorDims(2, 28, 28, 48), 3),
+        (MBConv(8, 4, 0.25), TensorDims(4, 14, 14, 128), 5),
+        (MBConv(1, 4, 0.25), TensorDims(2, 28, 28, 80), 5),
+    ],
+)
+def test_layer_wise_descriptors_without_gpu(block, dims, launches):
+    """WL_SCHEME_LAYER_WISE binds the reference's layer-by-layer schedule
+    (one launch per layer, intermediates through the workspace in HBM)."""
+    L = _lib.lib()
+    s = build_schedule(block, dims, ExecutionScheme.LAYER_WISE)
+    d = block_descriptor(block, dims, s.out_channels)
+    d.scheme = _lib.SCHEME_LAYER_WISE
+    assert L.wl_validate(ctypes.byref(d)) == 0
+    assert L.wl_kernel_launches(ctypes.byref(d)) == launches
+    m = dims.n * dims.h * dims.w
+    hid = block.expansion * dims.c
+    assert L.wl_workspace_bytes(ctypes.byref(d)) >= m * hid * 2  # the hidden tensor lives in HBM
+    ins = random_inputs(s, np.random.default_rng(1))
+    w = [ins[n] for n in weight_names(s)]
+    a = _lib.pack_weights(d, w)
+    assert a.nbytes == L.wl_packed_bytes(ctypes.byref(d)) and np.array_equal(a, _lib.pack_weights(d, w))
+
+
+def test_layer_wise_refuses_what_the_reference_does_not_schedule():
+    L = _lib.lib()
+    for blk, dims, k in ((ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 32), 48),
+                         (MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 48), 128),
+                         (Stem(16), TensorDims(2, 32, 32, 3), 16)):
+        s = build_schedule(blk, dims, out_channels=k)
+        d = block_descriptor(blk, dims, s.out_channels)
+        d.scheme = _lib.SCHEME_LAYER_WISE
+        assert L.wl_validate(ctypes.byref(d)) != 0
+    d = _desc(ConvFirst(8, 6), TensorDims(2, 28, 28, 48))
+    d.scheme = 7
+    assert L.wl_validate(ctypes.byref(d)) == _lib.lib().wl_validate(ctypes.byref(d)) != 0

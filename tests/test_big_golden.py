@@ -41,16 +41,18 @@ def test_oracle_matches_reference_at_config_size(name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("scheme", [ExecutionScheme.BLOCK_FUSION, ExecutionScheme.LAYER_WISE], ids=["fused", "lw"])
 @pytest.mark.parametrize("name", big_golden_names())
-def test_gpu_full_batch_matches_reference(name):
+def test_gpu_full_batch_matches_reference(name, scheme):
     """The fused kernel runs the WHOLE batch (its full-size launch plan);
-    the picked images must match the reference within the fp16 budget
+    so does the device layer-wise schedule (layerwise.cu); the picked
+    images must match the reference within the fp16 budget
     (max-rel 1e-2, L2-rel 2e-3)."""
     from paper_2404_03617_b200.machine import execute_numeric
 
     meta, ref = load_big_golden(name)
     block, ins = regenerate(meta)
-    s = build_schedule(block, TensorDims(*meta["dims"]))
+    s = build_schedule(block, TensorDims(*meta["dims"]), scheme)
     got = execute_numeric(s, ins)[meta["picks"]].astype(np.float64)
     m = np.abs(got - ref).max() / np.abs(ref).max()
     l2 = np.linalg.norm(got - ref) / np.linalg.norm(ref)
