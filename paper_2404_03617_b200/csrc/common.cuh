@@ -65,6 +65,16 @@ __device__ __forceinline__ uint4 bias_act8(const uint32_t* acc, const float* bia
   return q;
 }
 
+// 16-byte read-only global load the compiler may neither sink to its use nor
+// re-issue there (a prefetch meant to hide L2 latency behind other work)
+__device__ __forceinline__ uint4 ldg_pinned(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // 16 consecutive fp32 values (16-byte aligned) as four vector loads
 __device__ __forceinline__ void load16f(const float* p, float* out) {
 #pragma unroll

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(256) gconv_kernel(const __half* __restrict__ x
 // (8-channel group, pixel lane of 8), fixed-order partial sums; squeeze: warp
 // per output, lanes over the hidden channels (W_sq stored [sq][hid]).
 constexpr int kSeThreads = 256;
+constexpr int kSeSmemMax = 200 * 1024;
 __global__ void __launch_bounds__(kSeThreads) se_kernel(const __half* __restrict__ h2, const __half* __restrict__ wsqt,
                                                         const float* __restrict__ bsq, const __half* __restrict__ wex,
                                                         const float* __restrict__ bex, float* __restrict__ gates,
@@ -220,8 +221,8 @@ int lw_validate(const wl_block_desc& d) {
     return set_error(WL_EUNSUPPORTED, "the layer-wise schedule is the reference's (no LayerNorm)");
   if (d.kind == WL_KIND_MBCONV && (d.se_sq < 1 || (d.expansion * d.c) % 8))
     return set_error(WL_EUNSUPPORTED, "MBConv layer-wise: hidden % 8 == 0, se_sq >= 1");
-  if (d.kind == WL_KIND_MBCONV && (9 * d.expansion * d.c + d.se_sq) * 4 > 48 * 1024)
-    return set_error(WL_EUNSUPPORTED, "MBConv layer-wise: SE partial sums exceed 48 KB of shared memory");
+  if (d.kind == WL_KIND_MBCONV && (9 * d.expansion * d.c + d.se_sq) * 4 > kSeSmemMax)
+    return set_error(WL_EUNSUPPORTED, "MBConv layer-wise: SE partial sums exceed shared memory");
   return WL_OK;
 }
 int lw_wc(const wl_block_desc& d) {
@@ -359,7 +360,11 @@ int lw_fwd(const wl_block_desc& d, const void* xv, const void* p, void* zv, void
   }
   return gemm_run(hb, (int)M, hid, hid, pk + L.o_vt, C, hid, z, C, e2, st);
 }
-int lw_init() { return gemm_init(); }
+int lw_init() {
+  if (int e = gemm_init()) return e;
+  return check_cuda(cudaFuncSetAttribute(se_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSeSmemMax),
+                    "cudaFuncSetAttribute(se)");
+}
 }  // namespace
 
 int lw_launches(const wl_block_desc& d) {

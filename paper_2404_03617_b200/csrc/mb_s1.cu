@@ -50,6 +50,7 @@ constexpr int kMb1MaxStage = 20;
 struct Mb1Args {
   int n, H, W, C, hid, sq, nch, NT;
   int s_x, s_h1, s_h1_bytes, s_w, s_wex, s_hdr, s_se, s_bar, smem;
+  int s_h2;  // P = 8: the block's whole h2 (compact 64-row chunks) stays in shared memory
   int o_bexp, o_bconv, o_bprj, hdr_bytes;  // header (fp32) in the packed blob
   int64_t o_se, o_frag, o_wexp, o_wprj;    // packed-blob sections
   int o_bsq, o_wex, o_bex;                 // inside the SE section (fp16 matrices, fp32 biases)
@@ -75,6 +76,8 @@ struct Bars {
   uint64_t a_done;
   uint64_t pa_full[4], pa_ready[4], pa_empty[4];
   uint64_t z_full, se_full;
+  uint64_t sq_full;      // the E warps' squeeze outputs are in shared memory
+  uint64_t pool_full[2];  // a chunk's pooled sums are in shared memory
   uint64_t d_done;  // stage: block b's output tile is in place (x of block b + 1), hdr / W_ex free
   uint32_t tmem_base;
 };
@@ -131,17 +134,37 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
     if (a.trace && blockIdx.x == 0) a.trace[(slot)] = clock64();         \
   } while (0)
 
-// H: image rows (flat rows 16 H <= 128 NT); C: block channels (64 or 128)
+// flat-layout row pitch: 16 (W <= 15) or, for the 7x7 stage, 8 — row y's
+// right pad is row y + 1's left pad, so one m16 fragment covers two image rows
+// and the conv needs 4 fragments instead of 7
+__host__ __device__ constexpr int mb1_pitch(int h) { return h <= 7 ? 8 : 16; }
+// bytes of one h1 group plane: the flat image (16-row fragments), one zero image
+// row above, the rows the last fragment's dy = +1 / dx = +1 loads reach, margins
+__host__ __device__ constexpr int mb1_plane_bytes(int h) {
+  return (16 * ((mb1_pitch(h) * h + 15) / 16) + 3 * mb1_pitch(h) + 2) * 16;
+}
+
+// H: image rows (flat rows P H <= 128 NT); C: block channels (64 or 128)
 template <int H, int C, int ACT>
 __global__ void __launch_bounds__(mb1::kThreads, 1)
     mb_s1_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_z,
                  const __grid_constant__ Mb1Args a) {
   using namespace mb1;
-  constexpr int NT = (16 * H + 127) / 128;  // M tiles of the flat image
+  constexpr int P = mb1_pitch(H);            // flat row pitch
+  constexpr int NT = (P * H + 127) / 128;    // M tiles of the flat image
   constexpr int KH = C / 64;                 // 64-channel (128-byte) halves of x
   constexpr int XH = NT * 128 * 128;         // bytes of one x half
-  constexpr int GS = ((H + 3) * 16 + 2) * 16;  // bytes of one h1 group plane (halo rows, margins, P overrun)
-  static_assert(16 * H <= 256 && (C == 64 || C == 128), "geometry");
+  constexpr int GS = mb1_plane_bytes(H);     // bytes of one h1 group plane
+  static_assert(P * H <= 256 && (C == 64 || C == 128), "geometry");
+  // P = 8: the 16-row fragments of the flat image sit at A rows 32 k .. 32 k + 15
+  // (one per TMEM lane quadrant), so the expand and projection accumulators
+  // spread over all four quadrants and every epilogue warp has rows to drain
+  // (a flat 56-row image would leave quadrants 2 and 3 — and their warps — idle)
+  auto flat_of = [](int arow) -> int {
+    if constexpr (P == 8) return (arow & 31) < 16 ? (arow >> 5) * 16 + (arow & 15) : (1 << 20);
+    return arow;
+  };
+  static_assert(P == 16 || P * H <= 64, "P = 8 holds at most four 16-row fragments");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* s_x = smem + a.s_x;
   uint8_t* s_h1 = smem + a.s_h1;   // 2 buffers x 8 group planes; phase C ring overlays s_h1 .. s_w end
@@ -175,6 +198,9 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     mbar_init(&B.a_done, 1);
     mbar_init(&B.z_full, 1);
     mbar_init(&B.se_full, 1);
+    mbar_init(&B.sq_full, 32);
+    mbar_init(&B.pool_full[0], 256);
+    mbar_init(&B.pool_full[1], 256);
     mbar_init(&B.d_done, 256);
     fence_mbar_init();
   }
@@ -203,8 +229,14 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
         bulk_g2s(s_hdr, wp, a.hdr_bytes, &B.hdr_full);
         if (blk == 0) {
-          mbar_arrive_expect_tx(&B.x_full, KH * 64 * 2 * 16 * H);
-          for (int kh = 0; kh < KH; ++kh) tma_load_4d(s_x + kh * XH, &tmap_x, kh * 64, -1, 0, img, &B.x_full);
+          mbar_arrive_expect_tx(&B.x_full, P == 8 ? KH * ((H + 1) / 2) * 2048 : KH * 64 * 2 * P * H);
+          if constexpr (P == 8) {
+            for (int kh = 0; kh < KH; ++kh)
+              for (int k = 0; k < (H + 1) / 2; ++k)
+                tma_load_4d(s_x + kh * XH + k * 2048, &tmap_x, kh * 64, -1, 2 * k, img, &B.x_full);
+          } else {
+            for (int kh = 0; kh < KH; ++kh) tma_load_4d(s_x + kh * XH, &tmap_x, kh * 64, -1, 0, img, &B.x_full);
+          }
         } else {
           mbar_arrive(&B.x_full);  // the previous block's z, in place (its writers fenced before d_done)
         }
@@ -220,6 +252,25 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         // the h1 / W_exp buffers the ring overlays
         // ring of 4 half-chunks (32 hidden channels: NT x 8 KB of h2 + the
         // matching 4 K-columns of W_prj), so several reloads are in flight
+        if constexpr (P == 8) {
+          // h2 stays in shared memory: the ring streams W_prj chunks only (K = 64).
+          // Chunks 0 / 1 go to the W_exp buffers (free once the last two expands
+          // completed, before the conv ends), chunks 2 / 3 to the h1 buffers
+          for (int j = 0; j < nch; ++j) {
+            const int gq = blk * nch + j;
+            const int s = gq & 3, u = gq >> 2;
+            mbar_wait(&B.pa_empty[s], (u & 1) ^ 1);
+            if (j < 2) {
+              const int gl = blk * nch + nch - 2 + j;  // last expand that used W buffer j
+              mbar_wait(&B.w_empty[gl & 1], (gl >> 1) & 1);
+            } else if (j < 4) {
+              mbar_wait(&B.a_done, blk & 1);
+            }
+            mbar_arrive_expect_tx(&B.pa_full[s], 2 * vbytes);
+            bulk_g2s(s_w + s * a.slot_bytes, wp + a.o_wprj + (size_t)j * 2 * vbytes, 2 * vbytes,
+                     &B.pa_full[s]);
+          }
+        } else {
         mbar_wait(&B.a_done, blk & 1);
         for (int qq = 0; qq < 2 * nch; ++qq) {
           const int gq = blk * 2 * nch + qq;
@@ -232,12 +283,15 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           bulk_g2s(slot + NT * 8192, wp + a.o_wprj + (size_t)j * 2 * vbytes + half * vbytes, vbytes,
                    &B.pa_full[s]);
         }
+        }
       }
     }
   } else if (warp == kMma) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      const uint32_t idesc_e = make_idesc_f16(128, kHC);
+      // P = 8: M = 64 over the compact 64-row x tile; the accumulator rows land
+      // 16 per TMEM lane quadrant (rows 16k.. at lanes 32k..)
+      const uint32_t idesc_e = make_idesc_f16(P == 8 ? 64 : 128, kHC);
       const uint32_t idesc_z = make_idesc_f16(128, C);
       const uint32_t wbytes = kHC * C * 2;
       for (int blk = 0; blk < nblk; ++blk) {
@@ -265,6 +319,26 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         // Z of the previous block must have been drained (phase D) before the
         // first projection of this one overwrites it: d_done(blk - 1) precedes
         // x_full(blk), waited above
+        if constexpr (P == 8) {
+          const uint32_t idesc_z64 = make_idesc_f16(64, C);
+          for (int j = 0; j < nch; ++j) {
+            const int gq = blk * nch + j;
+            const int s = gq & 3, u = gq >> 2;
+            mbar_wait(&B.pa_full[s], u & 1);   // W_prj chunk landed
+            mbar_wait(&B.pa_ready[s], u & 1);  // h2 chunk gated
+            tc_fence_after();
+            MB1_TRACE(52 + j);
+            const uint32_t vb = smem_u32(s_w + s * a.slot_bytes);
+            const uint32_t hb = smem_u32(smem + a.s_h2) + j * 8192;
+#pragma unroll
+            for (int k = 0; k < kHC / 16; ++k) {
+              const uint64_t ad = make_sdesc(hb + k * 2 * 1024, 1024, 128);
+              const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
+              mma_ss(tmem + a.t_z, ad, bd, idesc_z64, (j > 0 || k > 0));
+            }
+            mma_commit(&B.pa_empty[s]);
+          }
+        } else {
         for (int qq = 0; qq < 2 * nch; ++qq) {
           const int gq = blk * 2 * nch + qq;
           const int s = gq & 3, u = gq >> 2;
@@ -283,6 +357,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
             }
           mma_commit(&B.pa_empty[s]);
         }
+        }
         mma_commit(&B.z_full);
       }
     }
@@ -292,6 +367,34 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     const float* s_bexp = reinterpret_cast<const float*>(s_hdr + a.o_bexp);
     const float* s_bprj = reinterpret_cast<const float*>(s_hdr + a.o_bprj);
     for (int blk = 0; blk < nblk; ++blk) {
+      // squeeze partials, chunk by chunk as the conv warps pool them (the E
+      // warps idle while the conv runs): thread (warp e, lane o) accumulates
+      // W_sq[c][o] pool[c] over its 8 channels c of every chunk, fixed order;
+      // its W_sq^T row segment is loaded one chunk ahead
+      const __half* wsqt = reinterpret_cast<const __half*>(wp_of(blk) + a.o_se);
+      const float* pool = reinterpret_cast<const float*>(s_se);
+      float sq_acc = 0.f;
+      // W_sq^T segments of chunks jj (in wq) and jj + 1 (wq_next): each load is
+      // issued a whole chunk before its use
+      uint4 wq = ldg_pinned(wsqt + (size_t)lane * a.hid + e * 8);
+      uint4 wq_next = nch > 1 ? ldg_pinned(wsqt + (size_t)lane * a.hid + kHC + e * 8) : wq;
+      auto squeeze_part = [&](int jj) {
+        const int gg = blk * nch + jj;
+        mbar_wait(&B.pool_full[gg & 1], (gg >> 1) & 1);
+        const float4 pa = *reinterpret_cast<const float4*>(pool + jj * kHC + e * 8);
+        const float4 pb = *reinterpret_cast<const float4*>(pool + jj * kHC + e * 8 + 4);
+        const __half* w8 = reinterpret_cast<const __half*>(&wq);
+        sq_acc = fmaf(pa.x, __half2float(w8[0]), sq_acc);
+        sq_acc = fmaf(pa.y, __half2float(w8[1]), sq_acc);
+        sq_acc = fmaf(pa.z, __half2float(w8[2]), sq_acc);
+        sq_acc = fmaf(pa.w, __half2float(w8[3]), sq_acc);
+        sq_acc = fmaf(pb.x, __half2float(w8[4]), sq_acc);
+        sq_acc = fmaf(pb.y, __half2float(w8[5]), sq_acc);
+        sq_acc = fmaf(pb.z, __half2float(w8[6]), sq_acc);
+        sq_acc = fmaf(pb.w, __half2float(w8[7]), sq_acc);
+        wq = wq_next;
+        if (jj + 2 < nch) wq_next = ldg_pinned(wsqt + (size_t)lane * a.hid + (jj + 2) * kHC + e * 8);
+      };
       mbar_wait(&B.hdr_full, blk & 1);
       for (int j = 0; j < nch; ++j) {
         const int g2 = blk * nch + j, b = g2 & 1, u = g2 >> 1;
@@ -299,6 +402,31 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         mbar_wait(&B.h1_empty[b], (u & 1) ^ 1);
         tc_fence_after();
         uint8_t* h1 = s_h1 + b * 8 * GS;
+        if constexpr (P == 8) {
+          // the quadrant's 16 real A rows spread over all 32 threads (16x256b):
+          // every lane converts 16 values instead of half the lanes converting 32
+          uint32_t v[16];
+          WL_TMEM_LD_16x256b_X4(tmem_lane_addr(tmem, q, a.t_e + b * NT * kHC + hh * 32), v);
+          tmem_ld_wait();
+          const int r0 = lane >> 2, c2 = (lane & 3) * 2;
+          const int f0 = 16 * q + r0, f1 = f0 + 8;  // flat rows
+          const bool ok0 = f0 < P * H && (f0 & 7) >= 1 && (f0 & 7) <= a.W;
+          const bool ok1 = f1 < P * H && (f1 & 7) >= 1 && (f1 & 7) <= a.W;
+          const float* bb = s_bexp + j * kHC + hh * 32 + c2;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 bv = *reinterpret_cast<const float2*>(bb + 8 * k);
+            __half2 h0 = act_h2<ACT>(__floats2half2_rn(__uint_as_float(v[4 * k]) + bv.x,
+                                                       __uint_as_float(v[4 * k + 1]) + bv.y));
+            __half2 h1v = act_h2<ACT>(__floats2half2_rn(__uint_as_float(v[4 * k + 2]) + bv.x,
+                                                        __uint_as_float(v[4 * k + 3]) + bv.y));
+            if (!ok0) h0 = __float2half2_rn(0.f);
+            if (!ok1) h1v = __float2half2_rn(0.f);
+            uint8_t* pl = h1 + (hh * 4 + k) * GS + c2 * 2;
+            if (f0 < P * H) *reinterpret_cast<__half2*>(pl + (f0 + P + 1) * 16) = h0;
+            if (f1 < P * H) *reinterpret_cast<__half2*>(pl + (f1 + P + 1) * 16) = h1v;
+          }
+        } else {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           uint32_t v[32];
@@ -306,22 +434,41 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           WL_TMEM_LD16(ta, v);
           WL_TMEM_LD16(ta + 16, (v + 16));
           tmem_ld_wait();
-          const int m = t * 128 + q * 32 + lane;
-          const int i = m & 15;
-          if (m < 16 * H) {
+          const int m = flat_of(t * 128 + q * 32 + lane);
+          const int i = m & (P - 1);
+          if (m < P * H) {
             const bool real = i >= 1 && i <= a.W;
             const float* bb = s_bexp + j * kHC + hh * 32;
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const uint4 val = real ? bias_act8<ACT>(v + 8 * g, bb + 8 * g) : make_uint4(0, 0, 0, 0);
-              *reinterpret_cast<uint4*>(h1 + (hh * 4 + g) * GS + (m + 17) * 16) = val;
+              *reinterpret_cast<uint4*>(h1 + (hh * 4 + g) * GS + (m + P + 1) * 16) = val;
             }
           }
+        }
         }
         tc_fence_before();
         mbar_arrive(&B.e_empty[b]);
         mbar_arrive(&B.h1_full[b]);
         if (e == 0 && lane == 0) MB1_TRACE(4 + j);
+        // chunk j - 2's pool was written after conv(j - 2) released h1[b], so
+        // it is (nearly) complete here, and h1(j) is already out
+        if (j >= 2) squeeze_part(j - 2);
+      }
+      // ---------------------------------------------- phase B (squeeze)
+      for (int jj = nch >= 2 ? nch - 2 : 0; jj < nch; ++jj) squeeze_part(jj);
+      {
+        float* scr = reinterpret_cast<float*>(s_se + a.hid * 4 + a.hid * 2);
+        const float bsq_o = lane < a.sq ? reinterpret_cast<const float*>(wp_of(blk) + a.o_se + a.o_bsq)[lane] : 0.f;
+        scr[e * 32 + lane] = sq_acc;
+        nbar(3, 256);
+        if (e == 0) {
+          float sv = 0.f;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) sv += scr[r * 32 + lane];
+          scr[256 + lane] = lane < a.sq ? fmaxf(sv * (1.f / (float)(a.H * a.W)) + bsq_o, 0.f) : 0.f;
+          mbar_arrive(&B.sq_full);
+        }
       }
       // ---------------------------------------------- phase D: z epilogue
       mbar_wait(&B.z_full, blk & 1);
@@ -330,8 +477,9 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       if (hh < KH) {
 #pragma unroll 1
         for (int t = 0; t < NT; ++t) {
-          const int m = t * 128 + q * 32 + lane;
-          uint8_t* xrow = s_x + hh * XH + m * 128;
+          const int m = t * 128 + q * 32 + lane;  // A row (TMEM lane)
+          const int xr = P == 8 ? flat_of(m) & 63 : m;  // x / z tile row (P = 8: compact)
+          uint8_t* xrow = s_x + hh * XH + xr * 128;
           uint32_t v[64];  // the row's 64 channels in one batch of TMEM loads
           const uint32_t za = tmem_lane_addr(tmem, q, a.t_z + t * C + hh * 64);
           WL_TMEM_LD16(za, v);
@@ -339,10 +487,10 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           WL_TMEM_LD16(za + 32, (v + 32));
           WL_TMEM_LD16(za + 48, (v + 48));
           tmem_ld_wait();
-          if (m < 16 * H) {
+          if (flat_of(m) < P * H) {
 #pragma unroll
             for (int c8 = 0; c8 < 8; ++c8) {
-              uint8_t* p = xrow + ((c8 ^ (m & 7)) << 4);
+              uint8_t* p = xrow + ((c8 ^ (xr & 7)) << 4);
               float res[8];
               unpack8(lds128(p), res);
               const float4 b0 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8);
@@ -371,7 +519,13 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           // a TMA store may not start at a negative coordinate (illegal instruction,
           // tools/probe_tma_store.cu): start at x = 0 one 128-byte row into the tile
           // (the 128B swizzle is address-based, so the shifted source stays valid)
-          for (int kh = 0; kh < KH; ++kh) tma_store_4d(&tmap_z, s_x + kh * XH + 128, kh * 64, 0, 0, img);
+          if constexpr (P == 8) {
+            for (int kh = 0; kh < KH; ++kh)
+              for (int k = 0; k < (H + 1) / 2; ++k)
+                tma_store_4d(&tmap_z, s_x + kh * XH + k * 2048 + 128, kh * 64, 0, 2 * k, img);
+          } else {
+            for (int kh = 0; kh < KH; ++kh) tma_store_4d(&tmap_z, s_x + kh * XH + 128, kh * 64, 0, 0, img);
+          }
           bulk_commit_s1();
           bulk_wait_read0_s1();  // the tile must outlive the reads only; the writes complete on their own
           MB1_TRACE(69);
@@ -388,51 +542,70 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     const uint32_t lrow = (lane & 15), lsel = lane >> 4;  // ldmatrix: row of the fragment, which fragment
     uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
     const __half2 one2 = __float2half2_rn(1.f), zero2 = __float2half2_rn(0.f);
-    const __half2 m0 = (gid >= 1 && gid <= a.W) ? one2 : zero2, m1 = (gid + 8 <= a.W) ? one2 : zero2;
+    // real pixels among the fragment rows gid / gid + 8 (the pads are zero)
+    const __half2 m0 = (gid >= 1 && gid <= a.W) ? one2 : zero2,
+                  m1 = P == 16 ? ((gid + 8 <= a.W) ? one2 : zero2) : m0;
     for (int blk = 0; blk < nblk; ++blk) {
     const uint8_t* wp = wp_of(blk);
     const uint32_t* frag = reinterpret_cast<const uint32_t*>(wp + a.o_frag);
-    const __half* wsq = reinterpret_cast<const __half*>(wp + a.o_se);
     // B fragments in pair order (t0,t1) (t3,t4) (t6,t7) (t2,t5) t8: each k16
     // pair is two consecutive registers (mb1_pack)
     uint32_t bw[9];
 #pragma unroll
     for (int tp = 0; tp < 9; ++tp) bw[tp] = __ldg(frag + ((size_t)(0 * 8 + g) * 9 + tp) * 32 + lane);
     mbar_wait(&B.hdr_full, blk & 1);
-    float s_acc = 0.f;  // squeeze partial of output lane (sq <= 32), summed over this warp's groups
+    // excite biases of this thread's first gate pair, needed after phase A
+    const float2 bex_pre = tid < hid / 2 ? __ldg(reinterpret_cast<const float2*>(wp + a.o_se + a.o_bex) + tid)
+                                         : make_float2(0.f, 0.f);
     for (int j = 0; j < nch; ++j) {
       const int g2 = blk * nch + j, b = g2 & 1, u = g2 >> 1;
+      if (tid == 0) MB1_TRACE(72 + j);
       const float2 bc = *reinterpret_cast<const float2*>(s_bconv + j * kHC + g * 8 + tq * 2);
-      // W_sq rows of this warp's 8 channels, output = lane (consumed after the pool below)
-      // (W_sq stored transposed: the lane's 8 channels are one 16-byte load)
-      const uint4 wq4 = __ldg(reinterpret_cast<const uint4*>(wsq + (size_t)lane * hid + j * kHC + g * 8));
-      const __half* wq = reinterpret_cast<const __half*>(&wq4);
+      // next chunk's B fragments: a whole chunk of conv work hides their L2 latency
+      uint32_t bwn[9];
+      if (j + 1 < nch) {
+#pragma unroll
+        for (int tp = 0; tp < 9; ++tp) bwn[tp] = __ldg(frag + ((size_t)((j + 1) * 8 + g) * 9 + tp) * 32 + lane);
+      }
+      if (tid == 0) MB1_TRACE(80 + j);
       mbar_wait(&B.h1_full[b], u & 1);
+      if (tid == 0) MB1_TRACE(12 + j);
       const uint32_t plane = smem_u32(s_h1 + b * 8 * GS + g * GS) + 16;  // + 1 margin row
-      // Q_r: x4 of padded row r at dx = -1 (lanes 0-15) and dx = 0 (lanes 16-31)
-      // P_r: x4 of dx = +1 at rows r (lanes 0-15) and r + 1 (lanes 16-31)
-      // so every HMMA A operand is one load's four consecutive registers
+      // row unit r = P flat rows (one padded image row). Q_r: x4 at unit r,
+      // dx = -1 (lanes 0-15) and dx = 0 (lanes 16-31); P_r: x4 of dx = +1 at
+      // units r (lanes 0-15) and r + 1 (lanes 16-31) — so every HMMA A operand
+      // is one load's four consecutive registers
       auto load_q = [&](int r, uint32_t* f) {
-        ldsm_x4(plane + (uint32_t)((r * 16 + (int)lsel - 1 + (int)lrow) * 16), f[0], f[1], f[2], f[3]);
+        ldsm_x4(plane + (uint32_t)((r * P + (int)lsel - 1 + (int)lrow) * 16), f[0], f[1], f[2], f[3]);
       };
       auto load_p = [&](int r, uint32_t* f) {
-        ldsm_x4(plane + (uint32_t)((r * 16 + 16 * (int)lsel + 1 + (int)lrow) * 16), f[0], f[1], f[2], f[3]);
+        ldsm_x4(plane + (uint32_t)((r * P + P * (int)lsel + 1 + (int)lrow) * 16), f[0], f[1], f[2], f[3]);
       };
-      uint32_t Q0[4], Q1[4], Q2[4], Q3[4], P0[4], P1[4], P2[4], P3[4];
       __half2 pool = zero2;
       // h2 rows go straight to the L2-resident workspace in the projection's
       // A layout [tile][group][row][16 B]: per warp store, 8 rows x 4 lanes x
       // 4 B = two whole 128-byte lines
-      uint8_t* h2c = h2img + (size_t)j * NT * 16384 + g * 2048 + tq * 4;
-      auto epi = [&](int y, const float* c0, const float* c1) {
+      // (P = 8: into the resident compact h2: [chunk][group][64 rows][16 B])
+      uint8_t* h2c = P == 8 ? smem + a.s_h2 + j * 8192 + g * 1024 + tq * 4
+                            : h2img + (size_t)j * NT * 16384 + g * 2048 + tq * 4;
+      // fragment f = flat rows 16 f .. 16 f + 15; v1: its rows gid + 8 are image pixels
+      auto epi = [&](int f, const float* c0, const float* c1, bool v1) {
         const __half2 h0 = __hmul2(act_h2<ACT>(__floats2half2_rn(c0[0] + c1[0], c0[1] + c1[1])), m0);
-        const __half2 h1v = __hmul2(act_h2<ACT>(__floats2half2_rn(c0[2] + c1[2], c0[3] + c1[3])), m1);
+        const __half2 h1v = __hmul2(act_h2<ACT>(__floats2half2_rn(c0[2] + c1[2], c0[3] + c1[3])), v1 ? m1 : zero2);
         pool = __hadd2(pool, __hadd2(h0, h1v));
-        const int mm = y * 16 + gid;
-        *reinterpret_cast<__half2*>(h2c + (mm >> 7) * 16384 + ((mm & 127) >> 3) * 128 + (mm & 7) * 16) = h0;
-        const int m8 = mm + 8;
-        *reinterpret_cast<__half2*>(h2c + (m8 >> 7) * 16384 + ((m8 & 127) >> 3) * 128 + (m8 & 7) * 16) = h1v;
+        if constexpr (P == 8) {
+          const int fr = f * 16 + gid;  // flat row = compact A row
+          *reinterpret_cast<__half2*>(h2c + fr * 16) = h0;
+          *reinterpret_cast<__half2*>(h2c + (fr + 8) * 16) = h1v;
+        } else {
+          const int mm = f * 16 + gid;
+          *reinterpret_cast<__half2*>(h2c + (mm >> 7) * 16384 + ((mm & 127) >> 3) * 128 + (mm & 7) * 16) = h0;
+          const int m8 = mm + 8;
+          *reinterpret_cast<__half2*>(h2c + (m8 >> 7) * 16384 + ((m8 & 127) >> 3) * 128 + (m8 & 7) * 16) = h1v;
+        }
       };
+      if constexpr (P == 16) {
+      uint32_t Q0[4], Q1[4], Q2[4], Q3[4], P0[4], P1[4], P2[4], P3[4];
       // output row y: Q_y.(t0,t1) + Q_{y+1}.(t3,t4) + Q_{y+2}.(t6,t7) + P_y.(t2,t5) + P_{y+2}[0:2].t8
       load_q(0, Q0);
       load_q(1, Q1);
@@ -456,8 +629,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         hmma16(b1, Q3[0], Q3[1], Q3[2], Q3[3], bw[4], bw[5]);
         hmma8(a0, P2[0], P2[1], bw[8]);
         hmma8(b0, P3[0], P3[1], bw[8]);
-        epi(y, a0, a1);
-        epi(y + 1, b0, b1);
+        epi(y, a0, a1, true);
+        epi(y + 1, b0, b1, true);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           Q0[k] = Q2[k];
@@ -478,16 +651,71 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         hmma8(a1, P2[0], P2[1], bw[8]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) a1[k] += a2[k];
-        epi(y, a0, a1);
+        epi(y, a0, a1, true);
       }
-      mbar_arrive(&B.h1_empty[b]);  // every ldmatrix of this buffer has completed (results consumed)
-      if (j + 1 < nch) {  // next chunk's B fragments: in flight under the pool / squeeze work below
+      } else {
+      // P = 8: fragment f covers image rows 2f, 2f + 1 and reads units
+      // s = 2f (dy = -1), 2f + 1 (dy = 0), 2f + 2 (dy = +1):
+      //   Q_s.(t0,t1) + Q_{s+1}.(t3,t4) + Q_{s+2}.(t6,t7) + P_s.(t2,t5) + P_{s+2}[0:2].t8
+      constexpr int NF = (P * H + 15) / 16;
+      uint32_t Q0[4], Q1[4], Q2[4], Q3[4], Q4[4], P0[4], P1[4], P2[4];
+      load_q(0, Q0);
+      load_p(0, P0);
 #pragma unroll
-        for (int tp = 0; tp < 9; ++tp) bw[tp] = __ldg(frag + ((size_t)((j + 1) * 8 + g) * 9 + tp) * 32 + lane);
+      for (int f = 0; f + 1 < NF; f += 2) {
+        const int s0 = 2 * f;
+        load_q(s0 + 1, Q1);
+        load_q(s0 + 2, Q2);
+        load_p(s0 + 2, P1);
+        load_q(s0 + 3, Q3);
+        load_q(s0 + 4, Q4);
+        load_p(s0 + 4, P2);
+        float a0[4] = {bc.x, bc.y, bc.x, bc.y}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+        float b0[4] = {bc.x, bc.y, bc.x, bc.y}, b1[4] = {0.f, 0.f, 0.f, 0.f};
+        hmma16(a0, Q0[0], Q0[1], Q0[2], Q0[3], bw[0], bw[1]);
+        hmma16(b0, Q2[0], Q2[1], Q2[2], Q2[3], bw[0], bw[1]);
+        hmma16(a1, P0[0], P0[1], P0[2], P0[3], bw[6], bw[7]);
+        hmma16(b1, P1[0], P1[1], P1[2], P1[3], bw[6], bw[7]);
+        hmma16(a0, Q1[0], Q1[1], Q1[2], Q1[3], bw[2], bw[3]);
+        hmma16(b0, Q3[0], Q3[1], Q3[2], Q3[3], bw[2], bw[3]);
+        hmma16(a1, Q2[0], Q2[1], Q2[2], Q2[3], bw[4], bw[5]);
+        hmma16(b1, Q4[0], Q4[1], Q4[2], Q4[3], bw[4], bw[5]);
+        hmma8(a0, P1[0], P1[1], bw[8]);
+        hmma8(b0, P2[0], P2[1], bw[8]);
+        epi(f, a0, a1, 2 * f + 1 < H);
+        epi(f + 1, b0, b1, 2 * f + 3 < H);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          Q0[k] = Q4[k];
+          P0[k] = P2[k];
+        }
+      }
+      if constexpr (NF % 2) {
+        constexpr int f = NF - 1, s0 = 2 * f;
+        load_q(s0 + 1, Q1);
+        load_q(s0 + 2, Q2);
+        load_p(s0 + 2, P1);
+        float a0[4] = {bc.x, bc.y, bc.x, bc.y}, a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+        hmma16(a0, Q0[0], Q0[1], Q0[2], Q0[3], bw[0], bw[1]);
+        hmma16(a1, P0[0], P0[1], P0[2], P0[3], bw[6], bw[7]);
+        hmma16(a2, Q1[0], Q1[1], Q1[2], Q1[3], bw[2], bw[3]);
+        hmma16(a0, Q2[0], Q2[1], Q2[2], Q2[3], bw[4], bw[5]);
+        hmma8(a1, P1[0], P1[1], bw[8]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a1[k] += a2[k];
+        epi(f, a0, a1, 2 * f + 1 < H);
+      }
+      }
+      if (tid == 0) MB1_TRACE(28 + j);
+      mbar_arrive(&B.h1_empty[b]);  // every ldmatrix of this buffer has completed (results consumed)
+      if (j + 1 < nch) {
+#pragma unroll
+        for (int tp = 0; tp < 9; ++tp) bw[tp] = bwn[tp];
       }
       if (tid == 0) MB1_TRACE(20 + j);
       // SE pool of the chunk (fp16 per lane over <= 2H rows, fp32 across lanes):
-      // reduce the 8 rows (gid) sharing a channel pair
+      // reduce the 8 rows (gid) sharing a channel pair; the sums go to shared
+      // memory for the E warps' squeeze
       const float2 pf = __half22float2(pool);
       float p0 = pf.x, p1 = pf.y;
 #pragma unroll
@@ -495,39 +723,35 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         p0 += __shfl_xor_sync(0xffffffffu, p0, sh);
         p1 += __shfl_xor_sync(0xffffffffu, p1, sh);
       }
-      // partial squeeze of this warp's 8 channels: lane = squeeze output
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float q0 = __shfl_sync(0xffffffffu, p0, c), q1 = __shfl_sync(0xffffffffu, p1, c);
-        s_acc += q0 * __half2float(wq[2 * c]) + q1 * __half2float(wq[2 * c + 1]);
-      }
+      if (gid == 0)
+        *reinterpret_cast<float2*>(reinterpret_cast<float*>(s_se) + j * kHC + g * 8 + tq * 2) = make_float2(p0, p1);
+      mbar_arrive(&B.pool_full[b]);
+      if (tid == 0) MB1_TRACE(44 + j);
     }
     // the producer reloads h2 through the async proxy: order every thread's
     // generic-proxy stores before it
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if constexpr (P == 16) asm volatile("fence.proxy.async.global;" ::: "memory");
     float* scr = reinterpret_cast<float*>(s_se + hid * 4 + hid * 2);
-    scr[g * 32 + lane] = s_acc;
     nbar(1, 256);
-    if (tid == 0) mbar_arrive(&B.a_done);
+    if (tid == 0) mbar_arrive(&B.a_done);  // pool sums complete: the E warps squeeze
     MB1_TRACE(1);
-    // ------------------------------------------------ phase B: squeeze-excite
+    // ------------------------------------------------ phase B: excite
     __half2* s_gate = reinterpret_cast<__half2*>(s_se + hid * 4);
-    const float* bsq = reinterpret_cast<const float*>(wp + a.o_se + a.o_bsq);
     const __half2* wex = reinterpret_cast<const __half2*>(s_wex);  // prefetched by the producer
     const float* bex = reinterpret_cast<const float*>(wp + a.o_se + a.o_bex);
-    const float inv_p = 1.f / (float)(a.H * a.W);
-    if (tid < sq) {
-      float acc = 0.f;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) acc += scr[r * 32 + tid];
-      scr[256 + tid] = fmaxf(acc * inv_p + bsq[tid], 0.f);
-    }
     mbar_wait(&B.se_full, blk & 1);
-    nbar(1, 256);
+    mbar_wait(&B.sq_full, blk & 1);
     {
       const float* s_s = scr + 256;
       for (int hp = tid; hp < hid / 2; hp += 256) {
-        float e0 = bex[2 * hp], e1 = bex[2 * hp + 1];
+        float e0, e1;
+        if (hp == tid) {
+          e0 = bex_pre.x;
+          e1 = bex_pre.y;
+        } else {
+          e0 = bex[2 * hp];
+          e1 = bex[2 * hp + 1];
+        }
 #pragma unroll 8
         for (int jj = 0; jj < sq; ++jj) {
           const float2 w = __half22float2(wex[(size_t)jj * (hid / 2) + hp]);
@@ -540,6 +764,30 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     }
     MB1_TRACE(2);
     // ------------------------------------------------ phase C: gate h2 chunks
+    if constexpr (P == 8) {
+      // the resident h2 ([chunk][group][64 rows][16 B]) gated in place chunk by
+      // chunk, each released to the projection MMAs as soon as it is done
+      uint4* h2s = reinterpret_cast<uint4*>(smem + a.s_h2);
+      for (int jj = 0; jj < nch; ++jj) {
+        const int gq = blk * nch + jj;
+        // an arrival may not run a full phase ahead of the MMA's wait: chunk
+        // jj - 4 (same barrier) must have been consumed
+        mbar_wait(&B.pa_empty[gq & 3], ((gq >> 2) & 1) ^ 1);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int id = jj * 512 + k * 256 + tid, gg = (id >> 6) & 7;
+          uint4 hv = h2s[id];
+          const uint4 gv = *reinterpret_cast<const uint4*>(s_gate + jj * (kHC / 2) + gg * 4);
+          __half2* h = reinterpret_cast<__half2*>(&hv);
+          const __half2* gt = reinterpret_cast<const __half2*>(&gv);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h[i] = __hmul2(h[i], gt[i]);
+          h2s[id] = hv;
+        }
+        fence_async_smem();
+        mbar_arrive(&B.pa_ready[gq & 3]);
+      }
+    } else {
     for (int qq = 0; qq < 2 * nch; ++qq) {
       const int gq = blk * 2 * nch + qq;
       const int s = gq & 3, u = gq >> 2, j = qq >> 1, half = qq & 1;
@@ -561,6 +809,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       fence_async_smem();
       mbar_arrive(&B.pa_ready[s]);
     }
+    }
     MB1_TRACE(3);
     }  // blocks
   }
@@ -576,6 +825,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
 // =================================================================== host
 }  // namespace wl
 
+#include <algorithm>
 #include <cstdlib>
 #include "launch.h"
 
@@ -596,20 +846,38 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   a.hid = d.expansion * d.c;
   a.sq = d.se_sq;
   a.nch = a.hid / mb1::kHC;
-  a.NT = (16 * a.H + 127) / 128;
+  a.NT = (mb1_pitch(a.H) * a.H + 127) / 128;
   const int C = a.C, hid = a.hid, NT = a.NT;
-  const int GS = ((a.H + 3) * 16 + 2) * 16;
+  const int GS = mb1_plane_bytes(a.H);
   // shared memory: x (swizzled halves) | h1 x2 | W_exp ring x2 (the phase C ring overlays h1 + ring) | hdr | SE | bars
   int o = 0;
   a.s_x = o;
   o += (C / 64) * NT * 128 * 128;
-  a.s_h1 = o;
   a.s_h1_bytes = 2 * 8 * GS;
-  o = align_up(o + a.s_h1_bytes, 128);
-  a.s_w = o;
-  o += 2 * mb1::kHC * C * 2;
-  a.slot_bytes = NT * 8192 + C * 32 * 2;
-  if (4 * a.slot_bytes > o - a.s_h1) return false;
+  const bool p8 = mb1_pitch(a.H) == 8;
+  // phase C ring slot: P = 16: h2 half-chunk (NT x 8 KB) + W_prj half-chunk;
+  // P = 8 (h2 resident): one W_prj chunk (C x 64 x 2)
+  a.slot_bytes = p8 ? C * mb1::kHC * 2 : NT * 8192 + C * 32 * 2;
+  const int wring = 2 * mb1::kHC * C * 2;
+  if (p8) {
+    // W_exp ring | h1 (>= 2 slots): the phase C ring's slots 0 / 1 are the W_exp
+    // buffers (free once the last two expands complete, before the conv ends),
+    // slots 2 / 3 the h1 buffers (free after phase A); the block's h2 stays resident
+    if (wring != 2 * a.slot_bytes || a.nch % 4) return false;
+    a.s_w = o;
+    o += wring;
+    a.s_h1 = o;
+    o = align_up(o + std::max(a.s_h1_bytes, 2 * a.slot_bytes), 1024);
+    a.s_h2 = o;
+    o += a.nch * 8192;
+  } else {
+    // the phase C ring (4 slots) overlays h1 + the W_exp ring: pad h1 when it is smaller
+    a.s_h1 = o;
+    o = align_up(o + std::max(a.s_h1_bytes, 4 * a.slot_bytes - wring), 128);
+    a.s_w = o;
+    o += wring;
+    if (4 * a.slot_bytes > o - a.s_h1) return false;
+  }
   a.o_bexp = 0;
   a.o_bconv = hid * 4;
   a.o_bprj = 2 * hid * 4;
@@ -621,7 +889,7 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   a.s_wex = align_up(o, 128);
   o = a.s_wex + a.sq * hid * 2;
   a.s_bar = align_up(o, 128);
-  a.smem = a.s_bar + 256;
+  a.smem = a.s_bar + align_up((int)sizeof(mb1::Bars), 16);
   // packed blob
   int64_t p = a.hdr_bytes;
   a.o_se = p;
@@ -672,7 +940,8 @@ Mb1K mb1_kernel(const wl_block_desc& d) {
 
 bool mb1_eligible(const wl_block_desc& d) {
   if (env_legacy() || d.kind != WL_KIND_MBCONV || d.stride != 1 || d.group_width != 8 || d.k != d.c) return false;
-  if ((d.c != 64 && d.c != 128) || d.w > 14 || (d.act != kSilu && d.act != kRelu)) return false;
+  if ((d.c != 64 && d.c != 128) || d.w > 14 || d.w > mb1_pitch(d.h) - 1 || (d.act != kSilu && d.act != kRelu))
+    return false;
   const int hid = d.expansion * d.c;
   if (hid % mb1::kHC || d.se_sq < 1 || d.se_sq > 32 || hid / 2 > 256 * 4) return false;
   Mb1Args a;
@@ -743,7 +1012,8 @@ static int mb1_launch(const wl_block_desc& d, Mb1Args& a, const void* x, void* z
   CUtensorMap tx, tz;
   const uint64_t dims[4] = {(uint64_t)d.c, (uint64_t)d.w, (uint64_t)d.h, (uint64_t)d.n};
   const uint64_t strides[3] = {(uint64_t)d.c * 2, (uint64_t)d.w * d.c * 2, (uint64_t)d.h * d.w * d.c * 2};
-  const uint32_t box[4] = {64, 16, (uint32_t)d.h, 1};
+  // P = 8: one box per pair of image rows (a 16-row fragment, placed at A rows 32 k)
+  const uint32_t box[4] = {64, (uint32_t)mb1_pitch(d.h), mb1_pitch(d.h) == 8 ? 2u : (uint32_t)d.h, 1};
   if (int e = encode_tmap(&tx, x, 4, dims, strides, box, true)) return e;
   if (int e = encode_tmap(&tz, z, 4, dims, strides, box, true)) return e;
   return launch_pdl(mb1_kernel(d), d.n, mb1::kThreads, a.smem, st, "mb_s1 launch", tx, tz, a);

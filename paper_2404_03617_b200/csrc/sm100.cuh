@@ -195,6 +195,18 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),       \
         "=r"(r[15])                                                                                       \
       : "r"(taddr))
+// 16x256b shape, 4 repetitions (32 columns): only TMEM lanes 32q..32q+15 are
+// read, spread over the whole warp like an mma.sync C fragment — thread t
+// holds, for column block k (8 columns), r[4k], r[4k+1] = (lane t/4, columns
+// 8k + 2(t%4), +1) and r[4k+2], r[4k+3] = (lane t/4 + 8, same columns)
+#define WL_TMEM_LD_16x256b_X4(taddr, r)                                                                   \
+  asm volatile(                                                                                           \
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "  \
+      "[%16];"                                                                                            \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),       \
+        "=r"(r[15])                                                                                       \
+      : "r"(taddr))
 #define WL_TMEM_LD8(taddr, r)                                                                             \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                   \
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \

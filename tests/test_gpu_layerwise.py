@@ -37,7 +37,7 @@ CASES = [
     ("mb_14", MBConv(8, 4, 0.25), TensorDims(4, 14, 14, 128)),
     ("mb_7", MBConv(8, 4, 0.25), TensorDims(4, 7, 7, 256)),
     ("mb_dw", MBConv(1, 4, 0.25), TensorDims(2, 28, 28, 80)),
-    ("mb_big_hidden", MBConv(8, 6, 0.25), TensorDims(2, 14, 14, 256)),  # conv weights read through L1
+    ("mb_big_hidden", MBConv(8, 6, 0.25), TensorDims(2, 14, 14, 256)),  # 1536 hidden channels: 24 conv slices, 55 KB SE partials
     ("ffn", FFN(4, "gelu"), TensorDims(2, 14, 14, 96)),
 ]
 

@@ -20,4 +20,6 @@ for h in [int(v) for v in (sys.argv[1:] or ["14", "7"])]:
     r = lambda v: (v - t[0]) if v else -1
     print(f"mb{h}: x@{r(t[70])} convA_end@{r(t[1])} SE_end@{r(t[2])} gate_end@{r(t[3])} z_full@{r(t[68])} stored@{r(t[69])}")
     for j in range(8):
-        print(f"  chunk {j}: expand@{r(t[36 + j])} h1_full@{r(t[4 + j])} conv_done@{r(t[20 + j])} proj@{r(t[52 + j])}")
+        print(f"  chunk {j}: expand@{r(t[36 + j])} h1_full@{r(t[4 + j])} conv_start@{r(t[12 + j])} "
+              f"top@{r(t[72 + j])} ldg_issued@{r(t[80 + j])} mma_epi_done@{r(t[28 + j])} conv_done@{r(t[20 + j])} squeeze_done@{r(t[44 + j])} proj@{r(t[52 + j])}")
+
