@@ -442,7 +442,8 @@ namespace {
 constexpr int kSmemMax = 232448;          // 227 KB per CTA
 constexpr int kSmemTwoPerSm = 112 * 1024;  // leaves room for 2 CTAs per SM
 
-bool cf_plan(const wl_block_desc& d, CfPlan& p) {
+// plan with hidden chunks of r channels (0 when r does not fit TMEM)
+bool cf_plan_r(const wl_block_desc& d, CfPlan& p, int r_want) {
   memset(&p, 0, sizeof(p));
   p.C = d.c;
   p.KS = d.ksize;
@@ -454,19 +455,8 @@ bool cf_plan(const wl_block_desc& d, CfPlan& p) {
   p.HW = p.TW + p.KS - 1;
   p.G = p.C / 8;
   const int zc = p.C, cc = p.T8 ? p.C : 0;
-  int best = 0;
-  for (int budget : {256, 512}) {
-    for (int r = 128; r >= 16; r -= 16) {
-      if (p.hid % r) continue;
-      const int cols = zc + cc + 2 * r + 2 * align_up(r / 2, 16);
-      if (cols <= budget) {
-        best = r;
-        break;
-      }
-    }
-    if (best) break;
-  }
-  if (!best) return false;
+  if (p.hid % r_want || zc + cc + 2 * r_want + 2 * align_up(r_want / 2, 16) > 512) return false;
+  const int best = r_want;
   p.r = best;
   p.nchunks = p.hid / p.r;
   p.t_z = 0;
@@ -544,6 +534,19 @@ bool cf_plan(const wl_block_desc& d, CfPlan& p) {
   p.s_bar = align_up(p.s_ring + ring, 128);
   p.smem_bytes = p.s_bar + 512;
   return true;
+}
+
+// Widest hidden chunk that still gives two CTAs per SM; else the widest that
+// fits one CTA. (Narrow chunks only pay when they buy the second CTA: for wide
+// blocks whose weights cannot fit twice, e.g. C = 96 x 6, a 16-wide chunk
+// turned the FFN into 36 latency-bound N = 16 steps per tile — 76k cycles per
+// tile at 56x56x96, measured.)
+bool cf_plan(const wl_block_desc& d, CfPlan& p) {
+  for (int r = 128; r >= 16; r -= 16)
+    if (cf_plan_r(d, p, r) && p.ctas_per_sm == 2) return true;
+  for (int r = 128; r >= 16; r -= 16)
+    if (cf_plan_r(d, p, r)) return true;
+  return false;
 }
 
 using CfKernel = void (*)(const CUtensorMap, const CfArgs);

@@ -13,6 +13,7 @@ CASES = {
     "cf112": (ConvFirst(8, 3), TensorDims(128, 112, 112, 16), None),
     "cf56": (ConvFirst(8, 6), TensorDims(128, 56, 56, 32), None),
     "cf28": (ConvFirst(8, 6), TensorDims(128, 28, 28, 48), None),
+    "cf96": (ConvFirst(8, 6), TensorDims(8, 56, 56, 96), None),
     "cfs2_112": (ConvFirst(8, 6, 2), TensorDims(128, 112, 112, 16), 32),
     "cfs2_56": (ConvFirst(8, 6, 2), TensorDims(128, 56, 56, 32), 48),
     "nano_s2b0": (ConvFirst(8, 6, 2), TensorDims(128, 112, 112, 32), 48),

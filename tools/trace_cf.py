@@ -7,7 +7,8 @@ from paper_2404_03617_b200.core import ConvFirst, TensorDims
 from paper_2404_03617_b200.blocks import FusedBlock
 cases = {"cf112": (ConvFirst(8, 3), TensorDims(128, 112, 112, 16)),
          "cf56": (ConvFirst(8, 6), TensorDims(128, 56, 56, 32)),
-         "cf28": (ConvFirst(8, 6), TensorDims(128, 28, 28, 48))}
+         "cf28": (ConvFirst(8, 6), TensorDims(128, 28, 28, 48)),
+         "cf96": (ConvFirst(8, 6), TensorDims(8, 56, 56, 96))}
 names = ["halo", "cv_go", "cv_iss", "cepi", "cepi_e", "ffn", "H", "H_e", "prj", "fin", "fin_e"]
 for nm in sys.argv[1:]:
     blk, dims = cases[nm]
