@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(scf::kThreads, 2)
     for (int e = 0; e < 4; ++e) {
       const int k = 16 * s + 2 * tq + (e & 1) + 8 * (e >> 1);
       const int kr = k / 9, ks = (k / 3) % 3, c = k % 3;
-      koff[s][e] = k < 27 ? kr * kPC + ks * 3 + c : -1;
+      // k >= 27 carries zero weights: any finite patch element will do
+      koff[s][e] = k < 27 ? kr * kPC + ks * 3 + c : 0;
     }
 
   if (threadIdx.x == 0) {
@@ -136,12 +137,14 @@ __global__ void __launch_bounds__(scf::kThreads, 2)
   __syncthreads();
   pdl_wait();
   const int my_tiles = blockIdx.x < a.tiles ? (a.tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int tpi = a.tiles_x * a.tiles_y;
   auto tile_of = [&](int t, int& img, int& y0, int& x0) {
     const int tile = blockIdx.x + t * gridDim.x;
-    img = tile / (a.tiles_x * a.tiles_y);
-    const int r = tile % (a.tiles_x * a.tiles_y);
-    y0 = (r / a.tiles_x) * kTY;
-    x0 = (r % a.tiles_x) * kTX;
+    img = tile / tpi;
+    const int r = tile - img * tpi;
+    const int ty = r / a.tiles_x;
+    y0 = ty * kTY;
+    x0 = (r - ty * a.tiles_x) * kTX;
   };
   auto load_patch = [&](int t) {
     int img, y0, x0;
@@ -157,15 +160,19 @@ __global__ void __launch_bounds__(scf::kThreads, 2)
   for (int t = 0; t < my_tiles; ++t) {
     int img, y0, x0;
     tile_of(t, img, y0, x0);
+    // the next tile's patch goes to the buffer tile t - 1 released (its stem
+    // ended before the barrier that closed tile t - 1): a whole tile of lead
+    if (threadIdx.x == 0 && t + 1 < my_tiles) load_patch(t + 1);
     const int pb = t & 1;
     mbar_wait(&bar[pb], (t >> 1) & 1);
     const __half* patch = s_patch[pb];
     // ------------------------------------------------------------ stem
     for (int mt = warp; mt < (kHR * kHP + 15) / 16; mt += 8) {
       const int p0 = mt * 16 + gid, p1 = p0 + 8;  // flat h pixels of this lane's two rows
-      const int pr0 = p0 / kHP, pc0 = p0 % kHP, pr1 = p1 / kHP, pc1 = p1 % kHP;
+      // rows past the plane gather from its last pixel (in bounds; results dropped)
+      const int q0 = min(p0, kHR * kHP - 1), q1 = min(p1, kHR * kHP - 1);
+      const int pr0 = q0 / kHP, pc0 = q0 % kHP, pr1 = q1 / kHP, pc1 = q1 % kHP;
       const int base0 = 2 * pr0 * kPC + 2 * pc0 * 3 + 7, base1 = 2 * pr1 * kPC + 2 * pc1 * 3 + 7;
-      const bool v0 = p0 < kHR * kHP, v1 = p1 < kHR * kHP;
       float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
@@ -173,8 +180,8 @@ __global__ void __launch_bounds__(scf::kThreads, 2)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int o = koff[s][q];
-          e[0][q] = (o >= 0 && v0) ? patch[base0 + o] : __float2half(0.f);
-          e[1][q] = (o >= 0 && v1) ? patch[base1 + o] : __float2half(0.f);
+          e[0][q] = patch[base0 + o];
+          e[1][q] = patch[base1 + o];
         }
         const uint32_t a0 = h2u(__halves2half2(e[0][0], e[0][1])), a1 = h2u(__halves2half2(e[1][0], e[1][1]));
         const uint32_t a2 = h2u(__halves2half2(e[0][2], e[0][3])), a3 = h2u(__halves2half2(e[1][2], e[1][3]));
@@ -197,7 +204,6 @@ __global__ void __launch_bounds__(scf::kThreads, 2)
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && t + 1 < my_tiles) load_patch(t + 1);  // this tile's patch is consumed
     // ------------------------------------------- conv -> expand -> project
     {
       const int r = warp + 1;  // h plane row of this warp's output row
