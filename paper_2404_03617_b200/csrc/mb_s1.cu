@@ -49,6 +49,7 @@ namespace wl {
 constexpr int kMb1MaxStage = 20;
 struct Mb1Args {
   int n, H, W, C, hid, sq, nch, NT;
+  int K;  // output channels (C for stride 1; stride 2: 64 or 128)
   int s_x, s_h1, s_h1_bytes, s_w, s_wex, s_hdr, s_se, s_bar, smem;
   int s_h2;  // P = 8: the block's whole h2 (compact 64-row chunks) stays in shared memory
   int o_bexp, o_bconv, o_bprj, hdr_bytes;  // header (fp32) in the packed blob
@@ -145,7 +146,11 @@ __host__ __device__ constexpr int mb1_plane_bytes(int h) {
 }
 
 // H: image rows (flat rows P H <= 128 NT); C: block channels (64 or 128)
-template <int H, int C, int ACT>
+// S2: the stride-2 block (H = 14 -> 7): the conv output is blurred (Triangle-3,
+// stride 2, reflect) in the conv warps' registers and h2 is stored at 7 x 7 in
+// the compact pitch-8 layout; SE, projection (M = 64) and the output run at
+// 7 x 7, without a shortcut (PAPER.md BlurPool downsampling; complexity.py:208-215)
+template <int H, int C, int ACT, bool S2>
 __global__ void __launch_bounds__(mb1::kThreads, 1)
     mb_s1_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_z,
                  const __grid_constant__ Mb1Args a) {
@@ -165,6 +170,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     return arow;
   };
   static_assert(P == 16 || P * H <= 64, "P = 8 holds at most four 16-row fragments");
+  static_assert(!S2 || (H == 14 && P == 16), "stride-2 variant: 14x14 -> 7x7");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* s_x = smem + a.s_x;
   uint8_t* s_h1 = smem + a.s_h1;   // 2 buffers x 8 group planes; phase C ring overlays s_h1 .. s_w end
@@ -270,6 +276,19 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
             bulk_g2s(s_w + s * a.slot_bytes, wp + a.o_wprj + (size_t)j * 2 * vbytes, 2 * vbytes,
                      &B.pa_full[s]);
           }
+        } else if constexpr (S2) {
+          // 7x7 h2 chunks (compact, 8 KB) + W_prj chunks (K x 64) through the ring
+          const uint32_t zbytes = a.K * kHC * 2;
+          mbar_wait(&B.a_done, blk & 1);
+          for (int j = 0; j < nch; ++j) {
+            const int gq = blk * nch + j;
+            const int s = gq & 3, u = gq >> 2;
+            mbar_wait(&B.pa_empty[s], (u & 1) ^ 1);
+            uint8_t* slot = s_h1 + s * a.slot_bytes;
+            mbar_arrive_expect_tx(&B.pa_full[s], 8192 + zbytes);
+            bulk_g2s(slot, a.h2 + ((size_t)img * nch + j) * 8192, 8192, &B.pa_full[s]);
+            bulk_g2s(slot + 8192, wp + a.o_wprj + (size_t)j * zbytes, zbytes, &B.pa_full[s]);
+          }
         } else {
         mbar_wait(&B.a_done, blk & 1);
         for (int qq = 0; qq < 2 * nch; ++qq) {
@@ -335,6 +354,23 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
               const uint64_t ad = make_sdesc(hb + k * 2 * 1024, 1024, 128);
               const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
               mma_ss(tmem + a.t_z, ad, bd, idesc_z64, (j > 0 || k > 0));
+            }
+            mma_commit(&B.pa_empty[s]);
+          }
+        } else if constexpr (S2) {
+          const uint32_t idesc_s2 = make_idesc_f16(64, a.K);
+          for (int j = 0; j < nch; ++j) {
+            const int gq = blk * nch + j;
+            const int s = gq & 3, u = gq >> 2;
+            mbar_wait(&B.pa_ready[s], u & 1);  // landed and gated
+            tc_fence_after();
+            MB1_TRACE(52 + j);
+            const uint32_t slot = smem_u32(s_h1 + s * a.slot_bytes);
+#pragma unroll
+            for (int k = 0; k < kHC / 16; ++k) {
+              const uint64_t ad = make_sdesc(slot + k * 2 * 1024, 1024, 128);
+              const uint64_t bd = make_sdesc(slot + 8192 + k * 2 * (a.K / 8) * 128, (a.K / 8) * 128, 128);
+              mma_ss(tmem + a.t_z, ad, bd, idesc_s2, (j > 0 || k > 0));
             }
             mma_commit(&B.pa_empty[s]);
           }
@@ -466,7 +502,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           float sv = 0.f;
 #pragma unroll
           for (int r = 0; r < 8; ++r) sv += scr[r * 32 + lane];
-          scr[256 + lane] = lane < a.sq ? fmaxf(sv * (1.f / (float)(a.H * a.W)) + bsq_o, 0.f) : 0.f;
+          const float inv_p = S2 ? 1.f / (float)((a.H / 2) * (a.W / 2)) : 1.f / (float)(a.H * a.W);
+          scr[256 + lane] = lane < a.sq ? fmaxf(sv * inv_p + bsq_o, 0.f) : 0.f;
           mbar_arrive(&B.sq_full);
         }
       }
@@ -474,7 +511,33 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       mbar_wait(&B.z_full, blk & 1);
       tc_fence_after();
       if (e == 0 && lane == 0) MB1_TRACE(68);
-      if (hh < KH) {
+      if constexpr (S2) {
+        // Z (M = 64): 7x7 compact row 16 q + lane at TMEM lane 32 q + lane; the
+        // x tile is dead (no shortcut), so z is staged over it
+        const int f = 16 * q + lane;
+        if (hh < a.K / 64) {
+          uint32_t v[64];
+          const uint32_t za = tmem_lane_addr(tmem, q, a.t_z + hh * 64);
+          WL_TMEM_LD16(za, v);
+          WL_TMEM_LD16(za + 16, (v + 16));
+          WL_TMEM_LD16(za + 32, (v + 32));
+          WL_TMEM_LD16(za + 48, (v + 48));
+          tmem_ld_wait();
+          if (lane < 16 && f < 56) {
+            uint8_t* zrow = s_x + hh * XH + f * 128;
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+              const float4 b0 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8);
+              const float4 b1 = *reinterpret_cast<const float4*>(s_bprj + hh * 64 + c8 * 8 + 4);
+              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+              float fz[8];
+#pragma unroll
+              for (int r = 0; r < 8; ++r) fz[r] = __uint_as_float(v[c8 * 8 + r]) + bb[r];
+              *reinterpret_cast<uint4*>(zrow + ((c8 ^ (f & 7)) << 4)) = pack8(fz);
+            }
+          }
+        }
+      } else if (hh < KH) {
 #pragma unroll 1
         for (int t = 0; t < NT; ++t) {
           const int m = t * 128 + q * 32 + lane;  // A row (TMEM lane)
@@ -519,7 +582,10 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           // a TMA store may not start at a negative coordinate (illegal instruction,
           // tools/probe_tma_store.cu): start at x = 0 one 128-byte row into the tile
           // (the 128B swizzle is address-based, so the shifted source stays valid)
-          if constexpr (P == 8) {
+          if constexpr (S2) {
+            for (int kh = 0; kh < a.K / 64; ++kh)
+              for (int k = 0; k < 4; ++k) tma_store_4d(&tmap_z, s_x + kh * XH + k * 2048 + 128, kh * 64, 0, 2 * k, img);
+          } else if constexpr (P == 8) {
             for (int kh = 0; kh < KH; ++kh)
               for (int k = 0; k < (H + 1) / 2; ++k)
                 tma_store_4d(&tmap_z, s_x + kh * XH + k * 2048 + 128, kh * 64, 0, 2 * k, img);
@@ -586,8 +652,47 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       // A layout [tile][group][row][16 B]: per warp store, 8 rows x 4 lanes x
       // 4 B = two whole 128-byte lines
       // (P = 8: into the resident compact h2: [chunk][group][64 rows][16 B])
+      // (S2: the blurred 7x7 h2 to the workspace in the same compact layout)
       uint8_t* h2c = P == 8 ? smem + a.s_h2 + j * 8192 + g * 1024 + tq * 4
+                     : S2   ? a.h2 + ((size_t)img * nch + j) * 8192 + g * 1024 + tq * 4
                             : h2img + (size_t)j * NT * 16384 + g * 2048 + tq * 4;
+      // S2: output row yo of the Triangle-3 blur from conv rows 2 yo - 1 (kept
+      // from the previous pair; row 1 reflected for yo = 0), 2 yo and 2 yo + 1;
+      // along W the lane holding column 2 xo (flat i = 2 xo + 1) combines its
+      // shuffled neighbours (column -1 reflects to 1)
+      float2 po0 = make_float2(0.f, 0.f), po1 = make_float2(0.f, 0.f);
+      auto epi_s2 = [&](int yo, const float* c0, const float* c1, const float* d0, const float* d1) {
+        const float2 e0 = __half22float2(__hmul2(act_h2<ACT>(__floats2half2_rn(c0[0] + c1[0], c0[1] + c1[1])), m0));
+        const float2 e1 = __half22float2(__hmul2(act_h2<ACT>(__floats2half2_rn(c0[2] + c1[2], c0[3] + c1[3])), m1));
+        const float2 o0 = __half22float2(__hmul2(act_h2<ACT>(__floats2half2_rn(d0[0] + d1[0], d0[1] + d1[1])), m0));
+        const float2 o1 = __half22float2(__hmul2(act_h2<ACT>(__floats2half2_rn(d0[2] + d1[2], d0[3] + d1[3])), m1));
+        const float2 p0 = yo == 0 ? o0 : po0, p1 = yo == 0 ? o1 : po1;
+        const float2 v0 = make_float2(0.25f * p0.x + 0.5f * e0.x + 0.25f * o0.x, 0.25f * p0.y + 0.5f * e0.y + 0.25f * o0.y);
+        const float2 v1 = make_float2(0.25f * p1.x + 0.5f * e1.x + 0.25f * o1.x, 0.25f * p1.y + 0.5f * e1.y + 0.25f * o1.y);
+        po0 = o0;
+        po1 = o1;
+        auto shf = [](float2 v, int src) {
+          return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+        };
+        const float2 up0 = shf(v0, (lane - 4) & 31), dn0 = shf(v0, (lane + 4) & 31);
+        const float2 up1 = shf(v1, (lane - 4) & 31), dn1 = shf(v1, (lane + 4) & 31);
+        const float2 first1 = shf(v1, tq);  // flat i = 8 (column 7)
+        // columns 0..7 (i = gid, gid odd -> xo = (gid - 1) / 2)
+        const float2 l0 = gid == 1 ? dn0 : up0, r0 = gid == 7 ? first1 : dn0;
+        // columns 8..13 (i = gid + 8, gid in {1, 3, 5} -> xo = 4, 5, 6)
+        const __half2 z0 = __floats2half2_rn(0.25f * l0.x + 0.5f * v0.x + 0.25f * r0.x,
+                                             0.25f * l0.y + 0.5f * v0.y + 0.25f * r0.y);
+        const __half2 z1 = __floats2half2_rn(0.25f * up1.x + 0.5f * v1.x + 0.25f * dn1.x,
+                                             0.25f * up1.y + 0.5f * v1.y + 0.25f * dn1.y);
+        if (gid & 1) {
+          *reinterpret_cast<__half2*>(h2c + (8 * yo + (gid - 1) / 2 + 1) * 16) = z0;
+          pool = __hadd2(pool, z0);
+          if (gid < 7) {
+            *reinterpret_cast<__half2*>(h2c + (8 * yo + (gid + 7) / 2 + 1) * 16) = z1;
+            pool = __hadd2(pool, z1);
+          }
+        }
+      };
       // fragment f = flat rows 16 f .. 16 f + 15; v1: its rows gid + 8 are image pixels
       auto epi = [&](int f, const float* c0, const float* c1, bool v1) {
         const __half2 h0 = __hmul2(act_h2<ACT>(__floats2half2_rn(c0[0] + c1[0], c0[1] + c1[1])), m0);
@@ -629,8 +734,12 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         hmma16(b1, Q3[0], Q3[1], Q3[2], Q3[3], bw[4], bw[5]);
         hmma8(a0, P2[0], P2[1], bw[8]);
         hmma8(b0, P3[0], P3[1], bw[8]);
-        epi(y, a0, a1, true);
-        epi(y + 1, b0, b1, true);
+        if constexpr (S2) {
+          epi_s2(y >> 1, a0, a1, b0, b1);
+        } else {
+          epi(y, a0, a1, true);
+          epi(y + 1, b0, b1, true);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           Q0[k] = Q2[k];
@@ -787,6 +896,26 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         fence_async_smem();
         mbar_arrive(&B.pa_ready[gq & 3]);
       }
+    } else if constexpr (S2) {
+      // each reloaded 7x7 chunk ([group][64 rows][16 B]) gated in its ring slot
+      for (int jj = 0; jj < nch; ++jj) {
+        const int gq = blk * nch + jj, s = gq & 3;
+        mbar_wait(&B.pa_full[s], (gq >> 2) & 1);
+        uint4* hs = reinterpret_cast<uint4*>(s_h1 + s * a.slot_bytes);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int id = k * 256 + tid, gg = id >> 6;
+          uint4 hv = hs[id];
+          const uint4 gv = *reinterpret_cast<const uint4*>(s_gate + jj * (kHC / 2) + gg * 4);
+          __half2* h = reinterpret_cast<__half2*>(&hv);
+          const __half2* gt = reinterpret_cast<const __half2*>(&gv);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h[i] = __hmul2(h[i], gt[i]);
+          hs[id] = hv;
+        }
+        fence_async_smem();
+        mbar_arrive(&B.pa_ready[s]);
+      }
     } else {
     for (int qq = 0; qq < 2 * nch; ++qq) {
       const int gq = blk * 2 * nch + qq;
@@ -843,6 +972,8 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   a.H = d.h;
   a.W = d.w;
   a.C = d.c;
+  a.K = d.stride == 2 ? d.k : d.c;
+  const bool s2 = d.stride == 2;
   a.hid = d.expansion * d.c;
   a.sq = d.se_sq;
   a.nch = a.hid / mb1::kHC;
@@ -857,7 +988,8 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   const bool p8 = mb1_pitch(a.H) == 8;
   // phase C ring slot: P = 16: h2 half-chunk (NT x 8 KB) + W_prj half-chunk;
   // P = 8 (h2 resident): one W_prj chunk (C x 64 x 2)
-  a.slot_bytes = p8 ? C * mb1::kHC * 2 : NT * 8192 + C * 32 * 2;
+  // S2: one 7x7 h2 chunk (8 KB) + one W_prj chunk (K x 64 x 2)
+  a.slot_bytes = p8 ? C * mb1::kHC * 2 : s2 ? 8192 + a.K * mb1::kHC * 2 : NT * 8192 + C * 32 * 2;
   const int wring = 2 * mb1::kHC * C * 2;
   if (p8) {
     // W_exp ring | h1 (>= 2 slots): the phase C ring's slots 0 / 1 are the W_exp
@@ -881,7 +1013,7 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   a.o_bexp = 0;
   a.o_bconv = hid * 4;
   a.o_bprj = 2 * hid * 4;
-  a.hdr_bytes = align_up(2 * hid * 4 + C * 4, 16);
+  a.hdr_bytes = align_up(2 * hid * 4 + a.K * 4, 16);
   a.s_hdr = align_up(o, 128);
   o = a.s_hdr + a.hdr_bytes;
   a.s_se = align_up(o, 128);
@@ -908,12 +1040,12 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   a.o_wprj = p;
   a.t_e = 0;
   a.t_z = 2 * NT * mb1::kHC;
-  const int cols = a.t_z + NT * C;
+  const int cols = a.t_z + (s2 ? a.K : NT * C);
   a.tmem_cols = 32;
   while (a.tmem_cols < cols) a.tmem_cols *= 2;
   return a.smem <= kSmemMax1 && cols <= 512;
 }
-int64_t mb1_blob_bytes(const Mb1Args& a) { return a.o_wprj + (int64_t)a.nch * a.C * mb1::kHC * 2; }
+int64_t mb1_blob_bytes(const Mb1Args& a) { return a.o_wprj + (int64_t)a.nch * a.K * mb1::kHC * 2; }
 
 static bool env_legacy() {
   static const bool v = getenv("WL_MB_LEGACY") != nullptr;  // A/B: force the block-diagonal tcgen05 conv kernel
@@ -922,24 +1054,30 @@ static bool env_legacy() {
 
 using Mb1K = void (*)(const CUtensorMap, const CUtensorMap, const Mb1Args);
 template <int C, int ACT>
-Mb1K mb1_pick_h(int h) {
+Mb1K mb1_pick_h(int h, bool s2) {
+  if (s2) return h == 14 ? mb_s1_kernel<14, C, ACT, true> : nullptr;
   switch (h) {
-    case 7: return mb_s1_kernel<7, C, ACT>;
-    case 8: return mb_s1_kernel<8, C, ACT>;
-    case 14: return mb_s1_kernel<14, C, ACT>;
-    case 16: return mb_s1_kernel<16, C, ACT>;
+    case 7: return mb_s1_kernel<7, C, ACT, false>;
+    case 8: return mb_s1_kernel<8, C, ACT, false>;
+    case 14: return mb_s1_kernel<14, C, ACT, false>;
+    case 16: return mb_s1_kernel<16, C, ACT, false>;
   }
   return nullptr;
 }
 Mb1K mb1_kernel(const wl_block_desc& d) {
-  if (d.c == 128) return d.act == kSilu ? mb1_pick_h<128, kSilu>(d.h) : mb1_pick_h<128, kRelu>(d.h);
-  if (d.c == 64) return d.act == kSilu ? mb1_pick_h<64, kSilu>(d.h) : mb1_pick_h<64, kRelu>(d.h);
+  const bool s2 = d.stride == 2;
+  if (d.c == 128) return d.act == kSilu ? mb1_pick_h<128, kSilu>(d.h, s2) : mb1_pick_h<128, kRelu>(d.h, s2);
+  if (d.c == 64) return d.act == kSilu ? mb1_pick_h<64, kSilu>(d.h, s2) : mb1_pick_h<64, kRelu>(d.h, s2);
   return nullptr;
 }
 }  // namespace
 
 bool mb1_eligible(const wl_block_desc& d) {
-  if (env_legacy() || d.kind != WL_KIND_MBCONV || d.stride != 1 || d.group_width != 8 || d.k != d.c) return false;
+  if (env_legacy() || d.kind != WL_KIND_MBCONV || d.group_width != 8) return false;
+  if (d.stride == 1 && d.k != d.c) return false;
+  // stride 2: the 14x14 -> 7x7 block (conv at 14x14, blur-pool, 7x7 tail)
+  if (d.stride == 2 && (d.h != 14 || d.w != 14 || (d.k != 64 && d.k != 128))) return false;
+  if (d.stride != 1 && d.stride != 2) return false;
   if ((d.c != 64 && d.c != 128) || d.w > 14 || d.w > mb1_pitch(d.h) - 1 || (d.act != kSilu && d.act != kRelu))
     return false;
   const int hid = d.expansion * d.c;
@@ -957,7 +1095,7 @@ int64_t mb1_packed_bytes(const wl_block_desc& d) {
 int64_t mb1_workspace(const wl_block_desc& d) {
   Mb1Args a;
   mb1_plan(d, a);
-  return kWsHeader1 + (int64_t)d.n * a.nch * a.NT * 16384;
+  return kWsHeader1 + (int64_t)d.n * a.nch * (d.stride == 2 ? 8192 : a.NT * 16384);
 }
 
 int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
@@ -972,7 +1110,8 @@ int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
     hb[i] = bexp[i];
     hb[hid + i] = bconv[i];
   }
-  for (int i = 0; i < C; ++i) hb[2 * hid + i] = bprj[i];
+  const int K = a.K;
+  for (int i = 0; i < K; ++i) hb[2 * hid + i] = bprj[i];
   uint8_t* se = out + a.o_se;
   for (int o = 0; o < sq; ++o)  // transposed [o][hid]; rows sq..31 stay zero
     for (int i = 0; i < hid; ++i) put_h(se, ((size_t)o * hid + i) * 2, wsq[(size_t)i * sq + o]);
@@ -999,11 +1138,11 @@ int mb1_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
     for (int nn = 0; nn < HC; ++nn)
       for (int k = 0; k < C; ++k) put_h(ch, core_off_h(nn, k, 1024), wexp[(size_t)k * hid + j * HC + nn]);
   }
-  // W_prj chunk j: B operand (N = C x K = 64 hidden), LBO = (C / 8) 128
+  // W_prj chunk j: B operand (N = K output channels x K = 64 hidden), LBO = (K / 8) 128
   for (int j = 0; j < a.nch; ++j) {
-    uint8_t* ch = out + a.o_wprj + (size_t)j * C * HC * 2;
-    for (int nn = 0; nn < C; ++nn)
-      for (int k = 0; k < HC; ++k) put_h(ch, core_off_h(nn, k, (C / 8) * 128), wprj[(size_t)(j * HC + k) * C + nn]);
+    uint8_t* ch = out + a.o_wprj + (size_t)j * K * HC * 2;
+    for (int nn = 0; nn < K; ++nn)
+      for (int k = 0; k < HC; ++k) put_h(ch, core_off_h(nn, k, (K / 8) * 128), wprj[(size_t)(j * HC + k) * K + nn]);
   }
   return WL_OK;
 }
@@ -1015,7 +1154,15 @@ static int mb1_launch(const wl_block_desc& d, Mb1Args& a, const void* x, void* z
   // P = 8: one box per pair of image rows (a 16-row fragment, placed at A rows 32 k)
   const uint32_t box[4] = {64, (uint32_t)mb1_pitch(d.h), mb1_pitch(d.h) == 8 ? 2u : (uint32_t)d.h, 1};
   if (int e = encode_tmap(&tx, x, 4, dims, strides, box, true)) return e;
-  if (int e = encode_tmap(&tz, z, 4, dims, strides, box, true)) return e;
+  if (d.stride == 2) {
+    // 7x7 output, stored as pairs of rows from the compact pitch-8 staging
+    const uint64_t zd[4] = {(uint64_t)d.k, (uint64_t)(d.w / 2), (uint64_t)(d.h / 2), (uint64_t)d.n};
+    const uint64_t zs[3] = {(uint64_t)d.k * 2, (uint64_t)(d.w / 2) * d.k * 2, (uint64_t)(d.h / 2) * (d.w / 2) * d.k * 2};
+    const uint32_t zb[4] = {64, 8, 2, 1};
+    if (int e = encode_tmap(&tz, z, 4, zd, zs, zb, true)) return e;
+  } else if (int e = encode_tmap(&tz, z, 4, dims, strides, box, true)) {
+    return e;
+  }
   return launch_pdl(mb1_kernel(d), d.n, mb1::kThreads, a.smem, st, "mb_s1 launch", tx, tz, a);
 }
 
@@ -1029,13 +1176,14 @@ int mb1_forward(const wl_block_desc& d, const void* x, const void* packed, void*
   return mb1_launch(d, a, x, z, st);
 }
 
-int mb1_stage_max(const wl_block_desc& d) { return mb1_eligible(d) ? kMb1MaxStage : 0; }
+int mb1_stage_max(const wl_block_desc& d) { return d.stride == 1 && mb1_eligible(d) ? kMb1MaxStage : 0; }
 
 // nblk consecutive identical stride-1 MBConv blocks in one launch: the image
 // stays in shared memory between blocks (the per-stage persistent kernel)
 int mb1_stage_forward(const wl_block_desc& d, int nblk, const void* x, const void* const* packed, void* z, void* ws,
                       cudaStream_t st) {
-  if (!mb1_eligible(d)) return set_error(WL_EUNSUPPORTED, "stage launch: block is not a stride-1 T=8 MBConv (W <= 14)");
+  if (d.stride != 1 || !mb1_eligible(d))
+    return set_error(WL_EUNSUPPORTED, "stage launch: block is not a stride-1 T=8 MBConv (W <= 14)");
   if (nblk < 1 || nblk > kMb1MaxStage)
     return set_error(WL_EUNSUPPORTED, "stage launch: 1..%d blocks (got %d)", kMb1MaxStage, nblk);
   Mb1Args a;
@@ -1054,12 +1202,13 @@ int mb1_stage_forward(const wl_block_desc& d, int nblk, const void* x, const voi
 int mb1_init() {
   for (int c : {64, 128})
     for (int act : {kSilu, kRelu})
-      for (int h : {7, 8, 14, 16}) {
+      for (int h : {7, 8, 14, 16, -14}) {  // -14: the stride-2 14x14 -> 7x7 variant
         wl_block_desc d;
         memset(&d, 0, sizeof(d));
         d.c = c;
         d.act = act;
-        d.h = h;
+        d.h = h < 0 ? -h : h;
+        d.stride = h < 0 ? 2 : 1;
         if (int e = check_cuda(cudaFuncSetAttribute(mb1_kernel(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     kSmemMax1),
                                "cudaFuncSetAttribute(mb_s1)"))

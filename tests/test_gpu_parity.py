@@ -70,6 +70,10 @@ CASES = [
     ("mbconv_small_c256", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 256), None),
     ("mbconv_s2_28", MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 48), 128),
     ("mbconv_s2_14", MBConv(8, 4, 0.25, 2), TensorDims(2, 14, 14, 128), 128),
+    # the stride-2 14x14 -> 7x7 variant of the mma.sync kernel: other widths, ReLU, odd batch
+    ("mbconv_s2_14_c64_k128_relu", MBConv(8, 4, 0.25, 2, "relu"), TensorDims(3, 14, 14, 64), 128),
+    ("mbconv_s2_14_c128_k64", MBConv(8, 2, 0.25, 2), TensorDims(2, 14, 14, 128), 64),
+    ("mbconv_s2_14_b129", MBConv(8, 4, 0.25, 2), TensorDims(129, 14, 14, 128), 128),
     ("stem_224", Stem(16), TensorDims(2, 224, 224, 3), None),
     ("stem_c32", Stem(32), TensorDims(1, 64, 48, 3), None),
     ("head_pico", Head(1280, 1000), TensorDims(5, 7, 7, 128), None),
