@@ -65,6 +65,9 @@ __device__ __forceinline__ uint4 bias_act8(const uint32_t* acc, const float* bia
   return q;
 }
 
+// named barrier over n threads (multiple of 32)
+__device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 // 16-byte read-only global load the compiler may neither sink to its use nor
 // re-issue there (a prefetch meant to hide L2 latency behind other work)
 __device__ __forceinline__ uint4 ldg_pinned(const void* p) {

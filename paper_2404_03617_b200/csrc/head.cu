@@ -25,97 +25,137 @@ struct HeadArgs {
   __half* feat;       // (n, E) pooled embedding
 };
 
+// Persistent: CTA c owns embedding chunk j = c % nce (its W1 chunk loaded once)
+// and loops over image groups g = c / nce, + nsl, ...; x tiles are double
+// buffered (TMA), the accumulators double buffered in TMEM, so group g + 1's
+// load and 1x1 conv overlap group g's epilogue. Warps 0-7: epilogue (bias +
+// phi, staged, per-image column sums); warp 8: loads and MMAs.
+constexpr int kHeadThreads = 288;
 template <int ACT>
-__global__ void __launch_bounds__(256, 1) head_pool_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                                                           const __grid_constant__ HeadArgs a) {
+__global__ void __launch_bounds__(kHeadThreads, 1) head_pool_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                                                                    const __grid_constant__ HeadArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* s_a = smem + a.s_a;    // [C/8][128][8]
   uint8_t* s_w = smem + a.s_w;    // NE x C chunk
-  uint8_t* s_st = smem + a.s_st;  // [NE/8][128][8] activated chunk
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.s_bar);  // 0 loads, 1 mma
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 2);
-  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, q = warp % 4, half = warp / 4;
-  const int grp = blockIdx.x / a.nce, j = blockIdx.x % a.nce;
-  const int p0 = grp * a.imgs * a.HW;
+  uint8_t* s_st = smem + a.s_st;  // [NE/8][128][8] activated tile
+  // bars: 0-1 x_full, 2-3 x_empty, 4-5 acc_full, 6-7 acc_empty, 8 w_full
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.s_bar);
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 9);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int j = blockIdx.x % a.nce, slice = blockIdx.x / a.nce;
+  const int nsl = ((int)gridDim.x - j + a.nce - 1) / a.nce;  // CTAs serving chunk j
+  const int groups = (a.P / a.HW + a.imgs - 1) / a.imgs;
+  const int my = slice < groups ? (groups - 1 - slice) / nsl + 1 : 0;
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar[i], 1);
+      mbar_init(&bar[2 + i], 1);
+      mbar_init(&bar[4 + i], 1);
+      mbar_init(&bar[6 + i], 256);
+    }
+    mbar_init(&bar[8], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc_n(tbase, a.tmem_cols);
+  if (warp == 8) tmem_alloc_n(tbase, a.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   pdl_wait();
   const uint32_t tmem = *tbase;
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bar[0], 128 * a.C * 2 + a.w1_chunk);
-    if (a.xsw) {
-      for (int cb = 0; cb < a.C / 64; ++cb)
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];" ::"r"(smem_u32(s_a + cb * 16384)),
-            "l"(&tmap_x), "r"(cb * 64), "r"(p0), "r"(smem_u32(&bar[0]))
-            : "memory");
-    } else {
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-          "[%5];" ::"r"(smem_u32(s_a)),
-          "l"(&tmap_x), "r"(0), "r"(p0), "r"(0), "r"(smem_u32(&bar[0]))
-          : "memory");
+  if (warp == 8) {
+    if (lane == 0) {
+      auto load_x = [&](int k) {
+        const int b = k & 1, p0 = (slice + k * nsl) * a.imgs * a.HW;
+        if (k >= 2) mbar_wait(&bar[2 + b], ((k >> 1) - 1) & 1);
+        uint8_t* s_a = smem + a.s_a + b * 128 * a.C * 2;
+        mbar_arrive_expect_tx(&bar[b], 128 * a.C * 2);
+        if (a.xsw) {
+          for (int cb = 0; cb < a.C / 64; ++cb)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3}], [%4];" ::"r"(smem_u32(s_a + cb * 16384)),
+                "l"(&tmap_x), "r"(cb * 64), "r"(p0), "r"(smem_u32(&bar[b]))
+                : "memory");
+        } else {
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+              "%4}], [%5];" ::"r"(smem_u32(s_a)),
+              "l"(&tmap_x), "r"(0), "r"(p0), "r"(0), "r"(smem_u32(&bar[b]))
+              : "memory");
+        }
+      };
+      mbar_arrive_expect_tx(&bar[8], a.w1_chunk);
+      bulk_g2s(s_w, a.w1 + align_up(a.E * 4, 128) + (size_t)j * a.w1_chunk, a.w1_chunk, &bar[8]);
+      if (my > 0) load_x(0);
+      if (my > 1) load_x(1);
+      mbar_wait(&bar[8], 0);
+      const uint32_t idesc = make_idesc_f16(128, a.NE);
+      for (int k = 0; k < my; ++k) {
+        const int b = k & 1, u = k >> 1;
+        mbar_wait(&bar[b], u & 1);
+        mbar_wait(&bar[6 + b], (u & 1) ^ 1);  // the epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + a.s_a + b * 128 * a.C * 2);
+        for (int kk = 0; kk < a.C / 16; ++kk) {
+          const uint64_t ad = a.xsw ? make_sdesc_sw128(sa + (kk / 4) * 16384) + (uint64_t)((kk % 4) * 2)
+                                    : make_sdesc(sa + kk * 2 * 2048, 2048, 128);
+          const uint64_t bd = make_sdesc(smem_u32(s_w) + kk * 2 * (a.NE * 16), a.NE * 16, 128);
+          mma_ss(tmem + b * a.NE, ad, bd, idesc, kk > 0);
+        }
+        mma_commit(&bar[4 + b]);
+        mma_commit(&bar[2 + b]);
+        if (k + 2 < my) load_x(k + 2);
+      }
     }
-    const uint8_t* chunk = a.w1 + align_up(a.E * 4, 128) + (size_t)j * a.w1_chunk;
-    bulk_g2s(s_w, chunk, a.w1_chunk, &bar[0]);
-    mbar_wait(&bar[0], 0);
-    tc_fence_after();
-    const uint32_t idesc = make_idesc_f16(128, a.NE);
-    for (int kk = 0; kk < a.C / 16; ++kk) {
-      const uint64_t ad = a.xsw ? make_sdesc_sw128(smem_u32(s_a) + (kk / 4) * 16384) + (uint64_t)((kk % 4) * 2)
-                                : make_sdesc(smem_u32(s_a) + kk * 2 * 2048, 2048, 128);
-      const uint64_t bd = make_sdesc(smem_u32(s_w) + kk * 2 * (a.NE * 16), a.NE * 16, 128);
-      mma_ss(tmem, ad, bd, idesc, kk > 0);
+  } else {
+    const int q = warp % 4, half = warp / 4;
+    const float* b1 = reinterpret_cast<const float*>(a.w1) + j * a.NE;
+    const int m = q * 32 + lane;
+    const float inv = 1.f / (float)a.HW;
+    const int i = lane >> 2, w = lane & 3;
+    for (int k = 0; k < my; ++k) {
+      const int b = k & 1, u = k >> 1, grp = slice + k * nsl;
+      mbar_wait(&bar[4 + b], u & 1);
+      tc_fence_after();
+      for (int c0 = half * 16; c0 < a.NE; c0 += 32) {
+        uint32_t v[16];
+        WL_TMEM_LD16(tmem_lane_addr(tmem, q, b * a.NE + c0), v);
+        tmem_ld_wait();
+        *reinterpret_cast<uint4*>(s_st + ((c0 / 8) * 128 + m) * 16) = bias_act8<ACT>(v, b1 + c0);
+        *reinterpret_cast<uint4*>(s_st + ((c0 / 8 + 1) * 128 + m) * 16) = bias_act8<ACT>(v + 8, b1 + c0 + 8);
+      }
+      tc_fence_before();
+      mbar_arrive(&bar[6 + b]);
+      nbar(1, 256);
+      // per-image column sums (fixed order): warp handles 8-channel groups g,
+      // lane = (pixel offset i, word w)
+      for (int g = warp; g < a.NE / 8; g += 8) {
+        const uint8_t* base = s_st + g * 128 * 16 + w * 4;
+        for (int im = 0; im < a.imgs; ++im) {
+          const int nimg = grp * a.imgs + im;
+          float s0 = 0.f, s1 = 0.f;
+          for (int p = im * a.HW + i; p < (im + 1) * a.HW; p += 8) {
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(base + p * 16));
+            s0 += f2.x;
+            s1 += f2.y;
+          }
+#pragma unroll
+          for (int sh = 4; sh < 32; sh <<= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, sh);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, sh);
+          }
+          if (i == 0 && (size_t)nimg * a.HW < (size_t)a.P) {
+            __half2 r = __floats2half2_rn(s0 * inv, s1 * inv);
+            *reinterpret_cast<__half2*>(a.feat + (size_t)nimg * a.E + j * a.NE + g * 8 + w * 2) = r;
+          }
+        }
+      }
+      nbar(1, 256);  // the staging tile is rewritten by the next group
     }
-    mma_commit(&bar[1]);
   }
-  mbar_wait(&bar[1], 0);
-  tc_fence_after();
-  const float* b1 = reinterpret_cast<const float*>(a.w1) + j * a.NE;
-  const int m = q * 32 + lane;
-  for (int c0 = half * 16; c0 < a.NE; c0 += 32) {
-    uint32_t v[16];
-    WL_TMEM_LD16(tmem_lane_addr(tmem, q, c0), v);
-    tmem_ld_wait();
-    *reinterpret_cast<uint4*>(s_st + ((c0 / 8) * 128 + m) * 16) = bias_act8<ACT>(v, b1 + c0);
-    *reinterpret_cast<uint4*>(s_st + ((c0 / 8 + 1) * 128 + m) * 16) = bias_act8<ACT>(v + 8, b1 + c0 + 8);
-  }
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
-  // per-image column sums: warp handles 8-channel groups g, lane = (pixel offset i, word w)
-  const float inv = 1.f / (float)a.HW;
-  const int i = lane >> 2, w = lane & 3;
-  for (int g = warp; g < a.NE / 8; g += 8) {
-    const uint8_t* base = s_st + g * 128 * 16 + w * 4;
-    for (int im = 0; im < a.imgs; ++im) {
-      const int nimg = grp * a.imgs + im;
-      float s0 = 0.f, s1 = 0.f;
-      for (int p = im * a.HW + i; p < (im + 1) * a.HW; p += 8) {
-        const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(base + p * 16));
-        s0 += f2.x;
-        s1 += f2.y;
-      }
-#pragma unroll
-      for (int s = 4; s < 32; s <<= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, s);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, s);
-      }
-      if (i == 0 && (size_t)nimg * a.HW < (size_t)a.P) {
-        __half2 r = __floats2half2_rn(s0 * inv, s1 * inv);
-        *reinterpret_cast<__half2*>(a.feat + (size_t)nimg * a.E + j * a.NE + g * 8 + w * 2) = r;
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 0) tmem_dealloc_n(tmem, a.tmem_cols);
+  if (warp == 8) tmem_dealloc_n(tmem, a.tmem_cols);
 }
 
 struct FcArgs {
@@ -200,6 +240,7 @@ __global__ void __launch_bounds__(128, 1) head_fc_kernel(const __grid_constant__
 // =================================================================== host
 #include <algorithm>
 #include <cstring>
+#include "gemm.h"
 #include "launch.h"
 
 namespace wl {
@@ -212,6 +253,7 @@ struct HeadPlan {
   HeadArgs h;
   FcArgs f;
   int64_t w1_bytes, w2_bytes;
+  bool fc_gemm;  // classifier on the persistent tcgen05 GEMM (W2^T [classes][E] fp16 + b2)
 };
 
 bool head_plan(const wl_block_desc& d, HeadPlan& P) {
@@ -233,14 +275,14 @@ bool head_plan(const wl_block_desc& d, HeadPlan& P) {
   P.w1_bytes = align_up(h.E * 4, 128) + (int64_t)h.nce * h.w1_chunk;
   int s = 0;
   h.s_a = s;
-  s += 128 * h.C * 2;
+  s += 2 * 128 * h.C * 2;  // double-buffered x tiles
   h.s_w = s;
   s += h.w1_chunk;
   h.s_st = s;
   s += 128 * h.NE * 2;
   h.s_bar = s;
-  if (s + 64 > kSmemMaxH) return false;
-  h.tmem_cols = std::max(32, h.NE);
+  if (s + 128 > kSmemMaxH) return false;
+  h.tmem_cols = std::max(32, 2 * h.NE);  // double-buffered accumulators
   f.E = h.E;
   f.classes = h.M;
   f.NC = 16;  // 63 class chunks: more CTAs share the K stream
@@ -249,7 +291,9 @@ bool head_plan(const wl_block_desc& d, HeadPlan& P) {
   f.nrows = d.n;
   f.stages = 8;
   f.w_chunk = f.NC * 64 * 2;
-  P.w2_bytes = align_up(h.M * 4, 128) + (int64_t)f.N * f.nkc * f.w_chunk;
+  P.fc_gemm = h.M % 8 == 0 && h.E % 8 == 0;
+  P.w2_bytes = P.fc_gemm ? align_up(h.M * 4, 128) + (int64_t)h.M * h.E * 2
+                         : align_up(h.M * 4, 128) + (int64_t)f.N * f.nkc * f.w_chunk;
   f.s_a = 0;
   f.s_w = f.stages * 16384;
   f.s_bar = f.s_w + f.stages * f.w_chunk;
@@ -308,6 +352,11 @@ int head_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   float* b2 = reinterpret_cast<float*>(o2);
   for (int m = 0; m < h.M; ++m) b2[m] = w[3][m];
   uint8_t* c2 = o2 + align_up(h.M * 4, 128);
+  if (P.fc_gemm) {  // W2^T: [classes][E], the GEMM's K-contiguous B operand
+    for (int m = 0; m < h.M; ++m)
+      for (int e = 0; e < h.E; ++e) put_h(c2, ((size_t)m * h.E + e) * 2, w[2][(size_t)e * h.M + m]);
+    return WL_OK;
+  }
   for (int cc = 0; cc < f.N; ++cc)
     for (int kc = 0; kc < f.nkc; ++kc) {
       uint8_t* blk = c2 + ((size_t)cc * f.nkc + kc) * f.w_chunk;
@@ -350,13 +399,21 @@ int head_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void
   h.w1 = reinterpret_cast<const uint8_t*>(p);
   h.feat = reinterpret_cast<__half*>(feat);
   const int groups = (d.n + h.imgs - 1) / h.imgs;
-  if (int e = launch_pdl(head_k(d.act), groups * h.nce, 256, h.s_bar + 64, st, "head_pool launch", tx, h)) return e;
+  // one CTA per SM at most (persistent over image groups)
+  const int grid = std::min(groups * h.nce, std::max(h.nce, kNumSMs));
+  if (int e = launch_pdl(head_k(d.act), grid, kHeadThreads, h.s_bar + 128, st, "head_pool launch", tx, h)) return e;
   f.w2 = reinterpret_cast<const uint8_t*>(p) + P.w1_bytes;
+  if (P.fc_gemm) {
+    GemmEpi ep;
+    ep.bias = reinterpret_cast<const float*>(f.w2);
+    return gemm_run(feat, d.n, h.E, h.E, f.w2 + align_up(h.M * 4, 128), h.M, h.E, z, h.M, ep, st);
+  }
   f.z = reinterpret_cast<__half*>(z);
   const int rows = (d.n + 127) / 128;
   return launch_pdl(head_fc_kernel, rows * f.N, 128, f.s_bar + 256, st, "head_fc launch", tf, f);
 }
 int head_init() {
+  if (int e = gemm_init()) return e;
   for (int act : {kRelu, kSilu, kGelu, kIdentity})
     if (int e = check_cuda(cudaFuncSetAttribute(head_k(act), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMaxH),
                            "cudaFuncSetAttribute(head)"))

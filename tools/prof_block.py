@@ -20,7 +20,7 @@ CASES = {
     "nano_s3b0": (ConvFirst(8, 6, 2), TensorDims(128, 56, 56, 48), 64),
     "small_s3b0": (ConvFirst(8, 6, 2), TensorDims(128, 56, 56, 64), 96),
     "stem": (Stem(16), TensorDims(128, 224, 224, 3), None),
-    "head": (Head(), TensorDims(128, 7, 7, 128), None),
+    "head": (Head(1280, 1000), TensorDims(128, 7, 7, 128), None),
     "cnx": (ConvNeXtBlock(), TensorDims(8, 56, 56, 96), None),
     "mbc2": (MBConv(1, 4, 0.25), TensorDims(128, 28, 28, 80), None),
     # ConvNeXt-T units at b128
