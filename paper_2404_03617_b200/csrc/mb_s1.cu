@@ -920,11 +920,14 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       const int gq = blk * 2 * nch + qq;
       const int s = gq & 3, u = gq >> 2, j = qq >> 1, half = qq & 1;
       mbar_wait(&B.pa_full[s], u & 1);
-      uint8_t* slot = s_h1 + s * a.slot_bytes;
+      // the gate scales W_prj's rows instead of h2: Z = h2 (diag(g) W_prj) touches the
+      // slot's W half (4 K-core columns of C 16-byte units: 8 KB at C = 128) instead of
+      // NT x 8 KB of h2 — half the shared-memory traffic of the gating pass
+      uint8_t* slot = s_h1 + s * a.slot_bytes + NT * 8192;
 #pragma unroll
-      for (int k = 0; k < NT * 2; ++k) {
-        const int id = tid + k * 256;  // 16-byte row (NT x 512 of them): tile, group gg of the half, row
-        const int gg = (id >> 7) & 3;
+      for (int k = 0; k < 4 * C / 256; ++k) {
+        const int id = tid + k * 256;  // 16-byte unit: K-core column gg (8 hidden channels), output row
+        const int gg = id / C;
         uint8_t* p = slot + id * 16;
         uint4 hv = lds128(p);
         const uint4 gv = *reinterpret_cast<const uint4*>(s_gate + j * (kHC / 2) + (half * 4 + gg) * 4);
