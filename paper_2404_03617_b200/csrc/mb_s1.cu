@@ -51,6 +51,7 @@ struct Mb1Args {
   int n, H, W, C, hid, sq, nch, NT;
   int K;  // output channels (C for stride 1; stride 2: 64 or 128)
   int s_x, s_h1, s_h1_bytes, s_w, s_wex, s_hdr, s_se, s_bar, smem;
+  int hdr_stride;
   int s_h2;  // P = 8: the block's whole h2 (compact 64-row chunks) stays in shared memory
   int o_bexp, o_bconv, o_bprj, hdr_bytes;  // header (fp32) in the packed blob
   int64_t o_se, o_frag, o_wexp, o_wprj;    // packed-blob sections
@@ -70,7 +71,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kProd = 0, kMma = 1, kE0 = 2, kC0 = 10;
 constexpr int kHC = 64;  // hidden channels per chunk (8 groups of T = 8)
 struct Bars {
-  uint64_t x_full, hdr_full;
+  uint64_t x_full, hdr_full[2];  // hdr double-buffered: block b + 1's header lands during block b
   uint64_t w_full[2], w_empty[2];
   uint64_t e_full[2], e_empty[2];
   uint64_t h1_full[2], h1_empty[2];
@@ -174,7 +175,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
   uint8_t* s_x = smem + a.s_x;
   uint8_t* s_h1 = smem + a.s_h1;   // 2 buffers x 8 group planes; phase C ring overlays s_h1 .. s_w end
   uint8_t* s_w = smem + a.s_w;     // W_exp ring, 2 x (64 x C fp16)
-  uint8_t* s_hdr = smem + a.s_hdr;
+  uint8_t* s_hdr0 = smem + a.s_hdr;  // two header buffers of a.hdr_stride bytes
+  auto hdr_of = [&](int blk) -> uint8_t* { return s_hdr0 + (blk & 1) * a.hdr_stride; };
   uint8_t* s_se = smem + a.s_se;   // pool f32[hid] | gates h2[hid/2] | scratch f32[256 + 32]
   uint8_t* s_wex = smem + a.s_wex; // W_ex (sq x hid fp16), prefetched for the excite
   Bars& B = *reinterpret_cast<Bars*>(smem + a.s_bar);
@@ -186,7 +188,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&B.x_full, 1);
-    mbar_init(&B.hdr_full, 1);
+    mbar_init(&B.hdr_full[0], 1);
+    mbar_init(&B.hdr_full[1], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&B.w_full[i], 1);
       mbar_init(&B.w_empty[i], 1);
@@ -228,11 +231,23 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       prefetch_tmap(&tmap_x);
       const uint32_t wbytes = kHC * C * 2, vbytes = C * 32 * 2;
       const uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
+      auto load_hdr = [&](int b) {
+        mbar_arrive_expect_tx(&B.hdr_full[b & 1], a.hdr_bytes);
+        bulk_g2s(hdr_of(b), wp_of(b), a.hdr_bytes, &B.hdr_full[b & 1]);
+      };
+      auto load_wexp = [&](int b, int j) {
+        const int g = b * nch + j, wb = g & 1, u = g >> 1;
+        mbar_wait(&B.w_empty[wb], (u & 1) ^ 1);
+        mbar_arrive_expect_tx(&B.w_full[wb], wbytes);
+        bulk_g2s(s_w + wb * wbytes, wp_of(b) + a.o_wexp + (size_t)j * wbytes, wbytes, &B.w_full[wb]);
+      };
+      int pre = 0;  // W_exp chunks of this block already issued during the previous one
+      load_hdr(0);
       for (int blk = 0; blk < nblk; ++blk) {
         const uint8_t* wp = wp_of(blk);
-        if (blk > 0) mbar_wait(&B.d_done, (blk - 1) & 1);  // previous block's phase D done: hdr, W_ex, x free
-        mbar_arrive_expect_tx(&B.hdr_full, a.hdr_bytes);
-        bulk_g2s(s_hdr, wp, a.hdr_bytes, &B.hdr_full);
+        if (blk > 0) mbar_wait(&B.d_done, (blk - 1) & 1);  // previous block's phase D done: W_ex, x free
+        // the other header buffer was block blk - 1's: free after its phase D
+        if (blk + 1 < nblk) load_hdr(blk + 1);
         if (blk == 0) {
           mbar_arrive_expect_tx(&B.x_full, P == 8 ? KH * ((H + 1) / 2) * 2048 : KH * 64 * 2 * P * H);
           if constexpr (P == 8) {
@@ -247,12 +262,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         }
         mbar_arrive_expect_tx(&B.se_full, a.sq * a.hid * 2);
         bulk_g2s(s_wex, wp + a.o_se + a.o_wex, a.sq * a.hid * 2, &B.se_full);
-        for (int j = 0; j < nch; ++j) {
-          const int g = blk * nch + j, b = g & 1, u = g >> 1;
-          mbar_wait(&B.w_empty[b], (u & 1) ^ 1);
-          mbar_arrive_expect_tx(&B.w_full[b], wbytes);
-          bulk_g2s(s_w + b * wbytes, wp + a.o_wexp + (size_t)j * wbytes, wbytes, &B.w_full[b]);
-        }
+        for (int j = pre; j < nch; ++j) load_wexp(blk, j);
+        pre = 0;
         // phase C: h2 chunks come back once phase A stored them all and released
         // the h1 / W_exp buffers the ring overlays
         // ring of 4 half-chunks (32 hidden channels: NT x 8 KB of h2 + the
@@ -301,6 +312,15 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           bulk_g2s(slot + NT * 8192, wp + a.o_wprj + (size_t)j * 2 * vbytes + half * vbytes, vbytes,
                    &B.pa_full[s]);
         }
+        }
+        if (blk + 1 < nblk) {
+          // the next block's first W_exp chunks go into the W ring as soon as the
+          // phase C ring overlaying it is consumed (its last projection MMAs
+          // committed), not after phase D: the next expand starts at d_done
+          const int gl = P == 8 ? blk * nch + nch - 1 : blk * 2 * nch + 2 * nch - 1;
+          mbar_wait(&B.pa_empty[gl & 3], (gl >> 2) & 1);
+          pre = nch < 2 ? nch : 2;
+          for (int j = 0; j < pre; ++j) load_wexp(blk + 1, j);
         }
       }
     }
@@ -399,8 +419,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
   } else if (warp < kC0) {
     // ---------------------------------------------- E warps: expand epilogue
     const int e = warp - kE0, q = warp & 3, hh = e >> 2;  // TMEM lane quadrant = warp % 4
-    const float* s_bexp = reinterpret_cast<const float*>(s_hdr + a.o_bexp);
-    const float* s_bprj = reinterpret_cast<const float*>(s_hdr + a.o_bprj);
+    const float* s_bexp = nullptr;
+    const float* s_bprj = nullptr;
     for (int blk = 0; blk < nblk; ++blk) {
       // squeeze partials, chunk by chunk as the conv warps pool them (the E
       // warps idle while the conv runs): thread (warp e, lane o) accumulates
@@ -430,7 +450,9 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
         wq = wq_next;
         if (jj + 2 < nch) wq_next = ldg_pinned(wsqt + (size_t)lane * a.hid + (jj + 2) * kHC + e * 8);
       };
-      mbar_wait(&B.hdr_full, blk & 1);
+      mbar_wait(&B.hdr_full[blk & 1], (blk >> 1) & 1);
+      s_bexp = reinterpret_cast<const float*>(hdr_of(blk) + a.o_bexp);
+      s_bprj = reinterpret_cast<const float*>(hdr_of(blk) + a.o_bprj);
       for (int j = 0; j < nch; ++j) {
         const int g2 = blk * nch + j, b = g2 & 1, u = g2 >> 1;
         mbar_wait(&B.e_full[b], u & 1);
@@ -603,7 +625,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     const int tid = threadIdx.x - kC0 * 32;
     const int gid = lane >> 2, tq = lane & 3;
     const int sq = a.sq, hid = a.hid;
-    const float* s_bconv = reinterpret_cast<const float*>(s_hdr + a.o_bconv);
+    const float* s_bconv = nullptr;
     const uint32_t lrow = (lane & 15), lsel = lane >> 4;  // ldmatrix: row of the fragment, which fragment
     uint8_t* h2img = a.h2 + (size_t)img * nch * NT * 16384;
     const __half2 one2 = __float2half2_rn(1.f), zero2 = __float2half2_rn(0.f);
@@ -618,7 +640,8 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
     uint32_t bw[9];
 #pragma unroll
     for (int tp = 0; tp < 9; ++tp) bw[tp] = __ldg(frag + ((size_t)(0 * 8 + g) * 9 + tp) * 32 + lane);
-    mbar_wait(&B.hdr_full, blk & 1);
+    mbar_wait(&B.hdr_full[blk & 1], (blk >> 1) & 1);
+    s_bconv = reinterpret_cast<const float*>(hdr_of(blk) + a.o_bconv);
     // excite biases of this thread's first gate pair, needed after phase A
     const float2 bex_pre = tid < hid / 2 ? __ldg(reinterpret_cast<const float2*>(wp + a.o_se + a.o_bex) + tid)
                                          : make_float2(0.f, 0.f);
@@ -1017,7 +1040,8 @@ bool mb1_plan(const wl_block_desc& d, Mb1Args& a) {
   a.o_bprj = 2 * hid * 4;
   a.hdr_bytes = align_up(2 * hid * 4 + a.K * 4, 16);
   a.s_hdr = align_up(o, 128);
-  o = a.s_hdr + a.hdr_bytes;
+  a.hdr_stride = align_up(a.hdr_bytes, 128);
+  o = a.s_hdr + 2 * a.hdr_stride;
   a.s_se = align_up(o, 128);
   o = a.s_se + hid * 4 + hid * 2 + (256 + 32) * 4;
   a.s_wex = align_up(o, 128);
