@@ -74,3 +74,17 @@ def test_layer_wise_block_module_graph_equals_eager():
     assert torch.equal(out, eager)
     fused = FusedBlock(MBConv(8, 4, 0.25), dims, weights=blk.weights)
     close(eager.float().cpu().numpy(), fused(x).float().cpu().numpy())
+
+
+@pytest.mark.parametrize("argv", [
+    ["--block", "convfirst", "--channels", "32", "--expansion", "6", "--size", "28x28", "--batch", "2", "--time", "5"],
+    ["--block", "mbconv", "--channels", "128", "--size", "14x14", "--batch", "4", "--time", "5"],
+    ["--block", "ffn", "--channels", "96", "--size", "7x7", "--batch", "2"],
+])
+def test_simulate_b200_fused_vs_layer_wise(argv, capsys):
+    """The reference's simulate check with both schedules on the device."""
+    from paper_2404_03617_b200 import simulate
+
+    assert simulate.main(argv) == simulate.EXIT_OK
+    out = capsys.readouterr().out
+    assert "layerwise" in out and "blockfusion" in out and "relative error" in out

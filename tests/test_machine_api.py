@@ -62,3 +62,15 @@ def test_microbatch_plan_reference_example():
     dev = DeviceSpec("a5000", 76.7e12, 479.375e9, l2_bytes=6 * 2**20)
     plan = microbatch_plan(StageSpec(MBConv(8, 4, 0.25), 10, 128), TensorDims(128, 16, 16, 128), dev)
     assert plan.feasible and plan.micro_batch == 22 and plan.weights_bytes == 3_358_720
+
+
+def test_simulate_without_gpu_is_a_usage_error(capsys):
+    """The B200 simulate leg (reference cli.py:283-325) has no CPU path."""
+    import torch
+
+    from paper_2404_03617_b200 import simulate
+
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only behaviour")
+    assert simulate.main(["--block", "convfirst", "--channels", "16"]) == simulate.EXIT_USAGE
+    assert "no CPU path" in capsys.readouterr().err
