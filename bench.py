@@ -181,6 +181,12 @@ def run_gpu(args):
 
     B = args.batch
     net = _net(args.model)
+    # pinned host batches for the e2e leg, allocated before anything else: pinned
+    # buffers allocated late in a process (after the model, its graph and the
+    # timed loop) copy at 37-43 GB/s instead of 55 GB/s on these boxes
+    # (tools/probe_h2d_alloc.py) — a serving process pins its staging buffers at start-up
+    in_shape = (B, *net.input_resolution, 3)
+    host_x = [torch.empty(in_shape, dtype=torch.float16, pin_memory=True) for _ in range(2)]
     model = FusedNetwork(net, batch=B, seed=1234)
     gen = torch.Generator(device="cuda").manual_seed(rank)
     model.x.normal_(generator=gen)
@@ -214,7 +220,8 @@ def run_gpu(args):
     # ---- end to end through the public API: pinned host batches -> logits on
     # host (FusedNetwork.run_host_batches: every step's H2D copy and D2H read
     # are inside the timed region; step i+1's copy overlaps step i's forward)
-    host_x = [torch.empty(model.x.shape, dtype=torch.float16, pin_memory=True) for _ in range(2)]
+    if tuple(host_x[0].shape) != tuple(model.x.shape):
+        host_x = [torch.empty(model.x.shape, dtype=torch.float16, pin_memory=True) for _ in range(2)]
     for hx in host_x:
         hx.copy_(model.x.cpu())
     host_out = [torch.empty(model.output.shape, dtype=torch.float16, pin_memory=True) for _ in range(2)]

@@ -1,0 +1,43 @@
+"""H2D bandwidth of pinned buffers allocated early (process start) vs late
+(after the model, its graph and the device-timed loop), same process."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2404_03617_b200.scheduler import FusedNetwork  # noqa: E402
+
+n = 128 * 224 * 224 * 3
+early = [torch.empty(n, dtype=torch.float16, pin_memory=True) for _ in range(2)]
+dev = torch.empty(n, dtype=torch.float16, device="cuda")
+
+
+def bw(bufs, reps=40):
+    for b in bufs:
+        dev.copy_(b, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(reps):
+        dev.copy_(bufs[i % 2], non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    return n * 2 * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+print(f"early, at start: {bw(early):.1f} GB/s")
+m = FusedNetwork(bench._net("convfirstnet-pico"), batch=128, seed=1)
+m.x.normal_()
+g = m.capture()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(20):
+    flush.fill_(1)
+    g.replay()
+torch.cuda.synchronize()
+late = [torch.empty(n, dtype=torch.float16, pin_memory=True) for _ in range(2)]
+for b in late:
+    b.copy_(m.x.reshape(-1).cpu())
+for k in range(3):
+    print(f"round {k}: early {bw(early):.1f} GB/s   late {bw(late):.1f} GB/s")
