@@ -66,6 +66,11 @@ CASES = [
     ("convfirst_s2_56", ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 32), 48),
     ("mbconv_14", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 128), None),
     ("mbconv_7_odd_batch", MBConv(8, 4, 0.25), TensorDims(3, 7, 7, 128), None),
+    # the pitch-8 7x7 path at other widths / activations, and a hidden width it
+    # does not take (6 chunks: the block-diagonal kernel runs it)
+    ("mbconv_7_c64", MBConv(8, 4, 0.25), TensorDims(3, 7, 7, 64), None),
+    ("mbconv_7_c128_a2_relu", MBConv(8, 2, 0.25, 1, "relu"), TensorDims(2, 7, 7, 128), None),
+    ("mbconv_7_hid384_fallback", MBConv(8, 3, 0.25), TensorDims(2, 7, 7, 128), None),
     ("mbconv_c2_config_shape", MBConv(1, 4, 0.25), TensorDims(4, 28, 28, 80), None),
     ("mbconv_small_c256", MBConv(8, 4, 0.25), TensorDims(2, 14, 14, 256), None),
     ("mbconv_s2_28", MBConv(8, 4, 0.25, 2), TensorDims(2, 28, 28, 48), 128),
