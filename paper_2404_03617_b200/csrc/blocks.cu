@@ -62,7 +62,7 @@ int kernel_launches(const wl_block_desc& d) {
       d.kind == WL_KIND_LN_HEAD)
     return 2;
   if (d.kind == WL_KIND_FFN) return ffn_launches(d);
-  if (cnx_wide(d)) return 1 + ffn_launches(d);
+  if (cnx_wide(d) || cf_wide(d)) return 1 + ffn_launches(d);
   if (d.kind == WL_KIND_MBCONV) return mb_kernel_launches(d);
   return 1;
 }

@@ -568,6 +568,7 @@ int cf_validate(const wl_block_desc& d) {
   if (d.act < 0 || d.act > 4) return set_error(WL_EINVAL, "unknown activation");
   if (d.stride == 2) return kCf2Family.validate(d);
   if (cnx_wide(d)) return cnx_wide_validate(d);
+  if (cf_wide(d)) return cf_wide_validate(d);
   if (d.act != kRelu && d.act != kSilu && d.act != kGelu)
     return set_error(WL_EUNSUPPORTED, "fused conv-first block supports relu/silu/gelu");
   const bool t8 = d.group_width == 8 && d.ksize == 3 && d.norm == WL_NORM_NONE;
@@ -609,6 +610,7 @@ int64_t cf_weight_numel(const wl_block_desc& d, int i) {
 int64_t cf_packed_bytes(const wl_block_desc& d) {
   if (d.stride == 2) return kCf2Family.packed_bytes(d);
   if (cnx_wide(d)) return cnx_wide_pb(d);
+  if (cf_wide(d)) return cf_wide_pb(d);
   CfPlan p;
   cf_plan(d, p);
   return (int64_t)p.hdr_bytes + (int64_t)p.nchunks * p.chunk_bytes;
@@ -617,6 +619,7 @@ int64_t cf_packed_bytes(const wl_block_desc& d) {
 int cf_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
   if (d.stride == 2) return kCf2Family.pack(d, w, out);
   if (cnx_wide(d)) return cnx_wide_pack(d, w, out);
+  if (cf_wide(d)) return cf_wide_pack(d, w, out);
   CfPlan p;
   cf_plan(d, p);
   memset(out, 0, (size_t)cf_packed_bytes(d));
@@ -672,12 +675,14 @@ int cf_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
 int64_t cf_workspace(const wl_block_desc& d) {
   if (d.stride == 2) return kCf2Family.workspace_bytes(d);
   if (cnx_wide(d)) return cnx_wide_ws(d);
+  if (cf_wide(d)) return cf_wide_ws(d);
   return 0;
 }
 
 int cf_forward(const wl_block_desc& d, const void* x, const void* packed, void* z, void* ws, cudaStream_t st) {
   if (d.stride == 2) return kCf2Family.forward(d, x, packed, z, ws, st);
   if (cnx_wide(d)) return cnx_wide_fwd(d, x, packed, z, ws, st);
+  if (cf_wide(d)) return cf_wide_fwd(d, x, packed, z, ws, st);
   CfPlan p;
   cf_plan(d, p);
   cf_register();

@@ -598,6 +598,78 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
                   reinterpret_cast<__half*>(z), hb, L.o_img < L.total ? pk + L.o_img : nullptr, st, d.dtype);
 }
 
+// ------------------------------------------------------- wide ConvFirst (no LayerNorm)
+// The reference's channel-partitioned schedule (machine.py:528-569) lets the
+// partial hidden sums meet in the GLOBAL tier; past one CTA's TMEM (C > 128)
+// the block runs as: grouped k x k conv + b_conv (CUDA cores, layerwise.cu) ->
+// xc (workspace) -> z = x + b + phi(xc U + a) V through the FFN rows (two
+// tcgen05 GEMMs per L2-sized row batch).
+// weights: w_conv (C,k,k,T), b_conv (C), u (C,hid), a (hid), v (hid,C), b (C)
+namespace {
+struct CfWideLayout {
+  int64_t o_conv, o_bconv, o_a, o_b, o_u, o_v, total;
+};
+CfWideLayout cf_wide_layout(const wl_block_desc& d) {
+  const int64_t C = d.c, hid = (int64_t)d.expansion * d.c, taps = (int64_t)d.ksize * d.ksize;
+  CfWideLayout L;
+  L.o_conv = 0;
+  L.o_bconv = a128(C * taps * d.group_width * 4);
+  L.o_a = L.o_bconv + a128(C * 4 + 64);
+  L.o_b = L.o_a + a128(hid * 4 + 64);
+  L.o_u = L.o_b + a128(C * 4 + 64);
+  L.o_v = L.o_u + a128(hid * C * 2);
+  L.total = L.o_v + a128(hid * C * 2);
+  return L;
+}
+}  // namespace
+
+bool cf_wide(const wl_block_desc& d) {
+  return d.kind == WL_KIND_CONVFIRST && d.norm == WL_NORM_NONE && d.stride == 1 && d.c > 128;
+}
+int cf_wide_validate(const wl_block_desc& d) {
+  if (int e = common_dims(d)) return e;
+  if (d.dtype != WL_DTYPE_F16) return set_error(WL_EUNSUPPORTED, "wide conv-first block: fp16");
+  if (d.c % 8) return set_error(WL_EUNSUPPORTED, "wide conv-first block: C %% 8 == 0");
+  if (d.group_width != 8 && d.group_width != 1)
+    return set_error(WL_EUNSUPPORTED, "wide conv-first block: T = 8 or 1 (got %d)", d.group_width);
+  if (d.ksize != 3 && !(d.ksize == 7 && d.group_width == 1))
+    return set_error(WL_EUNSUPPORTED, "wide conv-first block: 3x3, or 7x7 depthwise");
+  if (d.act != kRelu && d.act != kSilu && d.act != kGelu)
+    return set_error(WL_EUNSUPPORTED, "wide conv-first block supports relu/silu/gelu");
+  return WL_OK;
+}
+int64_t cf_wide_pb(const wl_block_desc& d) { return cf_wide_layout(d).total; }
+int cf_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out) {
+  const CfWideLayout L = cf_wide_layout(d);
+  const int C = d.c, hid = d.expansion * d.c;
+  memset(out, 0, (size_t)L.total);
+  put_f32(out, L.o_conv, w[0], (int64_t)C * d.ksize * d.ksize * d.group_width);
+  put_f32(out, L.o_bconv, w[1], C);
+  put_f32(out, L.o_a, w[3], hid);
+  put_f32(out, L.o_b, w[5], C);
+  put_t16(out, L.o_u, w[2], C, hid, d.dtype);
+  put_t16(out, L.o_v, w[4], hid, C, d.dtype);
+  return WL_OK;
+}
+int64_t cf_wide_ws(const wl_block_desc& d) {
+  const int64_t M = (int64_t)d.n * d.h * d.w, hid = (int64_t)d.expansion * d.c;
+  return kWsHdr + a128(M * d.c * 2) + a128(hidden_rows(M, (int)hid) * hid * 2);
+}
+int cf_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st) {
+  const CfWideLayout L = cf_wide_layout(d);
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(p);
+  const int64_t M = (int64_t)d.n * d.h * d.w;
+  __half* xc = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
+  __half* hb = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr + a128(M * d.c * 2));
+  if (int e = lw_gconv(d, d.c, reinterpret_cast<const __half*>(x), reinterpret_cast<const float*>(pk + L.o_conv),
+                       reinterpret_cast<const float*>(pk + L.o_bconv), xc, kIdentity, st))
+    return e;
+  return ffn_rows(xc, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
+                  reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
+                  reinterpret_cast<const float*>(pk + L.o_b), d.act, reinterpret_cast<const __half*>(x),
+                  reinterpret_cast<__half*>(z), hb, nullptr, st, d.dtype);
+}
+
 namespace {
 // ------------------------------------------------------- patchify stem
 // desc: c = input channels, k = output channels, ksize = patch = stride

@@ -88,6 +88,16 @@ int64_t cnx_wide_pb(const wl_block_desc& d);
 int cnx_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out);
 int64_t cnx_wide_ws(const wl_block_desc& d);
 int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st);
+// wide conv-first blocks without LayerNorm (C > 128, beyond the fused kernel's TMEM
+// plan): grouped conv kernel -> xc in the workspace, then the FFN rows (cnx.cu)
+bool cf_wide(const wl_block_desc& d);
+int cf_wide_validate(const wl_block_desc& d);
+int64_t cf_wide_pb(const wl_block_desc& d);
+int cf_wide_pack(const wl_block_desc& d, const float* const* w, uint8_t* out);
+int64_t cf_wide_ws(const wl_block_desc& d);
+int cf_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, void* ws, cudaStream_t st);
+int lw_gconv(const wl_block_desc& d, int C, const void* x, const float* w, const float* b, void* y, int act,
+             cudaStream_t st);  // fp16 x / y
 int ffn_row_batches(const wl_block_desc& d);
 int ffn_launches(const wl_block_desc& d);
 // fused FFN (ffn.cu): hidden kept on chip

@@ -367,6 +367,12 @@ int lw_init() {
 }
 }  // namespace
 
+// the grouped conv on its own (the wide ConvFirst route, cnx.cu: cf_wide_fwd)
+int lw_gconv(const wl_block_desc& d, int C, const void* x, const float* w, const float* b, void* y, int act,
+             cudaStream_t st) {
+  return gconv_run(d, C, reinterpret_cast<const __half*>(x), w, b, reinterpret_cast<__half*>(y), act, st);
+}
+
 int lw_launches(const wl_block_desc& d) {
   if (d.kind == WL_KIND_MBCONV) return 5;
   return d.kind == WL_KIND_CONVFIRST ? 3 : 2;

@@ -176,3 +176,17 @@ def test_layer_wise_refuses_what_the_reference_does_not_schedule():
     d = _desc(ConvFirst(8, 6), TensorDims(2, 28, 28, 48))
     d.scheme = 7
     assert L.wl_validate(ctypes.byref(d)) == _lib.lib().wl_validate(ctypes.byref(d)) != 0
+
+
+def test_wide_convfirst_descriptors_without_gpu():
+    """Conv-first blocks past the fused kernel's width (C > 128) validate and
+    plan three launches: grouped conv + two FFN GEMMs."""
+    L = _lib.lib()
+    for blk, dims in ((ConvFirst(8, 6), TensorDims(2, 28, 28, 192)), (ConvFirst(1, 4), TensorDims(2, 14, 14, 384))):
+        s = build_schedule(blk, dims)
+        d = block_descriptor(blk, dims, s.out_channels)
+        assert L.wl_validate(ctypes.byref(d)) == 0
+        assert L.wl_kernel_launches(ctypes.byref(d)) == 3
+        ins = random_inputs(s, np.random.default_rng(0))
+        a = _lib.pack_weights(d, [ins[n] for n in weight_names(s)])
+        assert a.nbytes == L.wl_packed_bytes(ctypes.byref(d)) and a.any()

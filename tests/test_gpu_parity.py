@@ -99,6 +99,10 @@ CASES = [
     ("mbconv_s2_32_c64_bands", MBConv(8, 4, 0.25, 2), TensorDims(2, 32, 32, 64), 160),
     ("mbconv_16_c256_bands", MBConv(8, 4, 0.25), TensorDims(2, 16, 16, 256), None),
     ("mbconv_8x8_c256_one_image", MBConv(8, 4, 0.25), TensorDims(2, 8, 8, 256), None),
+    # wide conv-first blocks (C > 128, no LayerNorm): grouped conv kernel + FFN rows
+    ("convfirst_wide_c192", ConvFirst(8, 6), TensorDims(2, 28, 28, 192), None),
+    ("convfirst_wide_c256_silu", ConvFirst(8, 4, 1, "silu"), TensorDims(3, 14, 14, 256), None),
+    ("convfirst_wide_c384_dw", ConvFirst(1, 4), TensorDims(2, 14, 14, 384), None),
     # ConvFirstNet-Small s3b0: FFN weights streamed through a chunk ring
     ("convfirst_s2_64_96_streamed", ConvFirst(8, 6, 2), TensorDims(2, 56, 56, 64), 96),
 ]
