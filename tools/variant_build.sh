@@ -1,0 +1,16 @@
+#!/bin/bash
+# Build build/var_<name>/libwlfuse.so with ONE csrc file replaced by a sed-edited copy
+# (timing experiments: WLFUSE_LIB_AB=build/var_<name>/libwlfuse.so python tools/prof_block.py ...)
+# usage: tools/variant_build.sh NAME FILE.cu 'sed-expr' ['sed-expr' ...]
+set -e
+cd "$(dirname "$0")/.."
+name=$1; file=$2; shift 2
+out=build/var_$name; mkdir -p $out
+args=(); for e in "$@"; do args+=(-e "$e"); done
+sed "${args[@]}" paper_2404_03617_b200/csrc/$file > paper_2404_03617_b200/csrc/_var_$file
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+  --expt-relaxed-constexpr -Iinclude -Ipaper_2404_03617_b200/csrc -c paper_2404_03617_b200/csrc/_var_$file -o $out/var.o
+rm -f paper_2404_03617_b200/csrc/_var_$file
+objs=$(ls build/obj/*.o | grep -v "/$(basename $file .cu).o$")
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libwlfuse.so $objs $out/var.o -lcuda
+echo built $out/libwlfuse.so
