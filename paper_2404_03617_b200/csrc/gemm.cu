@@ -326,10 +326,11 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
 }
 
 // =================================================================== host
-static int pick_bn(int N, int tiles_m) {
+static int pick_bn(int N, int tiles_m, bool whole_rows) {
   // few row tiles (e.g. the classifier, M = batch): 64-column tiles spread the
   // output over more SMs — each CTA's time is its A stream, not its N width
-  if (tiles_m * ((N + 255) / 256) < kNumSMs / 2) return N <= 64 ? align_up(N, 16) : 64;
+  // (not with the row-LayerNorm epilogue, which needs whole rows in one tile)
+  if (!whole_rows && tiles_m * ((N + 255) / 256) < kNumSMs / 2) return N <= 64 ? align_up(N, 16) : 64;
   if (N <= 256) return align_up(N, 16);
   int best = 256, waste = 1 << 30;
   for (int bn : {256, 192, 128}) {
@@ -351,7 +352,7 @@ int gemm_run(const void* A, int M, int K, int lda, const void* Bw, int N, int ld
   memset(&a, 0, sizeof(a));
   a.M = M;
   a.N = N;
-  a.BN = pick_bn(N, (M + 127) / 128);
+  a.BN = pick_bn(N, (M + 127) / 128, e.ln_g != nullptr);
   if (e.ln_g && (a.BN < N || N > 128 || e.act))
     return set_error(WL_EUNSUPPORTED, "gemm: the row-LayerNorm epilogue needs N <= 128 and no activation (N = %d)", N);
   a.tiles_m = (M + 127) / 128;
