@@ -41,3 +41,29 @@ for b in late:
     b.copy_(m.x.reshape(-1).cpu())
 for k in range(3):
     print(f"round {k}: early {bw(early):.1f} GB/s   late {bw(late):.1f} GB/s")
+
+# the same late buffers copied as two halves on two streams (two copy engines)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def bw2(bufs, reps=40):
+    half = n // 2
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in (s1, s2):
+        s.wait_event(e0)
+    for i in range(reps):
+        with torch.cuda.stream(s1):
+            dev[:half].copy_(bufs[i % 2][:half], non_blocking=True)
+        with torch.cuda.stream(s2):
+            dev[half:].copy_(bufs[i % 2][half:], non_blocking=True)
+    for s in (s1, s2):
+        torch.cuda.current_stream().wait_stream(s)
+    e1.record()
+    e1.synchronize()
+    return n * 2 * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+for k in range(3):
+    print(f"two streams {k}: early {bw2(early):.1f} GB/s   late {bw2(late):.1f} GB/s   late 1-stream {bw(late):.1f}")
