@@ -543,7 +543,10 @@ bool cf2_plan(const wl_block_desc& d, Cf2Args& a) {
   double best = 1e30;
   Cf2Args bestA{};
   // planner experiments: WL_CF2_R pins the band height (read once per process)
-  static const char* force_r = getenv("WL_CF2_R");
+  static const char* force_r = [] {
+    const char* e = getenv("WL_CF2_R");
+    return e && *e ? e : nullptr;  // empty = unset
+  }();
   for (int R = 1; R <= 8; ++R) {
     if (R > a.Ho) break;
     // measured: bands wider than 256 pixels lengthen each band's chain, and odd
