@@ -48,6 +48,7 @@ struct Args {
   __half* z;
   long long* trace;  // debug: CTA 0 clock64 stamps (wl_debug_set_trace)
   int t_z, t_e;  // TMEM column bases
+  int NE;        // E / H buffers in TMEM (3 when C + 3 HC fits: the next-but-one expansion need not wait for a projection)
   uint32_t tmem_cols;
   const float* a;  // hidden bias [hid]
   const float* b;  // output bias [C]
@@ -55,7 +56,7 @@ struct Args {
 struct Bars {
   uint64_t a_full[2], a_free[2], a_used[2], res_full[2];
   uint64_t u_full[16], u_empty[16], v_full[16], v_empty[16];
-  uint64_t e_full[2], h_full[2], p_done[2];
+  uint64_t e_full[3], h_full[3], p_done[3];
   uint64_t z_full, z_empty;
   uint32_t tmem_base;
 };
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
       mbar_init(&B.v_full[s], 1);
       mbar_init(&B.v_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       mbar_init(&B.e_full[i], 1);
       mbar_init(&B.h_full[i], kEpiWarps);
       mbar_init(&B.p_done[i], 1);
@@ -224,8 +225,8 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
         tc_fence_after();
         const uint32_t sx = sa + xb * a.slabs * 16384;
         auto expand = [&](int j) {
-          const int g = t * nch + j, b = g & 1;
-          if (g >= 2) mbar_wait(&B.p_done[b], ((g - 2) >> 1) & 1);  // H_{g-2} consumed
+          const int NE = a.NE, g = t * nch + j, b = g % NE;
+          if (g >= NE) mbar_wait(&B.p_done[b], ((g - NE) / NE) & 1);  // H_{g-NE} consumed
           FF_TRACE(16 + g * 4 + 0);
           const uint32_t d = tmem + a.t_e + b * HC;
           for (int sl = 0; sl < a.slabs; ++sl, ++useq) {
@@ -246,8 +247,8 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
           if (j == nch - 1) mma_commit(a.direct ? &B.a_free[xb] : &B.a_used[xb]);
         };
         auto project = [&](int j) {
-          const int g = t * nch + j, b = g & 1;
-          mbar_wait(&B.h_full[b], (g >> 1) & 1);
+          const int NE = a.NE, g = t * nch + j, b = g % NE;
+          mbar_wait(&B.h_full[b], (g / NE) & 1);
           if (j == 0 && t > 0) mbar_wait(&B.z_empty, (t - 1) & 1);
           FF_TRACE(16 + g * 4 + 1);
           for (int sl = 0; sl < HC / 64; ++sl, ++vseq) {
@@ -273,11 +274,10 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
           mma_commit(&B.p_done[b]);
           if (j == nch - 1) mma_commit(&B.z_full);
         };
-        expand(0);
-        if (nch > 1) expand(1);
+        for (int j = 0; j < nch && j < a.NE; ++j) expand(j);
         for (int j = 0; j < nch; ++j) {
           project(j);
-          if (j + 2 < nch) expand(j + 2);
+          if (j + a.NE < nch) expand(j + a.NE);
         }
       }
     }
@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
     for (int t = 0; t < my_tiles; ++t) {
       const int tile = blockIdx.x + t * gridDim.x;
       for (int j = 0; j < nch; ++j) {
-        const int g = t * nch + j, b = g & 1;
+        const int g = t * nch + j, b = g % a.NE;
         const float* aj = s_abias + ((j + rot) % nch) * HC + grp * hw;
-        mbar_wait(&B.e_full[b], (g >> 1) & 1);
+        mbar_wait(&B.e_full[b], (g / a.NE) & 1);
         tc_fence_after();
         if (threadIdx.x == 64) FF_TRACE(16 + g * 4 + 2);
         const uint32_t eb = tmem_lane_addr(tmem, q, a.t_e + b * HC + grp * hw);
@@ -444,7 +444,8 @@ bool ffn_fused_plan(int M, int C, int hid, ff::Args& a) {
   a.stage_bytes = 0;
   a.t_z = 0;
   a.t_e = C;
-  const int cols = C + 2 * a.HC;
+  a.NE = C + 3 * a.HC <= 512 ? 3 : 2;
+  const int cols = C + a.NE * a.HC;
   a.tmem_cols = 32;
   while (a.tmem_cols < (uint32_t)cols) a.tmem_cols *= 2;
   return a.tmem_cols <= 512;

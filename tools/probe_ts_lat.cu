@@ -46,13 +46,29 @@ __global__ void k_lat(long long* out, int reps) {
     }
     out[0] = tot / reps;
     stop = 1;
-  } else if (LD && warp >= 4 && warp < 8) {
+  } else if (LD == 1 && warp >= 4 && warp < 8) {
     const int q = warp % 4;
     uint32_t acc = 0;
     while (!stop) {
       uint32_t v[16];
       WL_TMEM_LD16(tmem_lane_addr(tmem, q, 384), v);
       tmem_ld_wait();
+      acc += v[0];
+    }
+    if (acc == 12345) out[1] = acc;
+  } else if (LD == 2 && warp >= 4 && warp < 8) {
+    // the FFN epilogue's pattern: tcgen05.ld 16 columns + tcgen05.st 8 packed columns
+    const int q = warp % 4;
+    uint32_t acc = 0;
+    while (!stop) {
+      uint32_t v[16];
+      WL_TMEM_LD16(tmem_lane_addr(tmem, q, 384), v);
+      tmem_ld_wait();
+      uint32_t o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = v[2 * i] ^ v[2 * i + 1];
+      WL_TMEM_ST8(tmem_lane_addr(tmem, q, 448), o);
+      tmem_st_wait();
       acc += v[0];
     }
     if (acc == 12345) out[1] = acc;
@@ -84,5 +100,8 @@ int main() {
   run<64, 1, 1>();
   run<128, 1, 0>();
   run<128, 1, 1>();
+  run<64, 0, 2>();
+  run<64, 1, 2>();
+  run<128, 1, 2>();
   return 0;
 }
