@@ -270,6 +270,219 @@ int dwln_segments(int N, int H, int RB) {
   return nseg < 1 ? 1 : nseg;
 }
 
+// 7x7 depthwise + LayerNorm for W % 7 == 0 (every ConvNeXt-T stage: 56, 28,
+// 14, 7). Same ring of padded input rows as dwln_kernel, but the block has
+// exactly one item per thread per band step — (output row, 7-pixel group,
+// 8 channels) — so the 56 accumulators stay in registers through the norm:
+//   pixel sums      -> segmented shuffle reduction over the lanes of a pixel
+//                      group; each warp's segment head stores its partial in
+//                      its own slot (no shared atomics: fp32 ones are CAS loops)
+//   mean            -> sum of (v - mean)^2 from the fp32 registers (the
+//                      reference's two-pass variance, no E[x^2] - mean^2)
+//   normalise       -> straight from registers to the output row
+// Three block barriers per step (the ring, the sums, the squares) and no
+// pre-norm round trip through shared memory.
+constexpr int kDw7Px = 7;
+constexpr int kDw7MaxThreads = 384;
+template <typename T, int CT>
+__global__ void __launch_bounds__(kDw7MaxThreads, 1)
+    dwln7_kernel(const T* __restrict__ x, const T* __restrict__ wdw, const float* __restrict__ bdw,
+                 const float* __restrict__ g, const float* __restrict__ be, T* __restrict__ y, int N, int H, int W,
+                 int C_rt, float eps, int RB, int nseg) {
+  constexpr int KS = 7, R = 3, PX = kDw7Px, NI = PX + 2 * R;
+  constexpr bool kF16 = Dt<T>::kIdescAB == 0;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int C = CT ? CT : C_rt;
+  const int C8 = C / 8, WG = W / PX, rowh = W * C;
+  const int NR = 2 * RB + 2 * R, WP = W + 2 * R, prowh = WP * C;
+  // NH: the most warps one pixel group's C8 lanes can span (a compile-time bound when C is)
+  constexpr int kNH = CT ? (CT / 8 + 30) / 32 + 1 : 4;
+  const int npx = RB * W, NH = CT ? kNH : (C8 + 30) / 32 + 1;
+  const float invC = 1.f / (float)C;
+  T* s_in = reinterpret_cast<T*>(dsm);                           // [NR][WP][C]
+  float* s_S = reinterpret_cast<float*>(s_in + (size_t)NR * prowh);  // [RB * W][NH] partial sums
+  float* s_Q = s_S + npx * NH;                                        // [RB * W][NH] partial squares
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+  const int c8 = tid % C8, rest = tid / C8, pg = rest % WG, ry = rest / WG;  // ry >= RB: padding thread
+  // lanes l and l + 2^k hold the same pixel group: the segmented reduction's adds
+  uint32_t seg = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    if (lane + (1 << k) < 32 && (tid + (1 << k)) / C8 == rest) seg |= 1u << k;
+  const bool head = lane == 0 || (tid - 1) / C8 != rest;
+  // the group's lanes span warps w0 .. w0 + nw - 1; this head's slot is warp - w0
+  const int w0 = rest * C8 / 32, nw = (rest * C8 + C8 - 1) / 32 - w0 + 1, hslot = tid / 32 - w0;
+  auto seg_sum = [&](float v) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const float o = __shfl_down_sync(0xffffffffu, v, 1 << k);
+      if (seg >> k & 1) v += o;
+    }
+    return v;
+  };
+  for (int i = tid; i < NR * WP * C8; i += nt) reinterpret_cast<uint4*>(s_in)[i] = make_uint4(0, 0, 0, 0);
+  pdl_wait();
+  __syncthreads();
+  const int SR = (H + nseg - 1) / nseg, per_row = rowh / 8;
+  for (int item = blockIdx.x; item < N * nseg; item += gridDim.x) {
+    const int img = item / nseg, ys = (item % nseg) * SR, ye = min(H, ys + SR);
+    if (ys >= ye) continue;
+    const int base = ys - R;
+    auto load_rows = [&](int lo, int hi) {
+      lo = max(lo, ys - R);
+      hi = min(hi, ye + R);
+      for (int iy = lo; iy < hi; ++iy) {  // row by row: no per-element division
+        T* dst = s_in + (size_t)((iy - base) % NR) * prowh + R * C;
+        if (iy >= 0 && iy < H) {
+          const T* src = x + ((size_t)img * H + iy) * rowh;
+          for (int off = tid; off < per_row; off += nt) cp_async16(dst + off * 8, src + off * 8);
+        } else {
+          for (int off = tid; off < per_row; off += nt) *reinterpret_cast<uint4*>(dst + off * 8) = make_uint4(0, 0, 0, 0);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    load_rows(ys - R, ys + RB + R);
+    for (int y0 = ys; y0 < ye; y0 += RB) {
+      // (the rows this prefetch overwrites were last read by the previous
+      // step's stencil, which every thread finished before its sum barrier)
+      load_rows(y0 + RB + R, y0 + 2 * RB + R);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+      const bool act = ry < min(RB, ye - y0);
+      float acc[PX][8];
+      {
+        float bias[8];
+        ld8f(bdw + c8 * 8, bias);
+#pragma unroll
+        for (int p = 0; p < PX; ++p)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[p][i] = bias[i];
+      }
+      if (act) {
+        __half2 h[PX][4];
+#pragma unroll
+        for (int p = 0; p < PX; ++p)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h[p][i] = __float2half2_rn(0.f);
+        int slot = (y0 + ry - R - base) % NR;
+#pragma unroll
+        for (int dy = 0; dy < KS; ++dy) {
+          const T* row = s_in + (size_t)slot * prowh + (size_t)pg * PX * C + c8 * 8;
+          slot = slot + 1 == NR ? 0 : slot + 1;
+          uint4 in[NI];
+#pragma unroll
+          for (int j = 0; j < NI; ++j) in[j] = lds128(row + (size_t)j * C);
+#pragma unroll
+          for (int dx = 0; dx < KS; ++dx) {
+            const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wdw + (size_t)(dy * KS + dx) * C + c8 * 8));
+            if constexpr (kF16) {
+              const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
+#pragma unroll
+              for (int p = 0; p < PX; ++p) {
+                const __half2* i2 = reinterpret_cast<const __half2*>(&in[p + dx]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[p][i] = __hfma2(i2[i], w2[i], h[p][i]);
+              }
+            } else {
+              float wf[8];
+              unpack8t<T>(wv, wf);
+#pragma unroll
+              for (int p = 0; p < PX; ++p) {
+                float xf[8];
+                unpack8t<T>(in[p + dx], xf);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[p][i] = fmaf(xf[i], wf[i], acc[p][i]);
+              }
+            }
+          }
+          if (kF16 && (dy == R || dy == KS - 1)) {  // widen twice per window (<= 4 rows of taps in half)
+#pragma unroll
+            for (int p = 0; p < PX; ++p)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 f = __half22float2(h[p][i]);
+                acc[p][2 * i] += f.x;
+                acc[p][2 * i + 1] += f.y;
+                h[p][i] = __float2half2_rn(0.f);
+              }
+          }
+        }
+      }
+      const int pix0 = ry * W + pg * PX;
+      // pixel sums (the padding / idle threads add zeros to their own segments)
+#pragma unroll
+      for (int p = 0; p < PX; ++p) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += acc[p][i];
+        s = seg_sum(act ? s : 0.f);
+        if (act && head) s_S[(pix0 + p) * NH + hslot] = s;
+      }
+      __syncthreads();
+      float mean[PX];
+#pragma unroll
+      for (int p = 0; p < PX; ++p) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < kNH; ++k)
+          if (k < nw) t += s_S[(pix0 + p) * NH + k];
+        mean[p] = act ? t * invC : 0.f;
+        float q = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q += (acc[p][i] - mean[p]) * (acc[p][i] - mean[p]);
+        q = seg_sum(act ? q : 0.f);
+        if (act && head) s_Q[(pix0 + p) * NH + hslot] = q;
+      }
+      __syncthreads();
+      if (act) {
+        float gg[8], bb[8];
+        ld8f(g + c8 * 8, gg);
+        ld8f(be + c8 * 8, bb);
+        T* yrow = y + ((size_t)img * H + y0 + ry) * rowh + (size_t)pg * PX * C + c8 * 8;
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          float t = 0.f;
+#pragma unroll
+          for (int k = 0; k < kNH; ++k)
+            if (k < nw) t += s_Q[(pix0 + p) * NH + k];
+          const float rstd = rsqrtf(t * invC + eps);
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = (acc[p][i] - mean[p]) * rstd * gg[i] + bb[i];
+          *reinterpret_cast<uint4*>(yrow + (size_t)p * C) = pack8t<T>(v);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+int dwln7_smem(int W, int C, int RB) { return (2 * RB + 6) * (W + 6) * C * 2 + 2 * RB * W * ((C / 8 + 30) / 32 + 1) * 4; }
+int dwln7_threads(int W, int C, int RB) { return (RB * (W / kDw7Px) * (C / 8) + 31) / 32 * 32; }
+// segments per image: waves of (image, segment) items x (band steps + ~0.75 of
+// a step for the window a segment loads before its first step) — at b128 one
+// segment per image (128 CTAs) beats four ragged ones on 148 SMs
+int dwln7_segments(int N, int H, int RB) {
+  int best = 1;
+  double best_cost = 1e30;
+  for (int nseg = 1; nseg * RB <= H; ++nseg) {
+    const int SR = (H + nseg - 1) / nseg, steps = (SR + RB - 1) / RB;
+    const int waves = (N * nseg + kNumSMs - 1) / kNumSMs;
+    const double cost = waves * (steps + 0.75);
+    if (cost < best_cost - 1e-9) best = nseg, best_cost = cost;
+  }
+  return best;
+}
+// rows per band step for the 7-pixel kernel (0: not eligible)
+int dwln7_rows(int KS, int W, int C) {
+  if (KS != 7 || W % kDw7Px || C % 8) return 0;
+  for (int rb : {4, 3, 2, 1})
+    if (dwln7_threads(W, C, rb) <= kDw7MaxThreads && dwln7_smem(W, C, rb) <= 232448) return rb;
+  return 0;
+}
+
 // LayerNorm per pixel; S2D: the output row is written in 2x2 space-to-depth
 // order A[(img, y/2, x/2)][((y%2) 2 + x%2) C + c]. CTA = P pixels x C/8
 // threads; one 16-byte chunk per thread, two-pass statistics over shared sums.
@@ -569,6 +782,29 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
   __half* xh = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr);
   __half* hb = reinterpret_cast<__half*>((uint8_t*)ws + kWsHdr + a128(M * d.c * 2));
   const float eps = d.ln_eps > 0 ? d.ln_eps : 1e-6f;
+  const int rb7 = dwln7_rows(d.ksize, d.w, d.c);
+  auto dw7 = [&]() {
+    const int nseg = dwln7_segments(d.n, d.h, rb7), grid = std::min(d.n * nseg, kNumSMs);
+    auto run7 = [&](auto kern, auto tag) {
+      using T = decltype(tag);
+      return launch_pdl(kern, grid, dwln7_threads(d.w, d.c, rb7), dwln7_smem(d.w, d.c, rb7), st, "dwln7 launch",
+                        reinterpret_cast<const T*>(x), reinterpret_cast<const T*>(pk + L.o_wdw),
+                        reinterpret_cast<const float*>(pk + L.o_bdw), reinterpret_cast<const float*>(pk + L.o_g),
+                        reinterpret_cast<const float*>(pk + L.o_be), reinterpret_cast<T*>(xh), d.n, d.h, d.w, d.c,
+                        eps, rb7, nseg);
+    };
+    auto pick7 = [&](auto tag) {
+      using T = decltype(tag);
+      switch (d.c) {
+        case 96: return run7(dwln7_kernel<T, 96>, tag);
+        case 192: return run7(dwln7_kernel<T, 192>, tag);
+        case 384: return run7(dwln7_kernel<T, 384>, tag);
+        case 768: return run7(dwln7_kernel<T, 768>, tag);
+      }
+      return run7(dwln7_kernel<T, 0>, tag);
+    };
+    return d.dtype == WL_DTYPE_BF16 ? pick7(__nv_bfloat16{}) : pick7(__half{});
+  };
   const int rb = dwln_rows(d.ksize, d.w, d.c), nseg = dwln_segments(d.n, d.h, rb);
   const int grid = std::min(d.n * nseg, kNumSMs);
   auto run_dw = [&](auto kern, auto tag) {
@@ -590,7 +826,7 @@ int cnx_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, 
     }
     return run_dw(dwln_kernel<7, T, 0>, tag);
   };
-  const int e = d.dtype == WL_DTYPE_BF16 ? pick(__nv_bfloat16{}) : pick(__half{});
+  const int e = rb7 ? dw7() : d.dtype == WL_DTYPE_BF16 ? pick(__nv_bfloat16{}) : pick(__half{});
   if (e) return e;
   return ffn_rows(xh, M, d.c, d.expansion * d.c, d.c, reinterpret_cast<const __half*>(pk + L.o_u),
                   reinterpret_cast<const float*>(pk + L.o_a), reinterpret_cast<const __half*>(pk + L.o_v),
@@ -879,7 +1115,11 @@ int cnx_init() {
                 set(dwln_kernel<7, __half, 192>), set(dwln_kernel<7, __half, 384>), set(dwln_kernel<7, __half, 768>),
                 set(dwln_kernel<3, __nv_bfloat16, 0>), set(dwln_kernel<7, __nv_bfloat16, 0>),
                 set(dwln_kernel<7, __nv_bfloat16, 96>), set(dwln_kernel<7, __nv_bfloat16, 192>),
-                set(dwln_kernel<7, __nv_bfloat16, 384>), set(dwln_kernel<7, __nv_bfloat16, 768>)})
+                set(dwln_kernel<7, __nv_bfloat16, 384>), set(dwln_kernel<7, __nv_bfloat16, 768>),
+                set(dwln7_kernel<__half, 0>), set(dwln7_kernel<__half, 96>), set(dwln7_kernel<__half, 192>),
+                set(dwln7_kernel<__half, 384>), set(dwln7_kernel<__half, 768>), set(dwln7_kernel<__nv_bfloat16, 0>),
+                set(dwln7_kernel<__nv_bfloat16, 96>), set(dwln7_kernel<__nv_bfloat16, 192>),
+                set(dwln7_kernel<__nv_bfloat16, 384>), set(dwln7_kernel<__nv_bfloat16, 768>)})
     if (e) return e;
   return WL_OK;
 }
