@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(kDw7MaxThreads, 1)
   T* s_in = reinterpret_cast<T*>(dsm);                           // [NR][WP][C]
   float* s_S = reinterpret_cast<float*>(s_in + (size_t)NR * prowh);  // [RB * W][NH] partial sums
   float* s_Q = s_S + npx * NH;                                        // [RB * W][NH] partial squares
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_Q + npx * NH);      // [2] ring-row groups (bulk copies)
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
   const int c8 = tid % C8, rest = tid / C8, pg = rest % WG, ry = rest / WG;  // ry >= RB: padding thread
   // lanes l and l + 2^k hold the same pixel group: the segmented reduction's adds
@@ -321,33 +322,46 @@ __global__ void __launch_bounds__(kDw7MaxThreads, 1)
     return v;
   };
   for (int i = tid; i < NR * WP * C8; i += nt) reinterpret_cast<uint4*>(s_in)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
   pdl_wait();
   __syncthreads();
   const int SR = (H + nseg - 1) / nseg, per_row = rowh / 8;
+  uint32_t grp = 0;  // ring-row groups issued so far (group g completes on s_bar[g & 1], phase (g >> 1) & 1)
   for (int item = blockIdx.x; item < N * nseg; item += gridDim.x) {
     const int img = item / nseg, ys = (item % nseg) * SR, ye = min(H, ys + SR);
     if (ys >= ye) continue;
     const int base = ys - R;
+    // one group of ring rows: each image row is one contiguous bulk copy (thread 0);
+    // rows outside the image are zero-filled by the block (ordered by the next barrier)
     auto load_rows = [&](int lo, int hi) {
       lo = max(lo, ys - R);
       hi = min(hi, ye + R);
-      for (int iy = lo; iy < hi; ++iy) {  // row by row: no per-element division
-        T* dst = s_in + (size_t)((iy - base) % NR) * prowh + R * C;
-        if (iy >= 0 && iy < H) {
-          const T* src = x + ((size_t)img * H + iy) * rowh;
-          for (int off = tid; off < per_row; off += nt) cp_async16(dst + off * 8, src + off * 8);
-        } else {
+      const int vlo = max(lo, 0), vhi = min(hi, H);
+      if (tid == 0) {
+        uint64_t* bar = &s_bar[grp & 1];
+        mbar_arrive_expect_tx(bar, vhi > vlo ? (uint32_t)((vhi - vlo) * rowh * (int)sizeof(T)) : 0u);
+        for (int iy = vlo; iy < vhi; ++iy)
+          bulk_g2s(s_in + (size_t)((iy - base) % NR) * prowh + R * C, x + ((size_t)img * H + iy) * rowh,
+                   rowh * (int)sizeof(T), bar);
+      }
+      for (int iy = lo; iy < hi; ++iy)
+        if (iy < 0 || iy >= H) {
+          T* dst = s_in + (size_t)((iy - base) % NR) * prowh + R * C;
           for (int off = tid; off < per_row; off += nt) *reinterpret_cast<uint4*>(dst + off * 8) = make_uint4(0, 0, 0, 0);
         }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
+      ++grp;
     };
     load_rows(ys - R, ys + RB + R);
     for (int y0 = ys; y0 < ye; y0 += RB) {
       // (the rows this prefetch overwrites were last read by the previous
       // step's stencil, which every thread finished before its sum barrier)
+      const uint32_t need = grp - 1;  // the group holding this step's newest rows
       load_rows(y0 + RB + R, y0 + 2 * RB + R);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      mbar_wait(&s_bar[need & 1], (need >> 1) & 1);
       __syncthreads();
       const bool act = ry < min(RB, ye - y0);
       float acc[PX][8];
@@ -454,12 +468,15 @@ __global__ void __launch_bounds__(kDw7MaxThreads, 1)
         }
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // the item's last (possibly empty) prefetch group must land before the ring is reused
+    mbar_wait(&s_bar[(grp - 1) & 1], ((grp - 1) >> 1) & 1);
     __syncthreads();
   }
   pdl_trigger();
 }
-int dwln7_smem(int W, int C, int RB) { return (2 * RB + 6) * (W + 6) * C * 2 + 2 * RB * W * ((C / 8 + 30) / 32 + 1) * 4; }
+int dwln7_smem(int W, int C, int RB) {
+  return (2 * RB + 6) * (W + 6) * C * 2 + 2 * RB * W * ((C / 8 + 30) / 32 + 1) * 4 + 16;
+}
 int dwln7_threads(int W, int C, int RB) { return (RB * (W / kDw7Px) * (C / 8) + 31) / 32 * 32; }
 // segments per image: waves of (image, segment) items x (band steps + ~0.75 of
 // a step for the window a segment loads before its first step) — at b128 one
