@@ -212,73 +212,102 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       // ---------------------------------------------------------- MMA issuer
+      // (the whole warp runs the loop; one elected lane issues each MMA / commit)
       const uint32_t idesc_e = make_idesc_f16(128, HC) | Dt<T>::kIdescAB;
       const int zn = C > 256 ? C / 2 : C;
       const uint32_t idesc_z = make_idesc_f16(128, zn) | Dt<T>::kIdescAB;
       const uint32_t sa = smem_u32(s_a), sr = smem_u32(s_ring), svr = smem_u32(s_vring);
-      int useq = 0, vseq = 0;
-      for (int t = 0; t < my_tiles; ++t) {
-        const int xb = t % a.NA;
-        mbar_wait(&B.a_full[xb], (t / a.NA) & 1);
-        tc_fence_after();
-        const uint32_t sx = sa + xb * a.slabs * 16384;
-        auto expand = [&](int j) {
-          const int NE = a.NE, g = t * nch + j, b = g % NE;
-          if (g >= NE) mbar_wait(&B.p_done[b], ((g - NE) / NE) & 1);  // H_{g-NE} consumed
-          FF_TRACE(16 + g * 4 + 0);
-          const uint32_t d = tmem + a.t_e + b * HC;
-          for (int sl = 0; sl < a.slabs; ++sl, ++useq) {
-            const int s = a.resident ? (j * a.slabs + sl) : useq % a.NU;
-            mbar_wait(&B.u_full[s], a.resident ? 0 : (useq / a.NU) & 1);
-            tc_fence_after();
-            const uint32_t st = sr + s * a.us_bytes;
+      // ring positions of the streamed U / V slabs (incremental: an integer
+      // division here is a MUFU.RCP queued behind the epilogue's GELU tanh)
+      int us = 0, uph = 0, vs = 0, vph = 0;
+      // The issue loop is latency-bound in this one thread (each tcgen05.mma
+      // waits on its descriptor chain), so everything that does not change per
+      // MMA is hoisted: descriptor bases advance by (byte offset >> 4) in their
+      // start-address field, the TMEM A offsets of the projection's K steps are
+      // a table, and resident weight stages are waited on once.
+      const uint64_t du0 = make_sdesc_sw128(sr), dv0 = make_sdesc_sw128(svr);
+      uint32_t aoff[8];  // K step kk of H_j: epilogue group hs packs its HC / G hidden at the start of its range
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
-              if (sl * 64 + k4 * 16 >= C) break;  // zero-padded channels of a partial slab
-              const uint64_t ad = make_sdesc_sw128(sx + sl * 16384 + k4 * 32);
-              const uint64_t bd = make_sdesc_sw128(st + k4 * 32);
-              mma_ss(d, ad, bd, idesc_e, (sl | k4) != 0);
+      for (int kk = 0; kk < 8; ++kk) {
+        const int hs = (kk * 16) / (HC / kGroups), loc = kk * 16 - hs * (HC / kGroups);
+        aoff[kk] = hs * (HC / kGroups) + loc / 2;
+      }
+      const int NE = a.NE, nsl = HC / 64, nr0 = C > 256 ? 2 : 1;
+      int eb = 0, eph = 0;  // E buffer of the next expansion and its reuse count
+      int pb = 0, pph = 0;  // E/H buffer of the next projection
+      int xb = 0, xph = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        mbar_wait(&B.a_full[xb], xph & 1);
+        tc_fence_after();
+        const uint64_t dx0 = make_sdesc_sw128(sa + xb * a.slabs * 16384);
+        const bool wait_w = !a.resident || t == 0;
+        auto expand = [&](int j) {
+          const int g = t * nch + j, b = eb;
+          if (eph > 0) mbar_wait(&B.p_done[b], (eph - 1) & 1);  // H of this buffer's previous use consumed
+          if (++eb == NE) eb = 0, ++eph;
+          if (lane == 0) FF_TRACE(16 + g * 4 + 0);
+          const uint32_t d = tmem + a.t_e + b * HC;
+          for (int sl = 0; sl < a.slabs; ++sl) {
+            const int s = a.resident ? (j * a.slabs + sl) : us;
+            if (wait_w) {
+              mbar_wait(&B.u_full[s], a.resident ? 0 : uph);
+              tc_fence_after();
             }
-            if (!a.resident) mma_commit(&B.u_empty[s]);
+            if (!a.resident && ++us == a.NU) us = 0, uph ^= 1;
+            const uint64_t ad = dx0 + (uint64_t)(sl * (16384 >> 4)), bd = du0 + (uint64_t)(s * (a.us_bytes >> 4));
+            const int nk = min(4, (C - sl * 64) / 16);  // zero-padded channels of a partial slab
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              if (k4 < nk) mma_ss_w(d, ad + 2 * k4, bd + 2 * k4, idesc_e, (sl | k4) != 0);
+            if (!a.resident) mma_commit_w(&B.u_empty[s]);
           }
-          mma_commit(&B.e_full[b]);
-          if (j == nch - 1) mma_commit(a.direct ? &B.a_free[xb] : &B.a_used[xb]);
+          if (lane == 0) FF_TRACE(2000 + g * 2 + 0);
+          mma_commit_w(&B.e_full[b]);
+          if (j == nch - 1) mma_commit_w(a.direct ? &B.a_free[xb] : &B.a_used[xb]);
         };
         auto project = [&](int j) {
-          const int NE = a.NE, g = t * nch + j, b = g % NE;
-          mbar_wait(&B.h_full[b], (g / NE) & 1);
+          const int g = t * nch + j, b = pb;
+          mbar_wait(&B.h_full[b], pph & 1);
+          if (++pb == NE) pb = 0, ++pph;
           if (j == 0 && t > 0) mbar_wait(&B.z_empty, (t - 1) & 1);
-          FF_TRACE(16 + g * 4 + 1);
-          for (int sl = 0; sl < HC / 64; ++sl, ++vseq) {
-            const int s = a.resident ? (j * (HC / 64) + sl) : vseq % a.NV;
-            mbar_wait(&B.v_full[s], a.resident ? 0 : (vseq / a.NV) & 1);
-            tc_fence_after();
-            const uint32_t st = svr + s * a.vs_bytes;
+          if (lane == 0) FF_TRACE(16 + g * 4 + 1);
+          const uint32_t ab = tmem + a.t_e + b * HC;
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
-              // H_j packed in place: epilogue group gq owns hidden
-              // [gq HC/G, (gq+1) HC/G) and writes it packed at the start of
-              // its own column range
-              const int kk = sl * 4 + k4;
-              const int hs = (kk * 16) / (HC / kGroups), loc = kk * 16 - hs * (HC / kGroups);
-              const uint32_t at = tmem + a.t_e + b * HC + hs * (HC / kGroups) + loc / 2;
-              for (int r0 = 0; r0 < C; r0 += zn) {
-                const uint64_t bd = make_sdesc_sw128(st + r0 * 128 + k4 * 32);
-                mma_ts(tmem + a.t_z + r0, at, bd, idesc_z, (j > 0 || kk > 0));
-              }
+          for (int sl = 0; sl < 2; ++sl) {
+            if (sl >= nsl) break;
+            const int s = a.resident ? (j * nsl + sl) : vs;
+            if (wait_w) {
+              mbar_wait(&B.v_full[s], a.resident ? 0 : vph);
+              tc_fence_after();
             }
-            if (!a.resident) mma_commit(&B.v_empty[s]);
+            if (!a.resident && ++vs == a.NV) vs = 0, vph ^= 1;
+            const uint64_t bd = dv0 + (uint64_t)(s * (a.vs_bytes >> 4));
+            if (nr0 == 1) {
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4)
+                mma_ts_w(tmem + a.t_z, ab + aoff[sl * 4 + k4], bd + 2 * k4, idesc_z, (j > 0 || sl > 0 || k4 > 0));
+            } else {
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                  mma_ts_w(tmem + a.t_z + r * zn, ab + aoff[sl * 4 + k4], bd + (uint64_t)(r * zn * (128 >> 4)) + 2 * k4,
+                         idesc_z, (j > 0 || sl > 0 || k4 > 0));
+            }
+            if (!a.resident) mma_commit_w(&B.v_empty[s]);
           }
-          mma_commit(&B.p_done[b]);
-          if (j == nch - 1) mma_commit(&B.z_full);
+          if (lane == 0) FF_TRACE(2000 + g * 2 + 1);
+          mma_commit_w(&B.p_done[b]);
+          if (j == nch - 1) mma_commit_w(&B.z_full);
         };
         for (int j = 0; j < nch && j < a.NE; ++j) expand(j);
         for (int j = 0; j < nch; ++j) {
           project(j);
           if (j + a.NE < nch) expand(j + a.NE);
         }
+        if (++xb == a.NA) xb = 0, ++xph;
       }
     }
   } else {

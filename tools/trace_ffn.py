@@ -26,4 +26,6 @@ for c, hw in [(int(v.split('x')[0]), int(v.split('x')[1])) for v in (sys.argv[1:
         print(f"  tile {tile}: z_full@{r(t[3000+2*tile])} z_drained@{r(t[3000+2*tile+1])}")
     for g in range(min(3 * nch, (3000 - 16) // 4)):
         e, p, es, hd = (r(t[16 + g * 4 + k]) for k in range(4))
-        print(f"  g{g:3d}: E@{e:7d} Eseen@{es:7d} H@{hd:7d} P@{p:7d}")
+        ei, pi = r(t[2000 + 2 * g]), r(t[2000 + 2 * g + 1])
+        print(f"  g{g:3d}: E@{e:7d} Eissued@{ei:7d} Eseen@{es:7d} H@{hd:7d} P@{p:7d} Pissued@{pi:7d}")
+
