@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       }
     }
   } else if (warp == kMma) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; one elected lane issues each MMA / commit
       // ------------------------------------------------------------ MMA issuer
       // P = 8: M = 64 over the compact 64-row x tile; the accumulator rows land
       // 16 per TMEM lane quadrant (rows 16k.. at lanes 32k..)
@@ -312,13 +312,13 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
       for (int blk = 0; blk < nblk; ++blk) {
         mbar_wait(&B.x_full, blk & 1);
         tc_fence_after();
-        MB1_TRACE(70);
+        if (lane == 0) MB1_TRACE(70);
         for (int j = 0; j < nch; ++j) {
           const int g = blk * nch + j, b = g & 1, u = g >> 1;
           mbar_wait(&B.w_full[b], u & 1);
           mbar_wait(&B.e_empty[b], (u & 1) ^ 1);
           tc_fence_after();
-          MB1_TRACE(36 + j);
+          if (lane == 0) MB1_TRACE(36 + j);
           const uint32_t wb = smem_u32(s_w + b * wbytes);
 #pragma unroll
           for (int t = 0; t < NT; ++t)
@@ -326,10 +326,10 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
             for (int k = 0; k < C / 16; ++k) {
               const uint64_t ad = make_sdesc_sw128(smem_u32(s_x) + (k / 4) * XH + t * 16384 + (k % 4) * 32);
               const uint64_t bd = make_sdesc(wb + k * 2 * 1024, 1024, 128);
-              mma_ss(tmem + a.t_e + (b * NT + t) * kHC, ad, bd, idesc_e, k > 0);
+              mma_ss_w(tmem + a.t_e + (b * NT + t) * kHC, ad, bd, idesc_e, k > 0);
             }
-          mma_commit(&B.e_full[b]);
-          mma_commit(&B.w_empty[b]);
+          mma_commit_w(&B.e_full[b]);
+          mma_commit_w(&B.w_empty[b]);
         }
         // Z of the previous block must have been drained (phase D) before the
         // first projection of this one overwrites it: d_done(blk - 1) precedes
@@ -342,16 +342,16 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
             mbar_wait(&B.pa_full[s], u & 1);   // W_prj chunk landed
             mbar_wait(&B.pa_ready[s], u & 1);  // h2 chunk gated
             tc_fence_after();
-            MB1_TRACE(52 + j);
+            if (lane == 0) MB1_TRACE(52 + j);
             const uint32_t vb = smem_u32(s_w + s * a.slot_bytes);
             const uint32_t hb = smem_u32(smem + a.s_h2) + j * 8192;
 #pragma unroll
             for (int k = 0; k < kHC / 16; ++k) {
               const uint64_t ad = make_sdesc(hb + k * 2 * 1024, 1024, 128);
               const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
-              mma_ss(tmem + a.t_z, ad, bd, idesc_z64, (j > 0 || k > 0));
+              mma_ss_w(tmem + a.t_z, ad, bd, idesc_z64, (j > 0 || k > 0));
             }
-            mma_commit(&B.pa_empty[s]);
+            mma_commit_w(&B.pa_empty[s]);
           }
         } else if constexpr (S2) {
           const uint32_t idesc_s2 = make_idesc_f16(64, a.K);
@@ -360,15 +360,15 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
             const int s = gq & 3, u = gq >> 2;
             mbar_wait(&B.pa_ready[s], u & 1);  // landed and gated
             tc_fence_after();
-            MB1_TRACE(52 + j);
+            if (lane == 0) MB1_TRACE(52 + j);
             const uint32_t slot = smem_u32(s_h1 + s * a.slot_bytes);
 #pragma unroll
             for (int k = 0; k < kHC / 16; ++k) {
               const uint64_t ad = make_sdesc(slot + k * 2 * 1024, 1024, 128);
               const uint64_t bd = make_sdesc(slot + 8192 + k * 2 * (a.K / 8) * 128, (a.K / 8) * 128, 128);
-              mma_ss(tmem + a.t_z, ad, bd, idesc_s2, (j > 0 || k > 0));
+              mma_ss_w(tmem + a.t_z, ad, bd, idesc_s2, (j > 0 || k > 0));
             }
-            mma_commit(&B.pa_empty[s]);
+            mma_commit_w(&B.pa_empty[s]);
           }
         } else {
         for (int qq = 0; qq < 2 * nch; ++qq) {
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
           const int s = gq & 3, u = gq >> 2;
           mbar_wait(&B.pa_ready[s], u & 1);
           tc_fence_after();
-          if (!(qq & 1)) MB1_TRACE(52 + (qq >> 1));
+          if (!(qq & 1)) if (lane == 0) MB1_TRACE(52 + (qq >> 1));
           const uint32_t slot = smem_u32(s_h1 + s * a.slot_bytes);
           const uint32_t vb = slot + NT * 8192;
 #pragma unroll
@@ -385,12 +385,12 @@ __global__ void __launch_bounds__(mb1::kThreads, 1)
             for (int k = 0; k < 2; ++k) {
               const uint64_t ad = make_sdesc(slot + t * 8192 + k * 2 * 2048, 2048, 128);
               const uint64_t bd = make_sdesc(vb + k * 2 * (C / 8) * 128, (C / 8) * 128, 128);
-              mma_ss(tmem + a.t_z + t * C, ad, bd, idesc_z, (qq > 0 || k > 0));
+              mma_ss_w(tmem + a.t_z + t * C, ad, bd, idesc_z, (qq > 0 || k > 0));
             }
-          mma_commit(&B.pa_empty[s]);
+          mma_commit_w(&B.pa_empty[s]);
         }
         }
-        mma_commit(&B.z_full);
+        mma_commit_w(&B.z_full);
       }
     }
   } else if (warp < kC0) {
