@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
+    {  // warp-converged issue: one elected lane issues each MMA / commit
       const uint32_t idesc_exp = make_idesc_f16(128, r);
       const uint32_t idesc_prj = make_idesc_f16(128, C);
       const uint32_t xc0 = smem_u32(s_xc), ring0 = smem_u32(s_ring);
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
       for (int it = 0; it < my_tiles; ++it) {
         const int xb = it & 1;
         mbar_wait(&B.xc_full[xb], (it >> 1) & 1);
-        CF_TRACE(it, 5);
+        if (lane == 0) CF_TRACE(it, 5);
         tc_fence_after();
         const uint32_t xcb = xc0 + xb * pl.xc_bytes;
         auto slot_addr = [&](int j, int g) -> uint32_t {
@@ -185,10 +185,10 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
 #pragma unroll 1
           for (int kk = 0; kk < r / 16; ++kk) {
             const uint64_t bd = make_sdesc(vbase + kk * 2 * (C * 16), C * 16, 128);
-            mma_ts(tmem + pl.t_z, tmem + pl.t_h + hb * pl.h_stride + kk * 8, bd, idesc_prj, (j > 0 || kk > 0));
+            mma_ts_w(tmem + pl.t_z, tmem + pl.t_h + hb * pl.h_stride + kk * 8, bd, idesc_prj, (j > 0 || kk > 0));
           }
-          mma_commit(&B.h_empty[hb]);
-          if (!pl.resident) mma_commit(&B.w_empty[g % S]);
+          mma_commit_w(&B.h_empty[hb]);
+          if (!pl.resident) mma_commit_w(&B.w_empty[g % S]);
         };
         for (int j = 0; j < nchunks; ++j) {
           const int g = it * nchunks + j, eb = g & 1;
@@ -199,15 +199,15 @@ __global__ void __launch_bounds__(cfk::kThreads, 2)
           for (int kk = 0; kk < C / 16; ++kk) {
             const uint64_t ad = make_sdesc(xcb + kk * 2 * 2048, 2048, 128);
             const uint64_t bd = make_sdesc(ubase + kk * 2 * (r * 16), r * 16, 128);
-            mma_ss(tmem + pl.t_e + eb * r, ad, bd, idesc_exp, kk > 0);
+            mma_ss_w(tmem + pl.t_e + eb * r, ad, bd, idesc_exp, kk > 0);
           }
-          mma_commit(&B.e_full[eb]);
-          if (j == nchunks - 1) mma_commit(&B.xc_empty[xb]);
+          mma_commit_w(&B.e_full[eb]);
+          if (j == nchunks - 1) mma_commit_w(&B.xc_empty[xb]);
           if (j > 0) issue_project(j - 1);
         }
         issue_project(nchunks - 1);
-        mma_commit(&B.z_full);
-        CF_TRACE(it, 8);
+        mma_commit_w(&B.z_full);
+        if (lane == 0) CF_TRACE(it, 8);
       }
     }
   } else if ((warp >= kHWarp0 && warp < kHWarp0 + 4) || warp >= 12) {

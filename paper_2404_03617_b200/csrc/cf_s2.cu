@@ -196,18 +196,18 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
-    if (lane == 0) {
+    {  // warp-converged issue: one elected lane issues each MMA / commit
       mbar_wait(&B.w_full, 0);
       const uint32_t cw = smem_u32(s_w + a.o_convw);
       const uint32_t idesc_c = make_idesc_f16(128, 16);
       const uint32_t idesc_e = make_idesc_f16(128, r);
       const uint32_t idesc_z = make_idesc_f16(128, K);
       auto conv_begin = [&](int i) {
-        if (i < 8) CF2_TRACE(8 + i * 24 + 1);
+        if (i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 1);
         mbar_wait(&B.x_full[i % a.x_bufs], (i / a.x_bufs) & 1);
         mbar_wait(&B.c_empty, (i & 1) ^ 1);  // previous band's conv accumulators drained
         tc_fence_after();
-        if (i < 8) CF2_TRACE(8 + i * 24 + 2);
+        if (i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 2);
       };
       auto conv_tiles = [&](int i, int t0, int t1) {
         const uint32_t x0 = smem_u32(s_x) + (i % a.x_bufs) * planes * a.x_alloc * 16;
@@ -219,16 +219,16 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
             const uint32_t d = tmem + a.t_c + t * C + 16 * pr;
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {  // incremental descriptors (cheap issue)
-              mma_ss(d, aa, bd, idesc_c, tap > 0);
+              mma_ss_w(d, aa, bd, idesc_c, tap > 0);
               aa += (tap % 3 == 2) ? (uint64_t)(Wp - 2) : 1ull;
               bd += 32;
             }
           }
       };
       auto conv_end = [&](int i) {
-        mma_commit(&B.conv_full);
-        mma_commit(&B.x_empty[i % a.x_bufs]);
-        if (i < 8) CF2_TRACE(8 + i * 24 + 3);
+        mma_commit_w(&B.conv_full);
+        mma_commit_w(&B.x_empty[i % a.x_bufs]);
+        if (i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 3);
       };
       // chunk j of band i (global index g): resident slot j, or ring stage g % ws
       auto chunk_addr = [&](int g, int j) -> uint32_t {
@@ -243,11 +243,11 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         const uint32_t aq = smem_u32(s_aq) + qs * a.aq_bytes;
         for (int t = 0; t < a.n_eh; ++t)
           for (int kk = 0; kk < r / 16; ++kk)
-            mma_ss(tmem + a.t_z + t * K, make_sdesc(aq + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
+            mma_ss_w(tmem + a.t_z + t * K, make_sdesc(aq + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
                    make_sdesc(vb + kk * 2 * (K * 16), K * 16, 128), idesc_z, (j > 0 || kk > 0));
-        mma_commit(&B.q_empty[qs]);
-        if (a.ws) mma_commit(&B.wr_empty[gq % a.ws]);
-        if (j == nch - 1) mma_commit(&B.z_full);
+        mma_commit_w(&B.q_empty[qs]);
+        if (a.ws) mma_commit_w(&B.wr_empty[gq % a.ws]);
+        if (j == nch - 1) mma_commit_w(&B.z_full);
       };
       // warp 1 issues the FFN (expand / project chunks); the grouped conv is
       // issued by warps 3 and 2 (below) and runs ahead as far as G1's drain
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         const int hb = i & 1;
         mbar_wait(&B.xh_full[hb], (i >> 1) & 1);
         tc_fence_after();
-        if (i < 8) CF2_TRACE(8 + i * 24 + 4);
+        if (i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 4);
         const uint32_t ah = smem_u32(s_ah) + hb * a.ah_bytes;
         for (int j = 0; j < nch; ++j) {
           const int gg = i * nch + j, es = gg & 1;
@@ -266,19 +266,19 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
           const uint32_t ub = chunk_addr(gg, j);
           for (int t = 0; t < a.n_eh; ++t)
             for (int kk = 0; kk < C / 16; ++kk)
-              mma_ss(tmem + a.t_e + (es * a.n_eh + t) * r, make_sdesc(ah + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
+              mma_ss_w(tmem + a.t_e + (es * a.n_eh + t) * r, make_sdesc(ah + (kk * 2 * MH + t * 128) * 16, MH * 16, 128),
                      make_sdesc(ub + kk * 2 * (r * 16), r * 16, 128), idesc_e, kk > 0);
-          mma_commit(&B.e_full[es]);
-          if (j == nch - 1) mma_commit(&B.xh_empty[hb]);
+          mma_commit_w(&B.e_full[es]);
+          if (j == nch - 1) mma_commit_w(&B.xh_empty[hb]);
           if (j > 0) issue_project(i, j - 1);
         }
         issue_project(i, nch - 1);
-        if (i < 8) CF2_TRACE(8 + i * 24 + 5);
+        if (i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 5);
       }
     }
   } else if (warp == 3 || warp == 2) {
     // ---------------- grouped-conv issuers: conv tiles split between two threads
-    if (lane == 0) {
+    {  // warp-converged issue: one elected lane issues each MMA / commit
       const int ci = warp == 3 ? 0 : 1;
       mbar_wait(&B.w_full, 0);
       const uint32_t cw = smem_u32(s_w + a.o_convw);
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
         mbar_wait(&B.x_full[xb], (i / a.x_bufs) & 1);
         mbar_wait(&B.c_empty, (i & 1) ^ 1);  // previous band's conv accumulators drained
         tc_fence_after();
-        if (ci == 0 && i < 8) CF2_TRACE(8 + i * 24 + 2);
+        if (ci == 0 && i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 2);
         const uint32_t x0 = smem_u32(s_x) + xb * planes * a.x_alloc * 16;
         for (int t = ci; t < a.n_ct; t += 2)
           for (int pr = 0; pr < C / 16; ++pr) {
@@ -297,14 +297,14 @@ __global__ void __launch_bounds__(cf2k::kThreads, 1)
             const uint32_t d = tmem + a.t_c + t * C + 16 * pr;
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
-              mma_ss(d, aa, bd, idesc_c, tap > 0);
+              mma_ss_w(d, aa, bd, idesc_c, tap > 0);
               aa += (tap % 3 == 2) ? (uint64_t)(Wp - 2) : 1ull;
               bd += 32;
             }
           }
-        mma_commit(&B.conv_full);
-        mma_commit(&B.x_empty[xb]);
-        if (ci == 0 && i < 8) CF2_TRACE(8 + i * 24 + 3);
+        mma_commit_w(&B.conv_full);
+        mma_commit_w(&B.x_empty[xb]);
+        if (ci == 0 && i < 8) if (lane == 0) CF2_TRACE(8 + i * 24 + 3);
       }
     }
   } else if (warp >= 4 && warp < 8) {

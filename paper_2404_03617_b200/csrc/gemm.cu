@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // warp-converged issue: one elected lane issues each MMA / commit
       // ---------------------------------------------------------- MMA issuer
       const uint32_t idesc = make_idesc_f16(128, a.BN) | Dt<T>::kIdescAB;
       int s = 0;
@@ -165,14 +165,14 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
           const uint32_t sa = smem_u32(smem + s * a.stage_bytes), sb = sa + 16384;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_ss(d, make_sdesc_sw128(sa + k * 32), make_sdesc_sw128(sb + k * 32), idesc, (kb | k) != 0);
-          mma_commit(&B.empty[s]);
+            mma_ss_w(d, make_sdesc_sw128(sa + k * 32), make_sdesc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+          mma_commit_w(&B.empty[s]);
           if (++s == a.stages) {
             s = 0;
             ph ^= 1;
           }
         }
-        mma_commit(&B.acc_full[ab]);
+        mma_commit_w(&B.acc_full[ab]);
       }
     }
   } else {
