@@ -33,7 +33,7 @@ constexpr int kBK = 64;
 constexpr int kMaxStages = 8;
 constexpr int kSmemMax = 232448;
 struct Args {
-  int M, N, BN, tiles_m, tiles, kblocks, stages, stage_bytes, s_stage, slabs;
+  int M, N, BN, tiles_m, tiles_n, tiles, kblocks, stages, stage_bytes, s_stage, slabs;
   int act, has_res;
   float ln_eps;
   const float* bias;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-        const int tn = tile / a.tiles_m, tm = tile % a.tiles_m;
+        const int tm = tile / a.tiles_n, tn = tile % a.tiles_n;  // m-major: the CTAs of one wave share A tiles through L2
         for (int kb = 0; kb < a.kblocks; ++kb) {
           mbar_wait(&B.empty[s], ph ^ 1);
           uint8_t* st = smem + s * a.stage_bytes;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(gm::kThreads, 1)
     int it = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
       const int ab = it & 1, u = it >> 1;
-      const int tn = tile / a.tiles_m, tm = tile % a.tiles_m;
+      const int tm = tile / a.tiles_n, tn = tile % a.tiles_n;  // m-major: the CTAs of one wave share A tiles through L2
       const int n0 = tn * a.BN;
       if (leader) {
         bulk_wait_read0_g();  // the previous tile's stores have left the staging buffer
@@ -356,7 +356,8 @@ int gemm_run(const void* A, int M, int K, int lda, const void* Bw, int N, int ld
   if (e.ln_g && (a.BN < N || N > 128 || e.act))
     return set_error(WL_EUNSUPPORTED, "gemm: the row-LayerNorm epilogue needs N <= 128 and no activation (N = %d)", N);
   a.tiles_m = (M + 127) / 128;
-  a.tiles = a.tiles_m * ((N + a.BN - 1) / a.BN);
+  a.tiles_n = (N + a.BN - 1) / a.BN;
+  a.tiles = a.tiles_m * a.tiles_n;
   a.kblocks = (K + gm::kBK - 1) / gm::kBK;
   a.stage_bytes = 16384 + a.BN * 128;
   a.slabs = (a.BN + 63) / 64;
