@@ -376,10 +376,14 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
       mbar_wait(&B.x_full, 0);
       if (a.x_tmem) mbar_wait(&B.x_ready, 0);
       WL_TRACE(2);
-      auto issue_expand = [&](int j) {
-        const int slot = j % S, eb = j % a.e_bufs;
+      // ring positions as counters (see the conv issuers)
+      int x_slot = 0, x_sph = 0, x_eb = 0;  // the next expansion's weight stage, its phase, its E buffer
+      auto issue_expand = [&](int j) {  // called for j = 0, 1, 2, ... in order
+        const int slot = x_slot, eb = x_eb;
         if (j < 20) WL_TRACE(232 + j);
-        mbar_wait(&B.w_full[slot], (j / S) & 1);
+        mbar_wait(&B.w_full[slot], x_sph & 1);
+        if (++x_slot == S) x_slot = 0, ++x_sph;
+        if (++x_eb == a.e_bufs) x_eb = 0;
         WL_TRACE(16 + 8 * j + 0);
         tc_fence_after();
         const uint32_t ub = ring0 + slot * a.chunk_bytes;
@@ -398,23 +402,30 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         mma_commit(&B.e_full[eb]);
       };
       issue_expand(0);
+      int m_slot = 0, m_hb = 0, m_hph = 0;  // chunk j's weight stage, h1 buffer and its phase
+      int d_hb = 0, d_hph = 0;             // the same for chunk jd = j + 1 - e_bufs (once jd >= 0)
       for (int j = 0; j < nch; ++j) {
-        const int slot = j % S, hb = j % a.h1_bufs;
+        const int slot = m_slot, hb = m_hb, hph = m_hph;
+        if (++m_slot == S) m_slot = 0;
+        if (++m_hb == a.h1_bufs) m_hb = 0, ++m_hph;
         if (T8) {
           // expansion j+1 reuses the E buffer of chunk j+1-e_bufs: wait for its drain
           const int jd = j + 1 - a.e_bufs;
           if (j + 1 < nch) {
-            if (jd >= 0) mbar_wait(&B.h1_full[jd % a.h1_bufs], (jd / a.h1_bufs) & 1);
+            if (jd >= 0) {
+              mbar_wait(&B.h1_full[d_hb], d_hph & 1);
+              if (++d_hb == a.h1_bufs) d_hb = 0, ++d_hph;
+            }
             issue_expand(j + 1);
           }
           mma_commit(&B.w_empty[slot]);
           continue;
         }
-        if (a.e_bufs == 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // E of chunk j consumed
+        if (a.e_bufs == 1) mbar_wait(&B.h1_full[hb], hph & 1);  // E of chunk j consumed
         if (j + 1 < nch) issue_expand(j + 1);
         if (T8) {
           const int cb = j % a.c_bufs;
-          if (a.e_bufs != 1) mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);
+          if (a.e_bufs != 1) mbar_wait(&B.h1_full[hb], hph & 1);
           if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
           WL_TRACE(16 + 8 * j + 1);
           tc_fence_after();
@@ -456,10 +467,13 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
     if (T8 && isx < NIS && lane == 0) {
       const uint32_t idesc_c = make_idesc_f16(128, 16);
       const uint32_t ring0 = smem_u32(s_ring);
+      // ring positions as counters (an integer division is a MUFU.RCP queued
+      // behind the epilogues' SiLU)
+      const int npr = HC / 16;
+      int slot = 0, hb = 0, cb = 0, hph = 0, cph = 0;
       for (int j = 0; j < nch; ++j) {
-        const int slot = j % S, hb = j % a.h1_bufs, cb = j % a.c_bufs;
-        mbar_wait(&B.h1_full[hb], (j / a.h1_bufs) & 1);  // h1 ready implies the chunk's weights landed
-        if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], ((j / a.c_bufs) & 1) ^ 1);
+        mbar_wait(&B.h1_full[hb], hph & 1);  // h1 ready implies the chunk's weights landed
+        if (j >= a.c_bufs) mbar_wait(&B.c_empty[cb], (cph & 1) ^ 1);
         if (isx == 0) WL_TRACE(16 + 8 * j + 1);
         tc_fence_after();
         const uint32_t h1a = smem_u32(hb ? smem + a.s_h1b : s_h1);
@@ -468,8 +482,9 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
         const uint32_t zaddr = ring0 + slot * a.chunk_bytes + a.u_bytes + E * 128;
         const uint64_t b_base = make_sdesc(zaddr - 128, 128, 128);
         const uint64_t b_step = (8ull << 16) + (8ull << 32) - 8ull;
-        for (int k = isx; k < a.n_ct * (HC / 16); k += NIS) {
-          const int t = k / (HC / 16), pr = k - t * (HC / 16);
+        int t = 0, pr = isx;  // k = t * npr + pr
+        while (pr >= npr) pr -= npr, ++t;
+        for (int k = isx; k < a.n_ct * npr; k += NIS) {
           {
             const uint32_t d = tmem + a.t_c + (cb * a.n_ct + t) * HC + 16 * pr;
             uint64_t ad = a_base + (uint64_t)(2 * pr * a.flat_h1 + t * 128), bd = b_base + (uint64_t)(pr * 9) * b_step;
@@ -480,11 +495,16 @@ __global__ void __launch_bounds__(mbk::kThreads, 1)
               bd += b_step;
             }
           }
+          pr += NIS;
+          while (pr >= npr) pr -= npr, ++t;
         }
         mma_commit(&B.c_full[cb]);
         mma_commit(&B.h1_empty[hb]);
         mma_commit(&B.w_empty[slot]);
         if (isx == 0) WL_TRACE(16 + 8 * j + 2);
+        if (++slot == S) slot = 0;
+        if (++hb == a.h1_bufs) hb = 0, ++hph;
+        if (++cb == a.c_bufs) cb = 0, ++cph;
       }
     }
   } else if (warp >= 4 && warp < 12) {
