@@ -61,8 +61,9 @@ int kernel_launches(const wl_block_desc& d) {
   if (d.kind == WL_KIND_HEAD || d.kind == WL_KIND_PATCH_STEM || d.kind == WL_KIND_DOWNSAMPLE ||
       d.kind == WL_KIND_LN_HEAD)
     return 2;
-  if (d.kind == WL_KIND_FFN) return ffn_launches(d);
-  if (cnx_wide(d) || cf_wide(d)) return 1 + ffn_launches(d);
+  if (d.kind == WL_KIND_FFN) return ffn_launches(d, true);
+  if (cnx_wide(d)) return 1 + ffn_launches(d, true);  // packed blob carries the fused kernel's weight images
+  if (cf_wide(d)) return 1 + ffn_launches(d, false);
   if (d.kind == WL_KIND_MBCONV) return mb_kernel_launches(d);
   return 1;
 }

@@ -629,13 +629,17 @@ int64_t hidden_rows(int64_t M, int hid) {
 // z = phi(x U + a) V + b (+ res): the fused kernel (hidden on chip, ffn.cu)
 // when its TMEM plan fits (C <= 384), else two GEMMs per row batch with the
 // hidden in the L2-resident workspace
+// the fused FFN kernel (hidden on chip) up to C = 256 when its weight images exist
+bool ffn_fused_route(int64_t M, int C, int hid) {
+  return C <= 256 && ffn_images_bytes(C, hid) > 0 && ffn_fused_ok(M, C, hid);
+}
 int ffn_rows(const __half* x, int64_t M, int C, int hid, int K, const __half* ut, const float* a, const __half* vt,
              const float* b, int act, const __half* res, __half* z, __half* hbuf, const uint8_t* wimg,
              cudaStream_t st, int dtype) {
-  // the fused kernel wins while its weights stay resident (C <= 128); from C = 192
-  // the two GEMMs with an L2-resident hidden are faster (ConvNeXt-T b128: 14x14 stage
-  // 250 vs 121 us, 28x28 stage 300 vs 272 us per block, profiles/r02_convnext_*)
-  if (K == C && C <= 128 && wimg && ffn_fused_ok(M, C, hid))
+  // the fused kernel (hidden on chip) up to C = 256; above, the two GEMMs with an
+  // L2-resident hidden (ConvNeXt-T b128 per block, after the FFN issuer rework:
+  // 28x28x192 180 vs 212 us fused vs GEMMs, 14x14x384 195 vs 121 us)
+  if (K == C && wimg && ffn_fused_route(M, C, hid))
     return ffn_fused_run(x, M, C, hid, wimg, a, b, act, res, z, st, dtype);
   const int64_t rb = hidden_rows(M, hid);
   for (int64_t r0 = 0; r0 < M; r0 += rb) {
@@ -749,9 +753,9 @@ int ffn_row_batches(const wl_block_desc& d) {
   const int64_t M = (int64_t)d.n * d.h * d.w, rb = hidden_rows(M, d.expansion * d.c);
   return (int)((M + rb - 1) / rb);
 }
-int ffn_launches(const wl_block_desc& d) {
+int ffn_launches(const wl_block_desc& d, bool images) {
   const int64_t M = (int64_t)d.n * d.h * d.w;
-  return d.c <= 128 && ffn_fused_ok(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
+  return images && ffn_fused_route(M, d.c, d.expansion * d.c) ? 1 : 2 * ffn_row_batches(d);
 }
 
 bool cnx_wide(const wl_block_desc& d) {

@@ -99,7 +99,7 @@ int cf_wide_fwd(const wl_block_desc& d, const void* x, const void* p, void* z, v
 int lw_gconv(const wl_block_desc& d, int C, const void* x, const float* w, const float* b, void* y, int act,
              cudaStream_t st);  // fp16 x / y
 int ffn_row_batches(const wl_block_desc& d);
-int ffn_launches(const wl_block_desc& d);
+int ffn_launches(const wl_block_desc& d, bool images);
 // fused FFN (ffn.cu): hidden kept on chip
 bool ffn_fused_ok(int64_t M, int C, int hid);
 int ffn_fused_run(const void* x, int64_t M, int C, int hid, const void* wimg, const float* abias, const float* bbias,
