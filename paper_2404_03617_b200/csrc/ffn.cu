@@ -351,14 +351,54 @@ __global__ void __launch_bounds__(ff::kThreads, 1)
       // --------------------------------------------- z = Z + b (+ res)
       const int xb = t % a.NA;
       uint8_t* s_x = s_a + xb * a.slabs * 16384;
+      const int units = C / 16, u_lo = grp * units / kGroups, u_hi = (grp + 1) * units / kGroups;
+      const int64_t grow = (int64_t)tile * 128 + r;
+      // direct stores: the residual rows are fetched from global before the wait
+      // for Z, so their latency hides under the tile's last projection
+      constexpr int kPre = 3;
+      const bool pre = a.direct && a.has_res && u_hi - u_lo <= kPre;
+      uint4 rpre[kPre][2];
+      if (pre) {
+#pragma unroll
+        for (int i = 0; i < kPre; ++i)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            rpre[i][hh] = (u_lo + i < u_hi && grow < a.M)
+                              ? __ldg(reinterpret_cast<const uint4*>(a.res + grow * C + (u_lo + i) * 16 + 8 * hh))
+                              : make_uint4(0, 0, 0, 0);
+      }
       mbar_wait(&B.z_full, t & 1);
       if (threadIdx.x == 64) FF_TRACE(3000 + 2 * t + 0);
       if (a.has_res && !a.direct) mbar_wait(&B.res_full[xb], (t / a.NA) & 1);
       tc_fence_after();
-      const int units = C / 16, u_lo = grp * units / kGroups, u_hi = (grp + 1) * units / kGroups;
       const uint32_t zb = tmem_lane_addr(tmem, q, a.t_z);
-      const int64_t grow = (int64_t)tile * 128 + r;
-      for (int u0 = u_lo; u0 < u_hi; u0 += 2) {
+      if (pre) {
+#pragma unroll
+        for (int i0 = 0; i0 < kPre; i0 += 2) {
+          if (u_lo + i0 >= u_hi) break;
+          uint32_t v[32];
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            if (i0 + jj < kPre && u_lo + i0 + jj < u_hi) WL_TMEM_LD16(zb + (u_lo + i0 + jj) * 16, (v + 16 * jj));
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            if (i0 + jj < kPre && u_lo + i0 + jj < u_hi && grow < a.M) {
+              const int c16 = (u_lo + i0 + jj) * 16;
+              float bb[16];
+              load16f(s_bbias + c16, bb);
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                float f[8], rr[8];
+                unpack8t<T>(rpre[i0 + jj][hh], rr);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[16 * jj + 8 * hh + i]) + bb[8 * hh + i] + rr[i];
+                *reinterpret_cast<uint4*>(a.z + grow * C + c16 + 8 * hh) = pack8t<T>(f);
+              }
+            }
+        }
+      }
+      for (int u0 = pre ? u_hi : u_lo; u0 < u_hi; u0 += 2) {
         uint32_t v[32];
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj)
