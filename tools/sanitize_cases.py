@@ -30,7 +30,7 @@ CASES = {
     # session 3: dwln7 + the fused FFN (C = 192 route, C = 96 direct stores with the residual
     # prefetch at 65536 pixels) and the two GEMMs (C = 384)
     "cnx_c192": (ConvNeXtBlock(7, 4, "gelu"), TensorDims(1, 14, 14, 192), None),
-    "cnx_c96_big": (ConvNeXtBlock(7, 4, "gelu"), TensorDims(1, 256, 256, 96), None),
+    "cnx_c96_big": (ConvNeXtBlock(7, 4, "gelu"), TensorDims(21, 56, 56, 96), None),
     "cnx_c384": (ConvNeXtBlock(7, 4, "gelu"), TensorDims(1, 14, 14, 384), None),
 }
 LAYER_WISE = {"lw_mbconv", "lw_convfirst"}
